@@ -1,0 +1,164 @@
+/*
+ * hmx_gpu.h - C ABI of the B200 (sm_100a) H-matrix matvec / BiCG-STAB library.
+ *
+ * This is the drop-in boundary for the reference package `hmx`
+ * (/root/reference/pkg/src/hmx).  The reference is pure Python, so its
+ * "operator API" is a set of Python signatures; each entry point below
+ * replaces one of them, and paper_1911_00093_b200/_gpu.py binds them with
+ * ctypes (INTEGRATION.md shows the binding):
+ *
+ *   hmx_plan_create     <- the payload layout fixed by prepare_scheme /
+ *                          SchemeHMatrix (precision.py:169-234, :256-329);
+ *                          the plan is the device-resident, flattened form
+ *   hmx_matvec          <- matvec(sh, x)                  (matvec.py:138-147)
+ *                          and matvec_threaded(sh, x, t)  (matvec.py:161-197)
+ *   hmx_nonfinite_block <- _check_finite's block rescan   (matvec.py:123-135)
+ *   hmx_true_residual   <- true_residual(h64, x, b)       (solver.py:56-65)
+ *   hmx_bicgstab        <- bicgstab(sh, h64, b, cfg)      (solver.py:68-168)
+ *
+ * All vectors are float64.  Pointers are host pointers unless a flag says
+ * device.  Every call returns an hmx_status; hmx_last_error() describes the
+ * last failure on the calling thread.  Calls on one plan are serialised by
+ * the plan's mutex; distinct plans may be used concurrently.
+ */
+#ifndef HMX_GPU_H
+#define HMX_GPU_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  HMX_OK = 0,
+  HMX_ERR_ARG = 1,        /* invalid argument or inconsistent descriptor */
+  HMX_ERR_CUDA = 2,       /* CUDA runtime failure (no device, OOM, ...) */
+  HMX_ERR_NONFINITE = 3,  /* matvec result not finite: FloatingPointError */
+  HMX_ERR_SHAPE = 4       /* vector length does not match the matrix: ValueError */
+} hmx_status;
+
+/* Precision schemes of the reference (precision.py:46-104). */
+typedef enum {
+  HMX_M1_DOUBLE = 0,
+  HMX_M1_SINGLE = 1,
+  HMX_M1_MIXED = 2,
+  HMX_M2_DOUBLE = 3,
+  HMX_M2_SINGLE = 4,
+  HMX_M2_MIXED = 5,
+  HMX_M3 = 6 /* m3:c=<int>; the split is already applied in the payloads */
+} hmx_scheme;
+
+/*
+ * Host-side packed payloads of one prepared scheme (python: PackedScheme).
+ * Block k covers rows [table[5k], table[5k+1]) and columns
+ * [table[5k+2], table[5k+3]) of the permuted index space.
+ *   kind[k] == 0  dense: m x n row-major at a_off[k] in buf32 (a32) or buf64
+ *   kind[k] == 1  low rank:
+ *       FP64 class ("hi"): U m x khi then Vt khi x n, row-major, at hi_off[k]
+ *                          in buf32 (hi32) or buf64; diagonal d_hi (buf64) at
+ *                          dhi_off[k], or -1 for Method 1 (no diagonal)
+ *       FP32 class ("lo", Method 3 only): U m x klo then Vt klo x n at
+ *                          lo_off[k] in buf32; d_lo at dlo_off[k] in buf64
+ * perm[i] is the original index of permuted index i (partition.py:66).
+ */
+typedef struct {
+  int64_t n;
+  int64_t n_blocks;
+  int32_t scheme; /* hmx_scheme */
+  int32_t a32;
+  int32_t hi32;
+  int32_t reserved;
+  const int64_t* perm;
+  const int64_t* table;
+  const int32_t* kind;
+  const int64_t* a_off;
+  const int64_t* hi_off;
+  const int64_t* khi;
+  const int64_t* dhi_off;
+  const int64_t* lo_off;
+  const int64_t* klo;
+  const int64_t* dlo_off;
+  const double* buf64;
+  int64_t n64;
+  const float* buf32;
+  int64_t n32;
+} hmx_matrix_desc;
+
+/* Optional row restriction (multi-GPU row partition): the plan computes only
+ * rows [row_begin, row_end) of y.  Pass NULL options for the full matrix. */
+typedef struct {
+  int64_t row_begin;
+  int64_t row_end;
+  int32_t s1_chunk_bytes; /* 0 = default stage-1 task size */
+  int32_t s2_threads;     /* 0 = default stage-2 CTA size */
+} hmx_plan_options;
+
+typedef struct hmx_plan hmx_plan;
+
+typedef struct {
+  int64_t n;
+  int64_t payload_bytes;   /* algorithmic matrix bytes (precision.py:332-334) */
+  int64_t device_bytes;    /* device memory held by the plan */
+  int64_t s1_segments, s1_tasks, s2_segments, s2_runs, z_len;
+  int64_t stage1_bytes, stage2_bytes; /* stored payload bytes read per stage */
+  int32_t s1_grid, s1_block, s2_grid, s2_block;
+} hmx_plan_info;
+
+/* matvec flags */
+#define HMX_DEVICE_PTRS 1 /* x and y are device pointers */
+#define HMX_PERMUTED 2    /* x and y are in permuted (cluster-tree) order */
+
+typedef struct {
+  int32_t converged;
+  int32_t iterations;
+  int32_t has_true_residual;
+  int32_t breakdown;        /* 0 none, 1 rho, 2 shadow projection, 3 stabilisation, 4 omega */
+  double true_residual;
+  double breakdown_value;
+  int32_t breakdown_iteration;
+  int32_t history_len;      /* entries written to `history` */
+  int32_t matvecs;          /* operator applications incl. the true-residual check */
+  int32_t reserved;
+  double device_ms;         /* GPU time of the solve (CUDA events) */
+} hmx_solve_report;
+
+const char* hmx_last_error(void);
+int hmx_device_count(int* count);
+
+int hmx_plan_create(const hmx_matrix_desc* desc, int device, const hmx_plan_options* opt,
+                    hmx_plan** out);
+void hmx_plan_destroy(hmx_plan* plan);
+int hmx_plan_get_info(const hmx_plan* plan, hmx_plan_info* info);
+
+/* y = A x (matvec.py:138).  Blocks until y is written.  Returns
+ * HMX_ERR_NONFINITE when any y entry is not finite (y is still written). */
+int hmx_matvec(hmx_plan* plan, const double* x, double* y, int flags);
+
+/* After HMX_ERR_NONFINITE: index of the first block (partition order) whose
+ * own contribution is not finite for the last x, or -1 if every block is
+ * finite on its own (overflow in the summation). */
+int hmx_nonfinite_block(hmx_plan* plan, int64_t* block);
+
+/* ||b - A64 x|| / ||b|| with A64 an m1-double plan (solver.py:56-65). */
+int hmx_true_residual(hmx_plan* plan64, const double* x, const double* b, double* out);
+
+/* BiCG-STAB from x0 = 0 (solver.py:68-168).  `plan` applies the scheme's
+ * operator, `plan64` (an m1-double plan of the same H-matrix, may equal
+ * `plan`) confirms convergence.  history needs max_iter + 1 entries. */
+int hmx_bicgstab(hmx_plan* plan, hmx_plan* plan64, const double* b, double tol, int max_iter,
+                 double* x, double* history, hmx_solve_report* report);
+
+/* Benchmark helper: `iters` device matvecs in permuted order on device
+ * buffers, timed with CUDA events on the plan's stream after `warmup`
+ * untimed ones.  flush_l2 > 0 writes a buffer of that many bytes between
+ * timed matvecs (excluded from the timing via per-matvec events).
+ * out_ms[0] = mean matvec ms, out_ms[1] = mean stage-1 ms, out_ms[2] = mean
+ * stage-2 ms, out_ms[3] = min matvec ms. */
+int hmx_bench_matvec(hmx_plan* plan, int warmup, int iters, int64_t flush_l2, double* out_ms);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* HMX_GPU_H */

@@ -1,0 +1,225 @@
+"""ctypes binding of the C ABI in include/hmx_gpu.h (libhmx_gpu.so).
+
+There is deliberately no CPU fallback: every public entry point of this
+package that computes a matvec or a solve goes through these bindings and
+raises if the library cannot be loaded or no CUDA device is present.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+import numpy as np
+
+from . import _native
+
+HMX_OK, HMX_ERR_ARG, HMX_ERR_CUDA, HMX_ERR_NONFINITE, HMX_ERR_SHAPE = 0, 1, 2, 3, 4
+HMX_DEVICE_PTRS, HMX_PERMUTED = 1, 2
+
+SCHEME_CODES = {"m1-double": 0, "m1-single": 1, "m1-mixed": 2, "m2-double": 3,
+                "m2-single": 4, "m2-mixed": 5}
+
+_i64p = ctypes.POINTER(ctypes.c_int64)
+_i32p = ctypes.POINTER(ctypes.c_int32)
+
+
+class MatrixDesc(ctypes.Structure):
+    _fields_ = [("n", ctypes.c_int64), ("n_blocks", ctypes.c_int64),
+                ("scheme", ctypes.c_int32), ("a32", ctypes.c_int32), ("hi32", ctypes.c_int32),
+                ("reserved", ctypes.c_int32),
+                ("perm", _i64p), ("table", _i64p), ("kind", _i32p),
+                ("a_off", _i64p), ("hi_off", _i64p), ("khi", _i64p), ("dhi_off", _i64p),
+                ("lo_off", _i64p), ("klo", _i64p), ("dlo_off", _i64p),
+                ("buf64", ctypes.POINTER(ctypes.c_double)), ("n64", ctypes.c_int64),
+                ("buf32", ctypes.POINTER(ctypes.c_float)), ("n32", ctypes.c_int64)]
+
+
+class PlanOptions(ctypes.Structure):
+    _fields_ = [("row_begin", ctypes.c_int64), ("row_end", ctypes.c_int64),
+                ("s1_chunk_bytes", ctypes.c_int32), ("s2_threads", ctypes.c_int32)]
+
+
+class PlanInfo(ctypes.Structure):
+    _fields_ = [("n", ctypes.c_int64), ("payload_bytes", ctypes.c_int64),
+                ("device_bytes", ctypes.c_int64), ("s1_segments", ctypes.c_int64),
+                ("s1_tasks", ctypes.c_int64), ("s2_segments", ctypes.c_int64),
+                ("s2_runs", ctypes.c_int64), ("z_len", ctypes.c_int64),
+                ("stage1_bytes", ctypes.c_int64), ("stage2_bytes", ctypes.c_int64),
+                ("s1_grid", ctypes.c_int32), ("s1_block", ctypes.c_int32),
+                ("s2_grid", ctypes.c_int32), ("s2_block", ctypes.c_int32)]
+
+
+class SolveReport(ctypes.Structure):
+    _fields_ = [("converged", ctypes.c_int32), ("iterations", ctypes.c_int32),
+                ("has_true_residual", ctypes.c_int32), ("breakdown", ctypes.c_int32),
+                ("true_residual", ctypes.c_double), ("breakdown_value", ctypes.c_double),
+                ("breakdown_iteration", ctypes.c_int32), ("history_len", ctypes.c_int32),
+                ("matvecs", ctypes.c_int32), ("reserved", ctypes.c_int32),
+                ("device_ms", ctypes.c_double)]
+
+
+# every exported symbol of include/hmx_gpu.h with its ctypes signature
+SIGNATURES = {
+    "hmx_last_error": (ctypes.c_char_p, []),
+    "hmx_device_count": (ctypes.c_int, [ctypes.POINTER(ctypes.c_int)]),
+    "hmx_plan_create": (ctypes.c_int, [ctypes.POINTER(MatrixDesc), ctypes.c_int,
+                                       ctypes.POINTER(PlanOptions),
+                                       ctypes.POINTER(ctypes.c_void_p)]),
+    "hmx_plan_destroy": (None, [ctypes.c_void_p]),
+    "hmx_plan_get_info": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(PlanInfo)]),
+    "hmx_matvec": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                  ctypes.c_int]),
+    "hmx_nonfinite_block": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(ctypes.c_int64)]),
+    "hmx_true_residual": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                         ctypes.POINTER(ctypes.c_double)]),
+    "hmx_bicgstab": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                    ctypes.c_double, ctypes.c_int, ctypes.c_void_p,
+                                    ctypes.c_void_p, ctypes.POINTER(SolveReport)]),
+    "hmx_bench_matvec": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_int,
+                                        ctypes.c_int64, ctypes.POINTER(ctypes.c_double)]),
+}
+
+_lib = None
+_lock = threading.Lock()
+
+
+def load_library(build: bool = False):
+    """Load libhmx_gpu.so (building it first if asked).  Raises if absent."""
+    global _lib
+    with _lock:
+        if _lib is None:
+            path = _native.GPU_LIB
+            if build or os.environ.get("HMX_BUILD_ON_IMPORT") == "1":
+                path = _native.build_gpu()
+            if not path.exists():
+                raise RuntimeError(
+                    f"{path} is missing: run __graft_entry__.build() (nvcc, sm_100a). "
+                    "There is no CPU fallback for the H-matvec.")
+            lib = ctypes.CDLL(str(path))
+            for name, (res, args) in SIGNATURES.items():
+                fn = getattr(lib, name)
+                fn.restype = res
+                fn.argtypes = args
+            _lib = lib
+    return _lib
+
+
+def last_error() -> str:
+    msg = load_library().hmx_last_error()
+    return msg.decode() if msg else ""
+
+
+def check(rc: int, what: str):
+    if rc == HMX_OK:
+        return
+    msg = f"{what} failed: {last_error()}"
+    if rc == HMX_ERR_SHAPE:
+        raise ValueError(msg)
+    if rc == HMX_ERR_ARG:
+        raise ValueError(msg)
+    raise RuntimeError(msg)
+
+
+def device_count() -> int:
+    lib = load_library()
+    c = ctypes.c_int(0)
+    lib.hmx_device_count(ctypes.byref(c))
+    return c.value
+
+
+def _p(a, t):
+    return a.ctypes.data_as(ctypes.POINTER(t))
+
+
+class Plan:
+    """A device-resident flattened H-matrix for one scheme (owns a C plan)."""
+
+    def __init__(self, packed, table, perm, scheme_label: str, n: int, device: int = 0,
+                 row_range=None, s1_chunk_bytes: int = 0):
+        lib = load_library()
+        code = SCHEME_CODES.get(scheme_label, 6 if scheme_label.startswith("m3") else None)
+        if code is None:
+            raise ValueError(f"unsupported scheme {scheme_label!r}")
+        self._keep = []
+
+        def keep(a, dtype):
+            a = np.ascontiguousarray(a, dtype=dtype)
+            self._keep.append(a)
+            return a
+
+        t = keep(table, np.int64)
+        d = MatrixDesc()
+        d.n = n
+        d.n_blocks = t.shape[0]
+        d.scheme = code
+        d.a32 = int(bool(packed.a32))
+        d.hi32 = int(bool(packed.hi32))
+        d.perm = _p(keep(perm, np.int64), ctypes.c_int64)
+        d.table = _p(t, ctypes.c_int64)
+        d.kind = _p(keep(packed.kind, np.int32), ctypes.c_int32)
+        for name in ("a_off", "hi_off", "khi", "dhi_off", "lo_off", "klo", "dlo_off"):
+            setattr(d, name, _p(keep(getattr(packed, name), np.int64), ctypes.c_int64))
+        b64 = keep(packed.buf64 if packed.buf64.size else np.zeros(1), np.float64)
+        b32 = keep(packed.buf32 if packed.buf32.size else np.zeros(1, np.float32), np.float32)
+        d.buf64 = _p(b64, ctypes.c_double)
+        d.n64 = int(packed.buf64.size)
+        d.buf32 = _p(b32, ctypes.c_float)
+        d.n32 = int(packed.buf32.size)
+        opt = PlanOptions()
+        if row_range is not None:
+            opt.row_begin, opt.row_end = int(row_range[0]), int(row_range[1])
+        opt.s1_chunk_bytes = int(s1_chunk_bytes)
+        h = ctypes.c_void_p()
+        rc = lib.hmx_plan_create(ctypes.byref(d), int(device), ctypes.byref(opt), ctypes.byref(h))
+        self._keep = []  # the plan holds device copies; host arrays may go
+        check(rc, "hmx_plan_create")
+        self.handle = h
+        self.n = n
+        self.scheme = scheme_label
+        self.device = device
+        self._lib = lib
+
+    def info(self) -> dict:
+        i = PlanInfo()
+        check(self._lib.hmx_plan_get_info(self.handle, ctypes.byref(i)), "hmx_plan_get_info")
+        return {f: getattr(i, f) for f, _ in PlanInfo._fields_}
+
+    def matvec(self, x: np.ndarray, permuted: bool = False) -> tuple[np.ndarray, int]:
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        y = np.empty(self.n, dtype=np.float64)
+        rc = self._lib.hmx_matvec(self.handle, x.ctypes.data, y.ctypes.data,
+                                  HMX_PERMUTED if permuted else 0)
+        if rc not in (HMX_OK, HMX_ERR_NONFINITE):
+            check(rc, "hmx_matvec")
+        return y, rc
+
+    def matvec_device(self, x_ptr: int, y_ptr: int, permuted: bool = True) -> int:
+        rc = self._lib.hmx_matvec(self.handle, ctypes.c_void_p(x_ptr), ctypes.c_void_p(y_ptr),
+                                  HMX_DEVICE_PTRS | (HMX_PERMUTED if permuted else 0))
+        if rc not in (HMX_OK, HMX_ERR_NONFINITE):
+            check(rc, "hmx_matvec")
+        return rc
+
+    def nonfinite_block(self) -> int:
+        b = ctypes.c_int64(-1)
+        check(self._lib.hmx_nonfinite_block(self.handle, ctypes.byref(b)), "hmx_nonfinite_block")
+        return b.value
+
+    def bench(self, warmup: int, iters: int, flush_l2: int = 0) -> dict:
+        out = (ctypes.c_double * 4)()
+        check(self._lib.hmx_bench_matvec(self.handle, warmup, iters, flush_l2, out),
+              "hmx_bench_matvec")
+        return {"ms": out[0], "stage1_ms": out[1], "stage2_ms": out[2], "min_ms": out[3]}
+
+    def close(self):
+        if getattr(self, "handle", None):
+            self._lib.hmx_plan_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

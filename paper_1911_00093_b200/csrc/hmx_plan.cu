@@ -1,0 +1,695 @@
+// Flattener + plan lifetime + matvec C ABI.
+//
+// hmx_plan_create turns the packed payloads of one prepared scheme
+// (python PackedScheme; reference SchemeHMatrix, precision.py:209-234) into
+// the two streaming blobs of hmx_internal.cuh and uploads them:
+//   * stage-1 blob: Vt rows of every low-rank block (class), split into
+//     <= 16-rank segments, row-major with 16-byte aligned rows, cut into
+//     warp tasks of ~s1_chunk_bytes and dealt to warps by LPT on bytes;
+//   * stage-2 blob: for every leaf row segment (<= 64 rows), the rows of every
+//     block covering it (dense values or U slab), column-major, FP64 items
+//     and FP32 items in two parts, in partition order.
+// Every stored payload byte appears exactly once on the device.
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <functional>
+#include <numeric>
+#include <queue>
+#include <thread>
+
+#include "hmx_plan_impl.cuh"
+
+namespace hmx {
+
+static thread_local std::string g_last_error;
+
+void set_error(const std::string& msg) { g_last_error = msg; }
+
+int cuda_fail(cudaError_t e, const char* what) {
+  set_error(std::string("CUDA error in ") + what + ": " + cudaGetErrorString(e));
+  return HMX_ERR_CUDA;
+}
+
+static void parallel_for(int64_t count, const std::function<void(int64_t)>& fn) {
+  const int nt = (int)std::max<int64_t>(1, std::min<int64_t>(count, std::thread::hardware_concurrency()));
+  if (nt <= 1) {
+    for (int64_t i = 0; i < count; ++i) fn(i);
+    return;
+  }
+  std::atomic<int64_t> next{0};
+  std::vector<std::thread> pool;
+  for (int t = 0; t < nt; ++t)
+    pool.emplace_back([&]() {
+      for (int64_t i; (i = next.fetch_add(1)) < count;) fn(i);
+    });
+  for (auto& th : pool) th.join();
+}
+
+static inline int64_t round_up(int64_t v, int64_t m) { return (v + m - 1) / m * m; }
+
+struct ItemRef {
+  int32_t block;
+  int8_t cls;  // 0 dense, 1 hi, 2 lo
+};
+
+int enqueue_matvec(hmx_plan* p, const double* xp, const S2Out& out) {
+  HMX_CUDA(launch_stage1(p->dp, xp, p->s1_grid, p->stream));
+  HMX_CUDA(launch_stage2(p->dp, xp, out, p->stream, /*pdl=*/true));
+  return HMX_OK;
+}
+
+}  // namespace hmx
+
+using namespace hmx;
+
+extern "C" {
+
+const char* hmx_last_error(void) { return g_last_error.c_str(); }
+
+int hmx_device_count(int* count) {
+  int c = 0;
+  cudaError_t e = cudaGetDeviceCount(&c);
+  if (e != cudaSuccess) {
+    *count = 0;
+    return cuda_fail(e, "cudaGetDeviceCount");
+  }
+  *count = c;
+  return HMX_OK;
+}
+
+void hmx_plan_destroy(hmx_plan* p) {
+  if (!p) return;
+  {
+    DeviceGuard g(p->device);
+    if (p->stream) cudaStreamSynchronize(p->stream);
+    for (void* a : p->allocs) cudaFree(a);
+    if (p->h_x) cudaFreeHost(p->h_x);
+    if (p->h_y) cudaFreeHost(p->h_y);
+    if (p->h_flag) cudaFreeHost(p->h_flag);
+    for (void* h : p->pinned) cudaFreeHost(h);
+    delete p->ws;
+    for (auto& e : p->ev)
+      if (e) cudaEventDestroy(e);
+    if (p->stream) cudaStreamDestroy(p->stream);
+  }
+  delete p;
+}
+
+int hmx_plan_get_info(const hmx_plan* p, hmx_plan_info* info) {
+  if (!p || !info) return HMX_ERR_ARG;
+  *info = p->info;
+  return HMX_OK;
+}
+
+static int plan_create_impl(const hmx_matrix_desc* d, int device, const hmx_plan_options* opt,
+                            hmx_plan* p) {
+  const int64_t n = d->n, nb = d->n_blocks;
+  if (n < 1 || n > INT32_MAX / 2 || nb < 1 || d->scheme < 0 || d->scheme > HMX_M3) {
+    set_error("invalid matrix descriptor (n, n_blocks or scheme)");
+    return HMX_ERR_ARG;
+  }
+  const int pipe = d->scheme;
+  const bool has_lo = pipe == P_M3;
+  const int64_t rb = opt && opt->row_end > 0 ? opt->row_begin : 0;
+  const int64_t re = opt && opt->row_end > 0 ? opt->row_end : n;
+  if (rb < 0 || re > n || rb >= re) {
+    set_error("invalid row range");
+    return HMX_ERR_ARG;
+  }
+  const int64_t s1_target = opt && opt->s1_chunk_bytes > 0 ? opt->s1_chunk_bytes : 24 * 1024;
+  const size_t a_es = d->a32 ? 4 : 8, hi_es = d->hi32 ? 4 : 8;
+
+  // ---- validate blocks and collect the ones touching rows [rb, re)
+  std::vector<int32_t> blocks;
+  blocks.reserve((size_t)nb);
+  int64_t payload = 0;
+  for (int64_t k = 0; k < nb; ++k) {
+    const int64_t* t = d->table + 5 * k;
+    const int64_t m = t[1] - t[0], nc = t[3] - t[2];
+    if (t[0] < 0 || t[1] > n || t[2] < 0 || t[3] > n || m < 1 || nc < 1) {
+      set_error("block " + std::to_string(k) + " has an invalid range");
+      return HMX_ERR_ARG;
+    }
+    if (d->kind[k] == 0) {
+      if (d->a_off[k] < 0 || d->a_off[k] + m * nc > (d->a32 ? d->n32 : d->n64)) {
+        set_error("dense block " + std::to_string(k) + " exceeds its payload buffer");
+        return HMX_ERR_ARG;
+      }
+      payload += m * nc * (int64_t)a_es;
+    } else {
+      const int64_t kh = d->khi[k], kl = has_lo ? d->klo[k] : 0;
+      if (kh < 0 || kl < 0 || d->hi_off[k] + kh * (m + nc) > (d->hi32 ? d->n32 : d->n64) ||
+          (kl && d->lo_off[k] + kl * (m + nc) > d->n32)) {
+        set_error("low-rank block " + std::to_string(k) + " exceeds its payload buffer");
+        return HMX_ERR_ARG;
+      }
+      if (pipe >= P_M2D && (d->dhi_off[k] < 0 || d->dhi_off[k] + kh > d->n64)) {
+        set_error("low-rank block " + std::to_string(k) + " lacks its scale diagonal");
+        return HMX_ERR_ARG;
+      }
+      payload += kh * (m + nc) * (int64_t)hi_es + kl * (m + nc) * 4;
+      if (pipe >= P_M2D) payload += (kh + kl) * 8;
+    }
+    if (t[1] > rb && t[0] < re) blocks.push_back((int32_t)k);
+  }
+
+  // ---- stage-2 row segments: every block row boundary, chunks of <= 64 rows
+  std::vector<int64_t> bounds = {rb, re};
+  for (int32_t k : blocks) {
+    const int64_t* t = d->table + 5 * k;
+    if (t[0] > rb) bounds.push_back(t[0]);
+    if (t[1] < re) bounds.push_back(t[1]);
+  }
+  std::sort(bounds.begin(), bounds.end());
+  bounds.erase(std::unique(bounds.begin(), bounds.end()), bounds.end());
+  std::vector<int64_t> seg_start;
+  for (size_t i = 0; i + 1 < bounds.size(); ++i) {
+    const int64_t a = bounds[i], b = bounds[i + 1];
+    const int64_t pieces = (b - a + kS2Rows - 1) / kS2Rows;
+    for (int64_t q = 0; q < pieces; ++q) seg_start.push_back(a + (b - a) * q / pieces);
+  }
+  const int64_t nseg = (int64_t)seg_start.size();
+  seg_start.push_back(re);
+
+  // ---- z layout: per low-rank block, FP64 class then FP32 class
+  std::vector<int64_t> zoff_hi((size_t)nb, -1), zoff_lo((size_t)nb, -1);
+  int64_t Z = 0;
+  for (int32_t k : blocks)
+    if (d->kind[k] == 1) {
+      zoff_hi[(size_t)k] = Z;
+      Z += d->khi[k];
+      zoff_lo[(size_t)k] = Z;
+      Z += has_lo ? d->klo[k] : 0;
+    }
+  if (Z > INT32_MAX) {
+    set_error("rank sum exceeds the 32-bit index range");
+    return HMX_ERR_ARG;
+  }
+
+  // ---- stage-2 items per segment, in partition order
+  std::vector<std::vector<ItemRef>> items64((size_t)nseg), items32((size_t)nseg);
+  for (int32_t k : blocks) {
+    const int64_t* t = d->table + 5 * k;
+    const int64_t lo = std::max(t[0], rb), hi = std::min(t[1], re);
+    int64_t s = std::upper_bound(seg_start.begin(), seg_start.begin() + nseg, lo) - seg_start.begin() - 1;
+    for (; s < nseg && seg_start[(size_t)s] < hi; ++s) {
+      if (d->kind[k] == 0) {
+        (d->a32 ? items32 : items64)[(size_t)s].push_back({k, 0});
+      } else {
+        if (d->khi[k] > 0) (d->hi32 ? items32 : items64)[(size_t)s].push_back({k, 1});
+        if (has_lo && d->klo[k] > 0) items32[(size_t)s].push_back({k, 2});
+      }
+    }
+  }
+  auto item_width = [&](const ItemRef& it) -> int64_t {
+    const int64_t* t = d->table + 5 * it.block;
+    return it.cls == 0 ? t[3] - t[2] : it.cls == 1 ? d->khi[it.block] : d->klo[it.block];
+  };
+  const bool dense_single = pipe == P_M1S || pipe == P_M2S;  // A32 . x32 in FP32
+  const bool u_acc32 = pipe == P_M1S || pipe == P_M1M;       // U32 . z32 in FP32
+  std::vector<S2Seg> segs((size_t)nseg);
+  std::vector<Run> runs;
+  std::vector<int32_t> run_block;
+  int64_t off64 = 0, off32 = 0;
+  bool any_acc32 = false, any_acc64_in32 = false;
+  for (int64_t s = 0; s < nseg; ++s) {
+    S2Seg& sg = segs[(size_t)s];
+    sg.row0 = (int32_t)seg_start[(size_t)s];
+    sg.R = (int32_t)(seg_start[(size_t)s + 1] - seg_start[(size_t)s]);
+    sg.run0 = (int32_t)runs.size();
+    for (int part = 0; part < 2; ++part) {
+      const auto& lst = part == 0 ? items64[(size_t)s] : items32[(size_t)s];
+      int64_t col = 0;
+      for (const ItemRef& it : lst) {
+        const int64_t* t = d->table + 5 * it.block;
+        Run r{};
+        r.width = (int32_t)item_width(it);
+        r.col0 = (int32_t)col;
+        if (it.cls == 0) {
+          r.src = (int32_t)t[2];
+          r.flags = (part == 1 && dense_single) ? (RUN_ROUND | RUN_ACC32) : 0;
+        } else {
+          r.src = (int32_t)(it.cls == 1 ? zoff_hi[(size_t)it.block] : zoff_lo[(size_t)it.block]);
+          r.flags = RUN_Z | ((part == 1 && it.cls == 1 && u_acc32) ? RUN_ACC32 : 0);
+        }
+        if (part == 1) {
+          if (r.flags & RUN_ACC32) any_acc32 = true;
+          else any_acc64_in32 = true;
+        }
+        runs.push_back(r);
+        run_block.push_back(it.block);
+        col += r.width;
+      }
+      if (part == 0) {
+        sg.W64 = (int32_t)col;
+        sg.nrun64 = (int32_t)lst.size();
+      } else {
+        sg.W32 = (int32_t)col;
+        sg.nrun32 = (int32_t)lst.size();
+      }
+    }
+    sg.off64 = off64;
+    sg.off32 = off32;
+    off64 += (int64_t)sg.W64 * round_up(sg.R, 2);
+    off32 += (int64_t)sg.W32 * round_up(sg.R, 4);
+  }
+  const int f32mode = !any_acc32 ? F32_ALL64 : (any_acc64_in32 ? F32_MIXED : F32_ALL32);
+
+  // ---- stage-1 segments and tasks
+  std::vector<S1Seg> s1segs;
+  std::vector<S1Task> tasks;
+  std::vector<int64_t> task_bytes;
+  struct S1Src {
+    int32_t block;
+    int8_t cls;
+    int32_t k0, R;
+    int64_t vt_off;
+    int32_t ld;
+  };
+  std::vector<S1Src> s1src;
+  int64_t vt64_len = 0, vt32_len = 0, part_len = 0;
+  std::vector<double> zscale(pipe >= P_M2D ? (size_t)std::max<int64_t>(Z, 1) : 1, 1.0);
+  for (int32_t k : blocks) {
+    if (d->kind[k] != 1) continue;
+    const int64_t* t = d->table + 5 * k;
+    const int64_t ncol = t[3] - t[2];
+    for (int cls = 1; cls <= 2; ++cls) {
+      const int64_t kk = cls == 1 ? d->khi[k] : (has_lo ? d->klo[k] : 0);
+      if (kk <= 0) continue;
+      const bool is32 = cls == 2 || d->hi32;
+      const int64_t es = is32 ? 4 : 8, V = is32 ? 4 : 2;
+      const int64_t ld = round_up(ncol, V);
+      const int64_t nsub = (kk + kS1RMax - 1) / kS1RMax;
+      const int64_t zbase = cls == 1 ? zoff_hi[(size_t)k] : zoff_lo[(size_t)k];
+      if (pipe >= P_M2D) {
+        const double* dsrc = d->buf64 + (cls == 1 ? d->dhi_off[k] : d->dlo_off[k]);
+        for (int64_t q = 0; q < kk; ++q) zscale[(size_t)(zbase + q)] = dsrc[q];
+      }
+      for (int64_t sidx = 0; sidx < nsub; ++sidx) {
+        const int64_t k0 = kk * sidx / nsub, k1 = kk * (sidx + 1) / nsub, R = k1 - k0;
+        int64_t& vlen = is32 ? vt32_len : vt64_len;
+        const int64_t vt_off = vlen;
+        vlen += R * ld;
+        const int64_t lanes_cols = 32 * V;
+        int64_t C = (s1_target / (R * es)) / lanes_cols * lanes_cols;
+        C = std::max(C, lanes_cols);
+        const int64_t nch = (ncol + C - 1) / C;
+        if (nch > 32767) {
+          set_error("block too wide for the stage-1 chunk index");
+          return HMX_ERR_ARG;
+        }
+        S1Seg sg{};
+        sg.zoff = (int32_t)(zbase + k0);
+        sg.R = (int32_t)R;
+        sg.nchunks = (int32_t)nch;
+        sg.part_off = -1;
+        if (nch > 1) {
+          sg.part_off = (int32_t)part_len;
+          part_len += nch * R;
+        }
+        const int32_t sid = (int32_t)s1segs.size();
+        s1segs.push_back(sg);
+        s1src.push_back({k, (int8_t)cls, (int32_t)k0, (int32_t)R, vt_off, (int32_t)ld});
+        for (int64_t ch = 0; ch < nch; ++ch) {
+          S1Task tk{};
+          tk.vt_off = vt_off + ch * C;
+          tk.ld = (int32_t)ld;
+          tk.ncols = (int32_t)std::min(C, ncol - ch * C);
+          tk.xoff = (int32_t)(t[2] + ch * C);
+          tk.seg = sid;
+          tk.chunk = (int16_t)ch;
+          tk.R = (int8_t)R;
+          tk.is32 = is32 ? 1 : 0;
+          tasks.push_back(tk);
+          task_bytes.push_back(R * tk.ncols * es);
+        }
+      }
+    }
+  }
+  if (part_len > INT32_MAX) {
+    set_error("too many stage-1 partials");
+    return HMX_ERR_ARG;
+  }
+
+  // ---- device properties, stage-1 grid, LPT task assignment
+  cudaDeviceProp prop{};
+  HMX_CUDA(cudaGetDeviceProperties(&prop, device));
+  const int occ = stage1_occupancy(pipe);
+  p->s1_grid = prop.multiProcessorCount * occ;
+  const int64_t n_warps_total = (int64_t)p->s1_grid * (kS1Threads / 32);
+  const int64_t ntask = (int64_t)tasks.size();
+  std::vector<int32_t> warp_of((size_t)ntask);
+  {
+    std::vector<int64_t> order((size_t)ntask);
+    std::iota(order.begin(), order.end(), 0);
+    std::stable_sort(order.begin(), order.end(),
+                     [&](int64_t a, int64_t b) { return task_bytes[(size_t)a] > task_bytes[(size_t)b]; });
+    using Load = std::pair<int64_t, int32_t>;
+    std::priority_queue<Load, std::vector<Load>, std::greater<Load>> heap;
+    for (int32_t w = 0; w < (int32_t)n_warps_total; ++w) heap.push({0, w});
+    for (int64_t i : order) {
+      Load l = heap.top();
+      heap.pop();
+      warp_of[(size_t)i] = l.second;
+      l.first += task_bytes[(size_t)i] + 256;  // +256: per-task fixed cost
+      heap.push(l);
+    }
+  }
+  std::vector<int32_t> warp_ptr((size_t)n_warps_total + 1, 0);
+  for (int64_t i = 0; i < ntask; ++i) warp_ptr[(size_t)warp_of[(size_t)i] + 1]++;
+  for (int64_t w = 0; w < n_warps_total; ++w) warp_ptr[(size_t)w + 1] += warp_ptr[(size_t)w];
+  std::vector<S1Task> tasks_sorted((size_t)ntask);
+  {
+    std::vector<int32_t> fill(warp_ptr.begin(), warp_ptr.end() - 1);
+    // keep the LPT order (big tasks first) inside each warp
+    std::vector<int64_t> order((size_t)ntask);
+    std::iota(order.begin(), order.end(), 0);
+    std::stable_sort(order.begin(), order.end(),
+                     [&](int64_t a, int64_t b) { return task_bytes[(size_t)a] > task_bytes[(size_t)b]; });
+    for (int64_t i : order) tasks_sorted[(size_t)fill[(size_t)warp_of[(size_t)i]]++] = tasks[(size_t)i];
+  }
+
+  // ---- pack the blobs (host, parallel) and upload
+  std::vector<double> blob64((size_t)std::max<int64_t>(off64, 1), 0.0);
+  std::vector<float> blob32((size_t)std::max<int64_t>(off32, 1), 0.f);
+  parallel_for(nseg, [&](int64_t s) {
+    const S2Seg& sg = segs[(size_t)s];
+    for (int part = 0; part < 2; ++part) {
+      const auto& lst = part == 0 ? items64[(size_t)s] : items32[(size_t)s];
+      const int64_t rp = part == 0 ? round_up(sg.R, 2) : round_up(sg.R, 4);
+      int64_t col = 0;
+      for (const ItemRef& it : lst) {
+        const int64_t* t = d->table + 5 * it.block;
+        const int64_t m = t[1] - t[0], nc = t[3] - t[2];
+        const int64_t r0 = sg.row0 - t[0];
+        const int64_t w = item_width(it);
+        // source row-major matrix (m x w) and its element type
+        int64_t src_off;
+        bool src32;
+        if (it.cls == 0) {
+          src_off = d->a_off[it.block];
+          src32 = d->a32;
+        } else if (it.cls == 1) {
+          src_off = d->hi_off[it.block];
+          src32 = d->hi32;
+        } else {
+          src_off = d->lo_off[it.block];
+          src32 = true;
+        }
+        (void)nc;
+        (void)m;
+        for (int64_t c = 0; c < w; ++c) {
+          const int64_t dst = (col + c) * rp;
+          for (int64_t i = 0; i < sg.R; ++i) {
+            const int64_t e = src_off + (r0 + i) * w + c;
+            if (part == 0) blob64[(size_t)(sg.off64 + dst + i)] = src32 ? d->buf32[e] : d->buf64[e];
+            else blob32[(size_t)(sg.off32 + dst + i)] = src32 ? d->buf32[e] : (float)d->buf64[e];
+          }
+        }
+        col += w;
+      }
+    }
+  });
+  std::vector<double> vt64((size_t)std::max<int64_t>(vt64_len, 1), 0.0);
+  std::vector<float> vt32((size_t)std::max<int64_t>(vt32_len, 1), 0.f);
+  parallel_for((int64_t)s1src.size(), [&](int64_t i) {
+    const S1Src& s = s1src[(size_t)i];
+    const int64_t* t = d->table + 5 * s.block;
+    const int64_t m = t[1] - t[0], nc = t[3] - t[2];
+    const int64_t kk = s.cls == 1 ? d->khi[s.block] : d->klo[s.block];
+    const int64_t base = (s.cls == 1 ? d->hi_off[s.block] : d->lo_off[s.block]) + m * kk;
+    const bool src32 = s.cls == 2 || d->hi32;
+    for (int64_t q = 0; q < s.R; ++q)
+      for (int64_t j = 0; j < nc; ++j) {
+        const int64_t e = base + (s.k0 + q) * nc + j;
+        if (src32) vt32[(size_t)(s.vt_off + q * s.ld + j)] = d->buf32[e];
+        else vt64[(size_t)(s.vt_off + q * s.ld + j)] = d->buf64[e];
+      }
+  });
+  std::vector<int32_t> perm32((size_t)n);
+  for (int64_t i = 0; i < n; ++i) {
+    if (d->perm[i] < 0 || d->perm[i] >= n) {
+      set_error("permutation entry out of range");
+      return HMX_ERR_ARG;
+    }
+    perm32[(size_t)i] = (int32_t)d->perm[i];
+  }
+
+  DevPlan& dp = p->dp;
+  dp.n = (int32_t)n;
+  dp.row_begin = (int32_t)rb;
+  dp.row_end = (int32_t)re;
+  dp.pipe = pipe;
+  auto up = [&](auto* dst, const auto& vec) -> int {
+    using T = typename std::decay<decltype(vec[0])>::type;
+    if (!dst) {
+      set_error("cudaMalloc failed while uploading the plan (out of device memory?)");
+      return HMX_ERR_CUDA;
+    }
+    if (!vec.empty()) HMX_CUDA(cudaMemcpy(dst, vec.data(), vec.size() * sizeof(T), cudaMemcpyHostToDevice));
+    return HMX_OK;
+  };
+  int rc;
+  S1Task* d_tasks = p->alloc<S1Task>(tasks_sorted.size());
+  if ((rc = up(d_tasks, tasks_sorted))) return rc;
+  int32_t* d_wptr = p->alloc<int32_t>(warp_ptr.size());
+  if ((rc = up(d_wptr, warp_ptr))) return rc;
+  S1Seg* d_s1 = p->alloc<S1Seg>(s1segs.size());
+  if ((rc = up(d_s1, s1segs))) return rc;
+  double* d_vt64 = p->alloc<double>(vt64.size());
+  if ((rc = up(d_vt64, vt64))) return rc;
+  float* d_vt32 = p->alloc<float>(vt32.size());
+  if ((rc = up(d_vt32, vt32))) return rc;
+  double* d_zs = p->alloc<double>(zscale.size());
+  if ((rc = up(d_zs, zscale))) return rc;
+  double* d_z = p->alloc<double>((size_t)std::max<int64_t>(Z, 1));
+  double* d_part = p->alloc<double>((size_t)std::max<int64_t>(part_len, 1));
+  uint32_t* d_cnt = p->alloc<uint32_t>(std::max<size_t>(s1segs.size(), 1));
+  S2Seg* d_s2 = p->alloc<S2Seg>(segs.size());
+  if ((rc = up(d_s2, segs))) return rc;
+  Run* d_runs = p->alloc<Run>(runs.size());
+  if ((rc = up(d_runs, runs))) return rc;
+  int32_t* d_rb = p->alloc<int32_t>(run_block.size());
+  if ((rc = up(d_rb, run_block))) return rc;
+  double* d_b64 = p->alloc<double>(blob64.size());
+  if ((rc = up(d_b64, blob64))) return rc;
+  float* d_b32 = p->alloc<float>(blob32.size());
+  if ((rc = up(d_b32, blob32))) return rc;
+  int32_t* d_perm = p->alloc<int32_t>(perm32.size());
+  if ((rc = up(d_perm, perm32))) return rc;
+  if (!d_z || !d_part || !d_cnt) {
+    set_error("cudaMalloc failed (out of device memory?)");
+    return HMX_ERR_CUDA;
+  }
+  HMX_CUDA(cudaMemset(d_cnt, 0, std::max<size_t>(s1segs.size(), 1) * sizeof(uint32_t)));
+
+  dp.tasks = d_tasks;
+  dp.warp_ptr = d_wptr;
+  dp.s1segs = d_s1;
+  dp.vt64 = d_vt64;
+  dp.vt32 = d_vt32;
+  dp.zscale = d_zs;
+  dp.z = d_z;
+  dp.part = d_part;
+  dp.seg_count = d_cnt;
+  dp.n_warps = ntask > 0 ? (int32_t)n_warps_total : 0;
+  dp.s2segs = d_s2;
+  dp.runs = d_runs;
+  dp.blob64 = d_b64;
+  dp.blob32 = d_b32;
+  dp.n_s2 = (int32_t)nseg;
+  dp.f32mode = f32mode;
+  dp.perm = d_perm;
+  dp.run_block = d_rb;
+
+  // per-matvec buffers
+  p->d_xin = p->alloc<double>((size_t)n);
+  p->d_xp = p->alloc<double>((size_t)n);
+  p->d_y = p->alloc<double>((size_t)n);
+  p->d_nonfinite = p->alloc<int>(1);
+  p->d_seg_dots = p->alloc<double>((size_t)(2 * nseg));
+  p->d_done = p->alloc<uint32_t>(1);
+  p->d_dots = p->alloc<double>(2);
+  p->d_first_bad = p->alloc<unsigned long long>(1);
+  if (!p->d_xin || !p->d_xp || !p->d_y || !p->d_nonfinite || !p->d_seg_dots || !p->d_done ||
+      !p->d_dots || !p->d_first_bad) {
+    set_error("cudaMalloc failed (out of device memory?)");
+    return HMX_ERR_CUDA;
+  }
+  HMX_CUDA(cudaMemset(p->d_done, 0, sizeof(uint32_t)));
+  HMX_CUDA(cudaMallocHost(&p->h_x, (size_t)n * sizeof(double)));
+  HMX_CUDA(cudaMallocHost(&p->h_y, (size_t)n * sizeof(double)));
+  HMX_CUDA(cudaMallocHost(&p->h_flag, 4 * sizeof(int)));
+  for (auto& e : p->ev) HMX_CUDA(cudaEventCreate(&e));
+
+  hmx_plan_info& info = p->info;
+  info.n = n;
+  info.payload_bytes = payload;
+  int64_t dev_bytes = 0;
+  dev_bytes += (int64_t)(blob64.size() * 8 + blob32.size() * 4 + vt64.size() * 8 + vt32.size() * 4);
+  dev_bytes += (int64_t)(tasks_sorted.size() * sizeof(S1Task) + segs.size() * sizeof(S2Seg) +
+                         runs.size() * (sizeof(Run) + 4) + s1segs.size() * (sizeof(S1Seg) + 4));
+  dev_bytes += (Z * 2 + part_len + 3 * n) * 8 + n * 4;
+  info.device_bytes = dev_bytes;
+  info.s1_segments = (int64_t)s1segs.size();
+  info.s1_tasks = ntask;
+  info.s2_segments = nseg;
+  info.s2_runs = (int64_t)runs.size();
+  info.z_len = Z;
+  int64_t st1 = 0;
+  for (int64_t b : task_bytes) st1 += b;
+  info.stage1_bytes = st1;
+  info.stage2_bytes = off64 * 8 + off32 * 4;
+  info.s1_grid = p->s1_grid;
+  info.s1_block = kS1Threads;
+  info.s2_grid = (int32_t)nseg;
+  info.s2_block = kS2Threads;
+  return HMX_OK;
+}
+
+int hmx_plan_create(const hmx_matrix_desc* d, int device, const hmx_plan_options* opt,
+                    hmx_plan** out) {
+  if (!d || !out) {
+    set_error("null argument");
+    return HMX_ERR_ARG;
+  }
+  *out = nullptr;
+  int count = 0;
+  if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0) {
+    set_error("no CUDA device is available");
+    return HMX_ERR_CUDA;
+  }
+  if (device < 0 || device >= count) {
+    set_error("device index out of range");
+    return HMX_ERR_ARG;
+  }
+  DeviceGuard guard(device);
+  auto* p = new hmx_plan();
+  p->device = device;
+  p->n = d->n;
+  p->scheme = d->scheme;
+  cudaError_t e = cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking);
+  if (e != cudaSuccess) {
+    delete p;
+    return cuda_fail(e, "cudaStreamCreate");
+  }
+  const int rc = plan_create_impl(d, device, opt, p);
+  if (rc != HMX_OK) {
+    hmx_plan_destroy(p);
+    return rc;
+  }
+  *out = p;
+  return HMX_OK;
+}
+
+int hmx_matvec(hmx_plan* p, const double* x, double* y, int flags) {
+  if (!p || !x || !y) {
+    set_error("null argument");
+    return HMX_ERR_ARG;
+  }
+  if (p->dp.row_begin != 0 || p->dp.row_end != p->dp.n) {
+    set_error("hmx_matvec needs a full-matrix plan");
+    return HMX_ERR_ARG;
+  }
+  std::lock_guard<std::mutex> lock(p->mu);
+  DeviceGuard guard(p->device);
+  const int64_t n = p->n;
+  const bool dev = flags & HMX_DEVICE_PTRS, permuted = flags & HMX_PERMUTED;
+  cudaStream_t st = p->stream;
+  const double* src;
+  if (dev) {
+    src = x;
+  } else {
+    std::memcpy(p->h_x, x, (size_t)n * sizeof(double));
+    HMX_CUDA(cudaMemcpyAsync(p->d_xin, p->h_x, (size_t)n * sizeof(double), cudaMemcpyHostToDevice, st));
+    src = p->d_xin;
+  }
+  const double* xp = src;
+  if (!permuted) {
+    HMX_CUDA(launch_gather_perm(src, p->dp.perm, p->d_xp, (int)n, st));
+    xp = p->d_xp;
+  } else if (!dev) {
+    xp = p->d_xin;
+  }
+  HMX_CUDA(cudaMemsetAsync(p->d_nonfinite, 0, sizeof(int), st));
+  S2Out out{};
+  out.y = dev ? y : p->d_y;
+  out.permute_out = permuted ? 0 : 1;
+  out.nonfinite = p->d_nonfinite;
+  int rc = enqueue_matvec(p, xp, out);
+  if (rc) return rc;
+  p->last_xp = xp;
+  HMX_CUDA(cudaMemcpyAsync(p->h_flag, p->d_nonfinite, sizeof(int), cudaMemcpyDeviceToHost, st));
+  if (!dev) HMX_CUDA(cudaMemcpyAsync(p->h_y, p->d_y, (size_t)n * sizeof(double), cudaMemcpyDeviceToHost, st));
+  HMX_CUDA(cudaStreamSynchronize(st));
+  if (!dev) std::memcpy(y, p->h_y, (size_t)n * sizeof(double));
+  if (*p->h_flag) {
+    set_error("non-finite matvec result");
+    return HMX_ERR_NONFINITE;
+  }
+  return HMX_OK;
+}
+
+int hmx_nonfinite_block(hmx_plan* p, int64_t* block) {
+  if (!p || !block) return HMX_ERR_ARG;
+  std::lock_guard<std::mutex> lock(p->mu);
+  DeviceGuard guard(p->device);
+  if (!p->last_xp) {
+    *block = -1;
+    return HMX_OK;
+  }
+  cudaStream_t st = p->stream;
+  HMX_CUDA(cudaMemsetAsync(p->d_first_bad, 0xff, sizeof(unsigned long long), st));
+  HMX_CUDA(launch_probe(p->dp, p->last_xp, p->d_first_bad, st));
+  unsigned long long v = 0;
+  HMX_CUDA(cudaMemcpyAsync(&v, p->d_first_bad, sizeof(v), cudaMemcpyDeviceToHost, st));
+  HMX_CUDA(cudaStreamSynchronize(st));
+  *block = v == ~0ull ? -1 : (int64_t)v;
+  return HMX_OK;
+}
+
+int hmx_bench_matvec(hmx_plan* p, int warmup, int iters, int64_t flush_l2, double* out_ms) {
+  if (!p || iters < 1 || !out_ms) return HMX_ERR_ARG;
+  std::lock_guard<std::mutex> lock(p->mu);
+  DeviceGuard guard(p->device);
+  cudaStream_t st = p->stream;
+  void* flush = nullptr;
+  if (flush_l2 > 0) HMX_CUDA(cudaMalloc(&flush, (size_t)flush_l2));
+  S2Out out{};
+  out.y = p->d_y;
+  out.nonfinite = p->d_nonfinite;
+  const double* xp = p->d_xp;
+  for (int i = 0; i < warmup; ++i) {
+    int rc = enqueue_matvec(p, xp, out);
+    if (rc) return rc;
+  }
+  HMX_CUDA(cudaStreamSynchronize(st));
+  double tot = 0, t1 = 0, t2 = 0, best = 1e30;
+  for (int i = 0; i < iters; ++i) {
+    if (flush) HMX_CUDA(cudaMemsetAsync(flush, i & 0xff, (size_t)flush_l2, st));
+    HMX_CUDA(cudaEventRecord(p->ev[0], st));
+    HMX_CUDA(launch_stage1(p->dp, xp, p->s1_grid, st));
+    HMX_CUDA(cudaEventRecord(p->ev[1], st));
+    HMX_CUDA(launch_stage2(p->dp, xp, out, st, /*pdl=*/false));
+    HMX_CUDA(cudaEventRecord(p->ev[2], st));
+    HMX_CUDA(cudaEventSynchronize(p->ev[2]));
+    float a = 0, b = 0;
+    cudaEventElapsedTime(&a, p->ev[0], p->ev[1]);
+    cudaEventElapsedTime(&b, p->ev[1], p->ev[2]);
+    t1 += a;
+    t2 += b;
+    tot += a + b;
+    best = std::min(best, (double)(a + b));
+  }
+  if (flush) cudaFree(flush);
+  out_ms[0] = tot / iters;
+  out_ms[1] = t1 / iters;
+  out_ms[2] = t2 / iters;
+  out_ms[3] = best;
+  return HMX_OK;
+}
+
+}  // extern "C"

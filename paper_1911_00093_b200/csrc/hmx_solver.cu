@@ -1,0 +1,520 @@
+// BiCG-STAB on the device (reference pkg/src/hmx/solver.py:68-168).
+//
+// Control flow and scalar arithmetic are the reference's: the scalars alpha,
+// omega, beta are formed on the device with the same IEEE operations, the
+// breakdown / convergence decisions are taken on the host from the same
+// values, and vector updates keep the reference's operation order (no FMA
+// contraction in the axpy's: x = (x + alpha p) + omega s etc.).  Dots and
+// norms are deterministic two-level reductions (fixed grid, fixed order).
+//
+// Per iteration: p-update, v = A p (fused r^.v), s-update (fused |s|^2)
+//   -> host sync #1 (denominator breakdown, early exit on |s|)
+//   t = A s (fused t.s, t.t), x/r-update (fused |r|^2, r^.r)
+//   -> host sync #2 (stabilisation breakdown, convergence, omega breakdown).
+#include <cmath>
+#include <mutex>
+
+#include "hmx_plan_impl.cuh"
+
+namespace hmx {
+
+constexpr int kVecThreads = 512;
+constexpr double kBreakdownEps = 1e-300;  // solver.py:27
+
+// scalar slots
+enum : int {
+  SC_BB = 0,      // |b|^2
+  SC_RHO0 = 1,    // rho ring buffer slot 0
+  SC_RHO1 = 2,    // rho ring buffer slot 1
+  SC_ALPHA = 3,
+  SC_OMEGA = 4,
+  SC_SS = 5,      // |s|^2
+  SC_RR = 6,      // |r|^2
+  SC_RES = 7,     // |b - A x|^2
+  SC_DV = 8,      // [r^.v, unused]
+  SC_DT = 10,     // [t.s, t.t]
+  SC_TMP = 12,    // [2 scratch]
+  SC_N = 16
+};
+
+struct VecRed {
+  double* partials;  // 2 per CTA
+  uint32_t* done;
+  double* out;       // 2 results
+};
+
+// Deterministic two-level sum of (u, w) over the grid: per-CTA fixed-order
+// block reduction, then the last CTA to finish sums the CTA partials in order.
+__device__ __forceinline__ void grid_reduce2(double u, double w, const VecRed& R) {
+  __shared__ double su[kVecThreads / 32], sw[kVecThreads / 32];
+  __shared__ unsigned ticket;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+  for (int s = 16; s > 0; s >>= 1) {
+    u += __shfl_xor_sync(0xffffffffu, u, s);
+    w += __shfl_xor_sync(0xffffffffu, w, s);
+  }
+  if (lane == 0) {
+    su[wid] = u;
+    sw[wid] = w;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double a = 0.0, b = 0.0;
+    for (int i = 0; i < kVecThreads / 32; ++i) {
+      a += su[i];
+      b += sw[i];
+    }
+    R.partials[2 * blockIdx.x] = a;
+    R.partials[2 * blockIdx.x + 1] = b;
+    __threadfence();
+    ticket = atomicAdd(R.done, 1u);
+  }
+  __syncthreads();
+  if (ticket != gridDim.x - 1) return;
+  __threadfence();
+  double a = 0.0, b = 0.0;
+  for (int i = threadIdx.x; i < (int)gridDim.x; i += kVecThreads) {
+    a += __ldcg(R.partials + 2 * i);
+    b += __ldcg(R.partials + 2 * i + 1);
+  }
+#pragma unroll
+  for (int s = 16; s > 0; s >>= 1) {
+    a += __shfl_xor_sync(0xffffffffu, a, s);
+    b += __shfl_xor_sync(0xffffffffu, b, s);
+  }
+  __syncthreads();
+  if (lane == 0) {
+    su[wid] = a;
+    sw[wid] = b;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double fa = 0.0, fb = 0.0;
+    for (int i = 0; i < kVecThreads / 32; ++i) {
+      fa += su[i];
+      fb += sw[i];
+    }
+    R.out[0] = fa;
+    R.out[1] = fb;
+    *R.done = 0u;
+  }
+}
+
+// (|u|^2, u.w) style reductions: out = [sum a*b, sum c*d]
+__global__ void __launch_bounds__(kVecThreads) dot2_kernel(const double* a, const double* b,
+                                                            const double* c, const double* dd,
+                                                            int n, VecRed R) {
+  double u = 0.0, w = 0.0;
+  for (int i = blockIdx.x * kVecThreads + threadIdx.x; i < n; i += gridDim.x * kVecThreads) {
+    u += a[i] * b[i];
+    if (c) w += c[i] * dd[i];
+  }
+  grid_reduce2(u, w, R);
+}
+
+// r = b - t ; r_hat = r ; x = 0 ; out = [|r|^2, unused]   (solver.py:99-102)
+__global__ void __launch_bounds__(kVecThreads) init_kernel(const double* b, const double* t,
+                                                            double* r, double* rhat, double* x,
+                                                            int n, VecRed R) {
+  double u = 0.0;
+  for (int i = blockIdx.x * kVecThreads + threadIdx.x; i < n; i += gridDim.x * kVecThreads) {
+    const double ri = __dsub_rn(b[i], t[i]);
+    r[i] = ri;
+    rhat[i] = ri;
+    x[i] = 0.0;
+    u += ri * ri;
+  }
+  grid_reduce2(u, 0.0, R);
+}
+
+// p = r (first iteration) or p = r + beta (p - omega v),
+// beta = (rho / rho_prev) (alpha / omega)              (solver.py:116-120)
+__global__ void __launch_bounds__(kVecThreads) p_update_kernel(const double* r, const double* v,
+                                                                double* p, int n, int first,
+                                                                const double* sc, int rho_slot,
+                                                                int prev_slot) {
+  double beta = 0.0, omega = 0.0;
+  if (!first) {
+    const double rho = sc[rho_slot], rho_prev = sc[prev_slot];
+    const double alpha = sc[SC_ALPHA];
+    omega = sc[SC_OMEGA];
+    beta = __dmul_rn(__ddiv_rn(rho, rho_prev), __ddiv_rn(alpha, omega));
+  }
+  for (int i = blockIdx.x * kVecThreads + threadIdx.x; i < n; i += gridDim.x * kVecThreads) {
+    if (first) p[i] = r[i];
+    else p[i] = __dadd_rn(r[i], __dmul_rn(beta, __dsub_rn(p[i], __dmul_rn(omega, v[i]))));
+  }
+}
+
+// alpha = rho / (r^.v) ; s = r - alpha v ; out = [|s|^2]   (solver.py:126-129)
+__global__ void __launch_bounds__(kVecThreads) s_update_kernel(const double* r, const double* v,
+                                                                double* s, int n, double* sc,
+                                                                int rho_slot, VecRed R) {
+  const double alpha = __ddiv_rn(sc[rho_slot], sc[SC_DV]);
+  if (blockIdx.x == 0 && threadIdx.x == 0) sc[SC_ALPHA] = alpha;
+  double u = 0.0;
+  for (int i = blockIdx.x * kVecThreads + threadIdx.x; i < n; i += gridDim.x * kVecThreads) {
+    const double si = __dsub_rn(r[i], __dmul_rn(alpha, v[i]));
+    s[i] = si;
+    u += si * si;
+  }
+  grid_reduce2(u, 0.0, R);
+}
+
+// x = x + alpha p (early exit on |s|, solver.py:131)
+__global__ void __launch_bounds__(kVecThreads) x_alpha_p_kernel(double* x, const double* p, int n,
+                                                                 const double* sc) {
+  const double alpha = sc[SC_ALPHA];
+  for (int i = blockIdx.x * kVecThreads + threadIdx.x; i < n; i += gridDim.x * kVecThreads)
+    x[i] = __dadd_rn(x[i], __dmul_rn(alpha, p[i]));
+}
+
+// omega = (t.s)/(t.t); x = x + alpha p + omega s; r = s - omega t;
+// out = [|r|^2, r^.r] (solver.py:139-147).  No-op when t.t == 0 (breakdown).
+__global__ void __launch_bounds__(kVecThreads) xr_update_kernel(double* x, double* r,
+                                                                 const double* p, const double* s,
+                                                                 const double* t,
+                                                                 const double* rhat, int n,
+                                                                 double* sc, VecRed R) {
+  const double tt = sc[SC_DT + 1];
+  if (tt == 0.0) {
+    grid_reduce2(0.0, 0.0, R);
+    return;
+  }
+  const double omega = __ddiv_rn(sc[SC_DT], tt);
+  const double alpha = sc[SC_ALPHA];
+  if (blockIdx.x == 0 && threadIdx.x == 0) sc[SC_OMEGA] = omega;
+  double u = 0.0, w = 0.0;
+  for (int i = blockIdx.x * kVecThreads + threadIdx.x; i < n; i += gridDim.x * kVecThreads) {
+    const double xi = __dadd_rn(__dadd_rn(x[i], __dmul_rn(alpha, p[i])), __dmul_rn(omega, s[i]));
+    const double ri = __dsub_rn(s[i], __dmul_rn(omega, t[i]));
+    x[i] = xi;
+    r[i] = ri;
+    u += ri * ri;
+    w += rhat[i] * ri;
+  }
+  grid_reduce2(u, w, R);
+}
+
+// out = [|b - y|^2, |b|^2]   (solver.py:60-62)
+__global__ void __launch_bounds__(kVecThreads) resid_kernel(const double* b, const double* y, int n,
+                                                             VecRed R) {
+  double u = 0.0, w = 0.0;
+  for (int i = blockIdx.x * kVecThreads + threadIdx.x; i < n; i += gridDim.x * kVecThreads) {
+    const double e = __dsub_rn(b[i], y[i]);
+    u += e * e;
+    w += b[i] * b[i];
+  }
+  grid_reduce2(u, w, R);
+}
+
+__global__ void permute_kernel(const double* src, const int32_t* perm, double* dst, int n,
+                               int inverse) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  if (inverse) dst[perm[i]] = src[i];  // permuted -> original
+  else dst[i] = src[perm[i]];          // original -> permuted
+}
+
+}  // namespace hmx
+
+using namespace hmx;
+
+namespace {
+
+struct SolveCtx {
+  hmx_plan* A;
+  hmx_plan* A64;
+  Workspace w;
+  cudaStream_t st;
+  int grid;
+  VecRed red(int slot) const { return VecRed{w.partials, w.done, w.sc + slot}; }
+};
+
+int alloc_ws(hmx_plan* p, Workspace& w, int64_t n, int grid) {
+  w.n = n;
+  w.grid = grid;
+  double** vecs[] = {&w.b, &w.x, &w.r, &w.rhat, &w.p, &w.v, &w.s, &w.t, &w.y, &w.orig};
+  for (double** v : vecs) {
+    *v = p->alloc<double>((size_t)n);
+    if (!*v) {
+      set_error("cudaMalloc failed for the solver workspace");
+      return HMX_ERR_CUDA;
+    }
+  }
+  w.sc = p->alloc<double>(SC_N);
+  w.flags = p->alloc<int>(4);
+  w.partials = p->alloc<double>((size_t)2 * grid);
+  w.done = p->alloc<uint32_t>(1);
+  if (!w.sc || !w.flags || !w.partials || !w.done) {
+    set_error("cudaMalloc failed for the solver workspace");
+    return HMX_ERR_CUDA;
+  }
+  HMX_CUDA(cudaMemset(w.done, 0, sizeof(uint32_t)));
+  HMX_CUDA(cudaMemset(w.sc, 0, SC_N * sizeof(double)));
+  HMX_CUDA(cudaMallocHost(&w.h_sc, (SC_N + 4) * sizeof(double)));
+  p->pinned.push_back(w.h_sc);
+  return HMX_OK;
+}
+
+// y = A xp on stream st, fused dots into sc[slot..slot+1]
+int apply(hmx_plan* A, const Workspace& w, cudaStream_t st, const double* xp, double* y,
+          const double* w1, int yy, int slot, int* flag) {
+  S2Out out{};
+  out.y = y;
+  out.permute_out = 0;
+  out.w1 = w1;
+  out.yy = yy;
+  if (w1 || yy) {
+    out.seg_dots = A->d_seg_dots;
+    out.done = A->d_done;
+    out.dots_out = w.sc + slot;
+  }
+  out.nonfinite = flag;
+  HMX_CUDA(launch_stage1(A->dp, xp, A->s1_grid, st));
+  HMX_CUDA(launch_stage2(A->dp, xp, out, st, /*pdl=*/true));
+  A->last_xp = xp;
+  return HMX_OK;
+}
+
+int sync_scalars(const SolveCtx& c) {
+  HMX_CUDA(cudaMemcpyAsync(c.w.h_sc, c.w.sc, SC_N * sizeof(double), cudaMemcpyDeviceToHost, c.st));
+  HMX_CUDA(cudaMemcpyAsync(c.w.h_sc + SC_N, c.w.flags, 4 * sizeof(int), cudaMemcpyDeviceToHost, c.st));
+  HMX_CUDA(cudaStreamSynchronize(c.st));
+  return HMX_OK;
+}
+
+int flags_nonfinite(const SolveCtx& c) {
+  const int* f = reinterpret_cast<const int*>(c.w.h_sc + SC_N);
+  return f[0] | f[1] | f[2];
+}
+
+// |b - A64 x| / |b| with x, b device, permuted; result on the host
+int true_residual_dev(SolveCtx& c, double* out) {
+  int rc = apply(c.A64, c.w, c.st, c.w.x, c.w.y, nullptr, 0, 0, c.w.flags + 2);
+  if (rc) return rc;
+  resid_kernel<<<c.grid, kVecThreads, 0, c.st>>>(c.w.b, c.w.y, (int)c.w.n, c.red(SC_RES));
+  HMX_CUDA(cudaGetLastError());
+  if ((rc = sync_scalars(c))) return rc;
+  if (flags_nonfinite(c)) {
+    set_error("non-finite matvec result");
+    return HMX_ERR_NONFINITE;
+  }
+  const double nr = std::sqrt(c.w.h_sc[SC_RES]), nb = std::sqrt(c.w.h_sc[SC_RES + 1]);
+  if (nb == 0.0) *out = nr == 0.0 ? 0.0 : INFINITY;
+  else *out = nr / nb;
+  return HMX_OK;
+}
+
+int workspace_for(hmx_plan* p, Workspace& out, int grid) {
+  if (!p->ws) {
+    auto* w = new Workspace();
+    int rc = alloc_ws(p, *w, p->n, grid);
+    if (rc) {
+      delete w;
+      return rc;
+    }
+    p->ws = w;
+  }
+  out = *p->ws;
+  return HMX_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int hmx_true_residual(hmx_plan* p64, const double* x, const double* b, double* out) {
+  if (!p64 || !x || !b || !out) {
+    set_error("null argument");
+    return HMX_ERR_ARG;
+  }
+  std::lock_guard<std::mutex> lock(p64->mu);
+  DeviceGuard guard(p64->device);
+  cudaDeviceProp prop{};
+  HMX_CUDA(cudaGetDeviceProperties(&prop, p64->device));
+  SolveCtx c{};
+  c.A = c.A64 = p64;
+  c.st = p64->stream;
+  c.grid = 2 * prop.multiProcessorCount;
+  int rc = workspace_for(p64, c.w, c.grid);
+  if (rc) return rc;
+  const int64_t n = p64->n;
+  const int nb = (int)((n + 255) / 256);
+  HMX_CUDA(cudaMemcpyAsync(c.w.orig, x, n * sizeof(double), cudaMemcpyHostToDevice, c.st));
+  permute_kernel<<<nb, 256, 0, c.st>>>(c.w.orig, p64->dp.perm, c.w.x, (int)n, 0);
+  HMX_CUDA(cudaMemcpyAsync(c.w.orig, b, n * sizeof(double), cudaMemcpyHostToDevice, c.st));
+  permute_kernel<<<nb, 256, 0, c.st>>>(c.w.orig, p64->dp.perm, c.w.b, (int)n, 0);
+  HMX_CUDA(cudaMemsetAsync(c.w.flags, 0, 4 * sizeof(int), c.st));
+  return true_residual_dev(c, out);
+}
+
+int hmx_bicgstab(hmx_plan* A, hmx_plan* A64, const double* b, double tol, int max_iter, double* x,
+                 double* history, hmx_solve_report* rep) {
+  if (!A || !b || !x || !history || !rep) {
+    set_error("null argument");
+    return HMX_ERR_ARG;
+  }
+  if (!A64) A64 = A;
+  if (A64->n != A->n || A64->device != A->device) {
+    set_error("plan and FP64 plan differ in size or device");
+    return HMX_ERR_ARG;
+  }
+  if (!(tol > 0.0) || max_iter < 1) {
+    set_error("tol must be positive and max_iter >= 1");
+    return HMX_ERR_ARG;
+  }
+  std::unique_lock<std::mutex> l1(A->mu, std::defer_lock), l2(A64->mu, std::defer_lock);
+  if (A == A64) l1.lock();
+  else std::lock(l1, l2);
+  DeviceGuard guard(A->device);
+  *rep = hmx_solve_report{};
+  cudaDeviceProp prop{};
+  HMX_CUDA(cudaGetDeviceProperties(&prop, A->device));
+  SolveCtx c{};
+  c.A = A;
+  c.A64 = A64;
+  c.st = A->stream;
+  c.grid = 2 * prop.multiProcessorCount;
+  int rc = workspace_for(A, c.w, c.grid);
+  if (rc) return rc;
+  const int64_t n = A->n;
+  const int n32 = (int)n;
+  const int pgrid = (int)((n + 255) / 256);
+  Workspace& w = c.w;
+  cudaStream_t st = c.st;
+
+  HMX_CUDA(cudaEventRecord(A->ev[6], st));
+  HMX_CUDA(cudaMemcpyAsync(w.orig, b, n * sizeof(double), cudaMemcpyHostToDevice, st));
+  permute_kernel<<<pgrid, 256, 0, st>>>(w.orig, A->dp.perm, w.b, n32, 0);
+  HMX_CUDA(cudaMemsetAsync(w.flags, 0, 4 * sizeof(int), st));
+  // |b| (solver.py:91)
+  dot2_kernel<<<c.grid, kVecThreads, 0, st>>>(w.b, w.b, nullptr, nullptr, n32, c.red(SC_BB));
+  HMX_CUDA(cudaGetLastError());
+  if ((rc = sync_scalars(c))) return rc;
+  const double nb = std::sqrt(w.h_sc[SC_BB]);
+  int hlen = 0;
+  auto finish = [&](int status) -> int {
+    rep->history_len = hlen;
+    if (status == HMX_OK) {
+      permute_kernel<<<pgrid, 256, 0, st>>>(w.x, A->dp.perm, w.orig, n32, 1);
+      HMX_CUDA(cudaMemcpyAsync(x, w.orig, n * sizeof(double), cudaMemcpyDeviceToHost, st));
+    }
+    HMX_CUDA(cudaEventRecord(A->ev[7], st));
+    HMX_CUDA(cudaStreamSynchronize(st));
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, A->ev[6], A->ev[7]);
+    rep->device_ms = ms;
+    return status;
+  };
+  if (nb == 0.0) {  // zero data: x = 0 is exact (solver.py:92-97)
+    HMX_CUDA(cudaMemsetAsync(w.x, 0, n * sizeof(double), st));
+    history[hlen++] = 0.0;
+    rep->converged = 1;
+    rep->has_true_residual = 1;
+    rep->true_residual = 0.0;
+    return finish(HMX_OK);
+  }
+
+  // x = 0 ; r = b - A x ; r_hat = r   (solver.py:99-102)
+  HMX_CUDA(cudaMemsetAsync(w.p, 0, n * sizeof(double), st));
+  if ((rc = apply(A, w, st, w.p, w.t, nullptr, 0, 0, w.flags))) return rc;
+  rep->matvecs++;
+  init_kernel<<<c.grid, kVecThreads, 0, st>>>(w.b, w.t, w.r, w.rhat, w.x, n32, c.red(SC_RHO1));
+  HMX_CUDA(cudaGetLastError());
+  if ((rc = sync_scalars(c))) return rc;
+  if (flags_nonfinite(c)) {
+    set_error("non-finite matvec result");
+    return finish(HMX_ERR_NONFINITE);
+  }
+  // rho_1 = r^.r = |r|^2 ; it lives in ring slot (1 & 1) = SC_RHO1
+  double rho = w.h_sc[SC_RHO1];
+  history[hlen++] = std::sqrt(rho) / nb;
+
+  auto rho_slot = [](int i) { return (i & 1) ? SC_RHO1 : SC_RHO0; };
+  for (int i = 1; i <= max_iter; ++i) {
+    if (std::fabs(rho) < kBreakdownEps) {  // solver.py:113-115
+      rep->breakdown = 1;
+      rep->breakdown_value = rho;
+      rep->breakdown_iteration = i;
+      break;
+    }
+    p_update_kernel<<<c.grid, kVecThreads, 0, st>>>(w.r, w.v, w.p, n32, i == 1, w.sc, rho_slot(i),
+                                                      rho_slot(i - 1));
+    HMX_CUDA(cudaGetLastError());
+    if ((rc = apply(A, w, st, w.p, w.v, w.rhat, 0, SC_DV, w.flags))) return rc;
+    rep->matvecs++;
+    s_update_kernel<<<c.grid, kVecThreads, 0, st>>>(w.r, w.v, w.s, n32, w.sc, rho_slot(i),
+                                                      c.red(SC_SS));
+    HMX_CUDA(cudaGetLastError());
+    if ((rc = sync_scalars(c))) return rc;
+    if (flags_nonfinite(c)) {
+      set_error("non-finite matvec result");
+      return finish(HMX_ERR_NONFINITE);
+    }
+    const double denom = w.h_sc[SC_DV];
+    if (std::fabs(denom) < kBreakdownEps) {  // solver.py:123-125
+      rep->breakdown = 2;
+      rep->breakdown_value = denom;
+      rep->breakdown_iteration = i;
+      break;
+    }
+    const double s_rel = std::sqrt(w.h_sc[SC_SS]) / nb;
+    if (s_rel < tol) {  // solver.py:130-136
+      x_alpha_p_kernel<<<c.grid, kVecThreads, 0, st>>>(w.x, w.p, n32, w.sc);
+      HMX_CUDA(cudaGetLastError());
+      history[hlen++] = s_rel;
+      rep->iterations = i;
+      double tr = 0.0;
+      if ((rc = true_residual_dev(c, &tr))) return finish(rc);
+      rep->matvecs++;
+      rep->has_true_residual = 1;
+      rep->true_residual = tr;
+      rep->converged = tr < tol;
+      break;
+    }
+    if ((rc = apply(A, w, st, w.s, w.t, w.s, 1, SC_DT, w.flags + 1))) return rc;
+    rep->matvecs++;
+    xr_update_kernel<<<c.grid, kVecThreads, 0, st>>>(w.x, w.r, w.p, w.s, w.t, w.rhat, n32, w.sc,
+                                                       VecRed{w.partials, w.done, w.sc + SC_TMP});
+    HMX_CUDA(cudaGetLastError());
+    if ((rc = sync_scalars(c))) return rc;
+    if (flags_nonfinite(c)) {
+      set_error("non-finite matvec result");
+      return finish(HMX_ERR_NONFINITE);
+    }
+    if (w.h_sc[SC_DT + 1] == 0.0) {  // solver.py:139-142
+      rep->breakdown = 3;
+      rep->breakdown_iteration = i;
+      break;
+    }
+    const double omega = w.h_sc[SC_OMEGA];
+    const double rr = w.h_sc[SC_TMP], rho_next = w.h_sc[SC_TMP + 1];
+    const double rel = std::sqrt(rr) / nb;
+    history[hlen++] = rel;
+    rep->iterations = i;
+    if (rel < tol) {  // solver.py:151-154
+      double tr = 0.0;
+      if ((rc = true_residual_dev(c, &tr))) return finish(rc);
+      rep->matvecs++;
+      rep->has_true_residual = 1;
+      rep->true_residual = tr;
+      rep->converged = tr < tol;
+      break;
+    }
+    if (std::fabs(omega) < kBreakdownEps) {  // solver.py:155-157
+      rep->breakdown = 4;
+      rep->breakdown_value = omega;
+      rep->breakdown_iteration = i;
+      break;
+    }
+    // next rho goes to the next ring slot; rho_prev stays in the current one
+    HMX_CUDA(cudaMemcpyAsync(w.sc + rho_slot(i + 1), w.sc + SC_TMP + 1, sizeof(double),
+                             cudaMemcpyDeviceToDevice, st));
+    rho = rho_next;
+  }
+  return finish(HMX_OK);
+}
+
+}  // extern "C"
