@@ -5,13 +5,12 @@
 
 namespace hmx {
 
-cudaError_t launch_stage1(const DevPlan& P, const double* x, int grid, cudaStream_t st);
+cudaError_t launch_stage1(const DevPlan& P, const double* x, cudaStream_t st);
 cudaError_t launch_stage2(const DevPlan& P, const double* x, const S2Out& out, cudaStream_t st,
                           bool pdl);
 cudaError_t launch_gather_perm(const double* x, const int32_t* perm, double* xp, int n,
                                cudaStream_t st);
 cudaError_t launch_probe(const DevPlan& P, const double* x, unsigned long long* first_bad,
                          cudaStream_t st);
-int stage1_occupancy(int pipe);
 
 }  // namespace hmx

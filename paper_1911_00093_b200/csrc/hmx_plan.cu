@@ -16,6 +16,8 @@
 #include <cstdio>
 #include <cstring>
 #include <functional>
+#include <map>
+#include <tuple>
 #include <numeric>
 #include <queue>
 #include <thread>
@@ -56,7 +58,7 @@ struct ItemRef {
 };
 
 int enqueue_matvec(hmx_plan* p, const double* xp, const S2Out& out) {
-  HMX_CUDA(launch_stage1(p->dp, xp, p->s1_grid, p->stream));
+  HMX_CUDA(launch_stage1(p->dp, xp, p->stream));
   HMX_CUDA(launch_stage2(p->dp, xp, out, p->stream, /*pdl=*/true));
   return HMX_OK;
 }
@@ -106,6 +108,7 @@ int hmx_plan_get_info(const hmx_plan* p, hmx_plan_info* info) {
 
 static int plan_create_impl(const hmx_matrix_desc* d, int device, const hmx_plan_options* opt,
                             hmx_plan* p) {
+  (void)device;
   const int64_t n = d->n, nb = d->n_blocks;
   if (n < 1 || n > INT32_MAX / 2 || nb < 1 || d->scheme < 0 || d->scheme > HMX_M3) {
     set_error("invalid matrix descriptor (n, n_blocks or scheme)");
@@ -119,7 +122,7 @@ static int plan_create_impl(const hmx_matrix_desc* d, int device, const hmx_plan
     set_error("invalid row range");
     return HMX_ERR_ARG;
   }
-  const int64_t s1_target = opt && opt->s1_chunk_bytes > 0 ? opt->s1_chunk_bytes : 24 * 1024;
+  const int64_t s1_target = opt && opt->s1_chunk_bytes > 0 ? opt->s1_chunk_bytes : 256 * 1024;
   const size_t a_es = d->a32 ? 4 : 8, hi_es = d->hi32 ? 4 : 8;
 
   // ---- validate blocks and collect the ones touching rows [rb, re)
@@ -146,7 +149,8 @@ static int plan_create_impl(const hmx_matrix_desc* d, int device, const hmx_plan
         set_error("low-rank block " + std::to_string(k) + " exceeds its payload buffer");
         return HMX_ERR_ARG;
       }
-      if (pipe >= P_M2D && (d->dhi_off[k] < 0 || d->dhi_off[k] + kh > d->n64)) {
+      if (pipe >= P_M2D && ((kh && (d->dhi_off[k] < 0 || d->dhi_off[k] + kh > d->n64)) ||
+                            (kl && (d->dlo_off[k] < 0 || d->dlo_off[k] + kl > d->n64)))) {
         set_error("low-rank block " + std::to_string(k) + " lacks its scale diagonal");
         return HMX_ERR_ARG;
       }
@@ -168,34 +172,133 @@ static int plan_create_impl(const hmx_matrix_desc* d, int device, const hmx_plan
   std::vector<int64_t> seg_start;
   for (size_t i = 0; i + 1 < bounds.size(); ++i) {
     const int64_t a = bounds[i], b = bounds[i + 1];
-    const int64_t pieces = (b - a + kS2Rows - 1) / kS2Rows;
+    const int64_t pieces = (b - a + kSegRows - 1) / kSegRows;
     for (int64_t q = 0; q < pieces; ++q) seg_start.push_back(a + (b - a) * q / pieces);
   }
-  const int64_t nseg = (int64_t)seg_start.size();
+  const int64_t nseg2 = (int64_t)seg_start.size();
   seg_start.push_back(re);
 
-  // ---- z layout: per low-rank block, FP64 class then FP32 class
+  // ---- stage-1 groups: rank rows of the blocks sharing a column cluster
+  // (and a storage class); z is laid out group by group so every stage-1
+  // segment writes a contiguous z range.
+  std::map<std::tuple<int, int64_t, int64_t>, std::vector<int32_t>> groups;
+  for (int32_t k : blocks) {
+    if (d->kind[k] != 1) continue;
+    const int64_t* t = d->table + 5 * k;
+    if (d->khi[k] > 0) groups[std::make_tuple(1, t[2], t[3])].push_back(k);
+    if (has_lo && d->klo[k] > 0) groups[std::make_tuple(2, t[2], t[3])].push_back(k);
+  }
   std::vector<int64_t> zoff_hi((size_t)nb, -1), zoff_lo((size_t)nb, -1);
   int64_t Z = 0;
-  for (int32_t k : blocks)
-    if (d->kind[k] == 1) {
-      zoff_hi[(size_t)k] = Z;
-      Z += d->khi[k];
-      zoff_lo[(size_t)k] = Z;
-      Z += has_lo ? d->klo[k] : 0;
+  for (auto& g : groups) {
+    const int cls = std::get<0>(g.first);
+    for (int32_t k : g.second) {
+      (cls == 1 ? zoff_hi : zoff_lo)[(size_t)k] = Z;
+      Z += cls == 1 ? d->khi[k] : d->klo[k];
     }
+  }
   if (Z > INT32_MAX) {
     set_error("rank sum exceeds the 32-bit index range");
     return HMX_ERR_ARG;
   }
 
-  // ---- stage-2 items per segment, in partition order
-  std::vector<std::vector<ItemRef>> items64((size_t)nseg), items32((size_t)nseg);
+  std::vector<Seg> seg1, seg2((size_t)nseg2);
+  std::vector<Run> runs;
+  std::vector<int32_t> run_block;
+  int64_t off64 = 0, off32 = 0;
+
+  // ---- stage-1 segments
+  const bool src_round = pipe == P_M1S || pipe == P_M2S;  // FP32 source shadow (matvec.py:119)
+  struct S1Fill {
+    int32_t seg;       // index into seg1 (pre-sort)
+    int32_t cls;
+    int64_t cs, ncol;  // cluster columns
+    int64_t c0;        // first column of this chunk within the cluster
+    std::vector<std::pair<int32_t, int32_t>>* rows;  // (block, rank) per output row
+    int32_t r0;
+  };
+  std::vector<std::vector<std::pair<int32_t, int32_t>>> group_rows;
+  group_rows.reserve(groups.size());
+  std::vector<S1Fill> fills;
+  std::vector<double> zscale(pipe >= P_M2D ? (size_t)std::max<int64_t>(Z, 1) : 1, 1.0);
+  int64_t part_len = 0;
+  int32_t n_red = 0;
+  int64_t s1_bytes = 0, s2_bytes = 0;
+  for (auto& g : groups) {
+    const int cls = std::get<0>(g.first);
+    const int64_t cs = std::get<1>(g.first), ncol = std::get<2>(g.first) - cs;
+    group_rows.emplace_back();
+    auto& rows = group_rows.back();
+    for (int32_t k : g.second) {
+      const int64_t kk = cls == 1 ? d->khi[k] : d->klo[k];
+      for (int64_t q = 0; q < kk; ++q) rows.push_back({k, (int32_t)q});
+      if (pipe >= P_M2D) {
+        const double* dsrc = d->buf64 + (cls == 1 ? d->dhi_off[k] : d->dlo_off[k]);
+        const int64_t z0 = cls == 1 ? zoff_hi[(size_t)k] : zoff_lo[(size_t)k];
+        for (int64_t q = 0; q < kk; ++q) zscale[(size_t)(z0 + q)] = dsrc[q];
+      }
+    }
+    const bool is32 = cls == 2 || d->hi32;
+    const int64_t es = is32 ? 4 : 8;
+    const int64_t rg = (int64_t)rows.size();
+    const int64_t pieces = (rg + kSegRows - 1) / kSegRows;
+    for (int64_t pc = 0; pc < pieces; ++pc) {
+      const int64_t r0 = rg * pc / pieces, r1 = rg * (pc + 1) / pieces, R = r1 - r0;
+      const int64_t rp = round_up(R, is32 ? 4 : 2);
+      int64_t C = std::max<int64_t>(1, s1_target / (rp * es));
+      const int64_t nch = (ncol + C - 1) / C;
+      C = (ncol + nch - 1) / nch;
+      const int32_t red = nch > 1 ? n_red++ : -1;
+      const int32_t poff = nch > 1 ? (int32_t)part_len : -1;
+      if (nch > 1) part_len += nch * R;
+      const auto& first = rows[(size_t)r0];
+      const int64_t zrow0 = (cls == 1 ? zoff_hi : zoff_lo)[(size_t)first.first] + first.second;
+      for (int64_t ch = 0; ch < nch; ++ch) {
+        const int64_t c0 = ch * C, w = std::min(C, ncol - c0);
+        Seg s{};
+        s.row0 = (int32_t)zrow0;
+        s.R = (int32_t)R;
+        s.run0 = (int32_t)runs.size();
+        s.red = red;
+        s.chunk = (int32_t)ch;
+        s.nchunks = (int32_t)nch;
+        s.part_off = poff;
+        Run r{};
+        r.src = (int32_t)(cs + c0);
+        r.width = (int32_t)w;
+        r.col0 = 0;
+        r.flags = (src_round ? RUN_ROUND : 0) | ((is32 && pipe == P_M1S) ? RUN_ACC32 : 0);
+        runs.push_back(r);
+        run_block.push_back(-1);
+        if (is32) {
+          s.off32 = off32;
+          s.W32 = (int32_t)w;
+          s.nrun32 = 1;
+          off32 += w * rp;
+        } else {
+          s.off64 = off64;
+          s.W64 = (int32_t)w;
+          s.nrun64 = 1;
+          off64 += w * rp;
+        }
+        s1_bytes += R * w * es;
+        fills.push_back({(int32_t)seg1.size(), cls, cs, ncol, c0, &rows, (int32_t)r0});
+        seg1.push_back(s);
+      }
+    }
+  }
+  if (part_len > INT32_MAX) {
+    set_error("too many stage-1 partials");
+    return HMX_ERR_ARG;
+  }
+
+  // ---- stage-2 items per row segment, in partition order
+  std::vector<std::vector<ItemRef>> items64((size_t)nseg2), items32((size_t)nseg2);
   for (int32_t k : blocks) {
     const int64_t* t = d->table + 5 * k;
     const int64_t lo = std::max(t[0], rb), hi = std::min(t[1], re);
-    int64_t s = std::upper_bound(seg_start.begin(), seg_start.begin() + nseg, lo) - seg_start.begin() - 1;
-    for (; s < nseg && seg_start[(size_t)s] < hi; ++s) {
+    int64_t s = std::upper_bound(seg_start.begin(), seg_start.begin() + nseg2, lo) - seg_start.begin() - 1;
+    for (; s < nseg2 && seg_start[(size_t)s] < hi; ++s) {
       if (d->kind[k] == 0) {
         (d->a32 ? items32 : items64)[(size_t)s].push_back({k, 0});
       } else {
@@ -210,16 +313,15 @@ static int plan_create_impl(const hmx_matrix_desc* d, int device, const hmx_plan
   };
   const bool dense_single = pipe == P_M1S || pipe == P_M2S;  // A32 . x32 in FP32
   const bool u_acc32 = pipe == P_M1S || pipe == P_M1M;       // U32 . z32 in FP32
-  std::vector<S2Seg> segs((size_t)nseg);
-  std::vector<Run> runs;
-  std::vector<int32_t> run_block;
-  int64_t off64 = 0, off32 = 0;
   bool any_acc32 = false, any_acc64_in32 = false;
-  for (int64_t s = 0; s < nseg; ++s) {
-    S2Seg& sg = segs[(size_t)s];
+  for (int64_t s = 0; s < nseg2; ++s) {
+    Seg& sg = seg2[(size_t)s];
     sg.row0 = (int32_t)seg_start[(size_t)s];
     sg.R = (int32_t)(seg_start[(size_t)s + 1] - seg_start[(size_t)s]);
     sg.run0 = (int32_t)runs.size();
+    sg.red = -1;
+    sg.nchunks = 1;
+    sg.part_off = -1;
     for (int part = 0; part < 2; ++part) {
       const auto& lst = part == 0 ? items64[(size_t)s] : items32[(size_t)s];
       int64_t col = 0;
@@ -255,138 +357,47 @@ static int plan_create_impl(const hmx_matrix_desc* d, int device, const hmx_plan
     sg.off32 = off32;
     off64 += (int64_t)sg.W64 * round_up(sg.R, 2);
     off32 += (int64_t)sg.W32 * round_up(sg.R, 4);
+    s2_bytes += (int64_t)sg.R * (sg.W64 * 8 + sg.W32 * 4);
   }
-  const int f32mode = !any_acc32 ? F32_ALL64 : (any_acc64_in32 ? F32_MIXED : F32_ALL32);
-
-  // ---- stage-1 segments and tasks
-  std::vector<S1Seg> s1segs;
-  std::vector<S1Task> tasks;
-  std::vector<int64_t> task_bytes;
-  struct S1Src {
-    int32_t block;
-    int8_t cls;
-    int32_t k0, R;
-    int64_t vt_off;
-    int32_t ld;
-  };
-  std::vector<S1Src> s1src;
-  int64_t vt64_len = 0, vt32_len = 0, part_len = 0;
-  std::vector<double> zscale(pipe >= P_M2D ? (size_t)std::max<int64_t>(Z, 1) : 1, 1.0);
-  for (int32_t k : blocks) {
-    if (d->kind[k] != 1) continue;
-    const int64_t* t = d->table + 5 * k;
-    const int64_t ncol = t[3] - t[2];
-    for (int cls = 1; cls <= 2; ++cls) {
-      const int64_t kk = cls == 1 ? d->khi[k] : (has_lo ? d->klo[k] : 0);
-      if (kk <= 0) continue;
-      const bool is32 = cls == 2 || d->hi32;
-      const int64_t es = is32 ? 4 : 8, V = is32 ? 4 : 2;
-      const int64_t ld = round_up(ncol, V);
-      const int64_t nsub = (kk + kS1RMax - 1) / kS1RMax;
-      const int64_t zbase = cls == 1 ? zoff_hi[(size_t)k] : zoff_lo[(size_t)k];
-      if (pipe >= P_M2D) {
-        const double* dsrc = d->buf64 + (cls == 1 ? d->dhi_off[k] : d->dlo_off[k]);
-        for (int64_t q = 0; q < kk; ++q) zscale[(size_t)(zbase + q)] = dsrc[q];
-      }
-      for (int64_t sidx = 0; sidx < nsub; ++sidx) {
-        const int64_t k0 = kk * sidx / nsub, k1 = kk * (sidx + 1) / nsub, R = k1 - k0;
-        int64_t& vlen = is32 ? vt32_len : vt64_len;
-        const int64_t vt_off = vlen;
-        vlen += R * ld;
-        const int64_t lanes_cols = 32 * V;
-        int64_t C = (s1_target / (R * es)) / lanes_cols * lanes_cols;
-        C = std::max(C, lanes_cols);
-        const int64_t nch = (ncol + C - 1) / C;
-        if (nch > 32767) {
-          set_error("block too wide for the stage-1 chunk index");
-          return HMX_ERR_ARG;
-        }
-        S1Seg sg{};
-        sg.zoff = (int32_t)(zbase + k0);
-        sg.R = (int32_t)R;
-        sg.nchunks = (int32_t)nch;
-        sg.part_off = -1;
-        if (nch > 1) {
-          sg.part_off = (int32_t)part_len;
-          part_len += nch * R;
-        }
-        const int32_t sid = (int32_t)s1segs.size();
-        s1segs.push_back(sg);
-        s1src.push_back({k, (int8_t)cls, (int32_t)k0, (int32_t)R, vt_off, (int32_t)ld});
-        for (int64_t ch = 0; ch < nch; ++ch) {
-          S1Task tk{};
-          tk.vt_off = vt_off + ch * C;
-          tk.ld = (int32_t)ld;
-          tk.ncols = (int32_t)std::min(C, ncol - ch * C);
-          tk.xoff = (int32_t)(t[2] + ch * C);
-          tk.seg = sid;
-          tk.chunk = (int16_t)ch;
-          tk.R = (int8_t)R;
-          tk.is32 = is32 ? 1 : 0;
-          tasks.push_back(tk);
-          task_bytes.push_back(R * tk.ncols * es);
-        }
-      }
-    }
-  }
-  if (part_len > INT32_MAX) {
-    set_error("too many stage-1 partials");
+  if ((int64_t)runs.size() > INT32_MAX || off64 < 0) {
+    set_error("plan too large");
     return HMX_ERR_ARG;
   }
+  const int f32mode2 = !any_acc32 ? F32_ALL64 : (any_acc64_in32 ? F32_MIXED : F32_ALL32);
 
-  // ---- device properties, stage-1 grid, LPT task assignment
-  cudaDeviceProp prop{};
-  HMX_CUDA(cudaGetDeviceProperties(&prop, device));
-  const int occ = stage1_occupancy(pipe);
-  p->s1_grid = prop.multiProcessorCount * occ;
-  const int64_t n_warps_total = (int64_t)p->s1_grid * (kS1Threads / 32);
-  const int64_t ntask = (int64_t)tasks.size();
-  std::vector<int32_t> warp_of((size_t)ntask);
-  {
-    std::vector<int64_t> order((size_t)ntask);
-    std::iota(order.begin(), order.end(), 0);
-    std::stable_sort(order.begin(), order.end(),
-                     [&](int64_t a, int64_t b) { return task_bytes[(size_t)a] > task_bytes[(size_t)b]; });
-    using Load = std::pair<int64_t, int32_t>;
-    std::priority_queue<Load, std::vector<Load>, std::greater<Load>> heap;
-    for (int32_t w = 0; w < (int32_t)n_warps_total; ++w) heap.push({0, w});
-    for (int64_t i : order) {
-      Load l = heap.top();
-      heap.pop();
-      warp_of[(size_t)i] = l.second;
-      l.first += task_bytes[(size_t)i] + 256;  // +256: per-task fixed cost
-      heap.push(l);
+  // ---- pack the blob (host, parallel)
+  std::vector<double> blob64((size_t)std::max<int64_t>(off64, 2), 0.0);
+  std::vector<float> blob32((size_t)std::max<int64_t>(off32, 4), 0.f);
+  parallel_for((int64_t)fills.size(), [&](int64_t i) {
+    const S1Fill& f = fills[(size_t)i];
+    const Seg& s = seg1[(size_t)f.seg];
+    const bool is32 = s.W32 > 0;
+    const int64_t rp = round_up(s.R, is32 ? 4 : 2);
+    const int64_t w = is32 ? s.W32 : s.W64;
+    for (int64_t t = 0; t < s.R; ++t) {
+      const auto& row = (*f.rows)[(size_t)(f.r0 + t)];
+      const int32_t k = row.first;
+      const int64_t* tb = d->table + 5 * k;
+      const int64_t m = tb[1] - tb[0];
+      const int64_t kk = f.cls == 1 ? d->khi[k] : d->klo[k];
+      const int64_t base = (f.cls == 1 ? d->hi_off[k] : d->lo_off[k]) + m * kk + (int64_t)row.second * f.ncol + f.c0;
+      const bool src32 = f.cls == 2 || d->hi32;
+      for (int64_t j = 0; j < w; ++j) {
+        if (is32) blob32[(size_t)(s.off32 + j * rp + t)] = src32 ? d->buf32[base + j] : (float)d->buf64[base + j];
+        else blob64[(size_t)(s.off64 + j * rp + t)] = src32 ? d->buf32[base + j] : d->buf64[base + j];
+      }
     }
-  }
-  std::vector<int32_t> warp_ptr((size_t)n_warps_total + 1, 0);
-  for (int64_t i = 0; i < ntask; ++i) warp_ptr[(size_t)warp_of[(size_t)i] + 1]++;
-  for (int64_t w = 0; w < n_warps_total; ++w) warp_ptr[(size_t)w + 1] += warp_ptr[(size_t)w];
-  std::vector<S1Task> tasks_sorted((size_t)ntask);
-  {
-    std::vector<int32_t> fill(warp_ptr.begin(), warp_ptr.end() - 1);
-    // keep the LPT order (big tasks first) inside each warp
-    std::vector<int64_t> order((size_t)ntask);
-    std::iota(order.begin(), order.end(), 0);
-    std::stable_sort(order.begin(), order.end(),
-                     [&](int64_t a, int64_t b) { return task_bytes[(size_t)a] > task_bytes[(size_t)b]; });
-    for (int64_t i : order) tasks_sorted[(size_t)fill[(size_t)warp_of[(size_t)i]]++] = tasks[(size_t)i];
-  }
-
-  // ---- pack the blobs (host, parallel) and upload
-  std::vector<double> blob64((size_t)std::max<int64_t>(off64, 1), 0.0);
-  std::vector<float> blob32((size_t)std::max<int64_t>(off32, 1), 0.f);
-  parallel_for(nseg, [&](int64_t s) {
-    const S2Seg& sg = segs[(size_t)s];
+  });
+  parallel_for(nseg2, [&](int64_t s) {
+    const Seg& sg = seg2[(size_t)s];
     for (int part = 0; part < 2; ++part) {
       const auto& lst = part == 0 ? items64[(size_t)s] : items32[(size_t)s];
       const int64_t rp = part == 0 ? round_up(sg.R, 2) : round_up(sg.R, 4);
       int64_t col = 0;
       for (const ItemRef& it : lst) {
         const int64_t* t = d->table + 5 * it.block;
-        const int64_t m = t[1] - t[0], nc = t[3] - t[2];
         const int64_t r0 = sg.row0 - t[0];
         const int64_t w = item_width(it);
-        // source row-major matrix (m x w) and its element type
         int64_t src_off;
         bool src32;
         if (it.cls == 0) {
@@ -399,35 +410,17 @@ static int plan_create_impl(const hmx_matrix_desc* d, int device, const hmx_plan
           src_off = d->lo_off[it.block];
           src32 = true;
         }
-        (void)nc;
-        (void)m;
-        for (int64_t c = 0; c < w; ++c) {
-          const int64_t dst = (col + c) * rp;
-          for (int64_t i = 0; i < sg.R; ++i) {
-            const int64_t e = src_off + (r0 + i) * w + c;
-            if (part == 0) blob64[(size_t)(sg.off64 + dst + i)] = src32 ? d->buf32[e] : d->buf64[e];
-            else blob32[(size_t)(sg.off32 + dst + i)] = src32 ? d->buf32[e] : (float)d->buf64[e];
+        for (int64_t i = 0; i < sg.R; ++i) {
+          const int64_t e0 = src_off + (r0 + i) * w;
+          for (int64_t c = 0; c < w; ++c) {
+            const int64_t dst = (col + c) * rp + i;
+            if (part == 0) blob64[(size_t)(sg.off64 + dst)] = src32 ? d->buf32[e0 + c] : d->buf64[e0 + c];
+            else blob32[(size_t)(sg.off32 + dst)] = src32 ? d->buf32[e0 + c] : (float)d->buf64[e0 + c];
           }
         }
         col += w;
       }
     }
-  });
-  std::vector<double> vt64((size_t)std::max<int64_t>(vt64_len, 1), 0.0);
-  std::vector<float> vt32((size_t)std::max<int64_t>(vt32_len, 1), 0.f);
-  parallel_for((int64_t)s1src.size(), [&](int64_t i) {
-    const S1Src& s = s1src[(size_t)i];
-    const int64_t* t = d->table + 5 * s.block;
-    const int64_t m = t[1] - t[0], nc = t[3] - t[2];
-    const int64_t kk = s.cls == 1 ? d->khi[s.block] : d->klo[s.block];
-    const int64_t base = (s.cls == 1 ? d->hi_off[s.block] : d->lo_off[s.block]) + m * kk;
-    const bool src32 = s.cls == 2 || d->hi32;
-    for (int64_t q = 0; q < s.R; ++q)
-      for (int64_t j = 0; j < nc; ++j) {
-        const int64_t e = base + (s.k0 + q) * nc + j;
-        if (src32) vt32[(size_t)(s.vt_off + q * s.ld + j)] = d->buf32[e];
-        else vt64[(size_t)(s.vt_off + q * s.ld + j)] = d->buf64[e];
-      }
   });
   std::vector<int32_t> perm32((size_t)n);
   for (int64_t i = 0; i < n; ++i) {
@@ -437,6 +430,11 @@ static int plan_create_impl(const hmx_matrix_desc* d, int device, const hmx_plan
     }
     perm32[(size_t)i] = (int32_t)d->perm[i];
   }
+  // stage-1 CTAs in decreasing size: chunked (long) segments start first and
+  // the many small ones fill the tail
+  std::stable_sort(seg1.begin(), seg1.end(), [](const Seg& a, const Seg& b) {
+    return (int64_t)a.R * (a.W64 * 2 + a.W32) > (int64_t)b.R * (b.W64 * 2 + b.W32);
+  });
 
   DevPlan& dp = p->dp;
   dp.n = (int32_t)n;
@@ -453,55 +451,47 @@ static int plan_create_impl(const hmx_matrix_desc* d, int device, const hmx_plan
     return HMX_OK;
   };
   int rc;
-  S1Task* d_tasks = p->alloc<S1Task>(tasks_sorted.size());
-  if ((rc = up(d_tasks, tasks_sorted))) return rc;
-  int32_t* d_wptr = p->alloc<int32_t>(warp_ptr.size());
-  if ((rc = up(d_wptr, warp_ptr))) return rc;
-  S1Seg* d_s1 = p->alloc<S1Seg>(s1segs.size());
-  if ((rc = up(d_s1, s1segs))) return rc;
-  double* d_vt64 = p->alloc<double>(vt64.size());
-  if ((rc = up(d_vt64, vt64))) return rc;
-  float* d_vt32 = p->alloc<float>(vt32.size());
-  if ((rc = up(d_vt32, vt32))) return rc;
-  double* d_zs = p->alloc<double>(zscale.size());
-  if ((rc = up(d_zs, zscale))) return rc;
-  double* d_z = p->alloc<double>((size_t)std::max<int64_t>(Z, 1));
-  double* d_part = p->alloc<double>((size_t)std::max<int64_t>(part_len, 1));
-  uint32_t* d_cnt = p->alloc<uint32_t>(std::max<size_t>(s1segs.size(), 1));
-  S2Seg* d_s2 = p->alloc<S2Seg>(segs.size());
-  if ((rc = up(d_s2, segs))) return rc;
+  Seg* d_seg1 = p->alloc<Seg>(std::max<size_t>(seg1.size(), 1));
+  if ((rc = up(d_seg1, seg1))) return rc;
+  Seg* d_seg2 = p->alloc<Seg>(seg2.size());
+  if ((rc = up(d_seg2, seg2))) return rc;
   Run* d_runs = p->alloc<Run>(runs.size());
   if ((rc = up(d_runs, runs))) return rc;
   int32_t* d_rb = p->alloc<int32_t>(run_block.size());
   if ((rc = up(d_rb, run_block))) return rc;
   double* d_b64 = p->alloc<double>(blob64.size());
   if ((rc = up(d_b64, blob64))) return rc;
+  std::vector<double>().swap(blob64);
   float* d_b32 = p->alloc<float>(blob32.size());
   if ((rc = up(d_b32, blob32))) return rc;
+  std::vector<float>().swap(blob32);
+  double* d_zs = p->alloc<double>(zscale.size());
+  if ((rc = up(d_zs, zscale))) return rc;
   int32_t* d_perm = p->alloc<int32_t>(perm32.size());
   if ((rc = up(d_perm, perm32))) return rc;
+  double* d_z = p->alloc<double>((size_t)std::max<int64_t>(Z, 1));
+  double* d_part = p->alloc<double>((size_t)std::max<int64_t>(part_len, 1));
+  uint32_t* d_cnt = p->alloc<uint32_t>((size_t)std::max<int32_t>(n_red, 1));
   if (!d_z || !d_part || !d_cnt) {
     set_error("cudaMalloc failed (out of device memory?)");
     return HMX_ERR_CUDA;
   }
-  HMX_CUDA(cudaMemset(d_cnt, 0, std::max<size_t>(s1segs.size(), 1) * sizeof(uint32_t)));
+  HMX_CUDA(cudaMemset(d_cnt, 0, (size_t)std::max<int32_t>(n_red, 1) * sizeof(uint32_t)));
 
-  dp.tasks = d_tasks;
-  dp.warp_ptr = d_wptr;
-  dp.s1segs = d_s1;
-  dp.vt64 = d_vt64;
-  dp.vt32 = d_vt32;
-  dp.zscale = d_zs;
-  dp.z = d_z;
-  dp.part = d_part;
-  dp.seg_count = d_cnt;
-  dp.n_warps = ntask > 0 ? (int32_t)n_warps_total : 0;
-  dp.s2segs = d_s2;
+  dp.seg1 = d_seg1;
+  dp.seg2 = d_seg2;
+  dp.n_seg1 = (int32_t)seg1.size();
+  dp.n_seg2 = (int32_t)nseg2;
   dp.runs = d_runs;
   dp.blob64 = d_b64;
   dp.blob32 = d_b32;
-  dp.n_s2 = (int32_t)nseg;
-  dp.f32mode = f32mode;
+  dp.f32mode1 = pipe == P_M1S ? F32_ALL32 : F32_ALL64;
+  dp.f32mode2 = f32mode2;
+  dp.zepi = pipe == P_M1D ? Z_NONE : (pipe == P_M1S || pipe == P_M1M) ? Z_ROUND32 : Z_SCALE;
+  dp.zscale = d_zs;
+  dp.z = d_z;
+  dp.part = d_part;
+  dp.red_count = d_cnt;
   dp.perm = d_perm;
   dp.run_block = d_rb;
 
@@ -510,7 +500,7 @@ static int plan_create_impl(const hmx_matrix_desc* d, int device, const hmx_plan
   p->d_xp = p->alloc<double>((size_t)n);
   p->d_y = p->alloc<double>((size_t)n);
   p->d_nonfinite = p->alloc<int>(1);
-  p->d_seg_dots = p->alloc<double>((size_t)(2 * nseg));
+  p->d_seg_dots = p->alloc<double>((size_t)(2 * nseg2));
   p->d_done = p->alloc<uint32_t>(1);
   p->d_dots = p->alloc<double>(2);
   p->d_first_bad = p->alloc<unsigned long long>(1);
@@ -528,25 +518,20 @@ static int plan_create_impl(const hmx_matrix_desc* d, int device, const hmx_plan
   hmx_plan_info& info = p->info;
   info.n = n;
   info.payload_bytes = payload;
-  int64_t dev_bytes = 0;
-  dev_bytes += (int64_t)(blob64.size() * 8 + blob32.size() * 4 + vt64.size() * 8 + vt32.size() * 4);
-  dev_bytes += (int64_t)(tasks_sorted.size() * sizeof(S1Task) + segs.size() * sizeof(S2Seg) +
-                         runs.size() * (sizeof(Run) + 4) + s1segs.size() * (sizeof(S1Seg) + 4));
-  dev_bytes += (Z * 2 + part_len + 3 * n) * 8 + n * 4;
-  info.device_bytes = dev_bytes;
-  info.s1_segments = (int64_t)s1segs.size();
-  info.s1_tasks = ntask;
-  info.s2_segments = nseg;
+  info.device_bytes = off64 * 8 + off32 * 4 +
+                      (int64_t)((seg1.size() + seg2.size()) * sizeof(Seg) + runs.size() * (sizeof(Run) + 4)) +
+                      (Z * 2 + part_len + 3 * n) * 8 + n * 4;
+  info.s1_segments = (int64_t)seg1.size();
+  info.s1_tasks = n_red;
+  info.s2_segments = nseg2;
   info.s2_runs = (int64_t)runs.size();
   info.z_len = Z;
-  int64_t st1 = 0;
-  for (int64_t b : task_bytes) st1 += b;
-  info.stage1_bytes = st1;
-  info.stage2_bytes = off64 * 8 + off32 * 4;
-  info.s1_grid = p->s1_grid;
-  info.s1_block = kS1Threads;
-  info.s2_grid = (int32_t)nseg;
-  info.s2_block = kS2Threads;
+  info.stage1_bytes = s1_bytes;
+  info.stage2_bytes = s2_bytes;
+  info.s1_grid = (int32_t)seg1.size();
+  info.s1_block = kSegThreads;
+  info.s2_grid = (int32_t)nseg2;
+  info.s2_block = kSegThreads;
   return HMX_OK;
 }
 
@@ -667,27 +652,42 @@ int hmx_bench_matvec(hmx_plan* p, int warmup, int iters, int64_t flush_l2, doubl
     if (rc) return rc;
   }
   HMX_CUDA(cudaStreamSynchronize(st));
-  double tot = 0, t1 = 0, t2 = 0, best = 1e30;
-  for (int i = 0; i < iters; ++i) {
-    if (flush) HMX_CUDA(cudaMemsetAsync(flush, i & 0xff, (size_t)flush_l2, st));
+  // (1) the timed steps: `iters` matvecs back to back (stage 2 launched with
+  // programmatic dependent launch, as in the solver), one event pair
+  float total = 0.f;
+  if (!flush) {
     HMX_CUDA(cudaEventRecord(p->ev[0], st));
-    HMX_CUDA(launch_stage1(p->dp, xp, p->s1_grid, st));
+    for (int i = 0; i < iters; ++i) {
+      int rc = enqueue_matvec(p, xp, out);
+      if (rc) return rc;
+    }
     HMX_CUDA(cudaEventRecord(p->ev[1], st));
-    HMX_CUDA(launch_stage2(p->dp, xp, out, st, /*pdl=*/false));
+    HMX_CUDA(cudaEventSynchronize(p->ev[1]));
+    cudaEventElapsedTime(&total, p->ev[0], p->ev[1]);
+  }
+  // (2) per-stage breakdown: events around each launch (no PDL), optional
+  // L2 flush between matvecs outside the events
+  double t1 = 0, t2 = 0, best = 1e30;
+  const int reps = flush ? iters : std::max(3, std::min(iters, 50));
+  for (int i = 0; i < reps; ++i) {
+    if (flush) HMX_CUDA(cudaMemsetAsync(flush, i & 0xff, (size_t)flush_l2, st));
     HMX_CUDA(cudaEventRecord(p->ev[2], st));
-    HMX_CUDA(cudaEventSynchronize(p->ev[2]));
+    HMX_CUDA(launch_stage1(p->dp, xp, st));
+    HMX_CUDA(cudaEventRecord(p->ev[3], st));
+    HMX_CUDA(launch_stage2(p->dp, xp, out, st, /*pdl=*/false));
+    HMX_CUDA(cudaEventRecord(p->ev[4], st));
+    HMX_CUDA(cudaEventSynchronize(p->ev[4]));
     float a = 0, b = 0;
-    cudaEventElapsedTime(&a, p->ev[0], p->ev[1]);
-    cudaEventElapsedTime(&b, p->ev[1], p->ev[2]);
+    cudaEventElapsedTime(&a, p->ev[2], p->ev[3]);
+    cudaEventElapsedTime(&b, p->ev[3], p->ev[4]);
     t1 += a;
     t2 += b;
-    tot += a + b;
     best = std::min(best, (double)(a + b));
   }
   if (flush) cudaFree(flush);
-  out_ms[0] = tot / iters;
-  out_ms[1] = t1 / iters;
-  out_ms[2] = t2 / iters;
+  out_ms[0] = flush ? (t1 + t2) / reps : (double)total / iters;
+  out_ms[1] = t1 / reps;
+  out_ms[2] = t2 / reps;
   out_ms[3] = best;
   return HMX_OK;
 }

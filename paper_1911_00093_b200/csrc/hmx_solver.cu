@@ -272,7 +272,7 @@ int apply(hmx_plan* A, const Workspace& w, cudaStream_t st, const double* xp, do
     out.dots_out = w.sc + slot;
   }
   out.nonfinite = flag;
-  HMX_CUDA(launch_stage1(A->dp, xp, A->s1_grid, st));
+  HMX_CUDA(launch_stage1(A->dp, xp, st));
   HMX_CUDA(launch_stage2(A->dp, xp, out, st, /*pdl=*/true));
   A->last_xp = xp;
   return HMX_OK;
