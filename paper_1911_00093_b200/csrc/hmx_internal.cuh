@@ -39,7 +39,7 @@ struct Seg {             // 64 bytes; one CTA
   int32_t red;           // stage 1: reduction group of a column-chunked segment, or -1
   int32_t chunk, nchunks;
   int32_t part_off;      // partial slots (nchunks * R doubles)
-  int32_t pad;
+  int32_t gtab;          // FP32 part: group column boundaries at gtab[gtab..gtab+G], or -1
 };
 static_assert(sizeof(Seg) == 64, "Seg layout");
 
@@ -79,6 +79,7 @@ struct DevPlan {
   int32_t f32mode1, f32mode2;
   int32_t zepi;
   int32_t pad;
+  const int32_t* gtab;            // item-aligned FP32 group boundaries (stage 2)
   const double* zscale;           // d per z entry (methods 2, 3)
   double* z;
   double* part;                   // stage-1 chunk partials

@@ -152,8 +152,14 @@ __global__ void __launch_bounds__(kSegThreads, 3) seg_kernel(DevPlan P, const Se
   for (int tc0 = 0; tc0 < sg.W32; tc0 += kSegWMax) {
     const int tw = min(kSegWMax, sg.W32 - tc0);
     const bool act = q32 < g32;
-    const int cb = act ? (int)((int64_t)tw * q32 / g32) : 0;
-    const int ce = act ? (int)((int64_t)tw * (q32 + 1) / g32) : 0;
+    int cb = act ? (int)((int64_t)tw * q32 / g32) : 0;
+    int ce = act ? (int)((int64_t)tw * (q32 + 1) / g32) : 0;
+    if (F32MODE != F32_ALL64 && OUT == OUT_Y && sg.gtab >= 0 && act) {
+      // FP32-accumulated items are never split between groups: every item
+      // row is one FP32 chain (reference: FP32 GEMV per block, matvec.py:57, :73)
+      cb = P.gtab[sg.gtab + q32];
+      ce = P.gtab[sg.gtab + q32 + 1];
+    }
     const float* __restrict__ col = P.blob32 + sg.off32 + (int64_t)tc0 * rp32 + 4 * p32;
     float4 m[8];
     int c = cb;
@@ -199,8 +205,16 @@ __global__ void __launch_bounds__(kSegThreads, 3) seg_kernel(DevPlan P, const Se
   if (tid < R) {
     if (sg.W64 > 0)
       for (int q = 0; q < g64; ++q) s += red64[q * rp64 + tid];
-    if (sg.W32 > 0)
-      for (int q = 0; q < g32; ++q) s += red32[q * rp32 + tid];
+    if (sg.W32 > 0) {
+      if (OUT == OUT_Z && F32MODE == F32_ALL32) {
+        // stage 1, m1-single: z = Vt32 . x32 accumulated in FP32 throughout
+        float f = 0.f;
+        for (int q = 0; q < g32; ++q) f += (float)red32[q * rp32 + tid];
+        s = (double)f;
+      } else {
+        for (int q = 0; q < g32; ++q) s += red32[q * rp32 + tid];
+      }
+    }
   }
 
   if constexpr (OUT == OUT_Z) {
@@ -217,7 +231,13 @@ __global__ void __launch_bounds__(kSegThreads, 3) seg_kernel(DevPlan P, const Se
         __threadfence();
         if (tid < R) {
           double t = 0.0;
-          for (int ch = 0; ch < sg.nchunks; ++ch) t += __ldcg(P.part + sg.part_off + ch * R + tid);
+          if (F32MODE == F32_ALL32) {
+            float f = 0.f;
+            for (int ch = 0; ch < sg.nchunks; ++ch) f += (float)__ldcg(P.part + sg.part_off + ch * R + tid);
+            t = (double)f;
+          } else {
+            for (int ch = 0; ch < sg.nchunks; ++ch) t += __ldcg(P.part + sg.part_off + ch * R + tid);
+          }
           P.z[sg.row0 + tid] = z_epilogue(P, t, sg.row0 + tid);
         }
         if (tid == 0) P.red_count[sg.red] = 0u;  // ready for the next matvec

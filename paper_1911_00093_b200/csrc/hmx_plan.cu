@@ -203,6 +203,7 @@ static int plan_create_impl(const hmx_matrix_desc* d, int device, const hmx_plan
   }
 
   std::vector<Seg> seg1, seg2((size_t)nseg2);
+  std::vector<int32_t> gtab;
   std::vector<Run> runs;
   std::vector<int32_t> run_block;
   int64_t off64 = 0, off32 = 0;
@@ -263,6 +264,7 @@ static int plan_create_impl(const hmx_matrix_desc* d, int device, const hmx_plan
         s.chunk = (int32_t)ch;
         s.nchunks = (int32_t)nch;
         s.part_off = poff;
+        s.gtab = -1;
         Run r{};
         r.src = (int32_t)(cs + c0);
         r.width = (int32_t)w;
@@ -352,6 +354,32 @@ static int plan_create_impl(const hmx_matrix_desc* d, int device, const hmx_plan
         sg.W32 = (int32_t)col;
         sg.nrun32 = (int32_t)lst.size();
       }
+    }
+    // item-aligned group boundaries for FP32-accumulated parts: greedy cut
+    // at the item boundary nearest each uniform boundary; an item wider than
+    // two group shares may still be cut (its FP32 chains then span >= W/G
+    // columns each)
+    sg.gtab = -1;
+    if (sg.W32 > 0 && sg.W32 <= kSegWMax && (dense_single || u_acc32)) {
+      const int64_t tpg = round_up(sg.R, 4) / 4, G = kSegThreads / tpg;
+      std::vector<int64_t> cuts;  // item start columns
+      for (int32_t j = 0; j < sg.nrun32; ++j) cuts.push_back(runs[(size_t)(sg.run0 + sg.nrun64 + j)].col0);
+      cuts.push_back(sg.W32);
+      sg.gtab = (int32_t)gtab.size();
+      gtab.push_back(0);
+      const double share = (double)sg.W32 / (double)G;
+      size_t k = 0;
+      for (int64_t q = 1; q < G; ++q) {
+        const double ideal = share * (double)q;
+        while (k + 1 < cuts.size() && (double)cuts[k + 1] <= ideal) ++k;
+        // nearest item boundary around `ideal`
+        int64_t best = cuts[k];
+        if (k + 1 < cuts.size() && (double)cuts[k + 1] - ideal < ideal - (double)cuts[k]) best = cuts[k + 1];
+        if (std::fabs((double)best - ideal) > share) best = (int64_t)(ideal + 0.5);
+        best = std::max<int64_t>(best, gtab.back());
+        gtab.push_back((int32_t)std::min<int64_t>(best, sg.W32));
+      }
+      gtab.push_back(sg.W32);
     }
     sg.off64 = off64;
     sg.off32 = off32;
@@ -469,6 +497,8 @@ static int plan_create_impl(const hmx_matrix_desc* d, int device, const hmx_plan
   if ((rc = up(d_zs, zscale))) return rc;
   int32_t* d_perm = p->alloc<int32_t>(perm32.size());
   if ((rc = up(d_perm, perm32))) return rc;
+  int32_t* d_gtab = p->alloc<int32_t>(std::max<size_t>(gtab.size(), 1));
+  if ((rc = up(d_gtab, gtab))) return rc;
   double* d_z = p->alloc<double>((size_t)std::max<int64_t>(Z, 1));
   double* d_part = p->alloc<double>((size_t)std::max<int64_t>(part_len, 1));
   uint32_t* d_cnt = p->alloc<uint32_t>((size_t)std::max<int32_t>(n_red, 1));
@@ -493,6 +523,7 @@ static int plan_create_impl(const hmx_matrix_desc* d, int device, const hmx_plan
   dp.part = d_part;
   dp.red_count = d_cnt;
   dp.perm = d_perm;
+  dp.gtab = d_gtab;
   dp.run_block = d_rb;
 
   // per-matvec buffers

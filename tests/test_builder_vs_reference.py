@@ -1,0 +1,51 @@
+"""This repo's host builder (csrc/hbuild.cpp) against the reference's build
+of BASELINE config 1 (golden/config1): identical mesh, permutation, block
+partition and ACA ranks; payload bytes equal per scheme; and (through the
+oracle) matvec outputs equal to the reference's to ACA-rounding accuracy."""
+
+import numpy as np
+import pytest
+
+from golden_util import FP64_ONLY, SCHEMES, config1_hmatrix, load
+
+
+@pytest.fixture(scope="module")
+def cfg1():
+    arr, meta = load("config1")
+    mesh, h = config1_hmatrix()
+    return arr, meta, mesh, h
+
+
+def test_mesh_and_partition_identical(cfg1):
+    arr, _, mesh, h = cfg1
+    assert np.array_equal(mesh.centroids, arr["centroids"])
+    assert np.array_equal(mesh.areas, arr["areas"])
+    assert np.array_equal(h.permutation, arr["perm"])
+    assert np.array_equal(h.partition.table, arr["table"])
+
+
+def test_ranks_identical(cfg1):
+    arr, _, _, h = cfg1
+    assert np.array_equal(h.packed.kinds, arr["kinds"])
+    assert np.array_equal(h.packed.ranks, arr["ranks"])
+
+
+@pytest.mark.parametrize("scheme", SCHEMES)
+def test_payload_bytes_and_matvec(hx, orc, cfg1, scheme):
+    arr, _, _, h = cfg1
+    sh = hx.prepare_scheme(h, scheme)
+    assert sh.payload_bytes == int(arr[f"bytes/{scheme}"])
+    y = orc.matvec(sh, arr["x"])
+    ref = arr[f"y/{scheme}"]
+    # FP64 factors agree to a few ulps (BLAS order inside ACA); after an FP32
+    # cast that can flip one rounding, hence the FP32-level bound there
+    tol = 1e-10 if scheme in FP64_ONLY else 1e-6
+    assert np.max(np.abs(y - ref)) <= tol * np.max(np.abs(ref))
+
+
+def test_builder_thread_count_independent(hx):
+    mesh = hx.jittered_sphere_mesh(2, seed=7)
+    a = hx.build_hmatrix(mesh, aca_tol=1e-5, threads=1)
+    b = hx.build_hmatrix(mesh, aca_tol=1e-5, threads=4)
+    assert np.array_equal(a.packed.data, b.packed.data)
+    assert np.array_equal(a.packed.ranks, b.packed.ranks)
