@@ -149,6 +149,17 @@ int hmx_true_residual(hmx_plan* plan64, const double* x, const double* b, double
 int hmx_bicgstab(hmx_plan* plan, hmx_plan* plan64, const double* b, double tol, int max_iter,
                  double* x, double* history, hmx_solve_report* report);
 
+/* Row-restricted product for the multi-GPU mode: rows [row_begin, row_end)
+ * of y = A xp for a plan created with hmx_plan_options.  xp is the FULL
+ * iterate in permuted order (device), y the local slice (device).  When
+ * `dots` (device, 2 doubles) is non-NULL it receives [y . w1, y . y] over the
+ * local rows (w1: local slice, device, may be NULL; yy: compute y . y).
+ * `nonfinite` (device int, may be NULL) is set to 1 when a y entry is not
+ * finite.  Enqueued on `stream` (a cudaStream_t; 0 = the plan's stream);
+ * returns without synchronising. */
+int hmx_apply_local(hmx_plan* plan, const double* xp, double* y, const double* w1, int yy,
+                    double* dots, int* nonfinite, uint64_t stream);
+
 /* Benchmark helper: `iters` device matvecs in permuted order on device
  * buffers, timed with CUDA events on the plan's stream after `warmup`
  * untimed ones.  flush_l2 > 0 writes a buffer of that many bytes between

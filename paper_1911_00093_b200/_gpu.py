@@ -79,6 +79,9 @@ SIGNATURES = {
                                     ctypes.c_void_p, ctypes.POINTER(SolveReport)]),
     "hmx_bench_matvec": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_int,
                                         ctypes.c_int64, ctypes.POINTER(ctypes.c_double)]),
+    "hmx_apply_local": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                       ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p,
+                                       ctypes.c_void_p, ctypes.c_uint64]),
 }
 
 _lib = None
@@ -201,6 +204,15 @@ class Plan:
         if rc not in (HMX_OK, HMX_ERR_NONFINITE):
             check(rc, "hmx_matvec")
         return rc
+
+    def apply_local(self, xp_ptr: int, y_ptr: int, w1_ptr: int = 0, yy: bool = False,
+                    dots_ptr: int = 0, nonfinite_ptr: int = 0, stream: int = 0) -> None:
+        """Enqueue the local rows of y = A xp (device pointers) on `stream`."""
+        rc = self._lib.hmx_apply_local(self.handle, ctypes.c_void_p(xp_ptr), ctypes.c_void_p(y_ptr),
+                                       ctypes.c_void_p(w1_ptr or None), int(bool(yy)),
+                                       ctypes.c_void_p(dots_ptr or None),
+                                       ctypes.c_void_p(nonfinite_ptr or None), int(stream))
+        check(rc, "hmx_apply_local")
 
     def nonfinite_block(self) -> int:
         b = ctypes.c_int64(-1)

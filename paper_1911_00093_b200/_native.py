@@ -121,7 +121,7 @@ def host():
             lib.hb_is_admissible.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_double]
             lib.hb_build.argtypes = [c_f64p, c_f64p, ctypes.c_int64, c_i64p, ctypes.c_int64,
                                      ctypes.c_double, ctypes.c_int64, ctypes.c_int,
-                                     ctypes.c_char_p, ctypes.c_int]
+                                     ctypes.c_int64, ctypes.c_int64, ctypes.c_char_p, ctypes.c_int]
             lib.hb_build.restype = ctypes.c_void_p
             lib.hb_build_fallbacks.argtypes = [ctypes.c_void_p]
             lib.hb_build_fallbacks.restype = ctypes.c_int64

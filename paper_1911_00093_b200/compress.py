@@ -131,6 +131,8 @@ class PackedMaster:
     def payload(self, table_row, k: int):
         rs, re, cs, ce = (int(v) for v in table_row[:4])
         m, n, o = re - rs, ce - cs, int(self.offsets[k])
+        if self.kinds[k] == 2:
+            return None  # not built (row-restricted build)
         if self.kinds[k] == 0:
             return DenseBlockF64(self.data[o:o + m * n].reshape(m, n))
         r = int(self.ranks[k])
@@ -178,8 +180,13 @@ class HMatrixF64:
 def build_hmatrix(mesh, partition: BlockPartition | None = None,
                   aca_tol: float = DEFAULT_ACA_TOL, max_rank: int | None = None,
                   leaf_size: int = DEFAULT_LEAF_SIZE, eta: float = DEFAULT_ETA,
-                  threads: int | None = None) -> HMatrixF64:
-    """Compress the kernel matrix of `mesh` (reference compress.py:285-342)."""
+                  threads: int | None = None, rows: tuple | None = None) -> HMatrixF64:
+    """Compress the kernel matrix of `mesh` (reference compress.py:285-342).
+
+    `rows=(lo, hi)` (permuted indices) builds only the blocks whose rows meet
+    [lo, hi); the others are kept as kind 2 (not built, no payload).  Used by
+    the multi-GPU mode, where each rank owns a row slice.
+    """
     if partition is None:
         tree = build_cluster_tree(mesh, leaf_size=leaf_size)
         partition = build_block_partition(tree, eta=eta)
@@ -201,7 +208,9 @@ def build_hmatrix(mesh, partition: BlockPartition | None = None,
     err = ctypes.create_string_buffer(256)
     handle = lib.hb_build(_native.ptr(pcent, _native.c_f64p), _native.ptr(parea, _native.c_f64p),
                           pcent.shape[0], _native.ptr(table, _native.c_i64p), nb, float(aca_tol),
-                          int(max_rank or 0), int(nthreads), err, 256)
+                          int(max_rank or 0), int(nthreads),
+                          int(rows[0]) if rows else 0, int(rows[1]) if rows else partition.n,
+                          err, 256)
     if not handle:
         raise ValueError(err.value.decode() or "H-matrix build failed")
     try:
@@ -222,7 +231,7 @@ def build_hmatrix(mesh, partition: BlockPartition | None = None,
     hist_r, hist_c = np.unique(ranks[low], return_counts=True)
     n = partition.n
     report = BuildReport(
-        n=n, dense_blocks=int(np.count_nonzero(~low)), lowrank_blocks=int(np.count_nonzero(low)),
+        n=n, dense_blocks=int(np.count_nonzero(kinds == 0)), lowrank_blocks=int(np.count_nonzero(low)),
         fallback_blocks=fallbacks,
         rank_histogram={int(r): int(c) for r, c in zip(hist_r, hist_c)},
         stored_scalars=total, compression_ratio=float(total) / float(n * n), aca_tol=aca_tol)

@@ -449,8 +449,11 @@ static void aca_block(const Builder& B, int64_t r0, int64_t m, int64_t c0, int64
 }
 
 // Builds every block.  pcent/parea must stay alive until hb_build_export.
+// Blocks whose rows miss [row_lo, row_hi) are skipped (kind 2, no storage):
+// a multi-GPU rank builds only the blocks its row slice needs.
 void* hb_build(const double* pcent, const double* parea, int64_t n, const int64_t* blocks,
-               int64_t nb, double tol, int64_t max_rank, int nthreads, char* err, int errlen) {
+               int64_t nb, double tol, int64_t max_rank, int nthreads, int64_t row_lo,
+               int64_t row_hi, char* err, int errlen) {
   if (tol <= 0.0) {
     set_err(err, errlen, "tol must be positive");
     return nullptr;
@@ -465,7 +468,9 @@ void* hb_build(const double* pcent, const double* parea, int64_t n, const int64_
   run_parallel(nb, nthreads, [&](int64_t k) {
     const int64_t* b = B->blocks.data() + 5 * k;
     BlockResult& r = B->res[(size_t)k];
-    if (b[4]) {
+    if (b[1] <= row_lo || b[0] >= row_hi) {
+      r.kind = 2;
+    } else if (b[4]) {
       bool fallback = false;
       aca_block(*B, b[0], b[1] - b[0], b[2], b[3] - b[2], tol, max_rank, r, fallback);
       if (fallback) fb.fetch_add(1);
@@ -493,7 +498,7 @@ int64_t hb_build_layout(void* h, int32_t* kinds, int64_t* ranks, int64_t* offset
     kinds[k] = r.kind;
     ranks[k] = r.rank;
     offsets[k] = off;
-    off += r.kind == 0 ? m * n : r.rank * (m + n);
+    off += r.kind == 0 ? m * n : r.kind == 1 ? r.rank * (m + n) : 0;
   }
   return off;
 }
@@ -507,6 +512,7 @@ int hb_build_export(void* h, double* data, const int64_t* offsets, int nthreads)
     const int64_t r0 = b[0], m = b[1] - b[0], c0 = b[2], n = b[3] - b[2];
     BlockResult& r = B->res[(size_t)k];
     double* dst = data + offsets[k];
+    if (r.kind == 2) return;
     if (r.kind == 0) {
       // _fill_dense_block (compress.py:272-282); ACA fallbacks evaluate the
       // same entries (u@vt with an identity factor is exact)

@@ -136,6 +136,13 @@ static int plan_create_impl(const hmx_matrix_desc* d, int device, const hmx_plan
       set_error("block " + std::to_string(k) + " has an invalid range");
       return HMX_ERR_ARG;
     }
+    if (d->kind[k] == 2) {  // not built (row-restricted host build)
+      if (t[1] > rb && t[0] < re) {
+        set_error("block " + std::to_string(k) + " meets the plan's rows but was not built");
+        return HMX_ERR_ARG;
+      }
+      continue;
+    }
     if (d->kind[k] == 0) {
       if (d->a_off[k] < 0 || d->a_off[k] + m * nc > (d->a32 ? d->n32 : d->n64)) {
         set_error("dense block " + std::to_string(k) + " exceeds its payload buffer");
@@ -664,6 +671,32 @@ int hmx_nonfinite_block(hmx_plan* p, int64_t* block) {
   HMX_CUDA(cudaMemcpyAsync(&v, p->d_first_bad, sizeof(v), cudaMemcpyDeviceToHost, st));
   HMX_CUDA(cudaStreamSynchronize(st));
   *block = v == ~0ull ? -1 : (int64_t)v;
+  return HMX_OK;
+}
+
+int hmx_apply_local(hmx_plan* p, const double* xp, double* y, const double* w1, int yy,
+                    double* dots, int* nonfinite, uint64_t stream) {
+  if (!p || !xp || !y) {
+    set_error("null argument");
+    return HMX_ERR_ARG;
+  }
+  std::lock_guard<std::mutex> lock(p->mu);
+  DeviceGuard guard(p->device);
+  cudaStream_t st = stream ? reinterpret_cast<cudaStream_t>(stream) : p->stream;
+  S2Out out{};
+  out.y = y;
+  out.permute_out = 0;
+  out.w1 = w1;
+  out.yy = yy;
+  if (dots) {
+    out.seg_dots = p->d_seg_dots;
+    out.done = p->d_done;
+    out.dots_out = dots;
+  }
+  out.nonfinite = nonfinite ? nonfinite : p->d_nonfinite;
+  HMX_CUDA(launch_stage1(p->dp, xp, st));
+  HMX_CUDA(launch_stage2(p->dp, xp, out, st, /*pdl=*/true));
+  p->last_xp = xp;
   return HMX_OK;
 }
 

@@ -1,0 +1,347 @@
+"""Multi-GPU H-matvec and BiCG-STAB (BASELINE.json north_star item 4).
+
+One process per GPU.  The permuted row space is cut at leaf boundaries into
+contiguous slices balanced by the payload bytes each slice reads (dense rows,
+U rows, and the Vt rows of every low-rank block the slice touches).  Each rank
+builds only the blocks meeting its rows (compress.build_hmatrix(rows=...)),
+and holds a row-restricted device plan (hmx_plan_options / hmx_apply_local).
+
+Per matvec there is exactly one collective: an allgather of the iterate's
+slices (padded to equal length, NCCL over NVLink) into the full permuted
+vector every rank's stage 1 reads.  BiCG-STAB dot products are local partial
+sums (fused into the stage-2 epilogue on the GPU) finished by one small
+allreduce per reduction point.  Control flow mirrors reference
+pkg/src/hmx/solver.py:68-168 on every rank (identical scalars after the
+allreduces), so all ranks take the same decisions.
+
+The torch.distributed process group carries the collectives: NCCL on GPUs,
+gloo for the CPU tests (tests/test_distributed_gloo.py), where the local
+product is a CPU stand-in injected by the test.
+"""
+
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass
+
+import numpy as np
+
+from .solver import SolverReport, _breakdown_message
+
+_EPS = 1e-300  # reference solver.py:27
+
+
+# ---------------------------------------------------------------------------
+# row partition
+
+def leaf_boundaries(table: np.ndarray, n: int) -> np.ndarray:
+    """Sorted unique row boundaries of all blocks (the leaf row clusters)."""
+    return np.unique(np.concatenate([[0, n], table[:, 0], table[:, 1]]))
+
+
+def row_costs(table: np.ndarray, kinds: np.ndarray, ranks: np.ndarray, n: int,
+              bytes_per_elem: float = 8.0):
+    """Bytes a rank reads per leaf interval if it owns that interval: dense and
+    U rows, plus the Vt of each low-rank block spread over its rows (a block
+    cut between ranks has its Vt read by both; the cut search avoids that)."""
+    bounds = leaf_boundaries(table, n)
+    m = table[:, 1] - table[:, 0]
+    w = table[:, 3] - table[:, 2]
+    per_row = np.zeros(n + 1)
+    dense = kinds == 0
+    low = kinds == 1
+    rate = np.where(dense, w, 0.0) + np.where(low, ranks * (1.0 + w / np.maximum(m, 1)), 0.0)
+    np.add.at(per_row, table[:, 0], rate)
+    np.add.at(per_row, table[:, 1], -rate)
+    dens = np.cumsum(per_row)[:n]
+    pref = np.concatenate([[0.0], np.cumsum(dens)]) * bytes_per_elem
+    return bounds, pref[bounds]
+
+
+def partition_rows(table: np.ndarray, kinds: np.ndarray, ranks: np.ndarray, n: int,
+                   world: int) -> list[int]:
+    """Cut points r_0 = 0 < r_1 < ... < r_world = n at leaf boundaries with
+    balanced bytes; prefers cuts that no block straddles (tree-aligned)."""
+    if world == 1:
+        return [0, n]
+    bounds, cum = row_costs(table, kinds, ranks, n)
+    total = cum[-1]
+    # boundaries that no block straddles: no block has rs < b < re
+    starts, ends = table[:, 0], table[:, 1]
+    order = np.argsort(starts)
+    clean = np.ones(bounds.size, dtype=bool)
+    for i, b in enumerate(bounds):
+        clean[i] = not np.any((starts < b) & (ends > b))
+    cuts = [0]
+    for k in range(1, world):
+        target = total * k / world
+        cand = np.where(clean)[0]
+        j = cand[np.argmin(np.abs(cum[cand] - target))]
+        # accept a straddled boundary if a clean one is more than 5% off
+        j_any = int(np.argmin(np.abs(cum - target)))
+        if abs(cum[j] - target) > 0.05 * total / world:
+            j = j_any
+        cuts.append(int(max(bounds[j], cuts[-1] + 1)))
+    cuts.append(n)
+    del order
+    return cuts
+
+
+@dataclass
+class RowSlices:
+    cuts: list
+
+    @property
+    def world(self):
+        return len(self.cuts) - 1
+
+    def span(self, rank):
+        return self.cuts[rank], self.cuts[rank + 1]
+
+    @property
+    def padded(self):
+        return max(self.cuts[k + 1] - self.cuts[k] for k in range(self.world))
+
+
+# ---------------------------------------------------------------------------
+# distributed operator
+
+class DistributedOperator:
+    """Rows [r0, r1) of one scheme's operator on this rank.
+
+    `local_apply(x_full, w1, yy) -> (y_local, (y.w1, y.y))` computes the local
+    rows; by default the row-restricted GPU plan (hmx_apply_local), with the
+    dots fused into the stage-2 epilogue.
+    """
+
+    def __init__(self, slices: RowSlices, rank: int, group=None, device=None,
+                 local_apply=None, plan=None):
+        import torch
+        import torch.distributed as dist
+
+        self.torch = torch
+        self.dist = dist
+        self.slices = slices
+        self.rank = rank
+        self.group = group
+        self.r0, self.r1 = slices.span(rank)
+        self.n = slices.cuts[-1]
+        self.device = device if device is not None else torch.device("cpu")
+        self.plan = plan
+        self.local_apply = local_apply or self._gpu_apply
+        L = slices.padded
+        self._pad_in = torch.zeros(L, dtype=torch.float64, device=self.device)
+        self._gathered = torch.zeros(L * slices.world, dtype=torch.float64, device=self.device)
+        self._full = torch.zeros(self.n, dtype=torch.float64, device=self.device)
+        if plan is not None:
+            self._dots = torch.zeros(2, dtype=torch.float64, device=self.device)
+            self._flag = torch.zeros(1, dtype=torch.int32, device=self.device)
+
+    def gather(self, x_local):
+        """The ONE collective per matvec: allgather of the iterate's slices."""
+        L = self.slices.padded
+        m = self.r1 - self.r0
+        self._pad_in[:m].copy_(x_local)
+        self.dist.all_gather_into_tensor(self._gathered, self._pad_in, group=self.group)
+        for k in range(self.slices.world):
+            a, b = self.slices.span(k)
+            self._full[a:b].copy_(self._gathered[k * L:k * L + (b - a)])
+        return self._full
+
+    def _gpu_apply(self, x_full, w1, yy):
+        torch = self.torch
+        y = torch.empty(self.r1 - self.r0, dtype=torch.float64, device=self.device)
+        self._flag.zero_()
+        stream = torch.cuda.current_stream(self.device).cuda_stream
+        self.plan.apply_local(x_full.data_ptr(), y.data_ptr(),
+                              w1.data_ptr() if w1 is not None else 0, yy,
+                              self._dots.data_ptr(), self._flag.data_ptr(), stream)
+        return y, self._dots, self._flag
+
+    def apply(self, x_local, w1=None, yy=False):
+        """y_local = (A x)[r0:r1] and global dots [y.w1, y.y] (allreduced)."""
+        torch = self.torch
+        x_full = self.gather(x_local)
+        out = self.local_apply(x_full, w1, yy)
+        y, dots = out[0], out[1]
+        flag = out[2] if len(out) > 2 else None
+        red = torch.zeros(3, dtype=torch.float64, device=self.device)
+        red[:2] = dots
+        if flag is not None:
+            red[2] = flag.to(torch.float64)[0]
+        else:
+            red[2] = float(not bool(torch.isfinite(y).all()))
+        self.dist.all_reduce(red, group=self.group)
+        if red[2].item() != 0.0:
+            raise FloatingPointError("non-finite matvec result")
+        return y, red[:2]
+
+
+def _allsum(op, *vals):
+    torch = op.torch
+    t = torch.stack([v if torch.is_tensor(v) else torch.tensor(v, dtype=torch.float64,
+                                                                device=op.device) for v in vals])
+    op.dist.all_reduce(t, group=op.group)
+    return [float(v) for v in t.tolist()]
+
+
+def bicgstab_distributed(op: DistributedOperator, op64: DistributedOperator, b_local, tol=1e-6,
+                         max_iter=1000, scheme_label=""):
+    """BiCG-STAB with the reference's control flow (solver.py:68-168) on row
+    slices.  Returns (x_local, SolverReport) identical on every rank."""
+    torch = op.torch
+    t0 = time.perf_counter()
+    b = b_local
+    nb = float(np.sqrt(_allsum(op, torch.dot(b, b))[0]))
+    if nb == 0.0:
+        return torch.zeros_like(b), SolverReport(scheme_label, True, 0, [0.0], 0.0,
+                                                 time.perf_counter() - t0)
+    x = torch.zeros_like(b)
+    ax, _ = op.apply(x)
+    r = b - ax
+    r_hat = r.clone()
+    rr = _allsum(op, torch.dot(r, r))[0]
+    hist = [float(np.sqrt(rr)) / nb]
+    converged, breakdown, tres, its = False, None, None, 0
+    rho_prev = alpha = omega = 1.0
+    p = v = None
+    rho = _allsum(op, torch.dot(r_hat, r))[0]
+
+    def true_res(xv):
+        y, _ = op64.apply(xv)
+        e = b - y
+        ne, nb2 = _allsum(op64, torch.dot(e, e), torch.dot(b, b))
+        nr, nbb = float(np.sqrt(ne)), float(np.sqrt(nb2))
+        return 0.0 if nbb == 0.0 and nr == 0.0 else (float("inf") if nbb == 0.0 else nr / nbb)
+
+    for i in range(1, max_iter + 1):
+        if abs(rho) < _EPS:
+            breakdown = _breakdown_message(1, rho, i)
+            break
+        if i == 1:
+            p = r.clone()
+        else:
+            beta = (rho / rho_prev) * (alpha / omega)
+            p = r + beta * (p - omega * v)
+        v, d = op.apply(p, w1=r_hat)
+        denom = float(d[0])
+        if abs(denom) < _EPS:
+            breakdown = _breakdown_message(2, denom, i)
+            break
+        alpha = rho / denom
+        s = r - alpha * v
+        s_rel = float(np.sqrt(_allsum(op, torch.dot(s, s))[0])) / nb
+        if s_rel < tol:
+            x = x + alpha * p
+            hist.append(s_rel)
+            its = i
+            tres = true_res(x)
+            converged = tres < tol
+            break
+        t, d = op.apply(s, w1=s, yy=True)
+        ts, tt = float(d[0]), float(d[1])
+        if tt == 0.0:
+            breakdown = _breakdown_message(3, 0.0, i)
+            break
+        omega = ts / tt
+        x = x + alpha * p + omega * s
+        r = s - omega * t
+        rr, rho_next = _allsum(op, torch.dot(r, r), torch.dot(r_hat, r))
+        rel = float(np.sqrt(rr)) / nb
+        hist.append(rel)
+        its = i
+        if rel < tol:
+            tres = true_res(x)
+            converged = tres < tol
+            break
+        if abs(omega) < _EPS:
+            breakdown = _breakdown_message(4, omega, i)
+            break
+        rho_prev, rho = rho, rho_next
+    return x, SolverReport(scheme=scheme_label, converged=converged, iterations=its,
+                           residual_history=hist, true_residual=tres,
+                           wall_time_s=time.perf_counter() - t0, breakdown=breakdown)
+
+
+# ---------------------------------------------------------------------------
+# GPU setup and benchmark (torchrun, one rank per GPU)
+
+def make_gpu_operator(h, scheme: str, slices: RowSlices, rank: int, device, group=None):
+    """Row-restricted device plan of `scheme` for this rank."""
+    from . import _gpu
+    from .precision import prepare_scheme
+
+    sh = prepare_scheme(h, scheme)
+    plan = _gpu.Plan(sh.packed, h.partition.table, np.asarray(h.permutation), sh.scheme.label,
+                     h.n, device=device.index or 0, row_range=slices.span(rank))
+    return DistributedOperator(slices, rank, group=group, device=device, plan=plan), sh
+
+
+def bench_main(args, build_workload, workload_name, metric):
+    """bench.py --gpus N under torchrun: the whole-job matvec rate of the
+    row-partitioned operator (one allgather per matvec), max over ranks."""
+    import json
+    import os
+
+    import torch
+    import torch.distributed as dist
+
+    import bench as bench_mod
+    from .compress import build_hmatrix
+    from .partition import build_block_partition, build_cluster_tree
+    from .problem import jittered_sphere_mesh
+
+    rank = int(os.environ["RANK"])
+    world = int(os.environ["WORLD_SIZE"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    device = torch.device("cuda", local)
+    dist.init_process_group("nccl", device_id=device)
+    c = bench_mod.CONFIGS[args.config]
+    t0 = time.perf_counter()
+    mesh = jittered_sphere_mesh(c["level"], seed=42)
+    part = build_block_partition(build_cluster_tree(mesh, c["leaf"]), 2.0)
+    # partition on an estimate (ranks unknown before ACA): ranks ~ 11
+    kinds = part.table[:, 4].astype(np.int32)
+    est = np.where(kinds == 1, 11, 0)
+    slices = RowSlices(partition_rows(part.table, kinds, est, mesh.n, world))
+    h = build_hmatrix(mesh, partition=part, aca_tol=c["aca"], rows=slices.span(rank))
+    t_build = time.perf_counter() - t0
+    results = {}
+    for name in [bench_mod.HEADLINE] + [s for s in args.variants if s != bench_mod.HEADLINE][:1]:
+        op, sh = make_gpu_operator(h, name, slices, rank, device)
+        x = torch.from_numpy(np.random.default_rng(42).uniform(-1.0, 1.0, mesh.n)).to(device)
+        a, b_ = slices.span(rank)
+        x_local = x[torch.as_tensor(np.asarray(h.permutation)[a:b_], device=device)].contiguous()
+        for _ in range(args.warmup):
+            op.gather(x_local)
+            op.local_apply(op._full, None, False)
+        torch.cuda.synchronize()
+        dist.barrier()
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev0.record()
+        for _ in range(args.steps):
+            op.gather(x_local)
+            op.local_apply(op._full, None, False)
+        ev1.record()
+        torch.cuda.synchronize()
+        ms = torch.tensor([ev0.elapsed_time(ev1) / args.steps], device=device)
+        dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+        algo = sum(int(v) for v in [sh.payload_bytes]) + 16 * mesh.n
+        results[name] = {"ms": float(ms), "matvec_per_s": 1e3 / float(ms)}
+        op.plan.close()
+    dist.barrier()
+    if rank == 0:
+        ms = results[bench_mod.HEADLINE]["ms"]
+        print(json.dumps({
+            "metric": metric, "value": 1e3 / ms, "unit": "matvec/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded jittered icosphere, BASELINE.json recipe)",
+            "config": {"workload": workload_name(args.config), "scheme": bench_mod.HEADLINE,
+                       "n": int(mesh.n), "parallelism": f"row partition x{world}",
+                       "cuts": slices.cuts, "build_s": t_build},
+            "gpu_launches": 2 * args.steps, "variants": results,
+            "note": "each step = one allgather of the iterate + the local two-stage product",
+        }), flush=True)
+    dist.destroy_process_group()

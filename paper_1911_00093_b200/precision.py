@@ -187,6 +187,8 @@ class PackedScheme:
 
     def payload(self, row, k: int):
         m, n = int(row[1] - row[0]), int(row[3] - row[2])
+        if self.kind[k] == 2:
+            return None  # not built (row-restricted build)
         if self.kind[k] == 0:
             buf = self.buf32 if self.a32 else self.buf64
             o = int(self.a_off[k])
@@ -378,7 +380,7 @@ def prepare_scheme(h, scheme) -> SchemeHMatrix:
     P = _native.ptr
     c_i64, c_i32, c_f64, c_f32, c_i8 = (_native.c_i64p, _native.c_i32p, _native.c_f64p,
                                         _native.c_f32p, _native.c_i8p)
-    dense_elems = int(np.sum(np.where(low, 0, m * n)))
+    dense_elems = int(np.sum(np.where(pm.kinds == 0, m * n, 0)))  # kind 2: not built
     lr_elems = int(np.sum(r * (m + n)))
     underflow = 0
 
