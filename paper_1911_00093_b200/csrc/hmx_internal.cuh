@@ -61,7 +61,8 @@ enum F32Mode : int { F32_ALL64 = 0, F32_ALL32 = 1, F32_MIXED = 2 };
 // Stage-1 epilogue per pipe (z = op(sum)).
 enum ZEpi : int { Z_NONE = 0, Z_ROUND32 = 1, Z_SCALE = 2 };
 
-constexpr int kSegRows = 64;      // max rows per segment
+constexpr int kSegRows = 64;      // max rows per stage-2 segment (leaf rows)
+constexpr int kS1Rows = 256;      // max rank rows per stage-1 segment
 constexpr int kSegThreads = 256;  // CTA size
 constexpr int kSegWMax = 2048;    // columns of g staged in shared memory per tile
 

@@ -21,25 +21,58 @@ enum Out : int { OUT_Y = 0, OUT_Z = 1 };
 // Stage a tile [tc0, tc0+tw) of one part's source vector g (x segments and z
 // vectors, in item order) into shared memory, plus FP32-part item flags
 // (bit 0: first column of an item, bit 1: item accumulates in FP32).
+// A single run (every stage-1 segment) is a contiguous copy.  Otherwise the
+// runs are expanded into a per-column source index in shared memory first,
+// so every column's load is independent (no dependent run lookups).
+constexpr int kRunsSmem = 512;
+constexpr int32_t kTagZ = 1 << 30, kTagRound = 1 << 29, kIdxMask = kTagRound - 1;
 template <bool FLAGS>
 __device__ __forceinline__ void gather_g(const DevPlan& P, const Run* __restrict__ runs, int nrun,
                                          int tc0, int tw, const double* __restrict__ x,
-                                         double* gs, uint8_t* fl) {
-  for (int c = threadIdx.x; c < tw; c += kSegThreads) {
-    const int col = tc0 + c;
-    int lo = 0, hi = nrun - 1;  // last run with col0 <= col
-    while (lo < hi) {
-      const int mid = (lo + hi + 1) >> 1;
-      if (__ldg(&runs[mid].col0) <= col) lo = mid;
-      else hi = mid - 1;
+                                         double* gs, uint8_t* fl, int32_t* sidx) {
+  if (nrun == 1) {
+    const Run r = runs[0];
+    const double* src = ((r.flags & RUN_Z) ? P.z : x) + r.src + (tc0 - r.col0);
+    const bool rnd = (r.flags & RUN_ROUND) != 0;
+    const uint8_t f32 = (r.flags & RUN_ACC32) ? 2 : 0;
+    for (int c = threadIdx.x; c < tw; c += kSegThreads) {
+      const double g = src[c];
+      gs[c] = rnd ? (double)(float)g : g;
+      if constexpr (FLAGS) fl[c] = (uint8_t)((tc0 + c == r.col0 ? 1 : 0) | f32);
     }
-    const Run r = runs[lo];
-    const int off = col - r.col0;
-    const double* src = (r.flags & RUN_Z) ? P.z : x;
-    double g = src[r.src + off];
-    if (r.flags & RUN_ROUND) g = (double)(float)g;
-    gs[c] = g;
-    if constexpr (FLAGS) fl[c] = (uint8_t)((off == 0 ? 1 : 0) | ((r.flags & RUN_ACC32) ? 2 : 0));
+    return;
+  }
+  // runs whose columns meet the tile: scatter their source indices
+  for (int j = threadIdx.x; j < nrun; j += kSegThreads) {
+    const Run r = runs[j];
+    const int lo = max(r.col0, tc0), hi = min(r.col0 + r.width, tc0 + tw);
+    const int32_t tag = ((r.flags & RUN_Z) ? kTagZ : 0) | ((r.flags & RUN_ROUND) ? kTagRound : 0);
+    const uint8_t f32 = (r.flags & RUN_ACC32) ? 2 : 0;
+    for (int col = lo; col < hi; ++col) {
+      sidx[col - tc0] = (r.src + (col - r.col0)) | tag;
+      if constexpr (FLAGS) fl[col - tc0] = (uint8_t)((col == r.col0 ? 1 : 0) | f32);
+    }
+  }
+  __syncthreads();
+  const double* __restrict__ z = P.z;
+  for (int c0 = threadIdx.x; c0 < tw; c0 += 4 * kSegThreads) {
+    int32_t id[4];
+    double v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int c = c0 + u * kSegThreads;
+      id[u] = c < tw ? sidx[c] : 0;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int c = c0 + u * kSegThreads;
+      v[u] = c < tw ? ((id[u] & kTagZ) ? z : x)[id[u] & kIdxMask] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int c = c0 + u * kSegThreads;
+      if (c < tw) gs[c] = (id[u] & kTagRound) ? (double)(float)v[u] : v[u];
+    }
   }
 }
 
@@ -55,6 +88,7 @@ __global__ void __launch_bounds__(kSegThreads, 3) seg_kernel(DevPlan P, const Se
                                                           const double* __restrict__ x, S2Out out) {
   __shared__ double gs[kSegWMax];
   __shared__ uint8_t fl[kSegWMax];
+  __shared__ int32_t sidx[kSegWMax];
   __shared__ double red64[2 * kSegThreads];
   __shared__ double red32[4 * kSegThreads];
   __shared__ double wred[2][kSegThreads / 32];
@@ -88,7 +122,7 @@ __global__ void __launch_bounds__(kSegThreads, 3) seg_kernel(DevPlan P, const Se
     }
     if (OUT == OUT_Y && tc0 == 0) asm volatile("griddepcontrol.wait;" ::: "memory");
     __syncthreads();
-    gather_g<false>(P, P.runs + sg.run0, sg.nrun64, tc0, tw, x, gs, fl);
+    gather_g<false>(P, P.runs + sg.run0, sg.nrun64, tc0, tw, x, gs, fl, sidx);
     __syncthreads();
     if (pre) {
 #pragma unroll
@@ -170,7 +204,8 @@ __global__ void __launch_bounds__(kSegThreads, 3) seg_kernel(DevPlan P, const Se
     }
     if (OUT == OUT_Y && tc0 == 0 && sg.W64 == 0) asm volatile("griddepcontrol.wait;" ::: "memory");
     __syncthreads();
-    gather_g<F32MODE != F32_ALL64>(P, P.runs + sg.run0 + sg.nrun64, sg.nrun32, tc0, tw, x, gs, fl);
+    gather_g<F32MODE != F32_ALL64>(P, P.runs + sg.run0 + sg.nrun64, sg.nrun32, tc0, tw, x, gs, fl,
+                                   sidx);
     __syncthreads();
     if (pre) {
 #pragma unroll

@@ -249,7 +249,7 @@ static int plan_create_impl(const hmx_matrix_desc* d, int device, const hmx_plan
     const bool is32 = cls == 2 || d->hi32;
     const int64_t es = is32 ? 4 : 8;
     const int64_t rg = (int64_t)rows.size();
-    const int64_t pieces = (rg + kSegRows - 1) / kSegRows;
+    const int64_t pieces = (rg + kS1Rows - 1) / kS1Rows;
     for (int64_t pc = 0; pc < pieces; ++pc) {
       const int64_t r0 = rg * pc / pieces, r1 = rg * (pc + 1) / pieces, R = r1 - r0;
       const int64_t rp = round_up(R, is32 ? 4 : 2);
