@@ -362,29 +362,35 @@ static int plan_create_impl(const hmx_matrix_desc* d, int device, const hmx_plan
         sg.nrun32 = (int32_t)lst.size();
       }
     }
-    // item-aligned group boundaries for FP32-accumulated parts: greedy cut
-    // at the item boundary nearest each uniform boundary; an item wider than
-    // two group shares may still be cut (its FP32 chains then span >= W/G
-    // columns each)
+    // item-aligned group boundaries for FP32-accumulated parts: a group
+    // boundary never falls strictly inside an FP32-accumulated item
+    // (RUN_ACC32), so each (row, block) is one FP32 chain as in the
+    // reference's FP32 GEMV; FP64-accumulated items may be cut anywhere.
+    // Targets are re-spread over the remaining groups after every cut.
     sg.gtab = -1;
     if (sg.W32 > 0 && sg.W32 <= kSegWMax && (dense_single || u_acc32)) {
       const int64_t tpg = round_up(sg.R, 4) / 4, G = kSegThreads / tpg;
-      std::vector<int64_t> cuts;  // item start columns
-      for (int32_t j = 0; j < sg.nrun32; ++j) cuts.push_back(runs[(size_t)(sg.run0 + sg.nrun64 + j)].col0);
-      cuts.push_back(sg.W32);
+      struct Span { int64_t a, b; };
+      std::vector<Span> acc;  // FP32-accumulated items of the part
+      for (int32_t j = 0; j < sg.nrun32; ++j) {
+        const Run& r = runs[(size_t)(sg.run0 + sg.nrun64 + j)];
+        if (r.flags & RUN_ACC32) acc.push_back({r.col0, (int64_t)r.col0 + r.width});
+      }
       sg.gtab = (int32_t)gtab.size();
       gtab.push_back(0);
-      const double share = (double)sg.W32 / (double)G;
+      int64_t prev = 0;
       size_t k = 0;
       for (int64_t q = 1; q < G; ++q) {
-        const double ideal = share * (double)q;
-        while (k + 1 < cuts.size() && (double)cuts[k + 1] <= ideal) ++k;
-        // nearest item boundary around `ideal`
-        int64_t best = cuts[k];
-        if (k + 1 < cuts.size() && (double)cuts[k + 1] - ideal < ideal - (double)cuts[k]) best = cuts[k + 1];
-        if (std::fabs((double)best - ideal) > share) best = (int64_t)(ideal + 0.5);
-        best = std::max<int64_t>(best, gtab.back());
-        gtab.push_back((int32_t)std::min<int64_t>(best, sg.W32));
+        const double share = (double)(sg.W32 - prev) / (double)(G - q + 1);
+        int64_t cut = (int64_t)std::llround((double)prev + share);
+        while (k < acc.size() && acc[k].b <= cut) ++k;
+        if (k < acc.size() && acc[k].a < cut && cut < acc[k].b) {
+          // inside an FP32 item: move to its nearer end
+          cut = (cut - acc[k].a <= acc[k].b - cut) ? acc[k].a : acc[k].b;
+        }
+        cut = std::min<int64_t>(std::max(cut, prev), sg.W32);
+        gtab.push_back((int32_t)cut);
+        prev = cut;
       }
       gtab.push_back(sg.W32);
     }
