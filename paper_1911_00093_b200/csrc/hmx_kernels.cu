@@ -84,7 +84,7 @@ __device__ __forceinline__ double z_epilogue(const DevPlan& P, double s, int zi)
 
 // One CTA = one segment: rows [row0, row0+R) of a column-major item stream.
 template <int F32MODE, int OUT>
-__global__ void __launch_bounds__(kSegThreads, 3) seg_kernel(DevPlan P, const Seg* __restrict__ segs,
+__global__ void __launch_bounds__(kSegThreads, 4) seg_kernel(DevPlan P, const Seg* __restrict__ segs,
                                                           const double* __restrict__ x, S2Out out) {
   __shared__ double gs[kSegWMax];
   __shared__ uint8_t fl[kSegWMax];
