@@ -99,6 +99,7 @@ struct S2Out {
   uint32_t* done;       // last-CTA counter
   double* dots_out;     // final [sum y*w1, sum y*y] (fixed-order reduction)
   int* nonfinite;       // set to 1 when any y entry is not finite
+  const int* skip;      // if non-null and *skip != 0 the launch is a no-op (solver guards)
 };
 
 // ---- device helpers ------------------------------------------------------------

@@ -94,6 +94,7 @@ __global__ void __launch_bounds__(kSegThreads, 4) seg_kernel(DevPlan P, const Se
   __shared__ double wred[2][kSegThreads / 32];
   __shared__ unsigned ticket;
 
+  if (out.skip != nullptr && *out.skip != 0) return;  // guarded launch (solver)
   const Seg sg = segs[blockIdx.x];
   const int R = sg.R;
   const int tid = threadIdx.x;
@@ -410,9 +411,10 @@ static cudaError_t launch_seg(const DevPlan& P, const Seg* segs, int nseg, const
   return cudaLaunchKernelEx(&cfg, seg_kernel<M, O>, P, segs, x, out);
 }
 
-cudaError_t launch_stage1(const DevPlan& P, const double* x, cudaStream_t st) {
+cudaError_t launch_stage1(const DevPlan& P, const double* x, cudaStream_t st, const int* skip) {
   if (P.n_seg1 == 0) return cudaSuccess;
   S2Out none{};
+  none.skip = skip;
   switch (P.f32mode1) {
     case F32_ALL32: return launch_seg<F32_ALL32, OUT_Z>(P, P.seg1, P.n_seg1, x, none, st, false);
     default: return launch_seg<F32_ALL64, OUT_Z>(P, P.seg1, P.n_seg1, x, none, st, false);

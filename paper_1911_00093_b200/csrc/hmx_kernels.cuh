@@ -5,7 +5,8 @@
 
 namespace hmx {
 
-cudaError_t launch_stage1(const DevPlan& P, const double* x, cudaStream_t st);
+cudaError_t launch_stage1(const DevPlan& P, const double* x, cudaStream_t st,
+                          const int* skip = nullptr);
 cudaError_t launch_stage2(const DevPlan& P, const double* x, const S2Out& out, cudaStream_t st,
                           bool pdl);
 cudaError_t launch_gather_perm(const double* x, const int32_t* perm, double* xp, int n,

@@ -46,6 +46,9 @@ struct Workspace {
   int* flags = nullptr;    // non-finite flags of the solver's matvecs
   double* partials = nullptr;
   uint32_t* done = nullptr;
+  int* stop = nullptr;      // solver decision word [stop, reason, iteration, spare]
+  double* hist = nullptr;   // device residual history
+  int hist_cap = 0;
   int grid = 0;
 };
 

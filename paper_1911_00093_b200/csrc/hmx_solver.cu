@@ -1,16 +1,21 @@
 // BiCG-STAB on the device (reference pkg/src/hmx/solver.py:68-168).
 //
-// Control flow and scalar arithmetic are the reference's: the scalars alpha,
-// omega, beta are formed on the device with the same IEEE operations, the
-// breakdown / convergence decisions are taken on the host from the same
-// values, and vector updates keep the reference's operation order (no FMA
-// contraction in the axpy's: x = (x + alpha p) + omega s etc.).  Dots and
-// norms are deterministic two-level reductions (fixed grid, fixed order).
+// Control flow and scalar arithmetic are the reference's: alpha, omega and
+// beta are formed on the device with the same IEEE operations, vector
+// updates keep the reference's operation order (no FMA contraction in the
+// axpy's: x = (x + alpha p) + omega s etc.), dots and norms are deterministic
+// two-level reductions (fixed grid, fixed order).
 //
-// Per iteration: p-update, v = A p (fused r^.v), s-update (fused |s|^2)
-//   -> host sync #1 (denominator breakdown, early exit on |s|)
-//   t = A s (fused t.s, t.t), x/r-update (fused |r|^2, r^.r)
-//   -> host sync #2 (stabilisation breakdown, convergence, omega breakdown).
+// Speculative batched launch: every kernel of an iteration first reads a
+// device `stop` word and becomes a no-op once it is set.  The device itself
+// records each decision the reference takes, at the same point and with the
+// same values (rho breakdown, shadow-projection breakdown, early exit on |s|,
+// stabilisation breakdown, convergence of |r|, omega breakdown, non-finite
+// matvec), so the host can enqueue several iterations per synchronisation and
+// act on the recorded outcome afterwards (FP64 true-residual confirmation,
+// breakdown report).  Per iteration: p-update, v = A p (fused r^.v),
+// s-update (fused |s|^2), t = A s (fused t.s, t.t), x/r-update (fused |r|^2,
+// r^.r).
 #include <cmath>
 #include <mutex>
 
@@ -34,8 +39,24 @@ enum : int {
   SC_DV = 8,      // [r^.v, unused]
   SC_DT = 10,     // [t.s, t.t]
   SC_TMP = 12,    // [2 scratch]
+  SC_NB = 14,     // |b|
+  SC_BVAL = 15,   // value reported with a breakdown
   SC_N = 16
 };
+
+// stop word layout (int[4]): [stop, reason, iteration, spare]
+enum : int {
+  R_NONE = 0, R_RHO = 1, R_DENOM = 2, R_TT = 3, R_OMEGA = 4, R_SEXIT = 5, R_CONV = 6,
+  R_NONFINITE = 7
+};
+
+__device__ __forceinline__ void set_stop(int* stop, int reason, int it, double* sc, double val) {
+  stop[1] = reason;
+  stop[2] = it;
+  sc[SC_BVAL] = val;
+  __threadfence();
+  stop[0] = 1;
+}
 
 struct VecRed {
   double* partials;  // 2 per CTA
@@ -45,7 +66,7 @@ struct VecRed {
 
 // Deterministic two-level sum of (u, w) over the grid: per-CTA fixed-order
 // block reduction, then the last CTA to finish sums the CTA partials in order.
-__device__ __forceinline__ void grid_reduce2(double u, double w, const VecRed& R) {
+__device__ __forceinline__ bool grid_reduce2(double u, double w, const VecRed& R) {
   __shared__ double su[kVecThreads / 32], sw[kVecThreads / 32];
   __shared__ unsigned ticket;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -71,7 +92,7 @@ __device__ __forceinline__ void grid_reduce2(double u, double w, const VecRed& R
     ticket = atomicAdd(R.done, 1u);
   }
   __syncthreads();
-  if (ticket != gridDim.x - 1) return;
+  if (ticket != gridDim.x - 1) return false;
   __threadfence();
   double a = 0.0, b = 0.0;
   for (int i = threadIdx.x; i < (int)gridDim.x; i += kVecThreads) {
@@ -98,7 +119,9 @@ __device__ __forceinline__ void grid_reduce2(double u, double w, const VecRed& R
     R.out[0] = fa;
     R.out[1] = fb;
     *R.done = 0u;
+    return true;
   }
+  return false;
 }
 
 // (|u|^2, u.w) style reductions: out = [sum a*b, sum c*d]
@@ -129,29 +152,49 @@ __global__ void __launch_bounds__(kVecThreads) init_kernel(const double* b, cons
 }
 
 // p = r (first iteration) or p = r + beta (p - omega v),
-// beta = (rho / rho_prev) (alpha / omega)              (solver.py:116-120)
+// beta = (rho / rho_prev) (alpha / omega)   (solver.py:112-120); first checks
+// the rho breakdown of iteration `it` (solver.py:113-115)
 __global__ void __launch_bounds__(kVecThreads) p_update_kernel(const double* r, const double* v,
-                                                                double* p, int n, int first,
-                                                                const double* sc, int rho_slot,
-                                                                int prev_slot) {
+                                                                double* p, int n, int it,
+                                                                double* sc, int rho_slot,
+                                                                int prev_slot, int* stop) {
+  if (*(volatile int*)stop) return;
+  const double rho = sc[rho_slot];
+  if (fabs(rho) < kBreakdownEps) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) set_stop(stop, R_RHO, it, sc, rho);
+    return;
+  }
   double beta = 0.0, omega = 0.0;
-  if (!first) {
-    const double rho = sc[rho_slot], rho_prev = sc[prev_slot];
+  if (it > 1) {
+    const double rho_prev = sc[prev_slot];
     const double alpha = sc[SC_ALPHA];
     omega = sc[SC_OMEGA];
     beta = __dmul_rn(__ddiv_rn(rho, rho_prev), __ddiv_rn(alpha, omega));
   }
   for (int i = blockIdx.x * kVecThreads + threadIdx.x; i < n; i += gridDim.x * kVecThreads) {
-    if (first) p[i] = r[i];
+    if (it == 1) p[i] = r[i];
     else p[i] = __dadd_rn(r[i], __dmul_rn(beta, __dsub_rn(p[i], __dmul_rn(omega, v[i]))));
   }
 }
 
-// alpha = rho / (r^.v) ; s = r - alpha v ; out = [|s|^2]   (solver.py:126-129)
+// alpha = rho / (r^.v) ; s = r - alpha v ; |s|^2 ; early exit on |s|/|b| < tol
+// (solver.py:122-136)
 __global__ void __launch_bounds__(kVecThreads) s_update_kernel(const double* r, const double* v,
                                                                 double* s, int n, double* sc,
-                                                                int rho_slot, VecRed R) {
-  const double alpha = __ddiv_rn(sc[rho_slot], sc[SC_DV]);
+                                                                int rho_slot, VecRed R, int it,
+                                                                double tol, double* hist,
+                                                                int* stop, const int* nonfin) {
+  if (*(volatile int*)stop) return;
+  if (*nonfin) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) set_stop(stop, R_NONFINITE, it, sc, 0.0);
+    return;
+  }
+  const double denom = sc[SC_DV];
+  if (fabs(denom) < kBreakdownEps) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) set_stop(stop, R_DENOM, it, sc, denom);
+    return;
+  }
+  const double alpha = __ddiv_rn(sc[rho_slot], denom);
   if (blockIdx.x == 0 && threadIdx.x == 0) sc[SC_ALPHA] = alpha;
   double u = 0.0;
   for (int i = blockIdx.x * kVecThreads + threadIdx.x; i < n; i += gridDim.x * kVecThreads) {
@@ -159,7 +202,13 @@ __global__ void __launch_bounds__(kVecThreads) s_update_kernel(const double* r, 
     s[i] = si;
     u += si * si;
   }
-  grid_reduce2(u, 0.0, R);
+  if (grid_reduce2(u, 0.0, R)) {  // last CTA, thread 0: the reduced |s|^2
+    const double s_rel = __ddiv_rn(sqrt(R.out[0]), sc[SC_NB]);
+    if (s_rel < tol) {
+      hist[it] = s_rel;
+      set_stop(stop, R_SEXIT, it, sc, s_rel);
+    }
+  }
 }
 
 // x = x + alpha p (early exit on |s|, solver.py:131)
@@ -171,15 +220,24 @@ __global__ void __launch_bounds__(kVecThreads) x_alpha_p_kernel(double* x, const
 }
 
 // omega = (t.s)/(t.t); x = x + alpha p + omega s; r = s - omega t;
-// out = [|r|^2, r^.r] (solver.py:139-147).  No-op when t.t == 0 (breakdown).
+// |r|^2, r^.r (solver.py:139-158): records the history entry, the next rho,
+// convergence of |r| and the omega breakdown.
 __global__ void __launch_bounds__(kVecThreads) xr_update_kernel(double* x, double* r,
                                                                  const double* p, const double* s,
                                                                  const double* t,
                                                                  const double* rhat, int n,
-                                                                 double* sc, VecRed R) {
+                                                                 double* sc, VecRed R, int it,
+                                                                 double tol, double* hist,
+                                                                 int next_slot, int* stop,
+                                                                 const int* nonfin) {
+  if (*(volatile int*)stop) return;
+  if (*nonfin) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) set_stop(stop, R_NONFINITE, it, sc, 0.0);
+    return;
+  }
   const double tt = sc[SC_DT + 1];
   if (tt == 0.0) {
-    grid_reduce2(0.0, 0.0, R);
+    if (blockIdx.x == 0 && threadIdx.x == 0) set_stop(stop, R_TT, it, sc, 0.0);
     return;
   }
   const double omega = __ddiv_rn(sc[SC_DT], tt);
@@ -194,7 +252,13 @@ __global__ void __launch_bounds__(kVecThreads) xr_update_kernel(double* x, doubl
     u += ri * ri;
     w += rhat[i] * ri;
   }
-  grid_reduce2(u, w, R);
+  if (grid_reduce2(u, w, R)) {
+    const double rel = __ddiv_rn(sqrt(R.out[0]), sc[SC_NB]);
+    hist[it] = rel;
+    sc[next_slot] = R.out[1];  // rho of the next iteration
+    if (rel < tol) set_stop(stop, R_CONV, it, sc, rel);
+    else if (fabs(omega) < kBreakdownEps) set_stop(stop, R_OMEGA, it, sc, omega);
+  }
 }
 
 // out = [|b - y|^2, |b|^2]   (solver.py:60-62)
@@ -245,6 +309,7 @@ int alloc_ws(hmx_plan* p, Workspace& w, int64_t n, int grid) {
   }
   w.sc = p->alloc<double>(SC_N);
   w.flags = p->alloc<int>(4);
+  w.stop = p->alloc<int>(4);
   w.partials = p->alloc<double>((size_t)2 * grid);
   w.done = p->alloc<uint32_t>(1);
   if (!w.sc || !w.flags || !w.partials || !w.done) {
@@ -253,15 +318,16 @@ int alloc_ws(hmx_plan* p, Workspace& w, int64_t n, int grid) {
   }
   HMX_CUDA(cudaMemset(w.done, 0, sizeof(uint32_t)));
   HMX_CUDA(cudaMemset(w.sc, 0, SC_N * sizeof(double)));
-  HMX_CUDA(cudaMallocHost(&w.h_sc, (SC_N + 4) * sizeof(double)));
+  HMX_CUDA(cudaMallocHost(&w.h_sc, (SC_N + 8) * sizeof(double)));
   p->pinned.push_back(w.h_sc);
   return HMX_OK;
 }
 
 // y = A xp on stream st, fused dots into sc[slot..slot+1]
 int apply(hmx_plan* A, const Workspace& w, cudaStream_t st, const double* xp, double* y,
-          const double* w1, int yy, int slot, int* flag) {
+          const double* w1, int yy, int slot, int* flag, const int* skip = nullptr) {
   S2Out out{};
+  out.skip = skip;
   out.y = y;
   out.permute_out = 0;
   out.w1 = w1;
@@ -272,18 +338,22 @@ int apply(hmx_plan* A, const Workspace& w, cudaStream_t st, const double* xp, do
     out.dots_out = w.sc + slot;
   }
   out.nonfinite = flag;
-  HMX_CUDA(launch_stage1(A->dp, xp, st));
+  HMX_CUDA(launch_stage1(A->dp, xp, st, skip));
   HMX_CUDA(launch_stage2(A->dp, xp, out, st, /*pdl=*/true));
   A->last_xp = xp;
   return HMX_OK;
 }
 
+// scalars, non-finite flags and the stop word in one pinned mirror
 int sync_scalars(const SolveCtx& c) {
   HMX_CUDA(cudaMemcpyAsync(c.w.h_sc, c.w.sc, SC_N * sizeof(double), cudaMemcpyDeviceToHost, c.st));
   HMX_CUDA(cudaMemcpyAsync(c.w.h_sc + SC_N, c.w.flags, 4 * sizeof(int), cudaMemcpyDeviceToHost, c.st));
+  HMX_CUDA(cudaMemcpyAsync(c.w.h_sc + SC_N + 2, c.w.stop, 4 * sizeof(int), cudaMemcpyDeviceToHost, c.st));
   HMX_CUDA(cudaStreamSynchronize(c.st));
   return HMX_OK;
 }
+
+const int* host_stop(const SolveCtx& c) { return reinterpret_cast<const int*>(c.w.h_sc + SC_N + 2); }
 
 int flags_nonfinite(const SolveCtx& c) {
   const int* f = reinterpret_cast<const int*>(c.w.h_sc + SC_N);
@@ -418,54 +488,103 @@ int hmx_bicgstab(hmx_plan* A, hmx_plan* A64, const double* b, double tol, int ma
   }
 
   // x = 0 ; r = b - A x ; r_hat = r   (solver.py:99-102)
+  if (w.hist_cap < max_iter + 2) {
+    double* hd = A->alloc<double>((size_t)max_iter + 2);
+    if (!hd) {
+      set_error("cudaMalloc failed for the residual history");
+      return HMX_ERR_CUDA;
+    }
+    A->ws->hist = w.hist = hd;
+    A->ws->hist_cap = w.hist_cap = max_iter + 2;
+  }
   HMX_CUDA(cudaMemsetAsync(w.p, 0, n * sizeof(double), st));
+  HMX_CUDA(cudaMemsetAsync(w.stop, 0, 4 * sizeof(int), st));
   if ((rc = apply(A, w, st, w.p, w.t, nullptr, 0, 0, w.flags))) return rc;
   rep->matvecs++;
   init_kernel<<<c.grid, kVecThreads, 0, st>>>(w.b, w.t, w.r, w.rhat, w.x, n32, c.red(SC_RHO1));
   HMX_CUDA(cudaGetLastError());
+  // |b| for the device-side relative residuals
+  HMX_CUDA(cudaMemcpyAsync(w.sc + SC_NB, &nb, sizeof(double), cudaMemcpyHostToDevice, st));
   if ((rc = sync_scalars(c))) return rc;
   if (flags_nonfinite(c)) {
     set_error("non-finite matvec result");
     return finish(HMX_ERR_NONFINITE);
   }
-  // rho_1 = r^.r = |r|^2 ; it lives in ring slot (1 & 1) = SC_RHO1
-  double rho = w.h_sc[SC_RHO1];
-  history[hlen++] = std::sqrt(rho) / nb;
+  // rho_1 = r^.r = |r|^2 lives in ring slot (1 & 1) = SC_RHO1
+  history[hlen++] = std::sqrt(w.h_sc[SC_RHO1]) / nb;
 
+  // Enqueue iterations in batches; kernels after a recorded decision are
+  // no-ops, so over-enqueueing only costs launches.
   auto rho_slot = [](int i) { return (i & 1) ? SC_RHO1 : SC_RHO0; };
-  for (int i = 1; i <= max_iter; ++i) {
-    if (std::fabs(rho) < kBreakdownEps) {  // solver.py:113-115
-      rep->breakdown = 1;
-      rep->breakdown_value = rho;
-      rep->breakdown_iteration = i;
+  int done_through = 0;  // iterations enqueued
+  int batch = 2;
+  int reason = R_NONE, stop_it = 0;
+  while (done_through < max_iter) {
+    const int last = std::min(max_iter, done_through + batch);
+    for (int i = done_through + 1; i <= last; ++i) {
+      p_update_kernel<<<c.grid, kVecThreads, 0, st>>>(w.r, w.v, w.p, n32, i, w.sc, rho_slot(i),
+                                                        rho_slot(i - 1), w.stop);
+      if ((rc = apply(A, w, st, w.p, w.v, w.rhat, 0, SC_DV, w.flags, w.stop))) return rc;
+      s_update_kernel<<<c.grid, kVecThreads, 0, st>>>(w.r, w.v, w.s, n32, w.sc, rho_slot(i),
+                                                        c.red(SC_SS), i, tol, w.hist, w.stop,
+                                                        w.flags);
+      if ((rc = apply(A, w, st, w.s, w.t, w.s, 1, SC_DT, w.flags + 1, w.stop))) return rc;
+      xr_update_kernel<<<c.grid, kVecThreads, 0, st>>>(
+          w.x, w.r, w.p, w.s, w.t, w.rhat, n32, w.sc, VecRed{w.partials, w.done, w.sc + SC_TMP},
+          i, tol, w.hist, rho_slot(i + 1), w.stop, w.flags + 1);
+    }
+    HMX_CUDA(cudaGetLastError());
+    done_through = last;
+    if ((rc = sync_scalars(c))) return rc;
+    const int* sw = host_stop(c);
+    if (sw[0]) {
+      reason = sw[1];
+      stop_it = sw[2];
       break;
     }
-    p_update_kernel<<<c.grid, kVecThreads, 0, st>>>(w.r, w.v, w.p, n32, i == 1, w.sc, rho_slot(i),
-                                                      rho_slot(i - 1));
-    HMX_CUDA(cudaGetLastError());
-    if ((rc = apply(A, w, st, w.p, w.v, w.rhat, 0, SC_DV, w.flags))) return rc;
-    rep->matvecs++;
-    s_update_kernel<<<c.grid, kVecThreads, 0, st>>>(w.r, w.v, w.s, n32, w.sc, rho_slot(i),
-                                                      c.red(SC_SS));
-    HMX_CUDA(cudaGetLastError());
-    if ((rc = sync_scalars(c))) return rc;
-    if (flags_nonfinite(c)) {
+    batch = std::min(batch * 2, 16);
+  }
+  // iterations completed, matvecs actually run
+  int completed;
+  if (reason == R_NONE) completed = max_iter;
+  else if (reason == R_RHO || reason == R_DENOM || reason == R_TT || reason == R_NONFINITE)
+    completed = stop_it - 1;
+  else completed = stop_it;  // R_SEXIT, R_CONV, R_OMEGA complete their iteration
+  rep->iterations = completed;
+  rep->matvecs += 2 * completed;
+  if (reason == R_RHO || reason == R_DENOM) rep->matvecs += (reason == R_DENOM) ? 1 : 0;
+  if (reason == R_SEXIT) rep->matvecs -= 1;  // t = A s skipped on the early exit
+  if (reason == R_TT) rep->matvecs += 2;
+  if (completed > 0) {
+    HMX_CUDA(cudaMemcpyAsync(history + 1, w.hist + 1, (size_t)completed * sizeof(double),
+                             cudaMemcpyDeviceToHost, st));
+    HMX_CUDA(cudaStreamSynchronize(st));
+    hlen += completed;
+  }
+  const double bval = w.h_sc[SC_BVAL];
+  switch (reason) {
+    case R_NONFINITE: {
+      const int* f = reinterpret_cast<const int*>(w.h_sc + SC_N);
+      A->last_xp = f[0] ? w.p : w.s;  // the failing product's input, for the probe
       set_error("non-finite matvec result");
       return finish(HMX_ERR_NONFINITE);
     }
-    const double denom = w.h_sc[SC_DV];
-    if (std::fabs(denom) < kBreakdownEps) {  // solver.py:123-125
-      rep->breakdown = 2;
-      rep->breakdown_value = denom;
-      rep->breakdown_iteration = i;
+    case R_RHO:    // solver.py:113-115
+    case R_DENOM:  // solver.py:123-125
+    case R_OMEGA:  // solver.py:155-157
+      rep->breakdown = reason == R_RHO ? 1 : reason == R_DENOM ? 2 : 4;
+      rep->breakdown_value = bval;
+      rep->breakdown_iteration = stop_it;
       break;
-    }
-    const double s_rel = std::sqrt(w.h_sc[SC_SS]) / nb;
-    if (s_rel < tol) {  // solver.py:130-136
+    case R_TT:     // solver.py:139-142
+      rep->breakdown = 3;
+      rep->breakdown_iteration = stop_it;
+      break;
+    case R_SEXIT:  // solver.py:130-136: x = x + alpha p, then confirm
       x_alpha_p_kernel<<<c.grid, kVecThreads, 0, st>>>(w.x, w.p, n32, w.sc);
       HMX_CUDA(cudaGetLastError());
-      history[hlen++] = s_rel;
-      rep->iterations = i;
+      /* fallthrough */
+    case R_CONV: {  // solver.py:151-154
       double tr = 0.0;
       if ((rc = true_residual_dev(c, &tr))) return finish(rc);
       rep->matvecs++;
@@ -474,45 +593,8 @@ int hmx_bicgstab(hmx_plan* A, hmx_plan* A64, const double* b, double tol, int ma
       rep->converged = tr < tol;
       break;
     }
-    if ((rc = apply(A, w, st, w.s, w.t, w.s, 1, SC_DT, w.flags + 1))) return rc;
-    rep->matvecs++;
-    xr_update_kernel<<<c.grid, kVecThreads, 0, st>>>(w.x, w.r, w.p, w.s, w.t, w.rhat, n32, w.sc,
-                                                       VecRed{w.partials, w.done, w.sc + SC_TMP});
-    HMX_CUDA(cudaGetLastError());
-    if ((rc = sync_scalars(c))) return rc;
-    if (flags_nonfinite(c)) {
-      set_error("non-finite matvec result");
-      return finish(HMX_ERR_NONFINITE);
-    }
-    if (w.h_sc[SC_DT + 1] == 0.0) {  // solver.py:139-142
-      rep->breakdown = 3;
-      rep->breakdown_iteration = i;
+    default:
       break;
-    }
-    const double omega = w.h_sc[SC_OMEGA];
-    const double rr = w.h_sc[SC_TMP], rho_next = w.h_sc[SC_TMP + 1];
-    const double rel = std::sqrt(rr) / nb;
-    history[hlen++] = rel;
-    rep->iterations = i;
-    if (rel < tol) {  // solver.py:151-154
-      double tr = 0.0;
-      if ((rc = true_residual_dev(c, &tr))) return finish(rc);
-      rep->matvecs++;
-      rep->has_true_residual = 1;
-      rep->true_residual = tr;
-      rep->converged = tr < tol;
-      break;
-    }
-    if (std::fabs(omega) < kBreakdownEps) {  // solver.py:155-157
-      rep->breakdown = 4;
-      rep->breakdown_value = omega;
-      rep->breakdown_iteration = i;
-      break;
-    }
-    // next rho goes to the next ring slot; rho_prev stays in the current one
-    HMX_CUDA(cudaMemcpyAsync(w.sc + rho_slot(i + 1), w.sc + SC_TMP + 1, sizeof(double),
-                             cudaMemcpyDeviceToDevice, st));
-    rho = rho_next;
   }
   return finish(HMX_OK);
 }
