@@ -112,43 +112,33 @@ __global__ void __launch_bounds__(kSegThreads, 4) seg_kernel(DevPlan P, const Se
     const int cb = act ? (int)((int64_t)tw * q64 / g64) : 0;
     const int ce = act ? (int)((int64_t)tw * (q64 + 1) / g64) : 0;
     const double* __restrict__ col = P.blob64 + sg.off64 + (int64_t)tc0 * rp64 + 2 * p64;
-    // first batch of payload loads is independent of g: issue it before the
-    // gather (and, in stage 2, before waiting on stage 1) to hide one latency
+    // batches of 8 columns, predicated at the end of the range (a short
+    // range -- small segments -- is still one batch, never a serial chain).
+    // The first batch is independent of g: it is issued before the gather
+    // (and, in stage 2, before waiting on stage 1) to hide one latency.
     double2 m[8];
     int c = cb;
-    const bool pre = c + 8 <= ce;
-    if (pre) {
 #pragma unroll
-      for (int u = 0; u < 8; ++u) m[u] = ld_stream(col + (int64_t)(c + u) * rp64, pol);
-    }
+    for (int u = 0; u < 8; ++u)
+      if (c + u < ce) m[u] = ld_stream(col + (int64_t)(c + u) * rp64, pol);
     if (OUT == OUT_Y && tc0 == 0) asm volatile("griddepcontrol.wait;" ::: "memory");
     __syncthreads();
     gather_g<false>(P, P.runs + sg.run0, sg.nrun64, tc0, tw, x, gs, fl, sidx);
     __syncthreads();
-    if (pre) {
+    for (;;) {
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
-        const double g = gs[c + u];
-        a0 = fma(m[u].x, g, a0);
-        a1 = fma(m[u].y, g, a1);
+        if (c + u < ce) {
+          const double g = gs[c + u];
+          a0 = fma(m[u].x, g, a0);
+          a1 = fma(m[u].y, g, a1);
+        }
       }
       c += 8;
-    }
-    for (; c + 8 <= ce; c += 8) {
+      if (c >= ce) break;
 #pragma unroll
-      for (int u = 0; u < 8; ++u) m[u] = ld_stream(col + (int64_t)(c + u) * rp64, pol);
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const double g = gs[c + u];
-        a0 = fma(m[u].x, g, a0);
-        a1 = fma(m[u].y, g, a1);
-      }
-    }
-    for (; c < ce; ++c) {
-      const double2 mm = ld_stream(col + (int64_t)c * rp64, pol);
-      const double g = gs[c];
-      a0 = fma(mm.x, g, a0);
-      a1 = fma(mm.y, g, a1);
+      for (int u = 0; u < 8; ++u)
+        if (c + u < ce) m[u] = ld_stream(col + (int64_t)(c + u) * rp64, pol);
     }
   }
 
@@ -198,28 +188,34 @@ __global__ void __launch_bounds__(kSegThreads, 4) seg_kernel(DevPlan P, const Se
     const float* __restrict__ col = P.blob32 + sg.off32 + (int64_t)tc0 * rp32 + 4 * p32;
     float4 m[8];
     int c = cb;
-    const bool pre = c + 8 <= ce;
-    if (pre) {
 #pragma unroll
-      for (int u = 0; u < 8; ++u) m[u] = ld_stream(col + (int64_t)(c + u) * rp32, pol);
-    }
+    for (int u = 0; u < 8; ++u)
+      if (c + u < ce) m[u] = ld_stream(col + (int64_t)(c + u) * rp32, pol);
     if (OUT == OUT_Y && tc0 == 0 && sg.W64 == 0) asm volatile("griddepcontrol.wait;" ::: "memory");
     __syncthreads();
     gather_g<F32MODE != F32_ALL64>(P, P.runs + sg.run0 + sg.nrun64, sg.nrun32, tc0, tw, x, gs, fl,
                                    sidx);
     __syncthreads();
-    if (pre) {
+    for (;;) {
+      if (c + 8 <= ce) {  // full batch: unpredicated hot path
 #pragma unroll
-      for (int u = 0; u < 8; ++u) consume(m[u], c + u);
+        for (int u = 0; u < 8; ++u) consume(m[u], c + u);
+      } else {
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (c + u < ce) consume(m[u], c + u);
+      }
       c += 8;
-    }
-    for (; c + 8 <= ce; c += 8) {
+      if (c >= ce) break;
+      if (c + 8 <= ce) {
 #pragma unroll
-      for (int u = 0; u < 8; ++u) m[u] = ld_stream(col + (int64_t)(c + u) * rp32, pol);
+        for (int u = 0; u < 8; ++u) m[u] = ld_stream(col + (int64_t)(c + u) * rp32, pol);
+      } else {
 #pragma unroll
-      for (int u = 0; u < 8; ++u) consume(m[u], c + u);
+        for (int u = 0; u < 8; ++u)
+          if (c + u < ce) m[u] = ld_stream(col + (int64_t)(c + u) * rp32, pol);
+      }
     }
-    for (; c < ce; ++c) consume(ld_stream(col + (int64_t)c * rp32, pol), c);
   }
   if constexpr (F32MODE != F32_ALL64) {
 #pragma unroll
