@@ -224,7 +224,7 @@ def run_ours(args):
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
-    if world > 1:
+    if world > 1 or args.distributed:
         from paper_1911_00093_b200 import distributed as dist_mod
         return dist_mod.bench_main(args, build_workload, workload_name, METRIC)
 
@@ -349,6 +349,8 @@ def main():
     ap.add_argument("--no-solve", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=12.0)
+    ap.add_argument("--distributed", action="store_true",
+                    help="use the row-partitioned multi-GPU path even at world size 1")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -155,8 +155,9 @@ int hmx_bicgstab(hmx_plan* plan, hmx_plan* plan64, const double* b, double tol, 
  * `dots` (device, 2 doubles) is non-NULL it receives [y . w1, y . y] over the
  * local rows (w1: local slice, device, may be NULL; yy: compute y . y).
  * `nonfinite` (device int, may be NULL) is set to 1 when a y entry is not
- * finite.  Enqueued on `stream` (a cudaStream_t; 0 = the plan's stream);
- * returns without synchronising. */
+ * finite.  Enqueued on `stream` (a cudaStream_t, 0 being the legacy default
+ * stream; UINT64_MAX = the plan's own stream); returns without
+ * synchronising. */
 int hmx_apply_local(hmx_plan* plan, const double* xp, double* y, const double* w1, int yy,
                     double* dots, int* nonfinite, uint64_t stream);
 

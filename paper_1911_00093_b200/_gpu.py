@@ -206,8 +206,11 @@ class Plan:
         return rc
 
     def apply_local(self, xp_ptr: int, y_ptr: int, w1_ptr: int = 0, yy: bool = False,
-                    dots_ptr: int = 0, nonfinite_ptr: int = 0, stream: int = 0) -> None:
-        """Enqueue the local rows of y = A xp (device pointers) on `stream`."""
+                    dots_ptr: int = 0, nonfinite_ptr: int = 0, stream: int | None = None) -> None:
+        """Enqueue the local rows of y = A xp (device pointers) on `stream`
+        (a cudaStream_t handle such as torch's `cuda_stream`; None = the
+        plan's own stream)."""
+        stream = (1 << 64) - 1 if stream is None else stream
         rc = self._lib.hmx_apply_local(self.handle, ctypes.c_void_p(xp_ptr), ctypes.c_void_p(y_ptr),
                                        ctypes.c_void_p(w1_ptr or None), int(bool(yy)),
                                        ctypes.c_void_p(dots_ptr or None),

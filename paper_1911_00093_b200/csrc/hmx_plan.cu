@@ -688,7 +688,9 @@ int hmx_apply_local(hmx_plan* p, const double* xp, double* y, const double* w1, 
   }
   std::lock_guard<std::mutex> lock(p->mu);
   DeviceGuard guard(p->device);
-  cudaStream_t st = stream ? reinterpret_cast<cudaStream_t>(stream) : p->stream;
+  // UINT64_MAX selects the plan's own stream; any other value (including 0,
+  // the legacy default stream) is used as given
+  cudaStream_t st = stream == UINT64_MAX ? p->stream : reinterpret_cast<cudaStream_t>(stream);
   S2Out out{};
   out.y = y;
   out.permute_out = 0;
