@@ -136,6 +136,10 @@ def host():
             lib.hb_scale_fill.argtypes = [c_f64p, ctypes.c_int64, c_i32p, c_i64p, c_i64p, c_i64p,
                                           c_i64p, c_i64p, c_i8p, c_i64p, c_i64p, c_f64p, c_f32p,
                                           c_f64p, c_f64p, c_i64p, ctypes.c_int]
+            lib.hb_cast_f32.argtypes = [c_f64p, ctypes.c_int64, c_f32p, c_i64p, ctypes.c_int]
+            lib.hb_cast_f32.restype = ctypes.c_int64
+            lib.hb_copy_f64.argtypes = [c_f64p, c_f64p, ctypes.c_int64, ctypes.c_int]
+            lib.hb_copy_f64.restype = None
             _host = lib
     return _host
 

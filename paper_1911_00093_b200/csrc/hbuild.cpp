@@ -637,3 +637,50 @@ int hb_scale_fill(const double* master, int64_t nb, const int32_t* kinds, const 
 }
 
 }  // extern "C"
+
+extern "C" {
+
+// Round-to-nearest FP32 copy of `src` (precision.py:241-253): returns the
+// index of the first element that overflows (finite -> inf), or -1, and the
+// number of nonzero values that lost all magnitude (|f32| < FLT_MIN).
+int64_t hb_cast_f32(const double* src, int64_t n, float* dst, int64_t* lost_out, int nthreads) {
+  const float f32_tiny = 1.17549435e-38f;
+  const int64_t chunk = 1 << 20;
+  const int64_t nchunks = (n + chunk - 1) / chunk;
+  std::vector<int64_t> first((size_t)std::max<int64_t>(nchunks, 1), -1), lost((size_t)std::max<int64_t>(nchunks, 1), 0);
+  run_parallel(nchunks, nthreads, [&](int64_t c) {
+    const int64_t a = c * chunk, b = std::min(n, a + chunk);
+    int64_t f = -1, l = 0;
+    for (int64_t i = a; i < b; ++i) {
+      const double v = src[i];
+      const float o = (float)v;
+      dst[i] = o;
+      if (f < 0 && std::isinf(o) && std::isfinite(v)) f = i;
+      if (v != 0.0 && std::fabs(o) < f32_tiny) ++l;
+    }
+    first[(size_t)c] = f;
+    lost[(size_t)c] = l;
+  });
+  int64_t f = -1, l = 0;
+  for (int64_t c = 0; c < nchunks; ++c) {
+    if (f < 0 && first[(size_t)c] >= 0) f = first[(size_t)c];
+    l += lost[(size_t)c];
+  }
+  *lost_out = l;
+  return f;
+}
+
+}  // extern "C"
+
+extern "C" {
+
+// dst[0:n] = src[0:n], in parallel chunks (host staging of large payloads).
+void hb_copy_f64(const double* src, double* dst, int64_t n, int nthreads) {
+  const int64_t chunk = 1 << 22;
+  run_parallel((n + chunk - 1) / chunk, nthreads, [&](int64_t c) {
+    const int64_t a = c * chunk, b = std::min(n, a + chunk);
+    std::memcpy(dst + a, src + a, (size_t)(b - a) * sizeof(double));
+  });
+}
+
+}  // extern "C"

@@ -16,6 +16,7 @@ payload objects are numpy views into it, materialised on demand.
 
 from __future__ import annotations
 
+import ctypes
 from dataclasses import dataclass
 
 import numpy as np
@@ -339,11 +340,13 @@ def _cast_checked(src64: np.ndarray, table, offsets, kinds, ranks, scheme_name="
     """Round-to-nearest FP32 copy of the packed buffer; FP32 overflow raises
     OverflowError naming the first offending block/array, underflow is counted
     (precision.py:241-253)."""
-    with np.errstate(over="ignore"):
-        out = src64.astype(np.float32)
-    bad = np.isinf(out) & np.isfinite(src64)
-    if np.any(bad):
-        first = int(np.argmax(bad))
+    src64 = np.ascontiguousarray(src64, dtype=np.float64)
+    out = np.empty(src64.size, dtype=np.float32)
+    lost = ctypes.c_int64(0)
+    first = int(_native.host().hb_cast_f32(_native.ptr(src64, _native.c_f64p), src64.size,
+                                           _native.ptr(out, _native.c_f32p), ctypes.byref(lost),
+                                           _native.host_threads()))
+    if first >= 0:
         k = int(np.searchsorted(offsets, first, side="right") - 1)
         m, n = int(table[k, 1] - table[k, 0]), int(table[k, 3] - table[k, 2])
         o = int(offsets[k])
@@ -355,8 +358,7 @@ def _cast_checked(src64: np.ndarray, table, offsets, kinds, ranks, scheme_name="
         peak = float(np.max(np.abs(arr)))
         raise OverflowError(f"FP32 overflow while casting {_where(table, k)}: |value| up to "
                             f"{peak:.6g} exceeds {_F32_MAX:.6g}")
-    lost = int(np.count_nonzero((src64 != 0.0) & (np.abs(out) < _F32_TINY)))
-    return out, lost
+    return out, int(lost.value)
 
 
 def prepare_scheme(h, scheme) -> SchemeHMatrix:
@@ -419,7 +421,7 @@ def prepare_scheme(h, scheme) -> SchemeHMatrix:
     # unit factors written into a copy of the master: U_hi/Vt_hi fit in the
     # block's original slot; the diagonal (reordered hi|lo) is appended
     work = np.empty(pm.data.size + rtot, dtype=np.float64)
-    work[:pm.data.size] = pm.data
+    lib.hb_copy_f64(P(pm.data, c_f64), P(work, c_f64), pm.data.size, th)
     dpos = pm.data.size
     buf32_lo = np.zeros(int(lo_sizes.sum()), dtype=np.float32)
     lost = np.zeros(nb, dtype=np.int64)
