@@ -63,8 +63,10 @@ enum ZEpi : int { Z_NONE = 0, Z_ROUND32 = 1, Z_SCALE = 2 };
 
 constexpr int kSegRows = 64;      // max rows per stage-2 segment (leaf rows)
 constexpr int kS1Rows = 256;      // max rank rows per stage-1 segment
-constexpr int kSegThreads = 256;  // CTA size
-constexpr int kSegWMax = 2048;    // columns of g staged in shared memory per tile
+constexpr int kSegThreads = 256;  // stage-2 CTA size (thread-group layout of gtab)
+constexpr int kS1Threads = 128;   // stage-1 CTA size
+constexpr int kSegWMax = 2048;    // columns of g staged in shared memory per tile (stage 2)
+constexpr int kS1WMax = 1024;     // max columns per stage-1 segment chunk
 
 // Device-visible plan (passed by value to kernels).
 struct DevPlan {

@@ -26,7 +26,7 @@ enum Out : int { OUT_Y = 0, OUT_Z = 1 };
 // so every column's load is independent (no dependent run lookups).
 constexpr int kRunsSmem = 512;
 constexpr int32_t kTagZ = 1 << 30, kTagRound = 1 << 29, kIdxMask = kTagRound - 1;
-template <bool FLAGS>
+template <bool FLAGS, int NT>
 __device__ __forceinline__ void gather_g(const DevPlan& P, const Run* __restrict__ runs, int nrun,
                                          int tc0, int tw, const double* __restrict__ x,
                                          double* gs, uint8_t* fl, int32_t* sidx) {
@@ -35,7 +35,7 @@ __device__ __forceinline__ void gather_g(const DevPlan& P, const Run* __restrict
     const double* src = ((r.flags & RUN_Z) ? P.z : x) + r.src + (tc0 - r.col0);
     const bool rnd = (r.flags & RUN_ROUND) != 0;
     const uint8_t f32 = (r.flags & RUN_ACC32) ? 2 : 0;
-    for (int c = threadIdx.x; c < tw; c += kSegThreads) {
+    for (int c = threadIdx.x; c < tw; c += NT) {
       const double g = src[c];
       gs[c] = rnd ? (double)(float)g : g;
       if constexpr (FLAGS) fl[c] = (uint8_t)((tc0 + c == r.col0 ? 1 : 0) | f32);
@@ -43,7 +43,7 @@ __device__ __forceinline__ void gather_g(const DevPlan& P, const Run* __restrict
     return;
   }
   // runs whose columns meet the tile: scatter their source indices
-  for (int j = threadIdx.x; j < nrun; j += kSegThreads) {
+  for (int j = threadIdx.x; j < nrun; j += NT) {
     const Run r = runs[j];
     const int lo = max(r.col0, tc0), hi = min(r.col0 + r.width, tc0 + tw);
     const int32_t tag = ((r.flags & RUN_Z) ? kTagZ : 0) | ((r.flags & RUN_ROUND) ? kTagRound : 0);
@@ -55,22 +55,22 @@ __device__ __forceinline__ void gather_g(const DevPlan& P, const Run* __restrict
   }
   __syncthreads();
   const double* __restrict__ z = P.z;
-  for (int c0 = threadIdx.x; c0 < tw; c0 += 4 * kSegThreads) {
+  for (int c0 = threadIdx.x; c0 < tw; c0 += 4 * NT) {
     int32_t id[4];
     double v[4];
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
-      const int c = c0 + u * kSegThreads;
+      const int c = c0 + u * NT;
       id[u] = c < tw ? sidx[c] : 0;
     }
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
-      const int c = c0 + u * kSegThreads;
+      const int c = c0 + u * NT;
       v[u] = c < tw ? ((id[u] & kTagZ) ? z : x)[id[u] & kIdxMask] : 0.0;
     }
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
-      const int c = c0 + u * kSegThreads;
+      const int c = c0 + u * NT;
       if (c < tw) gs[c] = (id[u] & kTagRound) ? (double)(float)v[u] : v[u];
     }
   }
@@ -83,15 +83,17 @@ __device__ __forceinline__ double z_epilogue(const DevPlan& P, double s, int zi)
 }
 
 // One CTA = one segment: rows [row0, row0+R) of a column-major item stream.
-template <int F32MODE, int OUT>
-__global__ void __launch_bounds__(kSegThreads, 4) seg_kernel(DevPlan P, const Seg* __restrict__ segs,
+template <int F32MODE, int OUT, int NT>
+__global__ void __launch_bounds__(NT, 1024 / NT) seg_kernel(DevPlan P, const Seg* __restrict__ segs,
                                                           const double* __restrict__ x, S2Out out) {
-  __shared__ double gs[kSegWMax];
-  __shared__ uint8_t fl[kSegWMax];
-  __shared__ int32_t sidx[kSegWMax];
-  __shared__ double red64[2 * kSegThreads];
-  __shared__ double red32[4 * kSegThreads];
-  __shared__ double wred[2][kSegThreads / 32];
+  // stage 1 segments have a single run (no index expansion) and <= 1024 columns
+  constexpr int WMAX = OUT == OUT_Z ? kS1WMax : kSegWMax;
+  __shared__ double gs[WMAX];
+  __shared__ uint8_t fl[WMAX];
+  __shared__ int32_t sidx[OUT == OUT_Z ? 1 : kSegWMax];
+  __shared__ double red64[2 * NT];
+  __shared__ double red32[4 * NT];
+  __shared__ double wred[2][NT / 32];
   __shared__ unsigned ticket;
 
   if (out.skip != nullptr && *out.skip != 0) return;  // guarded launch (solver)
@@ -103,11 +105,11 @@ __global__ void __launch_bounds__(kSegThreads, 4) seg_kernel(DevPlan P, const Se
   // ---------------- FP64 part: 2 rows x 16 bytes per thread
   const int rp64 = (R + 1) & ~1;
   const int tpg64 = rp64 >> 1;
-  const int g64 = kSegThreads / tpg64;
+  const int g64 = NT / tpg64;
   const int q64 = tid / tpg64, p64 = tid - q64 * tpg64;
   double a0 = 0.0, a1 = 0.0;
-  for (int tc0 = 0; tc0 < sg.W64; tc0 += kSegWMax) {
-    const int tw = min(kSegWMax, sg.W64 - tc0);
+  for (int tc0 = 0; tc0 < sg.W64; tc0 += WMAX) {
+    const int tw = min(WMAX, sg.W64 - tc0);
     const bool act = q64 < g64;
     const int cb = act ? (int)((int64_t)tw * q64 / g64) : 0;
     const int ce = act ? (int)((int64_t)tw * (q64 + 1) / g64) : 0;
@@ -123,7 +125,7 @@ __global__ void __launch_bounds__(kSegThreads, 4) seg_kernel(DevPlan P, const Se
       if (c + u < ce) m[u] = ld_stream(col + (int64_t)(c + u) * rp64, pol);
     if (OUT == OUT_Y && tc0 == 0) asm volatile("griddepcontrol.wait;" ::: "memory");
     __syncthreads();
-    gather_g<false>(P, P.runs + sg.run0, sg.nrun64, tc0, tw, x, gs, fl, sidx);
+    gather_g<false, NT>(P, P.runs + sg.run0, sg.nrun64, tc0, tw, x, gs, fl, sidx);
     __syncthreads();
     for (;;) {
 #pragma unroll
@@ -145,7 +147,7 @@ __global__ void __launch_bounds__(kSegThreads, 4) seg_kernel(DevPlan P, const Se
   // ---------------- FP32 part: 4 rows x 16 bytes per thread
   const int rp32 = (R + 3) & ~3;
   const int tpg32 = rp32 >> 2;
-  const int g32 = kSegThreads / tpg32;
+  const int g32 = NT / tpg32;
   const int q32 = tid / tpg32, p32 = tid - q32 * tpg32;
   double b[4] = {0.0, 0.0, 0.0, 0.0};
   float b32[4] = {0.f, 0.f, 0.f, 0.f};
@@ -174,8 +176,8 @@ __global__ void __launch_bounds__(kSegThreads, 4) seg_kernel(DevPlan P, const Se
       }
     }
   };
-  for (int tc0 = 0; tc0 < sg.W32; tc0 += kSegWMax) {
-    const int tw = min(kSegWMax, sg.W32 - tc0);
+  for (int tc0 = 0; tc0 < sg.W32; tc0 += WMAX) {
+    const int tw = min(WMAX, sg.W32 - tc0);
     const bool act = q32 < g32;
     int cb = act ? (int)((int64_t)tw * q32 / g32) : 0;
     int ce = act ? (int)((int64_t)tw * (q32 + 1) / g32) : 0;
@@ -193,7 +195,7 @@ __global__ void __launch_bounds__(kSegThreads, 4) seg_kernel(DevPlan P, const Se
       if (c + u < ce) m[u] = ld_stream(col + (int64_t)(c + u) * rp32, pol);
     if (OUT == OUT_Y && tc0 == 0 && sg.W64 == 0) asm volatile("griddepcontrol.wait;" ::: "memory");
     __syncthreads();
-    gather_g<F32MODE != F32_ALL64>(P, P.runs + sg.run0 + sg.nrun64, sg.nrun32, tc0, tw, x, gs, fl,
+    gather_g<F32MODE != F32_ALL64, NT>(P, P.runs + sg.run0 + sg.nrun64, sg.nrun32, tc0, tw, x, gs, fl,
                                    sidx);
     __syncthreads();
     for (;;) {
@@ -233,44 +235,46 @@ __global__ void __launch_bounds__(kSegThreads, 4) seg_kernel(DevPlan P, const Se
     for (int i = 0; i < 4; ++i) red32[q32 * rp32 + 4 * p32 + i] = b[i];
   }
   __syncthreads();
-  double s = 0.0;
-  if (tid < R) {
+  // row sums over groups (fixed order); a thread owns rows tid, tid + NT, ...
+  auto row_sum = [&](int t) -> double {
+    double s = 0.0;
     if (sg.W64 > 0)
-      for (int q = 0; q < g64; ++q) s += red64[q * rp64 + tid];
+      for (int q = 0; q < g64; ++q) s += red64[q * rp64 + t];
     if (sg.W32 > 0) {
       if (OUT == OUT_Z && F32MODE == F32_ALL32) {
         // stage 1, m1-single: z = Vt32 . x32 accumulated in FP32 throughout
         float f = 0.f;
-        for (int q = 0; q < g32; ++q) f += (float)red32[q * rp32 + tid];
+        for (int q = 0; q < g32; ++q) f += (float)red32[q * rp32 + t];
         s = (double)f;
       } else {
-        for (int q = 0; q < g32; ++q) s += red32[q * rp32 + tid];
+        for (int q = 0; q < g32; ++q) s += red32[q * rp32 + t];
       }
     }
-  }
+    return s;
+  };
 
   if constexpr (OUT == OUT_Z) {
     // ---------------- stage-1 epilogue: z (or a chunk partial)
     if (sg.nchunks == 1) {
-      if (tid < R) P.z[sg.row0 + tid] = z_epilogue(P, s, sg.row0 + tid);
+      for (int t = tid; t < R; t += NT) P.z[sg.row0 + t] = z_epilogue(P, row_sum(t), sg.row0 + t);
     } else {
-      if (tid < R) P.part[sg.part_off + sg.chunk * R + tid] = s;
+      for (int t = tid; t < R; t += NT) P.part[sg.part_off + sg.chunk * R + t] = row_sum(t);
       __threadfence();
       __syncthreads();
       if (tid == 0) ticket = atomicAdd(P.red_count + sg.red, 1u);
       __syncthreads();
       if (ticket == (unsigned)(sg.nchunks - 1)) {
         __threadfence();
-        if (tid < R) {
-          double t = 0.0;
+        for (int t = tid; t < R; t += NT) {
+          double v = 0.0;
           if (F32MODE == F32_ALL32) {
             float f = 0.f;
-            for (int ch = 0; ch < sg.nchunks; ++ch) f += (float)__ldcg(P.part + sg.part_off + ch * R + tid);
-            t = (double)f;
+            for (int ch = 0; ch < sg.nchunks; ++ch) f += (float)__ldcg(P.part + sg.part_off + ch * R + t);
+            v = (double)f;
           } else {
-            for (int ch = 0; ch < sg.nchunks; ++ch) t += __ldcg(P.part + sg.part_off + ch * R + tid);
+            for (int ch = 0; ch < sg.nchunks; ++ch) v += __ldcg(P.part + sg.part_off + ch * R + t);
           }
-          P.z[sg.row0 + tid] = z_epilogue(P, t, sg.row0 + tid);
+          P.z[sg.row0 + t] = z_epilogue(P, v, sg.row0 + t);
         }
         if (tid == 0) P.red_count[sg.red] = 0u;  // ready for the next matvec
       }
@@ -280,14 +284,15 @@ __global__ void __launch_bounds__(kSegThreads, 4) seg_kernel(DevPlan P, const Se
   } else {
     // ---------------- stage-2 epilogue: y, finite flag, fused dots
     double d0 = 0.0, d1 = 0.0;
-    if (tid < R) {
-      const int row = sg.row0 + tid;
+    for (int t = tid; t < R; t += NT) {
+      const double s = row_sum(t);
+      const int row = sg.row0 + t;
       const int li = row - P.row_begin;
       if (!isfinite(s)) *out.nonfinite = 1;
       if (out.permute_out) out.y[P.perm[row]] = s;
       else out.y[li] = s;
-      if (out.w1) d0 = s * out.w1[li];
-      if (out.yy) d1 = s * s;
+      if (out.w1) d0 += s * out.w1[li];
+      if (out.yy) d1 += s * s;
     }
     if (out.seg_dots == nullptr) return;
     // per-segment dot partials, then the last CTA reduces all segment
@@ -305,7 +310,7 @@ __global__ void __launch_bounds__(kSegThreads, 4) seg_kernel(DevPlan P, const Se
     __syncthreads();
     if (tid == 0) {
       double e0 = 0.0, e1 = 0.0;
-      for (int w = 0; w < kSegThreads / 32; ++w) {
+      for (int w = 0; w < NT / 32; ++w) {
         e0 += wred[0][w];
         e1 += wred[1][w];
       }
@@ -318,7 +323,7 @@ __global__ void __launch_bounds__(kSegThreads, 4) seg_kernel(DevPlan P, const Se
     if (ticket != gridDim.x - 1) return;
     __threadfence();
     double e0 = 0.0, e1 = 0.0;
-    for (int i = tid; i < (int)gridDim.x; i += kSegThreads) {
+    for (int i = tid; i < (int)gridDim.x; i += NT) {
       e0 += __ldcg(out.seg_dots + 2 * i);
       e1 += __ldcg(out.seg_dots + 2 * i + 1);
     }
@@ -335,7 +340,7 @@ __global__ void __launch_bounds__(kSegThreads, 4) seg_kernel(DevPlan P, const Se
     __syncthreads();
     if (tid == 0) {
       double f0 = 0.0, f1 = 0.0;
-      for (int w = 0; w < kSegThreads / 32; ++w) {
+      for (int w = 0; w < NT / 32; ++w) {
         f0 += wred[0][w];
         f1 += wred[1][w];
       }
@@ -391,12 +396,12 @@ __global__ void probe_kernel(DevPlan P, const double* __restrict__ x, unsigned l
 // ------------------------------------------------------------------------------
 // launchers
 
-template <int M, int O>
+template <int M, int O, int NT = kSegThreads>
 static cudaError_t launch_seg(const DevPlan& P, const Seg* segs, int nseg, const double* x,
                               const S2Out& out, cudaStream_t st, bool pdl) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)nseg);
-  cfg.blockDim = dim3(kSegThreads);
+  cfg.blockDim = dim3(NT);
   cfg.dynamicSmemBytes = 0;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
@@ -404,7 +409,7 @@ static cudaError_t launch_seg(const DevPlan& P, const Seg* segs, int nseg, const
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = pdl ? 1 : 0;
-  return cudaLaunchKernelEx(&cfg, seg_kernel<M, O>, P, segs, x, out);
+  return cudaLaunchKernelEx(&cfg, seg_kernel<M, O, NT>, P, segs, x, out);
 }
 
 cudaError_t launch_stage1(const DevPlan& P, const double* x, cudaStream_t st, const int* skip) {
@@ -412,8 +417,8 @@ cudaError_t launch_stage1(const DevPlan& P, const double* x, cudaStream_t st, co
   S2Out none{};
   none.skip = skip;
   switch (P.f32mode1) {
-    case F32_ALL32: return launch_seg<F32_ALL32, OUT_Z>(P, P.seg1, P.n_seg1, x, none, st, false);
-    default: return launch_seg<F32_ALL64, OUT_Z>(P, P.seg1, P.n_seg1, x, none, st, false);
+    case F32_ALL32: return launch_seg<F32_ALL32, OUT_Z, kS1Threads>(P, P.seg1, P.n_seg1, x, none, st, false);
+    default: return launch_seg<F32_ALL64, OUT_Z, kS1Threads>(P, P.seg1, P.n_seg1, x, none, st, false);
   }
 }
 
