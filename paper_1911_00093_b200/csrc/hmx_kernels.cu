@@ -151,6 +151,11 @@ __global__ void __launch_bounds__(NT, 1024 / NT) seg_kernel(DevPlan P, const Seg
   const int q32 = tid / tpg32, p32 = tid - q32 * tpg32;
   double b[4] = {0.0, 0.0, 0.0, 0.0};
   float b32[4] = {0.f, 0.f, 0.f, 0.f};
+  // FP32-accumulated columns start at c32 (FP64-accumulated items first;
+  // -1: no group table, fall back to the per-column flag)
+  int c32 = -1;
+  if (F32MODE == F32_MIXED && OUT == OUT_Y && sg.gtab >= 0) c32 = P.gtab[sg.gtab + g32 + 1];
+  int tile0 = 0;
   auto consume = [&](const float4& mv4, int cc) {
     const double g = gs[cc];
     const float mv[4] = {mv4.x, mv4.y, mv4.z, mv4.w};
@@ -158,15 +163,16 @@ __global__ void __launch_bounds__(NT, 1024 / NT) seg_kernel(DevPlan P, const Seg
 #pragma unroll
       for (int i = 0; i < 4; ++i) b[i] = fma((double)mv[i], g, b[i]);
     } else {
-      const uint8_t f = fl[cc];
-      if (f & 1) {  // first column of an item: close the previous FP32 partial
+      bool acc32 = true;
+      if (F32MODE == F32_MIXED) acc32 = c32 >= 0 ? (tile0 + cc >= c32) : (fl[cc] & 2) != 0;
+      if (acc32) {
+        if (fl[cc] & 1) {  // first column of an item: close the previous FP32 partial
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          b[i] += (double)b32[i];
-          b32[i] = 0.f;
+          for (int i = 0; i < 4; ++i) {
+            b[i] += (double)b32[i];
+            b32[i] = 0.f;
+          }
         }
-      }
-      if (F32MODE == F32_ALL32 || (f & 2)) {
         const float gf = (float)g;
 #pragma unroll
         for (int i = 0; i < 4; ++i) b32[i] = fmaf(mv[i], gf, b32[i]);
@@ -178,6 +184,7 @@ __global__ void __launch_bounds__(NT, 1024 / NT) seg_kernel(DevPlan P, const Seg
   };
   for (int tc0 = 0; tc0 < sg.W32; tc0 += WMAX) {
     const int tw = min(WMAX, sg.W32 - tc0);
+    tile0 = tc0;
     const bool act = q32 < g32;
     int cb = act ? (int)((int64_t)tw * q32 / g32) : 0;
     int ce = act ? (int)((int64_t)tw * (q32 + 1) / g32) : 0;

@@ -323,6 +323,16 @@ static int plan_create_impl(const hmx_matrix_desc* d, int device, const hmx_plan
   const bool dense_single = pipe == P_M1S || pipe == P_M2S;  // A32 . x32 in FP32
   const bool u_acc32 = pipe == P_M1S || pipe == P_M1M;       // U32 . z32 in FP32
   bool any_acc32 = false, any_acc64_in32 = false;
+  // FP32 part: FP64-accumulated items first, then FP32-accumulated ones, so
+  // the kernel switches accumulation mode once per part instead of testing
+  // every column (the switch column is stored after the group table)
+  auto item_acc32 = [&](const ItemRef& it) {
+    return it.cls == 0 ? dense_single : (it.cls == 1 && u_acc32);
+  };
+  for (auto& lst : items32)
+    std::stable_sort(lst.begin(), lst.end(), [&](const ItemRef& a, const ItemRef& b) {
+      return (int)item_acc32(a) < (int)item_acc32(b);
+    });
   for (int64_t s = 0; s < nseg2; ++s) {
     Seg& sg = seg2[(size_t)s];
     sg.row0 = (int32_t)seg_start[(size_t)s];
@@ -393,6 +403,7 @@ static int plan_create_impl(const hmx_matrix_desc* d, int device, const hmx_plan
         prev = cut;
       }
       gtab.push_back(sg.W32);
+      gtab.push_back((int32_t)(acc.empty() ? sg.W32 : acc.front().a));  // first FP32-accumulated column
     }
     sg.off64 = off64;
     sg.off32 = off32;
