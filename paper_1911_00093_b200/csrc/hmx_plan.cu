@@ -20,6 +20,8 @@
 #include <tuple>
 #include <numeric>
 #include <queue>
+#include <chrono>
+#include <cstdlib>
 #include <thread>
 
 #include "hmx_plan_impl.cuh"
@@ -122,6 +124,8 @@ static int plan_create_impl(const hmx_matrix_desc* d, int device, const hmx_plan
     set_error("invalid row range");
     return HMX_ERR_ARG;
   }
+  const auto t_start = std::chrono::steady_clock::now();
+  auto secs = [&]() { return std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count(); };
   const int64_t s1_target = opt && opt->s1_chunk_bytes > 0 ? opt->s1_chunk_bytes : 256 * 1024;
   const size_t a_es = d->a32 ? 4 : 8, hi_es = d->hi32 ? 4 : 8;
 
@@ -417,15 +421,17 @@ static int plan_create_impl(const hmx_matrix_desc* d, int device, const hmx_plan
   }
   const int f32mode2 = !any_acc32 ? F32_ALL64 : (any_acc64_in32 ? F32_MIXED : F32_ALL32);
 
-  // ---- pack the blob (host, parallel)
-  std::vector<double> blob64((size_t)std::max<int64_t>(off64, 2), 0.0);
-  std::vector<float> blob32((size_t)std::max<int64_t>(off32, 4), 0.f);
-  parallel_for((int64_t)fills.size(), [&](int64_t i) {
+  // ---- packing of one blob unit (a stage-1 segment, or one part of a
+  // stage-2 segment) into a staging window whose first element is blob
+  // element w0; padding rows stay zero
+  const std::vector<Seg> seg1_fill = seg1;  // fill order (seg1 is re-sorted below)
+  auto pack_s1 = [&](int64_t i, double* b64, float* b32, int64_t w0) {
     const S1Fill& f = fills[(size_t)i];
-    const Seg& s = seg1[(size_t)f.seg];
+    const Seg& s = seg1_fill[(size_t)f.seg];
     const bool is32 = s.W32 > 0;
     const int64_t rp = round_up(s.R, is32 ? 4 : 2);
     const int64_t w = is32 ? s.W32 : s.W64;
+    const int64_t o = (is32 ? s.off32 : s.off64) - w0;
     for (int64_t t = 0; t < s.R; ++t) {
       const auto& row = (*f.rows)[(size_t)(f.r0 + t)];
       const int32_t k = row.first;
@@ -435,45 +441,64 @@ static int plan_create_impl(const hmx_matrix_desc* d, int device, const hmx_plan
       const int64_t base = (f.cls == 1 ? d->hi_off[k] : d->lo_off[k]) + m * kk + (int64_t)row.second * f.ncol + f.c0;
       const bool src32 = f.cls == 2 || d->hi32;
       for (int64_t j = 0; j < w; ++j) {
-        if (is32) blob32[(size_t)(s.off32 + j * rp + t)] = src32 ? d->buf32[base + j] : (float)d->buf64[base + j];
-        else blob64[(size_t)(s.off64 + j * rp + t)] = src32 ? d->buf32[base + j] : d->buf64[base + j];
+        if (is32) b32[(size_t)(o + j * rp + t)] = src32 ? d->buf32[base + j] : (float)d->buf64[base + j];
+        else b64[(size_t)(o + j * rp + t)] = src32 ? d->buf32[base + j] : d->buf64[base + j];
       }
     }
-  });
-  parallel_for(nseg2, [&](int64_t s) {
+  };
+  auto pack_s2 = [&](int64_t s, int part, double* b64, float* b32, int64_t w0) {
     const Seg& sg = seg2[(size_t)s];
-    for (int part = 0; part < 2; ++part) {
-      const auto& lst = part == 0 ? items64[(size_t)s] : items32[(size_t)s];
-      const int64_t rp = part == 0 ? round_up(sg.R, 2) : round_up(sg.R, 4);
-      int64_t col = 0;
-      for (const ItemRef& it : lst) {
-        const int64_t* t = d->table + 5 * it.block;
-        const int64_t r0 = sg.row0 - t[0];
-        const int64_t w = item_width(it);
-        int64_t src_off;
-        bool src32;
-        if (it.cls == 0) {
-          src_off = d->a_off[it.block];
-          src32 = d->a32;
-        } else if (it.cls == 1) {
-          src_off = d->hi_off[it.block];
-          src32 = d->hi32;
-        } else {
-          src_off = d->lo_off[it.block];
-          src32 = true;
-        }
-        for (int64_t i = 0; i < sg.R; ++i) {
-          const int64_t e0 = src_off + (r0 + i) * w;
-          for (int64_t c = 0; c < w; ++c) {
-            const int64_t dst = (col + c) * rp + i;
-            if (part == 0) blob64[(size_t)(sg.off64 + dst)] = src32 ? d->buf32[e0 + c] : d->buf64[e0 + c];
-            else blob32[(size_t)(sg.off32 + dst)] = src32 ? d->buf32[e0 + c] : (float)d->buf64[e0 + c];
-          }
-        }
-        col += w;
+    const auto& lst = part == 0 ? items64[(size_t)s] : items32[(size_t)s];
+    const int64_t rp = part == 0 ? round_up(sg.R, 2) : round_up(sg.R, 4);
+    const int64_t o = (part == 0 ? sg.off64 : sg.off32) - w0;
+    int64_t col = 0;
+    for (const ItemRef& it : lst) {
+      const int64_t* t = d->table + 5 * it.block;
+      const int64_t r0 = sg.row0 - t[0];
+      const int64_t w = item_width(it);
+      int64_t src_off;
+      bool src32;
+      if (it.cls == 0) {
+        src_off = d->a_off[it.block];
+        src32 = d->a32;
+      } else if (it.cls == 1) {
+        src_off = d->hi_off[it.block];
+        src32 = d->hi32;
+      } else {
+        src_off = d->lo_off[it.block];
+        src32 = true;
       }
+      for (int64_t i = 0; i < sg.R; ++i) {
+        const int64_t e0 = src_off + (r0 + i) * w;
+        for (int64_t c = 0; c < w; ++c) {
+          const int64_t dst = o + (col + c) * rp + i;
+          if (part == 0) b64[(size_t)dst] = src32 ? d->buf32[e0 + c] : d->buf64[e0 + c];
+          else b32[(size_t)dst] = src32 ? d->buf32[e0 + c] : (float)d->buf64[e0 + c];
+        }
+      }
+      col += w;
     }
-  });
+  };
+  // units per blob, in offset order (offsets were handed out sequentially)
+  struct Unit {
+    int64_t off, len;  // elements
+    int32_t idx;
+    int8_t stage, part;
+  };
+  std::vector<Unit> units[2];
+  for (int64_t i = 0; i < (int64_t)fills.size(); ++i) {
+    const Seg& s = seg1[(size_t)fills[(size_t)i].seg];
+    const bool is32 = s.W32 > 0;
+    if (is32) units[1].push_back({s.off32, (int64_t)s.W32 * round_up(s.R, 4), (int32_t)i, 1, 1});
+    else units[0].push_back({s.off64, (int64_t)s.W64 * round_up(s.R, 2), (int32_t)i, 1, 0});
+  }
+  for (int64_t s = 0; s < nseg2; ++s) {
+    const Seg& sg = seg2[(size_t)s];
+    if (sg.W64) units[0].push_back({sg.off64, (int64_t)sg.W64 * round_up(sg.R, 2), (int32_t)s, 2, 0});
+    if (sg.W32) units[1].push_back({sg.off32, (int64_t)sg.W32 * round_up(sg.R, 4), (int32_t)s, 2, 1});
+  }
+  for (auto& u : units)
+    std::sort(u.begin(), u.end(), [](const Unit& a, const Unit& b) { return a.off < b.off; });
   std::vector<int32_t> perm32((size_t)n);
   for (int64_t i = 0; i < n; ++i) {
     if (d->perm[i] < 0 || d->perm[i] >= n) {
@@ -511,12 +536,76 @@ static int plan_create_impl(const hmx_matrix_desc* d, int device, const hmx_plan
   if ((rc = up(d_runs, runs))) return rc;
   int32_t* d_rb = p->alloc<int32_t>(run_block.size());
   if ((rc = up(d_rb, run_block))) return rc;
-  double* d_b64 = p->alloc<double>(blob64.size());
-  if ((rc = up(d_b64, blob64))) return rc;
-  std::vector<double>().swap(blob64);
-  float* d_b32 = p->alloc<float>(blob32.size());
-  if ((rc = up(d_b32, blob32))) return rc;
-  std::vector<float>().swap(blob32);
+  const double t_meta = secs();
+  // ---- blobs: packed window by window into pinned staging buffers and
+  // uploaded asynchronously, so packing overlaps the copies and the host
+  // never holds a second full copy of the payload
+  double* d_b64 = p->alloc<double>((size_t)std::max<int64_t>(off64, 2));
+  float* d_b32 = p->alloc<float>((size_t)std::max<int64_t>(off32, 4));
+  if (!d_b64 || !d_b32) {
+    set_error("cudaMalloc failed while uploading the plan (out of device memory?)");
+    return HMX_ERR_CUDA;
+  }
+  HMX_CUDA(cudaMemsetAsync(d_b64, 0, (size_t)std::max<int64_t>(off64, 2) * 8, p->stream));
+  HMX_CUDA(cudaMemsetAsync(d_b32, 0, (size_t)std::max<int64_t>(off32, 4) * 4, p->stream));
+  {
+    const int64_t kWinBytes = int64_t(64) << 20;
+    int64_t max_unit = 0;
+    for (int b = 0; b < 2; ++b)
+      for (const Unit& u : units[b]) max_unit = std::max(max_unit, u.len * (b ? 4 : 8));
+    const size_t stage_bytes = (size_t)std::max(kWinBytes, max_unit);
+    constexpr int kBufs = 3;
+    struct Stage {
+      void* h = nullptr;
+      cudaEvent_t ev = nullptr;
+    } st[kBufs];
+    int rc2 = HMX_OK;
+    for (auto& b : st) {
+      if (cudaMallocHost(&b.h, stage_bytes) != cudaSuccess || cudaEventCreateWithFlags(&b.ev, cudaEventDisableTiming) != cudaSuccess) {
+        rc2 = cuda_fail(cudaGetLastError(), "pinned staging for the plan upload");
+        break;
+      }
+    }
+    int64_t win_no = 0;
+    for (int b = 0; b < 2 && rc2 == HMX_OK; ++b) {
+      const auto& us = units[b];
+      const int64_t es = b ? 4 : 8;
+      for (size_t i = 0; i < us.size() && rc2 == HMX_OK;) {
+        size_t j = i + 1;
+        const int64_t w0 = us[i].off;
+        int64_t w1 = us[i].off + us[i].len;
+        while (j < us.size() && (us[j].off + us[j].len - w0) * es <= kWinBytes) w1 = us[j].off + us[j++].len;
+        Stage& sb = st[win_no++ % kBufs];
+        if (cudaEventSynchronize(sb.ev) != cudaSuccess) {
+          rc2 = cuda_fail(cudaGetLastError(), "plan upload");
+          break;
+        }
+        std::memset(sb.h, 0, (size_t)((w1 - w0) * es));
+        double* h64 = static_cast<double*>(sb.h);
+        float* h32 = static_cast<float*>(sb.h);
+        parallel_for((int64_t)(j - i), [&](int64_t q) {
+          const Unit& u = us[i + (size_t)q];
+          if (u.stage == 1) pack_s1(u.idx, h64, h32, w0);
+          else pack_s2(u.idx, u.part, h64, h32, w0);
+        });
+        void* dst = b ? (void*)(d_b32 + w0) : (void*)(d_b64 + w0);
+        cudaError_t e1 = cudaMemcpyAsync(dst, sb.h, (size_t)((w1 - w0) * es), cudaMemcpyHostToDevice, p->stream);
+        if (e1 == cudaSuccess) e1 = cudaEventRecord(sb.ev, p->stream);
+        if (e1 != cudaSuccess) rc2 = cuda_fail(e1, "plan upload");
+        i = j;
+      }
+    }
+    cudaError_t es_ = cudaStreamSynchronize(p->stream);
+    if (rc2 == HMX_OK && es_ != cudaSuccess) rc2 = cuda_fail(es_, "plan upload");
+    for (auto& b : st) {
+      if (b.ev) cudaEventDestroy(b.ev);
+      if (b.h) cudaFreeHost(b.h);
+    }
+    if (rc2 != HMX_OK) return rc2;
+  }
+  if (std::getenv("HMX_PLAN_TIMING"))
+    std::fprintf(stderr, "hmx_plan_create: layout %.3f s, pack+upload %.3f s (%.2f GB)\n", t_meta,
+                 secs() - t_meta, (off64 * 8.0 + off32 * 4.0) / 1e9);
   double* d_zs = p->alloc<double>(zscale.size());
   if ((rc = up(d_zs, zscale))) return rc;
   int32_t* d_perm = p->alloc<int32_t>(perm32.size());
