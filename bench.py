@@ -34,6 +34,9 @@ CONFIGS = {
     2: dict(level=5, leaf=32, aca=1e-4),
     3: dict(level=6, leaf=64, aca=1e-5),
     4: dict(level=7, leaf=64, aca=1e-5),
+    # two unit spheres at (0,0,0) and (3,0,0), potentials +1 / -1, b = voltages
+    5: dict(level=8, leaf=64, aca=1e-4, centers=((0.0, 0.0, 0.0), (3.0, 0.0, 0.0)),
+            voltages=(1.0, -1.0)),
 }
 HEADLINE = "m1-double"
 VARIANTS = ["m1-double", "m1-mixed", "m2-mixed", "m3:c=3", "m3:c=-1"]
@@ -111,16 +114,22 @@ def build_workload(cfg_id: int):
     import paper_1911_00093_b200 as hx
     c = CONFIGS[cfg_id]
     t0 = time.perf_counter()
-    mesh = hx.jittered_sphere_mesh(c["level"], seed=42)
+    mesh = hx.jittered_sphere_mesh(c["level"], seed=42, centers=c.get("centers", ((0.0, 0.0, 0.0),)),
+                                   voltages=c.get("voltages"))
     h = hx.build_hmatrix(mesh, aca_tol=c["aca"], leaf_size=c["leaf"], eta=2.0)
     x = np.random.default_rng(42).uniform(-1.0, 1.0, mesh.n)
-    b = mesh.centroids[:, 2].copy()
+    b = hx.right_hand_side(mesh) if "voltages" in c else mesh.centroids[:, 2].copy()
     return mesh, h, x, b, time.perf_counter() - t0
 
 
 def workload_name(cfg_id):
     c = CONFIGS[cfg_id]
-    n = 20 * 4 ** c["level"]
+    k = len(c.get("centers", (0,)))
+    n = k * 20 * 4 ** c["level"]
+    if k > 1:
+        return (f"config{cfg_id}: {k} jittered unit icospheres level {c['level']} centred at "
+                f"{list(c['centers'])} (N={n}), leaf {c['leaf']}, eta 2.0, ACA {c['aca']:g}; "
+                f"x ~ U(-1,1) seed 42; b = sphere potentials {list(c['voltages'])}")
     return (f"config{cfg_id}: jittered unit icosphere level {c['level']} (N={n}), leaf {c['leaf']}, "
             f"eta 2.0, ACA {c['aca']:g}; x ~ U(-1,1) seed 42; b = centroid z")
 

@@ -228,6 +228,10 @@ class Plan:
               "hmx_bench_matvec")
         return {"ms": out[0], "stage1_ms": out[1], "stage2_ms": out[2], "min_ms": out[3]}
 
+    @property
+    def closed(self) -> bool:
+        return not getattr(self, "handle", None)
+
     def close(self):
         if getattr(self, "handle", None):
             self._lib.hmx_plan_destroy(self.handle)

@@ -72,17 +72,22 @@ def _packed_of(sh) -> PackedScheme:
 def get_plan(sh, device: int | None = None) -> "_gpu.Plan":
     """Device plan of a prepared scheme, created on first use and cached."""
     dev = default_device() if device is None else device
-    plan = getattr(sh, "_hmx_gpu_plan", None)
-    if plan is not None and plan.device == dev:
+    scheme = sh.scheme if not isinstance(sh.scheme, str) else parse_scheme(sh.scheme)
+    # every m1-double scheme of one H-matrix is the FP64 masters: one device
+    # copy, shared with the true-residual operator (get_plan64)
+    owner, attr = sh, "_hmx_gpu_plan"
+    if scheme.label == "m1-double" and getattr(sh, "base", None) is not None:
+        owner, attr = sh.base, "_hmx_gpu_plan64"
+    plan = getattr(owner, attr, None)
+    if plan is not None and plan.device == dev and not plan.closed:
         return plan
     with _plan_lock:
-        plan = getattr(sh, "_hmx_gpu_plan", None)
-        if plan is None or plan.device != dev:
-            scheme = sh.scheme if not isinstance(sh.scheme, str) else parse_scheme(sh.scheme)
+        plan = getattr(owner, attr, None)
+        if plan is None or plan.device != dev or plan.closed:
             plan = _gpu.Plan(_packed_of(sh), _table(sh.base), np.asarray(sh.base.permutation),
                              scheme.label, int(sh.n), device=dev)
             try:
-                object.__setattr__(sh, "_hmx_gpu_plan", plan)
+                object.__setattr__(owner, attr, plan)
             except Exception:
                 pass
     return plan
