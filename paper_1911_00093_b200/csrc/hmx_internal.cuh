@@ -39,7 +39,8 @@ struct Seg {             // 64 bytes; one CTA
   int32_t red;           // stage 1: reduction group of a column-chunked segment, or -1
   int32_t chunk, nchunks;
   int32_t part_off;      // partial slots (nchunks * R doubles)
-  int32_t gtab;          // FP32 part: group column boundaries at gtab[gtab..gtab+G], or -1
+  int32_t gtab;          // FP32 part: group cuts gtab[gtab..gtab+G] then the first FP32-
+                         // accumulated column; <= -2: that column alone at gtab[-2-gtab]; -1: none
 };
 static_assert(sizeof(Seg) == 64, "Seg layout");
 

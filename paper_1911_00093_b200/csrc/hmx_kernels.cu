@@ -14,13 +14,23 @@
 // Every f32-accumulated partial is widened once and added in f64.
 #include "hmx_kernels.cuh"
 
+#ifndef HMX_MIXED_MINB
+#define HMX_MIXED_MINB 4
+#endif
+
 namespace hmx {
 
 enum Out : int { OUT_Y = 0, OUT_Z = 1 };
 
+// Shared-memory slot of an FP32-accumulated column: the FP32 source value in
+// the low word, 1 in the high word on the first column of an item.
+__device__ __forceinline__ double acc32_slot(float g, bool start) {
+  return __hiloint2double(start ? 1 : 0, __float_as_int(g));
+}
+
 // Stage a tile [tc0, tc0+tw) of one part's source vector g (x segments and z
-// vectors, in item order) into shared memory, plus FP32-part item flags
-// (bit 0: first column of an item, bit 1: item accumulates in FP32).
+// vectors, in item order) into shared memory; FP32-accumulated columns are
+// stored as acc32_slot (fl: scratch flags, bit 0 item start, bit 1 FP32 item).
 // A single run (every stage-1 segment) is a contiguous copy.  Otherwise the
 // runs are expanded into a per-column source index in shared memory first,
 // so every column's load is independent (no dependent run lookups).
@@ -37,8 +47,8 @@ __device__ __forceinline__ void gather_g(const DevPlan& P, const Run* __restrict
     const uint8_t f32 = (r.flags & RUN_ACC32) ? 2 : 0;
     for (int c = threadIdx.x; c < tw; c += NT) {
       const double g = src[c];
-      gs[c] = rnd ? (double)(float)g : g;
-      if constexpr (FLAGS) fl[c] = (uint8_t)((tc0 + c == r.col0 ? 1 : 0) | f32);
+      if (FLAGS && f32) gs[c] = acc32_slot((float)g, tc0 + c == r.col0);
+      else gs[c] = rnd ? (double)(float)g : g;
     }
     return;
   }
@@ -71,7 +81,11 @@ __device__ __forceinline__ void gather_g(const DevPlan& P, const Run* __restrict
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       const int c = c0 + u * NT;
-      if (c < tw) gs[c] = (id[u] & kTagRound) ? (double)(float)v[u] : v[u];
+      if (c < tw) {
+        const uint8_t f = FLAGS ? fl[c] : 0;
+        if (FLAGS && (f & 2)) gs[c] = acc32_slot((float)v[u], f & 1);
+        else gs[c] = (id[u] & kTagRound) ? (double)(float)v[u] : v[u];
+      }
     }
   }
 }
@@ -84,7 +98,7 @@ __device__ __forceinline__ double z_epilogue(const DevPlan& P, double s, int zi)
 
 // One CTA = one segment: rows [row0, row0+R) of a column-major item stream.
 template <int F32MODE, int OUT, int NT>
-__global__ void __launch_bounds__(NT, 1024 / NT) seg_kernel(DevPlan P, const Seg* __restrict__ segs,
+__global__ void __launch_bounds__(NT, (OUT == OUT_Y && F32MODE != F32_ALL64) ? HMX_MIXED_MINB : 1024 / NT) seg_kernel(DevPlan P, const Seg* __restrict__ segs,
                                                           const double* __restrict__ x, S2Out out) {
   // stage 1 segments have a single run (no index expansion) and <= 1024 columns
   constexpr int WMAX = OUT == OUT_Z ? kS1WMax : kSegWMax;
@@ -144,6 +158,13 @@ __global__ void __launch_bounds__(NT, 1024 / NT) seg_kernel(DevPlan P, const Seg
     }
   }
 
+  // FP64-part partials go to shared memory now (frees their registers for
+  // the FP32 part; red64 is read only in the epilogue)
+  if (sg.W64 > 0 && q64 < g64) {
+    red64[q64 * rp64 + 2 * p64] = a0;
+    red64[q64 * rp64 + 2 * p64 + 1] = a1;
+  }
+
   // ---------------- FP32 part: 4 rows x 16 bytes per thread
   const int rp32 = (R + 3) & ~3;
   const int tpg32 = rp32 >> 2;
@@ -151,40 +172,44 @@ __global__ void __launch_bounds__(NT, 1024 / NT) seg_kernel(DevPlan P, const Seg
   const int q32 = tid / tpg32, p32 = tid - q32 * tpg32;
   double b[4] = {0.0, 0.0, 0.0, 0.0};
   float b32[4] = {0.f, 0.f, 0.f, 0.f};
-  // FP32-accumulated columns start at c32 (FP64-accumulated items first;
-  // -1: no group table, fall back to the per-column flag)
-  int c32 = -1;
-  if (F32MODE == F32_MIXED && OUT == OUT_Y && sg.gtab >= 0) c32 = P.gtab[sg.gtab + g32 + 1];
-  int tile0 = 0;
-  auto consume = [&](const float4& mv4, int cc) {
+  // the part holds FP64-accumulated items first, then FP32-accumulated ones
+  // from column c32 on (plan: gtab after the group cuts, or alone at -2-gtab)
+  int c32 = sg.W32;
+  if constexpr (F32MODE == F32_ALL32) c32 = 0;
+  if constexpr (F32MODE == F32_MIXED) {
+    if (sg.gtab >= 0) c32 = P.gtab[sg.gtab + g32 + 1];
+    else if (sg.gtab <= -2) c32 = P.gtab[-2 - sg.gtab];
+  }
+  // widened FP32 data, FP64 accumulation
+  auto consume64 = [&](const float4& v, int cc) {
     const double g = gs[cc];
-    const float mv[4] = {mv4.x, mv4.y, mv4.z, mv4.w};
-    if constexpr (F32MODE == F32_ALL64) {
+    b[0] = fma((double)v.x, g, b[0]);
+    b[1] = fma((double)v.y, g, b[1]);
+    b[2] = fma((double)v.z, g, b[2]);
+    b[3] = fma((double)v.w, g, b[3]);
+  };
+  // FP32 chain per (row, item): the gathered slot holds the FP32 source in
+  // its low word and "first column of an item" in its high word
+  auto consume32 = [&](const float4& v, int cc) {
+    const double e = gs[cc];
+    // item start: close the previous FP32 partial (a real branch: the
+    // compiler would otherwise predicate the flush onto every column)
+    if (OUT == OUT_Y && __double2hiint(e) != 0) {
 #pragma unroll
-      for (int i = 0; i < 4; ++i) b[i] = fma((double)mv[i], g, b[i]);
-    } else {
-      bool acc32 = true;
-      if (F32MODE == F32_MIXED) acc32 = c32 >= 0 ? (tile0 + cc >= c32) : (fl[cc] & 2) != 0;
-      if (acc32) {
-        if (fl[cc] & 1) {  // first column of an item: close the previous FP32 partial
-#pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            b[i] += (double)b32[i];
-            b32[i] = 0.f;
-          }
-        }
-        const float gf = (float)g;
-#pragma unroll
-        for (int i = 0; i < 4; ++i) b32[i] = fmaf(mv[i], gf, b32[i]);
-      } else {
-#pragma unroll
-        for (int i = 0; i < 4; ++i) b[i] = fma((double)mv[i], g, b[i]);
+      for (int i = 0; i < 4; ++i) {
+        b[i] += (double)b32[i];
+        b32[i] = 0.f;
       }
+      __syncwarp(__activemask());
     }
+    const float gf = __int_as_float(__double2loint(e));
+    b32[0] = fmaf(v.x, gf, b32[0]);
+    b32[1] = fmaf(v.y, gf, b32[1]);
+    b32[2] = fmaf(v.z, gf, b32[2]);
+    b32[3] = fmaf(v.w, gf, b32[3]);
   };
   for (int tc0 = 0; tc0 < sg.W32; tc0 += WMAX) {
     const int tw = min(WMAX, sg.W32 - tc0);
-    tile0 = tc0;
     const bool act = q32 < g32;
     int cb = act ? (int)((int64_t)tw * q32 / g32) : 0;
     int ce = act ? (int)((int64_t)tw * (q32 + 1) / g32) : 0;
@@ -194,36 +219,56 @@ __global__ void __launch_bounds__(NT, 1024 / NT) seg_kernel(DevPlan P, const Seg
       cb = P.gtab[sg.gtab + q32];
       ce = P.gtab[sg.gtab + q32 + 1];
     }
+    // [cb, cm): FP64-accumulated columns, [cm, ce): FP32-accumulated ones
+    const int cm = min(ce, max(cb, c32 - tc0));
     const float* __restrict__ col = P.blob32 + sg.off32 + (int64_t)tc0 * rp32 + 4 * p32;
     float4 m[8];
-    int c = cb;
+    {
+      const int e0 = cb < cm ? cm : ce;
 #pragma unroll
-    for (int u = 0; u < 8; ++u)
-      if (c + u < ce) m[u] = ld_stream(col + (int64_t)(c + u) * rp32, pol);
+      for (int u = 0; u < 8; ++u)
+        if (cb + u < e0) m[u] = ld_stream(col + (int64_t)(cb + u) * rp32, pol);
+    }
     if (OUT == OUT_Y && tc0 == 0 && sg.W64 == 0) asm volatile("griddepcontrol.wait;" ::: "memory");
     __syncthreads();
     gather_g<F32MODE != F32_ALL64, NT>(P, P.runs + sg.run0 + sg.nrun64, sg.nrun32, tc0, tw, x, gs, fl,
-                                   sidx);
+                                       sidx);
     __syncthreads();
-    for (;;) {
-      if (c + 8 <= ce) {  // full batch: unpredicated hot path
+    // batches of 8 columns: unpredicated when full, predicated at the end
+    auto drain = [&](int c, int e, auto&& consume) {
+      for (;;) {
+        if (c + 8 <= e) {
 #pragma unroll
-        for (int u = 0; u < 8; ++u) consume(m[u], c + u);
-      } else {
+          for (int u = 0; u < 8; ++u) consume(m[u], c + u);
+        } else {
 #pragma unroll
-        for (int u = 0; u < 8; ++u)
-          if (c + u < ce) consume(m[u], c + u);
+          for (int u = 0; u < 8; ++u)
+            if (c + u < e) consume(m[u], c + u);
+        }
+        c += 8;
+        if (c >= e) break;
+        if (c + 8 <= e) {
+#pragma unroll
+          for (int u = 0; u < 8; ++u) m[u] = ld_stream(col + (int64_t)(c + u) * rp32, pol);
+        } else {
+#pragma unroll
+          for (int u = 0; u < 8; ++u)
+            if (c + u < e) m[u] = ld_stream(col + (int64_t)(c + u) * rp32, pol);
+        }
       }
-      c += 8;
-      if (c >= ce) break;
-      if (c + 8 <= ce) {
+    };
+    if constexpr (F32MODE != F32_ALL32) {
+      if (cb < cm) {
+        drain(cb, cm, consume64);
+        if (cm < ce) {
 #pragma unroll
-        for (int u = 0; u < 8; ++u) m[u] = ld_stream(col + (int64_t)(c + u) * rp32, pol);
-      } else {
-#pragma unroll
-        for (int u = 0; u < 8; ++u)
-          if (c + u < ce) m[u] = ld_stream(col + (int64_t)(c + u) * rp32, pol);
+          for (int u = 0; u < 8; ++u)
+            if (cm + u < ce) m[u] = ld_stream(col + (int64_t)(cm + u) * rp32, pol);
+        }
       }
+    }
+    if constexpr (F32MODE != F32_ALL64) {
+      if (cm < ce) drain(cm, ce, consume32);
     }
   }
   if constexpr (F32MODE != F32_ALL64) {
@@ -233,10 +278,6 @@ __global__ void __launch_bounds__(NT, 1024 / NT) seg_kernel(DevPlan P, const Seg
 
   // ---------------- fixed-order reduction over thread groups
   __syncthreads();
-  if (sg.W64 > 0 && q64 < g64) {
-    red64[q64 * rp64 + 2 * p64] = a0;
-    red64[q64 * rp64 + 2 * p64 + 1] = a1;
-  }
   if (sg.W32 > 0 && q32 < g32) {
 #pragma unroll
     for (int i = 0; i < 4; ++i) red32[q32 * rp32 + 4 * p32 + i] = b[i];

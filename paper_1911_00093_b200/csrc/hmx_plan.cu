@@ -324,6 +324,8 @@ static int plan_create_impl(const hmx_matrix_desc* d, int device, const hmx_plan
     const int64_t* t = d->table + 5 * it.block;
     return it.cls == 0 ? t[3] - t[2] : it.cls == 1 ? d->khi[it.block] : d->klo[it.block];
   };
+  const char* dw_env = std::getenv("HMX_DENSE_WEIGHT");
+  const double dense_weight = dw_env ? std::atof(dw_env) : 1.8;
   const bool dense_single = pipe == P_M1S || pipe == P_M2S;  // A32 . x32 in FP32
   const bool u_acc32 = pipe == P_M1S || pipe == P_M1M;       // U32 . z32 in FP32
   bool any_acc32 = false, any_acc64_in32 = false;
@@ -394,9 +396,36 @@ static int plan_create_impl(const hmx_matrix_desc* d, int device, const hmx_plan
       gtab.push_back(0);
       int64_t prev = 0;
       size_t k = 0;
+      // balance estimated cost, not columns: when the part mixes FP64- and
+      // FP32-accumulated items, a dense-block column costs dense_weight
+      // relative to a low-rank slab column (measured on config 4: m1-mixed
+      // and m2-single stage 2 -4..-7 %; pure FP32 parts balance by columns)
+      const bool mixed_part = !acc.empty() && acc.front().a > 0;
+      std::vector<double> wcol(1, 0.0);  // cost prefix at every item boundary
+      std::vector<int64_t> ccol(1, 0);
+      for (int32_t j = 0; j < sg.nrun32; ++j) {
+        const Run& r = runs[(size_t)(sg.run0 + sg.nrun64 + j)];
+        const double w = (mixed_part && !(r.flags & RUN_Z)) ? dense_weight : 1.0;
+        ccol.push_back(ccol.back() + r.width);
+        wcol.push_back(wcol.back() + w * r.width);
+      }
+      auto cost_at = [&](int64_t c) {
+        const size_t i = (size_t)(std::upper_bound(ccol.begin(), ccol.end(), c) - ccol.begin()) - 1;
+        if (i + 1 >= ccol.size()) return wcol.back();
+        const double w = (wcol[i + 1] - wcol[i]) / (double)(ccol[i + 1] - ccol[i]);
+        return wcol[i] + w * (double)(c - ccol[i]);
+      };
+      auto col_at = [&](double t) {
+        const size_t i = (size_t)(std::upper_bound(wcol.begin(), wcol.end(), t) - wcol.begin()) - 1;
+        if (i + 1 >= wcol.size()) return (double)ccol.back();
+        const double w = (wcol[i + 1] - wcol[i]) / (double)(ccol[i + 1] - ccol[i]);
+        return (double)ccol[i] + (t - wcol[i]) / w;
+      };
+      const double total = wcol.back();
       for (int64_t q = 1; q < G; ++q) {
-        const double share = (double)(sg.W32 - prev) / (double)(G - q + 1);
-        int64_t cut = (int64_t)std::llround((double)prev + share);
+        const double pc = cost_at(prev);
+        const double share = (total - pc) / (double)(G - q + 1);
+        int64_t cut = (int64_t)std::llround(col_at(pc + share));
         while (k < acc.size() && acc[k].b <= cut) ++k;
         if (k < acc.size() && acc[k].a < cut && cut < acc[k].b) {
           // inside an FP32 item: move to its nearer end
@@ -408,6 +437,18 @@ static int plan_create_impl(const hmx_matrix_desc* d, int device, const hmx_plan
       }
       gtab.push_back(sg.W32);
       gtab.push_back((int32_t)(acc.empty() ? sg.W32 : acc.front().a));  // first FP32-accumulated column
+    } else if (sg.W32 > kSegWMax && (dense_single || u_acc32)) {
+      // wide part (tiled, no group cuts): only the first FP32-accumulated column
+      int32_t first = sg.W32;
+      for (int32_t j = 0; j < sg.nrun32; ++j) {
+        const Run& r = runs[(size_t)(sg.run0 + sg.nrun64 + j)];
+        if (r.flags & RUN_ACC32) {
+          first = r.col0;
+          break;
+        }
+      }
+      sg.gtab = -2 - (int32_t)gtab.size();
+      gtab.push_back(first);
     }
     sg.off64 = off64;
     sg.off32 = off32;
