@@ -77,8 +77,6 @@ struct hmx_plan {
   double* d_dots = nullptr;      // 2 reduced dots
   unsigned long long* d_first_bad = nullptr;
   // pinned host staging
-  double* h_x = nullptr;
-  double* h_y = nullptr;
   int* h_flag = nullptr;
   // input of the most recent matvec (for the non-finite probe)
   const double* last_xp = nullptr;
