@@ -28,27 +28,49 @@ __device__ __forceinline__ double acc32_slot(float g, bool start) {
   return __hiloint2double(start ? 1 : 0, __float_as_int(g));
 }
 
+// 8-byte asynchronous global -> shared copies (the x / z segments of a tile)
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"((unsigned)__cvta_generic_to_shared(smem)),
+               "l"(gmem)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
+}
+
 // Stage a tile [tc0, tc0+tw) of one part's source vector g (x segments and z
-// vectors, in item order) into shared memory; FP32-accumulated columns are
-// stored as acc32_slot (fl: scratch flags, bit 0 item start, bit 1 FP32 item).
-// A single run (every stage-1 segment) is a contiguous copy.  Otherwise the
-// runs are expanded into a per-column source index in shared memory first,
-// so every column's load is independent (no dependent run lookups).
-constexpr int kRunsSmem = 512;
+// vectors, in item order) into shared memory with cp.async; FP32-accumulated
+// columns are then rewritten as acc32_slot and FP32-shadow columns rounded
+// (fl: scratch flags, bit 0 item start, bit 1 FP32 item).  A single run
+// (every stage-1 segment) is a contiguous copy.  Otherwise the runs are first
+// expanded into a per-column source index in shared memory, so every
+// column's copy is independent (no dependent run lookups).
 constexpr int32_t kTagZ = 1 << 30, kTagRound = 1 << 29, kIdxMask = kTagRound - 1;
-template <bool FLAGS, int NT>
+template <bool FLAGS, int NT, int WMAX>
 __device__ __forceinline__ void gather_g(const DevPlan& P, const Run* __restrict__ runs, int nrun,
                                          int tc0, int tw, const double* __restrict__ x,
                                          double* gs, uint8_t* fl, int32_t* sidx) {
+  constexpr int PER = WMAX / NT;  // columns per thread
   if (nrun == 1) {
     const Run r = runs[0];
     const double* src = ((r.flags & RUN_Z) ? P.z : x) + r.src + (tc0 - r.col0);
     const bool rnd = (r.flags & RUN_ROUND) != 0;
-    const uint8_t f32 = (r.flags & RUN_ACC32) ? 2 : 0;
-    for (int c = threadIdx.x; c < tw; c += NT) {
-      const double g = src[c];
-      if (FLAGS && f32) gs[c] = acc32_slot((float)g, tc0 + c == r.col0);
-      else gs[c] = rnd ? (double)(float)g : g;
+    const bool f32 = FLAGS && (r.flags & RUN_ACC32);
+#pragma unroll
+    for (int u = 0; u < PER; ++u) {
+      const int c = threadIdx.x + u * NT;
+      if (c < tw) cp_async8(gs + c, src + c);
+    }
+    cp_async_wait_all();
+    if (rnd || f32) {
+#pragma unroll
+      for (int u = 0; u < PER; ++u) {
+        const int c = threadIdx.x + u * NT;
+        if (c < tw) {
+          const double g = gs[c];
+          gs[c] = f32 ? acc32_slot((float)g, tc0 + c == r.col0) : (double)(float)g;
+        }
+      }
     }
     return;
   }
@@ -65,27 +87,21 @@ __device__ __forceinline__ void gather_g(const DevPlan& P, const Run* __restrict
   }
   __syncthreads();
   const double* __restrict__ z = P.z;
-  for (int c0 = threadIdx.x; c0 < tw; c0 += 4 * NT) {
-    int32_t id[4];
-    double v[4];
+  int32_t id[PER];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int c = c0 + u * NT;
-      id[u] = c < tw ? sidx[c] : 0;
-    }
+  for (int u = 0; u < PER; ++u) {
+    const int c = threadIdx.x + u * NT;
+    id[u] = c < tw ? sidx[c] : 0;
+    if (c < tw) cp_async8(gs + c, ((id[u] & kTagZ) ? z : x) + (id[u] & kIdxMask));
+  }
+  cp_async_wait_all();
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int c = c0 + u * NT;
-      v[u] = c < tw ? ((id[u] & kTagZ) ? z : x)[id[u] & kIdxMask] : 0.0;
-    }
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int c = c0 + u * NT;
-      if (c < tw) {
-        const uint8_t f = FLAGS ? fl[c] : 0;
-        if (FLAGS && (f & 2)) gs[c] = acc32_slot((float)v[u], f & 1);
-        else gs[c] = (id[u] & kTagRound) ? (double)(float)v[u] : v[u];
-      }
+  for (int u = 0; u < PER; ++u) {
+    const int c = threadIdx.x + u * NT;
+    if (c < tw) {
+      const uint8_t f = FLAGS ? fl[c] : 0;
+      if (FLAGS && (f & 2)) gs[c] = acc32_slot((float)gs[c], f & 1);
+      else if (id[u] & kTagRound) gs[c] = (double)(float)gs[c];
     }
   }
 }
@@ -139,7 +155,7 @@ __global__ void __launch_bounds__(NT, (OUT == OUT_Y && F32MODE != F32_ALL64) ? H
       if (c + u < ce) m[u] = ld_stream(col + (int64_t)(c + u) * rp64, pol);
     if (OUT == OUT_Y && tc0 == 0) asm volatile("griddepcontrol.wait;" ::: "memory");
     __syncthreads();
-    gather_g<false, NT>(P, P.runs + sg.run0, sg.nrun64, tc0, tw, x, gs, fl, sidx);
+    gather_g<false, NT, WMAX>(P, P.runs + sg.run0, sg.nrun64, tc0, tw, x, gs, fl, sidx);
     __syncthreads();
     for (;;) {
 #pragma unroll
@@ -231,8 +247,8 @@ __global__ void __launch_bounds__(NT, (OUT == OUT_Y && F32MODE != F32_ALL64) ? H
     }
     if (OUT == OUT_Y && tc0 == 0 && sg.W64 == 0) asm volatile("griddepcontrol.wait;" ::: "memory");
     __syncthreads();
-    gather_g<F32MODE != F32_ALL64, NT>(P, P.runs + sg.run0 + sg.nrun64, sg.nrun32, tc0, tw, x, gs, fl,
-                                       sidx);
+    gather_g<F32MODE != F32_ALL64, NT, WMAX>(P, P.runs + sg.run0 + sg.nrun64, sg.nrun32, tc0, tw, x, gs,
+                                             fl, sidx);
     __syncthreads();
     // batches of 8 columns: unpredicated when full, predicated at the end
     auto drain = [&](int c, int e, auto&& consume) {
