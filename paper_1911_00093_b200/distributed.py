@@ -133,19 +133,21 @@ class DistributedOperator:
         self._pad_in = torch.zeros(L, dtype=torch.float64, device=self.device)
         self._gathered = torch.zeros(L * slices.world, dtype=torch.float64, device=self.device)
         self._full = torch.zeros(self.n, dtype=torch.float64, device=self.device)
+        # position of every permuted index in the padded allgather buffer
+        # (one index_select un-pads it)
+        self._unpad = torch.cat([torch.arange(k * L, k * L + (b - a), dtype=torch.int64)
+                                 for k, (a, b) in enumerate(slices.span(q) for q in range(slices.world))]
+                                ).to(self.device)
         if plan is not None:
             self._dots = torch.zeros(2, dtype=torch.float64, device=self.device)
             self._flag = torch.zeros(1, dtype=torch.int32, device=self.device)
 
     def gather(self, x_local):
         """The ONE collective per matvec: allgather of the iterate's slices."""
-        L = self.slices.padded
         m = self.r1 - self.r0
         self._pad_in[:m].copy_(x_local)
         self.dist.all_gather_into_tensor(self._gathered, self._pad_in, group=self.group)
-        for k in range(self.slices.world):
-            a, b = self.slices.span(k)
-            self._full[a:b].copy_(self._gathered[k * L:k * L + (b - a)])
+        self.torch.index_select(self._gathered, 0, self._unpad, out=self._full)
         return self._full
 
     def _gpu_apply(self, x_full, w1, yy):
@@ -279,7 +281,9 @@ def make_gpu_operator(h, scheme: str, slices: RowSlices, rank: int, device, grou
 
 def bench_main(args, build_workload, workload_name, metric):
     """bench.py --gpus N under torchrun: the whole-job matvec rate of the
-    row-partitioned operator (one allgather per matvec), max over ranks."""
+    row-partitioned operator (one allgather per matvec), max over ranks.
+    Same JSON contract as the single-GPU line (roofline of rank 0's stage-2
+    kernel, end-to-end rate with host slices, clocks of rank 0's GPU)."""
     import json
     import os
 
@@ -291,15 +295,19 @@ def bench_main(args, build_workload, workload_name, metric):
     from .partition import build_block_partition, build_cluster_tree
     from .problem import jittered_sphere_mesh
 
-    rank = int(os.environ["RANK"])
-    world = int(os.environ["WORLD_SIZE"])
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", rank))
     torch.cuda.set_device(local)
     device = torch.device("cuda", local)
-    dist.init_process_group("nccl", device_id=device)
+    if not dist.is_initialized():
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29517")
+        dist.init_process_group("nccl", device_id=device, rank=rank, world_size=world)
     c = bench_mod.CONFIGS[args.config]
     t0 = time.perf_counter()
-    mesh = jittered_sphere_mesh(c["level"], seed=42)
+    mesh = jittered_sphere_mesh(c["level"], seed=42, centers=c.get("centers", ((0.0, 0.0, 0.0),)),
+                                voltages=c.get("voltages"))
     part = build_block_partition(build_cluster_tree(mesh, c["leaf"]), 2.0)
     # partition on an estimate (ranks unknown before ACA): ranks ~ 11
     kinds = part.table[:, 4].astype(np.int32)
@@ -307,32 +315,67 @@ def bench_main(args, build_workload, workload_name, metric):
     slices = RowSlices(partition_rows(part.table, kinds, est, mesh.n, world))
     h = build_hmatrix(mesh, partition=part, aca_tol=c["aca"], rows=slices.span(rank))
     t_build = time.perf_counter() - t0
-    results = {}
-    for name in [bench_mod.HEADLINE] + [s for s in args.variants if s != bench_mod.HEADLINE][:1]:
-        op, sh = make_gpu_operator(h, name, slices, rank, device)
-        x = torch.from_numpy(np.random.default_rng(42).uniform(-1.0, 1.0, mesh.n)).to(device)
-        a, b_ = slices.span(rank)
-        x_local = x[torch.as_tensor(np.asarray(h.permutation)[a:b_], device=device)].contiguous()
-        for _ in range(args.warmup):
-            op.gather(x_local)
-            op.local_apply(op._full, None, False)
-        torch.cuda.synchronize()
+    peak, peak_src = bench_mod.measured_peak()
+    a, b_ = slices.span(rank)
+    x_np = np.random.default_rng(42).uniform(-1.0, 1.0, mesh.n)
+    x_host = torch.from_numpy(np.ascontiguousarray(x_np[np.asarray(h.permutation)[a:b_]])).pin_memory()
+    y_host = torch.empty(b_ - a, dtype=torch.float64).pin_memory()
+    results, clocks, headline = {}, None, None
+
+    def step(op, x_local):
+        op.gather(x_local)
+        return op.local_apply(op._full, None, False)[0]
+
+    def timed(fn, k):
         dist.barrier()
-        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        ev0.record()
-        for _ in range(args.steps):
-            op.gather(x_local)
-            op.local_apply(op._full, None, False)
-        ev1.record()
         torch.cuda.synchronize()
-        ms = torch.tensor([ev0.elapsed_time(ev1) / args.steps], device=device)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(k):
+            fn()
+        e1.record()
+        torch.cuda.synchronize()
+        ms = torch.tensor([e0.elapsed_time(e1) / k], device=device)
         dist.all_reduce(ms, op=dist.ReduceOp.MAX)
-        algo = sum(int(v) for v in [sh.payload_bytes]) + 16 * mesh.n
-        results[name] = {"ms": float(ms), "matvec_per_s": 1e3 / float(ms)}
+        return float(ms)
+
+    names = [bench_mod.HEADLINE] + [s for s in args.variants if s != bench_mod.HEADLINE][:1]
+    for name in names:
+        op, sh = make_gpu_operator(h, name, slices, rank, device)
+        x_local = x_host.to(device)
+        for _ in range(args.warmup):
+            step(op, x_local)
+        if name == bench_mod.HEADLINE and rank == 0:
+            with bench_mod.ClockSampler(local) as clk:
+                ms = timed(lambda: step(op, x_local), args.steps)
+            clocks = clk.summary()
+        else:
+            ms = timed(lambda: step(op, x_local), args.steps)
+        local_bytes = torch.tensor([float(op.plan.info()["payload_bytes"])], device=device)
+        dist.all_reduce(local_bytes)
+        r = op.plan.bench(3, max(10, args.steps // 2))  # local two-stage product alone
+        info = op.plan.info()
+        entry = {"ms": ms, "matvec_per_s": 1e3 / ms, "payload_bytes_all_ranks": float(local_bytes),
+                 "local_ms_rank0": r["ms"], "stage1_ms_rank0": r["stage1_ms"],
+                 "stage2_ms_rank0": r["stage2_ms"], "rows_rank0": b_ - a}
+        if name == bench_mod.HEADLINE:
+            # end to end: this rank's x slice from pinned host memory, the
+            # allgather, the local product, its y slice back to the host
+            def e2e_step():
+                x_local.copy_(x_host, non_blocking=True)
+                y = step(op, x_local)
+                y_host.copy_(y, non_blocking=True)
+            e2e_ms = timed(e2e_step, max(5, min(args.steps, 50)))
+            entry["e2e_ms"] = e2e_ms
+            s2_bytes = info["stage2_bytes"] + 8 * (b_ - a)
+            headline = (entry, s2_bytes, r, info)
+        results[name] = entry
         op.plan.close()
     dist.barrier()
     if rank == 0:
-        ms = results[bench_mod.HEADLINE]["ms"]
+        entry, s2_bytes, r, info = headline
+        ms = entry["ms"]
+        dom = s2_bytes / (r["stage2_ms"] * 1e6)
         print(json.dumps({
             "metric": metric, "value": 1e3 / ms, "unit": "matvec/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
@@ -340,8 +383,17 @@ def bench_main(args, build_workload, workload_name, metric):
             "data": "synthetic (seeded jittered icosphere, BASELINE.json recipe)",
             "config": {"workload": workload_name(args.config), "scheme": bench_mod.HEADLINE,
                        "n": int(mesh.n), "parallelism": f"row partition x{world}",
-                       "cuts": slices.cuts, "build_s": t_build},
-            "gpu_launches": 2 * args.steps, "variants": results,
-            "note": "each step = one allgather of the iterate + the local two-stage product",
+                       "cuts": slices.cuts, "build_s": t_build,
+                       "l2": "per-rank payload >> 126 MB L2 at configs 4-5 (no flush)"},
+            "roofline": {"bound": "hbm", "achieved": dom, "peak": peak, "unit": "GB/s",
+                         "frac": dom / peak, "traffic": None, "peak_source": peak_src,
+                         "kernel": "rank 0 stage-2 seg_kernel (local rows)",
+                         "algorithmic_bytes_per_launch": s2_bytes},
+            "cpu_baseline": None,
+            "e2e": {"value": 1e3 / entry["e2e_ms"], "unit": "matvec/s",
+                    "h2d_bytes_per_step": 8 * int(mesh.n), "d2h_bytes_per_step": 8 * int(mesh.n)},
+            "gpu_launches": 2 * args.steps, "clocks": clocks, "variants": results,
+            "note": "each step = one NCCL allgather of the iterate + the local two-stage product; "
+                    "cpu_baseline is reported by the N=1 run",
         }), flush=True)
     dist.destroy_process_group()
