@@ -15,6 +15,11 @@
  *   hmx_nonfinite_block <- _check_finite's block rescan   (matvec.py:123-135)
  *   hmx_true_residual   <- true_residual(h64, x, b)       (solver.py:56-65)
  *   hmx_bicgstab        <- bicgstab(sh, h64, b, cfg)      (solver.py:68-168)
+ *   hmx_master_create + hmx_plan_create_prepared
+ *                       <- prepare_scheme(h, scheme) run on the device from
+ *                          FP64 masters uploaded once: scale_decompose,
+ *                          split_indices, _cast_fp32 (precision.py:121-162,
+ *                          :241-329), then the plan, with no payload upload
  *
  * All vectors are float64.  Pointers are host pointers unless a flag says
  * device.  Every call returns an hmx_status; hmx_last_error() describes the
@@ -35,7 +40,8 @@ typedef enum {
   HMX_ERR_ARG = 1,        /* invalid argument or inconsistent descriptor */
   HMX_ERR_CUDA = 2,       /* CUDA runtime failure (no device, OOM, ...) */
   HMX_ERR_NONFINITE = 3,  /* matvec result not finite: FloatingPointError */
-  HMX_ERR_SHAPE = 4       /* vector length does not match the matrix: ValueError */
+  HMX_ERR_SHAPE = 4,      /* vector length does not match the matrix: ValueError */
+  HMX_ERR_OVERFLOW = 5    /* FP32 cast overflow while preparing a scheme: OverflowError */
 } hmx_status;
 
 /* Precision schemes of the reference (precision.py:46-104). */
@@ -105,6 +111,35 @@ typedef struct {
   int32_t s1_grid, s1_block, s2_grid, s2_block;
 } hmx_plan_info;
 
+/*
+ * FP64 masters of one H-matrix (python PackedMaster; reference HMatrixF64,
+ * compress.py:236-253), uploaded once by hmx_master_create:
+ *   kind[k] == 0  dense m x n row-major at offset[k]
+ *   kind[k] == 1  low rank: U m x rank[k] then Vt rank[k] x n at offset[k]
+ *   kind[k] == 2  not built (row-restricted build)
+ */
+typedef struct {
+  int64_t n;
+  int64_t n_blocks;
+  const int64_t* perm;
+  const int64_t* table;
+  const int32_t* kind;
+  const int64_t* offset;
+  const int64_t* rank;
+  const double* data;
+  int64_t n_data;
+} hmx_master_desc;
+
+typedef struct hmx_master hmx_master;
+
+/* What prepare_scheme reports besides the payloads (SchemeHMatrix fields). */
+typedef struct {
+  int64_t payload_bytes;   /* precision.py:332-334 */
+  int64_t underflow_count; /* nonzero values whose FP32 cast is below FLT_MIN (precision.py:241-253) */
+  int64_t overflow_block;  /* first block (partition order) whose FP32 cast overflows, else -1 */
+  int64_t fp32_ranks;      /* Method 3: ranks in the FP32 class */
+} hmx_prepare_info;
+
 /* matvec flags */
 #define HMX_DEVICE_PTRS 1 /* x and y are device pointers */
 #define HMX_PERMUTED 2    /* x and y are in permuted (cluster-tree) order */
@@ -160,6 +195,22 @@ int hmx_bicgstab(hmx_plan* plan, hmx_plan* plan64, const double* b, double tol, 
  * synchronising. */
 int hmx_apply_local(hmx_plan* plan, const double* xp, double* y, const double* w1, int yy,
                     double* dots, int* nonfinite, uint64_t stream);
+
+/* Upload the FP64 masters of one H-matrix once (device-resident). */
+int hmx_master_create(const hmx_master_desc* desc, int device, hmx_master** out);
+void hmx_master_destroy(hmx_master* master);
+
+/* prepare_scheme(h, scheme) on the device followed by hmx_plan_create: the
+ * scaling (scale_decompose), the Method-3 split (split_indices, with the
+ * threshold factor 10**(-c) passed as split_factor, computed by the caller
+ * exactly as the reference does) and the FP32 casts run on the GPU, reading
+ * the resident masters; no payload crosses the host link.  The plan is
+ * identical to hmx_plan_create on the host-prepared payloads of the same
+ * scheme.  Returns HMX_ERR_OVERFLOW (info->overflow_block set) when an FP32
+ * cast overflows.  underflow_count covers the whole matrix for a full plan
+ * (opt NULL). */
+int hmx_plan_create_prepared(hmx_master* master, int scheme, double split_factor,
+                             const hmx_plan_options* opt, hmx_plan** out, hmx_prepare_info* info);
 
 /* Benchmark helper: `iters` device matvecs in permuted order on device
  * buffers, timed with CUDA events on the plan's stream after `warmup`

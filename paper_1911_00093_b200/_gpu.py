@@ -15,7 +15,7 @@ import numpy as np
 
 from . import _native
 
-HMX_OK, HMX_ERR_ARG, HMX_ERR_CUDA, HMX_ERR_NONFINITE, HMX_ERR_SHAPE = 0, 1, 2, 3, 4
+HMX_OK, HMX_ERR_ARG, HMX_ERR_CUDA, HMX_ERR_NONFINITE, HMX_ERR_SHAPE, HMX_ERR_OVERFLOW = 0, 1, 2, 3, 4, 5
 HMX_DEVICE_PTRS, HMX_PERMUTED = 1, 2
 
 SCHEME_CODES = {"m1-double": 0, "m1-single": 1, "m1-mixed": 2, "m2-double": 3,
@@ -60,6 +60,18 @@ class SolveReport(ctypes.Structure):
                 ("device_ms", ctypes.c_double)]
 
 
+class MasterDesc(ctypes.Structure):
+    _fields_ = [("n", ctypes.c_int64), ("n_blocks", ctypes.c_int64),
+                ("perm", _i64p), ("table", _i64p), ("kind", _i32p), ("offset", _i64p),
+                ("rank", _i64p), ("data", ctypes.POINTER(ctypes.c_double)),
+                ("n_data", ctypes.c_int64)]
+
+
+class PrepareInfo(ctypes.Structure):
+    _fields_ = [("payload_bytes", ctypes.c_int64), ("underflow_count", ctypes.c_int64),
+                ("overflow_block", ctypes.c_int64), ("fp32_ranks", ctypes.c_int64)]
+
+
 # every exported symbol of include/hmx_gpu.h with its ctypes signature
 SIGNATURES = {
     "hmx_last_error": (ctypes.c_char_p, []),
@@ -82,6 +94,13 @@ SIGNATURES = {
     "hmx_apply_local": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
                                        ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p,
                                        ctypes.c_void_p, ctypes.c_uint64]),
+    "hmx_master_create": (ctypes.c_int, [ctypes.POINTER(MasterDesc), ctypes.c_int,
+                                         ctypes.POINTER(ctypes.c_void_p)]),
+    "hmx_master_destroy": (None, [ctypes.c_void_p]),
+    "hmx_plan_create_prepared": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_double,
+                                                ctypes.POINTER(PlanOptions),
+                                                ctypes.POINTER(ctypes.c_void_p),
+                                                ctypes.POINTER(PrepareInfo)]),
 }
 
 _lib = None
@@ -184,6 +203,37 @@ class Plan:
         self.device = device
         self._lib = lib
 
+    @classmethod
+    def prepared(cls, master: "Master", scheme_label: str, split_factor: float = 0.0,
+                 row_range=None) -> tuple["Plan", dict]:
+        """prepare_scheme + plan on the device from resident masters
+        (hmx_plan_create_prepared).  Raises OverflowError like the reference's
+        _cast_fp32 (precision.py:241-253); the message is completed by the
+        caller, which knows the block geometry."""
+        lib = load_library()
+        code = SCHEME_CODES.get(scheme_label, 6 if scheme_label.startswith("m3") else None)
+        if code is None:
+            raise ValueError(f"unsupported scheme {scheme_label!r}")
+        opt = PlanOptions()
+        if row_range is not None:
+            opt.row_begin, opt.row_end = int(row_range[0]), int(row_range[1])
+        h = ctypes.c_void_p()
+        info = PrepareInfo()
+        rc = lib.hmx_plan_create_prepared(master.handle, code, float(split_factor),
+                                          ctypes.byref(opt), ctypes.byref(h), ctypes.byref(info))
+        out = {f: getattr(info, f) for f, _ in PrepareInfo._fields_}
+        if rc == HMX_ERR_OVERFLOW:
+            raise OverflowError(f"block {out['overflow_block']}")
+        check(rc, "hmx_plan_create_prepared")
+        self = cls.__new__(cls)
+        self._keep = []
+        self.handle = h
+        self.n = master.n
+        self.scheme = scheme_label
+        self.device = master.device
+        self._lib = lib
+        return self, out
+
     def info(self) -> dict:
         i = PlanInfo()
         check(self._lib.hmx_plan_get_info(self.handle, ctypes.byref(i)), "hmx_plan_get_info")
@@ -235,6 +285,52 @@ class Plan:
     def close(self):
         if getattr(self, "handle", None):
             self._lib.hmx_plan_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class Master:
+    """FP64 masters of one H-matrix resident on a device (hmx_master_create);
+    schemes are then prepared on the device with Plan.prepared."""
+
+    def __init__(self, packed_master, table, perm, n: int, device: int = 0):
+        lib = load_library()
+        keep = [np.ascontiguousarray(perm, dtype=np.int64),
+                np.ascontiguousarray(table, dtype=np.int64),
+                np.ascontiguousarray(packed_master.kinds, dtype=np.int32),
+                np.ascontiguousarray(packed_master.offsets, dtype=np.int64),
+                np.ascontiguousarray(packed_master.ranks, dtype=np.int64),
+                np.ascontiguousarray(packed_master.data, dtype=np.float64)]
+        d = MasterDesc()
+        d.n = int(n)
+        d.n_blocks = keep[1].shape[0]
+        d.perm = _p(keep[0], ctypes.c_int64)
+        d.table = _p(keep[1], ctypes.c_int64)
+        d.kind = _p(keep[2], ctypes.c_int32)
+        d.offset = _p(keep[3], ctypes.c_int64)
+        d.rank = _p(keep[4], ctypes.c_int64)
+        d.data = _p(keep[5] if keep[5].size else np.zeros(1), ctypes.c_double)
+        d.n_data = int(keep[5].size)
+        h = ctypes.c_void_p()
+        check(lib.hmx_master_create(ctypes.byref(d), int(device), ctypes.byref(h)),
+              "hmx_master_create")
+        self.handle = h
+        self.n = int(n)
+        self.device = int(device)
+        self._lib = lib
+
+    @property
+    def closed(self) -> bool:
+        return not getattr(self, "handle", None)
+
+    def close(self):
+        if getattr(self, "handle", None):
+            self._lib.hmx_master_destroy(self.handle)
             self.handle = None
 
     def __del__(self):

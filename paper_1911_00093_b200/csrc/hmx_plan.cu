@@ -106,8 +106,10 @@ int hmx_plan_get_info(const hmx_plan* p, hmx_plan_info* info) {
   return HMX_OK;
 }
 
-static int plan_create_impl(const hmx_matrix_desc* d, int device, const hmx_plan_options* opt,
-                            hmx_plan* p) {
+}  // extern "C"
+
+int hmx::plan_create_impl(const hmx_matrix_desc* d, int device, const hmx_plan_options* opt,
+                          hmx_plan* p, const DevSource* dsrc) {
   (void)device;
   const int64_t n = d->n, nb = d->n_blocks;
   if (n < 1 || n > INT32_MAX / 2 || nb < 1 || d->scheme < 0 || d->scheme > HMX_M3) {
@@ -587,7 +589,52 @@ static int plan_create_impl(const hmx_matrix_desc* d, int device, const hmx_plan
   }
   HMX_CUDA(cudaMemsetAsync(d_b64, 0, (size_t)std::max<int64_t>(off64, 2) * 8, p->stream));
   HMX_CUDA(cudaMemsetAsync(d_b32, 0, (size_t)std::max<int64_t>(off32, 4) * 4, p->stream));
-  {
+  if (dsrc) {
+    // payload values come from the device-resident masters (hmx_prepare.cu)
+    std::vector<PackRow> prow;
+    std::vector<size_t> gbase(group_rows.size());
+    for (size_t g = 0; g < group_rows.size(); ++g) {
+      gbase[g] = prow.size();
+      for (const auto& r : group_rows[g]) prow.push_back({r.first, r.second});
+    }
+    std::vector<PackS1> ps1;
+    ps1.reserve(fills.size());
+    for (const S1Fill& f : fills) {
+      const Seg& sg = seg1_fill[(size_t)f.seg];
+      const bool is32 = sg.W32 > 0;
+      PackS1 u{};
+      u.dst = is32 ? sg.off32 : sg.off64;
+      u.rows = (int64_t)gbase[(size_t)(f.rows - group_rows.data())] + f.r0;
+      u.R = sg.R;
+      u.rp = (int32_t)round_up(sg.R, is32 ? 4 : 2);
+      u.w = is32 ? sg.W32 : sg.W64;
+      u.c0 = (int32_t)f.c0;
+      u.is32 = is32;
+      u.cls = f.cls;
+      ps1.push_back(u);
+    }
+    std::vector<PackS2> ps2;
+    std::vector<PackItem> pit;
+    for (int64_t q = 0; q < nseg2; ++q) {
+      const Seg& sg = seg2[(size_t)q];
+      for (int part = 0; part < 2; ++part) {
+        const auto& lst = part == 0 ? items64[(size_t)q] : items32[(size_t)q];
+        if (lst.empty()) continue;
+        PackS2 u{};
+        u.dst = part == 0 ? sg.off64 : sg.off32;
+        u.R = sg.R;
+        u.rp = (int32_t)round_up(sg.R, part == 0 ? 2 : 4);
+        u.row0 = sg.row0;
+        u.item0 = (int32_t)pit.size();
+        u.nitems = (int32_t)lst.size();
+        u.is32 = part;
+        for (const ItemRef& it : lst) pit.push_back({it.block, it.cls, (int32_t)item_width(it), 0});
+        ps2.push_back(u);
+      }
+    }
+    const int prc = device_pack(*dsrc, ps1, prow, ps2, pit, d_b64, d_b32, p->stream);
+    if (prc != HMX_OK) return prc;
+  } else {
     const int64_t kWinBytes = int64_t(64) << 20;
     int64_t max_unit = 0;
     for (int b = 0; b < 2; ++b)
@@ -716,6 +763,8 @@ static int plan_create_impl(const hmx_matrix_desc* d, int device, const hmx_plan
   return HMX_OK;
 }
 
+extern "C" {
+
 int hmx_plan_create(const hmx_matrix_desc* d, int device, const hmx_plan_options* opt,
                     hmx_plan** out) {
   if (!d || !out) {
@@ -742,7 +791,7 @@ int hmx_plan_create(const hmx_matrix_desc* d, int device, const hmx_plan_options
     delete p;
     return cuda_fail(e, "cudaStreamCreate");
   }
-  const int rc = plan_create_impl(d, device, opt, p);
+  const int rc = plan_create_impl(d, device, opt, p, nullptr);
   if (rc != HMX_OK) {
     hmx_plan_destroy(p);
     return rc;

@@ -94,6 +94,46 @@ struct hmx_plan {
 
 namespace hmx {
 
+// Device-side payload source of hmx_plan_create_prepared: the resident FP64
+// masters plus the per-rank scaling/classification computed on the device.
+struct DevSource {
+  const double* data = nullptr;     // masters (hmx_master_desc layout)
+  const int64_t* table = nullptr;   // n_blocks x 5
+  const int64_t* offset = nullptr;  // per block
+  const int64_t* rank = nullptr;    // per block (full rank)
+  const int64_t* roff = nullptr;    // per block: first rank slot (prefix of ranks)
+  const int64_t* khi = nullptr;     // per block: FP64-class ranks
+  const int32_t* cls_idx = nullptr; // per rank slot: original rank index, class order (hi, then lo)
+  const double* colmag = nullptr;   // per rank slot (original order), nullptr = unscaled
+  const double* rowmag = nullptr;
+  unsigned long long* lost = nullptr;  // FP32 underflow counter
+  long long* overflow = nullptr;       // first overflowing block (min)
+};
+
+// Pack program for the device: one unit per stage-1 segment / stage-2 part.
+struct PackS1 {
+  int64_t dst;      // element offset in blob64 / blob32
+  int64_t rows;     // offset into the (block, class position) row list
+  int32_t R, rp, w, c0;
+  int32_t is32, cls;  // cls 1 = FP64 class / plain factors, 2 = FP32 class
+};
+struct PackS2 {
+  int64_t dst;
+  int32_t R, rp, row0, item0, nitems, is32;
+};
+struct PackItem {
+  int32_t block, cls, width, pad;  // cls 0 dense, 1 hi, 2 lo
+};
+struct PackRow {
+  int32_t block, q;
+};
+int device_pack(const DevSource& src, const std::vector<PackS1>& s1, const std::vector<PackRow>& rows,
+                const std::vector<PackS2>& s2, const std::vector<PackItem>& items, double* b64, float* b32,
+                cudaStream_t st);
+
+int plan_create_impl(const hmx_matrix_desc* d, int device, const hmx_plan_options* opt, hmx_plan* p,
+                     const DevSource* dsrc);
+
 // Enqueues y = A xp (both device, permuted order unless permute_out) on the
 // plan's stream with the stage-2 epilogue options `out` (y/nonfinite filled
 // in by the caller).

@@ -33,17 +33,21 @@ def test_ctypes_layouts_match_header(tmp_path):
     from paper_1911_00093_b200 import _gpu
     src = tmp_path / "layout.c"
     src.write_text('#include <stdio.h>\n#include <stddef.h>\n#include "hmx_gpu.h"\n'
-                   "int main(void){printf(\"%zu %zu %zu %zu %zu %zu\\n\","
+                   "int main(void){printf(\"%zu %zu %zu %zu %zu %zu %zu %zu %zu\\n\","
                    "sizeof(hmx_matrix_desc), offsetof(hmx_matrix_desc, buf32),"
                    "sizeof(hmx_plan_options), sizeof(hmx_plan_info),"
-                   "sizeof(hmx_solve_report), offsetof(hmx_solve_report, device_ms));return 0;}\n")
+                   "sizeof(hmx_solve_report), offsetof(hmx_solve_report, device_ms),"
+                   "sizeof(hmx_master_desc), offsetof(hmx_master_desc, n_data),"
+                   "sizeof(hmx_prepare_info));return 0;}\n")
     exe = tmp_path / "layout"
     subprocess.run(["gcc", "-I", str(ROOT / "include"), str(src), "-o", str(exe)], check=True)
     got = [int(v) for v in subprocess.run([str(exe)], capture_output=True, text=True,
                                           check=True).stdout.split()]
     want = [ctypes.sizeof(_gpu.MatrixDesc), _gpu.MatrixDesc.buf32.offset,
             ctypes.sizeof(_gpu.PlanOptions), ctypes.sizeof(_gpu.PlanInfo),
-            ctypes.sizeof(_gpu.SolveReport), _gpu.SolveReport.device_ms.offset]
+            ctypes.sizeof(_gpu.SolveReport), _gpu.SolveReport.device_ms.offset,
+            ctypes.sizeof(_gpu.MasterDesc), _gpu.MasterDesc.n_data.offset,
+            ctypes.sizeof(_gpu.PrepareInfo)]
     assert got == want
 
 
