@@ -402,12 +402,12 @@ int hmx_true_residual(hmx_plan* p64, const double* x, const double* b, double* o
   }
   std::lock_guard<std::mutex> lock(p64->mu);
   DeviceGuard guard(p64->device);
-  cudaDeviceProp prop{};
-  HMX_CUDA(cudaGetDeviceProperties(&prop, p64->device));
+  int sms = 0;  // (cudaGetDeviceProperties costs milliseconds; the attribute does not)
+  HMX_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, p64->device));
   SolveCtx c{};
   c.A = c.A64 = p64;
   c.st = p64->stream;
-  c.grid = 2 * prop.multiProcessorCount;
+  c.grid = 2 * sms;
   int rc = workspace_for(p64, c.w, c.grid);
   if (rc) return rc;
   const int64_t n = p64->n;
@@ -440,13 +440,13 @@ int hmx_bicgstab(hmx_plan* A, hmx_plan* A64, const double* b, double tol, int ma
   else std::lock(l1, l2);
   DeviceGuard guard(A->device);
   *rep = hmx_solve_report{};
-  cudaDeviceProp prop{};
-  HMX_CUDA(cudaGetDeviceProperties(&prop, A->device));
+  int sms = 0;
+  HMX_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, A->device));
   SolveCtx c{};
   c.A = A;
   c.A64 = A64;
   c.st = A->stream;
-  c.grid = 2 * prop.multiProcessorCount;
+  c.grid = 2 * sms;
   int rc = workspace_for(A, c.w, c.grid);
   if (rc) return rc;
   const int64_t n = A->n;
