@@ -92,6 +92,10 @@ void hmx_plan_destroy(hmx_plan* p) {
     for (void* a : p->allocs) cudaFree(a);
     if (p->h_flag) cudaFreeHost(p->h_flag);
     for (void* h : p->pinned) cudaFreeHost(h);
+    if (p->ws) {
+      if (p->ws->loop_exec) cudaGraphExecDestroy(p->ws->loop_exec);
+      if (p->ws->loop_graph) cudaGraphDestroy(p->ws->loop_graph);
+    }
     delete p->ws;
     for (auto& e : p->ev)
       if (e) cudaEventDestroy(e);

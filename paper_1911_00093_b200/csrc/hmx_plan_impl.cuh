@@ -50,6 +50,15 @@ struct Workspace {
   double* hist = nullptr;   // device residual history
   int hist_cap = 0;
   int grid = 0;
+  int* ictl = nullptr;      // iteration control [i, max_iter, -, -]
+  // graph-resident iteration loop (CUDA graph with a WHILE conditional node),
+  // built on first use; rebuilt when the history buffer moves
+  cudaGraph_t loop_graph = nullptr;
+  cudaGraphExec_t loop_exec = nullptr;
+  const double* loop_hist = nullptr;
+  bool loop_failed = false;
+  // (copied by value into solver contexts: the owner, hmx_plan_destroy,
+  // releases the graph)
 };
 
 }  // namespace hmx

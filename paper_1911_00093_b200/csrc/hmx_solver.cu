@@ -17,6 +17,7 @@
 // s-update (fused |s|^2), t = A s (fused t.s, t.t), x/r-update (fused |r|^2,
 // r^.r).
 #include <cmath>
+#include <cstdlib>
 #include <mutex>
 
 #include "hmx_plan_impl.cuh"
@@ -41,8 +42,12 @@ enum : int {
   SC_TMP = 12,    // [2 scratch]
   SC_NB = 14,     // |b|
   SC_BVAL = 15,   // value reported with a breakdown
-  SC_N = 16
+  SC_TOL = 16,    // tol of the running solve
+  SC_N = 18
 };
+
+// iteration control (int[4]): [current iteration i, max_iter, spare, spare]
+__device__ __forceinline__ int rho_slot_of(int it) { return (it & 1) ? SC_RHO1 : SC_RHO0; }
 
 // stop word layout (int[4]): [stop, reason, iteration, spare]
 enum : int {
@@ -155,10 +160,11 @@ __global__ void __launch_bounds__(kVecThreads) init_kernel(const double* b, cons
 // beta = (rho / rho_prev) (alpha / omega)   (solver.py:112-120); first checks
 // the rho breakdown of iteration `it` (solver.py:113-115)
 __global__ void __launch_bounds__(kVecThreads) p_update_kernel(const double* r, const double* v,
-                                                                double* p, int n, int it,
-                                                                double* sc, int rho_slot,
-                                                                int prev_slot, int* stop) {
+                                                                double* p, int n, const int* ictl,
+                                                                double* sc, int* stop) {
   if (*(volatile int*)stop) return;
+  const int it = ictl[0];
+  const int rho_slot = rho_slot_of(it), prev_slot = rho_slot_of(it - 1);
   const double rho = sc[rho_slot];
   if (fabs(rho) < kBreakdownEps) {
     if (blockIdx.x == 0 && threadIdx.x == 0) set_stop(stop, R_RHO, it, sc, rho);
@@ -181,10 +187,13 @@ __global__ void __launch_bounds__(kVecThreads) p_update_kernel(const double* r, 
 // (solver.py:122-136)
 __global__ void __launch_bounds__(kVecThreads) s_update_kernel(const double* r, const double* v,
                                                                 double* s, int n, double* sc,
-                                                                int rho_slot, VecRed R, int it,
-                                                                double tol, double* hist,
-                                                                int* stop, const int* nonfin) {
+                                                                VecRed R, const int* ictl,
+                                                                double* hist, int* stop,
+                                                                const int* nonfin) {
   if (*(volatile int*)stop) return;
+  const int it = ictl[0];
+  const int rho_slot = rho_slot_of(it);
+  const double tol = sc[SC_TOL];
   if (*nonfin) {
     if (blockIdx.x == 0 && threadIdx.x == 0) set_stop(stop, R_NONFINITE, it, sc, 0.0);
     return;
@@ -226,11 +235,13 @@ __global__ void __launch_bounds__(kVecThreads) xr_update_kernel(double* x, doubl
                                                                  const double* p, const double* s,
                                                                  const double* t,
                                                                  const double* rhat, int n,
-                                                                 double* sc, VecRed R, int it,
-                                                                 double tol, double* hist,
-                                                                 int next_slot, int* stop,
-                                                                 const int* nonfin) {
+                                                                 double* sc, VecRed R,
+                                                                 const int* ictl, double* hist,
+                                                                 int* stop, const int* nonfin) {
   if (*(volatile int*)stop) return;
+  const int it = ictl[0];
+  const int next_slot = rho_slot_of(it + 1);
+  const double tol = sc[SC_TOL];
   if (*nonfin) {
     if (blockIdx.x == 0 && threadIdx.x == 0) set_stop(stop, R_NONFINITE, it, sc, 0.0);
     return;
@@ -273,6 +284,14 @@ __global__ void __launch_bounds__(kVecThreads) resid_kernel(const double* b, con
   grid_reduce2(u, w, R);
 }
 
+// end of an iteration: next i; in the graph-resident loop also the loop
+// condition (continue while no decision is recorded and i <= max_iter)
+__global__ void advance_kernel(int* ictl, const int* stop, cudaGraphConditionalHandle loop, int in_graph) {
+  const bool go = !*(volatile const int*)stop;
+  if (go) ictl[0] += 1;
+  if (in_graph) cudaGraphSetConditional(loop, (go && ictl[0] <= ictl[1]) ? 1u : 0u);
+}
+
 __global__ void permute_kernel(const double* src, const int32_t* perm, double* dst, int n,
                                int inverse) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -310,9 +329,10 @@ int alloc_ws(hmx_plan* p, Workspace& w, int64_t n, int grid) {
   w.sc = p->alloc<double>(SC_N);
   w.flags = p->alloc<int>(4);
   w.stop = p->alloc<int>(4);
+  w.ictl = p->alloc<int>(4);
   w.partials = p->alloc<double>((size_t)2 * grid);
   w.done = p->alloc<uint32_t>(1);
-  if (!w.sc || !w.flags || !w.partials || !w.done) {
+  if (!w.sc || !w.flags || !w.stop || !w.ictl || !w.partials || !w.done) {
     set_error("cudaMalloc failed for the solver workspace");
     return HMX_ERR_CUDA;
   }
@@ -358,6 +378,59 @@ const int* host_stop(const SolveCtx& c) { return reinterpret_cast<const int*>(c.
 int flags_nonfinite(const SolveCtx& c) {
   const int* f = reinterpret_cast<const int*>(c.w.h_sc + SC_N);
   return f[0] | f[1] | f[2];
+}
+
+// One BiCG-STAB iteration (solver.py:112-158), every kernel guarded by the
+// stop word; the iteration number and tol live on the device (ictl, SC_TOL)
+// so the same launches serve every iteration and can be captured once.
+int enqueue_iteration(const SolveCtx& c, int n32, cudaGraphConditionalHandle loop, int in_graph) {
+  const Workspace& w = c.w;
+  cudaStream_t st = c.st;
+  int rc;
+  p_update_kernel<<<c.grid, kVecThreads, 0, st>>>(w.r, w.v, w.p, n32, w.ictl, w.sc, w.stop);
+  if ((rc = apply(c.A, w, st, w.p, w.v, w.rhat, 0, SC_DV, w.flags, w.stop))) return rc;
+  s_update_kernel<<<c.grid, kVecThreads, 0, st>>>(w.r, w.v, w.s, n32, w.sc, c.red(SC_SS), w.ictl, w.hist,
+                                                    w.stop, w.flags);
+  if ((rc = apply(c.A, w, st, w.s, w.t, w.s, 1, SC_DT, w.flags + 1, w.stop))) return rc;
+  xr_update_kernel<<<c.grid, kVecThreads, 0, st>>>(w.x, w.r, w.p, w.s, w.t, w.rhat, n32, w.sc,
+                                                     VecRed{w.partials, w.done, w.sc + SC_TMP}, w.ictl,
+                                                     w.hist, w.stop, w.flags + 1);
+  advance_kernel<<<1, 1, 0, st>>>(w.ictl, w.stop, loop, in_graph);
+  HMX_CUDA(cudaGetLastError());
+  return HMX_OK;
+}
+
+// The whole iteration loop as one CUDA graph: a WHILE conditional node whose
+// body is one captured iteration; advance_kernel clears the condition when a
+// decision is recorded or max_iter is reached.  One launch and one host
+// synchronisation per solve, no speculative iterations.
+int build_loop_graph(const SolveCtx& c, Workspace& ws, int n32) {
+  if (ws.loop_exec) cudaGraphExecDestroy(ws.loop_exec);
+  if (ws.loop_graph) cudaGraphDestroy(ws.loop_graph);
+  ws.loop_exec = nullptr;
+  ws.loop_graph = nullptr;
+  cudaGraph_t g = nullptr;
+  HMX_CUDA(cudaGraphCreate(&g, 0));
+  ws.loop_graph = g;
+  cudaGraphConditionalHandle h;
+  HMX_CUDA(cudaGraphConditionalHandleCreate(&h, g, 1, cudaGraphCondAssignDefault));
+  cudaGraphNodeParams np{};
+  np.type = cudaGraphNodeTypeConditional;
+  np.conditional.handle = h;
+  np.conditional.type = cudaGraphCondTypeWhile;
+  np.conditional.size = 1;
+  cudaGraphNode_t node;
+  HMX_CUDA(cudaGraphAddNode(&node, g, nullptr, 0, &np));
+  cudaGraph_t body = np.conditional.phGraph_out[0];
+  HMX_CUDA(cudaStreamBeginCaptureToGraph(c.st, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+  const int rc = enqueue_iteration(c, n32, h, 1);
+  cudaGraph_t captured = nullptr;
+  const cudaError_t e = cudaStreamEndCapture(c.st, &captured);
+  if (rc) return rc;
+  HMX_CUDA(e);
+  HMX_CUDA(cudaGraphInstantiate(&ws.loop_exec, g, 0));
+  ws.loop_hist = c.w.hist;
+  return HMX_OK;
 }
 
 // |b - A64 x| / |b| with x, b device, permuted; result on the host
@@ -513,36 +586,56 @@ int hmx_bicgstab(hmx_plan* A, hmx_plan* A64, const double* b, double tol, int ma
   // rho_1 = r^.r = |r|^2 lives in ring slot (1 & 1) = SC_RHO1
   history[hlen++] = std::sqrt(w.h_sc[SC_RHO1]) / nb;
 
-  // Enqueue iterations in batches; kernels after a recorded decision are
-  // no-ops, so over-enqueueing only costs launches.
-  auto rho_slot = [](int i) { return (i & 1) ? SC_RHO1 : SC_RHO0; };
-  int done_through = 0;  // iterations enqueued
-  int batch = 2;
+  // iteration control on the device: i = 1, max_iter, tol
+  {
+    const int ctl[4] = {1, max_iter, 0, 0};
+    HMX_CUDA(cudaMemcpyAsync(w.ictl, ctl, sizeof(ctl), cudaMemcpyHostToDevice, st));
+    HMX_CUDA(cudaMemcpyAsync(w.sc + SC_TOL, &tol, sizeof(double), cudaMemcpyHostToDevice, st));
+  }
   int reason = R_NONE, stop_it = 0;
-  while (done_through < max_iter) {
-    const int last = std::min(max_iter, done_through + batch);
-    for (int i = done_through + 1; i <= last; ++i) {
-      p_update_kernel<<<c.grid, kVecThreads, 0, st>>>(w.r, w.v, w.p, n32, i, w.sc, rho_slot(i),
-                                                        rho_slot(i - 1), w.stop);
-      if ((rc = apply(A, w, st, w.p, w.v, w.rhat, 0, SC_DV, w.flags, w.stop))) return rc;
-      s_update_kernel<<<c.grid, kVecThreads, 0, st>>>(w.r, w.v, w.s, n32, w.sc, rho_slot(i),
-                                                        c.red(SC_SS), i, tol, w.hist, w.stop,
-                                                        w.flags);
-      if ((rc = apply(A, w, st, w.s, w.t, w.s, 1, SC_DT, w.flags + 1, w.stop))) return rc;
-      xr_update_kernel<<<c.grid, kVecThreads, 0, st>>>(
-          w.x, w.r, w.p, w.s, w.t, w.rhat, n32, w.sc, VecRed{w.partials, w.done, w.sc + SC_TMP},
-          i, tol, w.hist, rho_slot(i + 1), w.stop, w.flags + 1);
+  bool looped = false;
+  Workspace& ws = *A->ws;
+  if (!ws.loop_failed && !std::getenv("HMX_SOLVER_NO_GRAPH")) {
+    if (!ws.loop_exec || ws.loop_hist != w.hist) {
+      if (build_loop_graph(c, ws, n32) != HMX_OK) {
+        // e.g. a driver without conditional graph nodes: keep the batched path
+        cudaStreamCaptureStatus cs;
+        if (cudaStreamIsCapturing(st, &cs) == cudaSuccess && cs != cudaStreamCaptureStatusNone) {
+          cudaGraph_t junk = nullptr;
+          cudaStreamEndCapture(st, &junk);
+          if (junk) cudaGraphDestroy(junk);
+        }
+        cudaGetLastError();
+        ws.loop_failed = true;
+      }
     }
-    HMX_CUDA(cudaGetLastError());
-    done_through = last;
-    if ((rc = sync_scalars(c))) return rc;
+    if (!ws.loop_failed) {
+      HMX_CUDA(cudaGraphLaunch(ws.loop_exec, st));
+      if ((rc = sync_scalars(c))) return rc;
+      looped = true;
+    }
+  }
+  if (!looped) {
+    // speculative batches: kernels after a recorded decision are no-ops, so
+    // over-enqueueing only costs launches
+    int done_through = 0;
+    int batch = 2;
+    while (done_through < max_iter) {
+      const int last = std::min(max_iter, done_through + batch);
+      for (int i = done_through + 1; i <= last; ++i)
+        if ((rc = enqueue_iteration(c, n32, 0, 0))) return rc;
+      done_through = last;
+      if ((rc = sync_scalars(c))) return rc;
+      if (host_stop(c)[0]) break;
+      batch = std::min(batch * 2, 16);
+    }
+  }
+  {
     const int* sw = host_stop(c);
     if (sw[0]) {
       reason = sw[1];
       stop_it = sw[2];
-      break;
     }
-    batch = std::min(batch * 2, 16);
   }
   // iterations completed, matvecs actually run
   int completed;
