@@ -113,7 +113,10 @@ def load_library(build: bool = False):
     with _lock:
         if _lib is None:
             path = _native.GPU_LIB
-            if build or os.environ.get("HMX_BUILD_ON_IMPORT") == "1":
+            if os.environ.get("HMX_GPU_LIB"):  # A/B experiments with another build
+                from pathlib import Path
+                path = Path(os.environ["HMX_GPU_LIB"])
+            elif build or os.environ.get("HMX_BUILD_ON_IMPORT") == "1":
                 path = _native.build_gpu()
             if not path.exists():
                 raise RuntimeError(
