@@ -129,6 +129,10 @@ __global__ void __launch_bounds__(NT, (OUT == OUT_Y && F32MODE != F32_ALL64) ? H
   __shared__ unsigned ticket;
 
   if (out.skip != nullptr && *out.skip != 0) return;  // guarded launch (solver)
+  // stage 1: let the dependent stage-2 grid launch as soon as every stage-1
+  // CTA has started (its CTAs then fill the SMs stage 1's tail frees and
+  // prefetch; griddepcontrol.wait in stage 2 still waits for all of stage 1)
+  if (OUT == OUT_Z) asm volatile("griddepcontrol.launch_dependents;");
   const Seg sg = segs[blockIdx.x];
   const int R = sg.R;
   const int tid = threadIdx.x;
@@ -380,8 +384,7 @@ __global__ void __launch_bounds__(NT, (OUT == OUT_Y && F32MODE != F32_ALL64) ? H
         if (tid == 0) P.red_count[sg.red] = 0u;  // ready for the next matvec
       }
     }
-    // let the dependent stage-2 grid launch (programmatic dependent launch)
-    asm volatile("griddepcontrol.launch_dependents;");
+
   } else {
     // ---------------- stage-2 epilogue: y, finite flag, fused dots
     double d0 = 0.0, d1 = 0.0;
