@@ -1,6 +1,6 @@
 """Parity and solver diagnostics at a large BASELINE config (default 5).
 
-  python tools/large_check.py [--config 5] [--schemes m1-double ...] [--max-iter 300]
+  python tests/diagnostics/large_check.py [--config 5] [--schemes m1-double ...] [--max-iter 300]
 
 GPU matvec of each scheme against the oracle's full matvec (numpy, one pass),
 then a BiCG-STAB solve whose residual history is printed every 10 iterations.
@@ -13,7 +13,7 @@ from pathlib import Path
 
 import numpy as np
 
-ROOT = Path(__file__).resolve().parents[1]
+ROOT = Path(__file__).resolve().parents[2]
 sys.path.insert(0, str(ROOT))
 
 import bench  # noqa: E402

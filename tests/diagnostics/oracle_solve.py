@@ -1,7 +1,7 @@
 """Reference-algorithm BiCG-STAB (the oracle port of solver.py, numpy, CPU)
 on this repo's config-4 H-matrix, for comparison with the GPU solves.
 
-  python tools/oracle_solve.py <out.json> <scheme> [<scheme> ...]
+  python tests/diagnostics/oracle_solve.py <out.json> <scheme> [<scheme> ...]
 
 Test/diagnostic tool (imports the oracle as the checker); ~5-10 min per
 scheme at config 4.
@@ -13,7 +13,7 @@ from pathlib import Path
 
 import numpy as np
 
-ROOT = Path(__file__).resolve().parents[1]
+ROOT = Path(__file__).resolve().parents[2]
 sys.path.insert(0, str(ROOT))
 
 import bench  # noqa: E402
