@@ -31,6 +31,9 @@ def main():
     n = mesh.n
     print("device bench ms", plan.bench(3, 50)["ms"])
     print("hx.matvec           median/min ms %.3f %.3f" % wall(lambda: hx.matvec(sh, x)))
+    import torch as _t
+    xpin = _t.from_numpy(x).pin_memory().numpy()
+    print("hx.matvec pinned x  median/min ms %.3f %.3f" % wall(lambda: hx.matvec(sh, xpin)))
     print("plan.matvec         median/min ms %.3f %.3f" % wall(lambda: plan.matvec(x)))
     xd = torch.from_numpy(x).cuda()
     yd = torch.empty(n, dtype=torch.float64, device="cuda")
