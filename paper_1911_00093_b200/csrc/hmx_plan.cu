@@ -114,7 +114,6 @@ int hmx_plan_get_info(const hmx_plan* p, hmx_plan_info* info) {
 
 int hmx::plan_create_impl(const hmx_matrix_desc* d, int device, const hmx_plan_options* opt,
                           hmx_plan* p, const DevSource* dsrc) {
-  (void)device;
   const int64_t n = d->n, nb = d->n_blocks;
   if (n < 1 || n > INT32_MAX / 2 || nb < 1 || d->scheme < 0 || d->scheme > HMX_M3) {
     set_error("invalid matrix descriptor (n, n_blocks or scheme)");
@@ -130,7 +129,7 @@ int hmx::plan_create_impl(const hmx_matrix_desc* d, int device, const hmx_plan_o
   }
   const auto t_start = std::chrono::steady_clock::now();
   auto secs = [&]() { return std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count(); };
-  const int64_t s1_target = opt && opt->s1_chunk_bytes > 0 ? opt->s1_chunk_bytes : 256 * 1024;
+  int64_t s1_target = opt && opt->s1_chunk_bytes > 0 ? opt->s1_chunk_bytes : 256 * 1024;
   const size_t a_es = d->a32 ? 4 : 8, hi_es = d->hi32 ? 4 : 8;
 
   // ---- validate blocks and collect the ones touching rows [rb, re)
@@ -217,6 +216,23 @@ int hmx::plan_create_impl(const hmx_matrix_desc* d, int device, const hmx_plan_o
     return HMX_ERR_ARG;
   }
 
+  // Small problems: a 256 KB chunk streams for ~15 us on one CTA (128
+  // threads x 8 loads in flight), the whole of stage 1 at N = 20,480.  Aim
+  // for about one chunk per resident CTA slot, between 64 KB and 256 KB
+  // (measured: config 2 best at 64 KB, configs 3-4 at 256 KB).
+  if (!(opt && opt->s1_chunk_bytes > 0)) {
+    int64_t s1_total = 0;
+    for (auto& g : groups) {
+      const int cls = std::get<0>(g.first);
+      const int64_t ncol = std::get<2>(g.first) - std::get<1>(g.first);
+      const int64_t es = (cls == 2 || d->hi32) ? 4 : 8;
+      for (int32_t k : g.second) s1_total += (cls == 1 ? d->khi[k] : d->klo[k]) * ncol * es;
+    }
+    int sms = 148;
+    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device) != cudaSuccess) sms = 148;
+    const int64_t slots = (int64_t)std::max(sms, 1) * (1024 / kS1Threads);
+    s1_target = std::min<int64_t>(s1_target, std::max<int64_t>(64 * 1024, s1_total / slots));
+  }
   std::vector<Seg> seg1, seg2((size_t)nseg2);
   std::vector<int32_t> gtab;
   std::vector<Run> runs;
