@@ -96,8 +96,8 @@ typedef struct {
 typedef struct {
   int64_t row_begin;
   int64_t row_end;
-  int32_t s1_chunk_bytes; /* 0 = default stage-1 task size */
-  int32_t s2_threads;     /* 0 = default stage-2 CTA size */
+  int32_t s1_chunk_bytes; /* stage-1 column-chunk target; 0 = adaptive (64-256 KB) */
+  int32_t reserved;       /* must be 0 */
 } hmx_plan_options;
 
 typedef struct hmx_plan hmx_plan;
@@ -106,7 +106,9 @@ typedef struct {
   int64_t n;
   int64_t payload_bytes;   /* algorithmic matrix bytes (precision.py:332-334) */
   int64_t device_bytes;    /* device memory held by the plan */
-  int64_t s1_segments, s1_tasks, s2_segments, s2_runs, z_len;
+  int64_t s1_segments;  /* stage-1 segments (one CTA each) */
+  int64_t s1_tasks;     /* column-chunked stage-1 row groups (last-arriver reductions) */
+  int64_t s2_segments, s2_runs, z_len;
   int64_t stage1_bytes, stage2_bytes; /* stored payload bytes read per stage */
   int32_t s1_grid, s1_block, s2_grid, s2_block;
 } hmx_plan_info;

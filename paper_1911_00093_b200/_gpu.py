@@ -38,7 +38,7 @@ class MatrixDesc(ctypes.Structure):
 
 class PlanOptions(ctypes.Structure):
     _fields_ = [("row_begin", ctypes.c_int64), ("row_end", ctypes.c_int64),
-                ("s1_chunk_bytes", ctypes.c_int32), ("s2_threads", ctypes.c_int32)]
+                ("s1_chunk_bytes", ctypes.c_int32), ("reserved", ctypes.c_int32)]
 
 
 class PlanInfo(ctypes.Structure):
