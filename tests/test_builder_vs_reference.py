@@ -49,3 +49,19 @@ def test_builder_thread_count_independent(hx):
     b = hx.build_hmatrix(mesh, aca_tol=1e-5, threads=4)
     assert np.array_equal(a.packed.data, b.packed.data)
     assert np.array_equal(a.packed.ranks, b.packed.ranks)
+
+
+def test_interchange_formats_byte_identical(hx, tmp_path):
+    """dump_partition / export_mesh (reference partition.py:172-177,
+    problem.py:260-267) write the reference's files byte for byte at config 1
+    (golden/interchange.json, hashed from the reference's own output)."""
+    import hashlib
+    import json
+    from pathlib import Path
+    gold = json.loads((Path(__file__).parent / "golden" / "interchange.json").read_text())
+    mesh, h = config1_hmatrix()
+    hx.dump_partition(h.partition, tmp_path / "p.txt")
+    hx.export_mesh(mesh, tmp_path / "m.txt")
+    for key, name in (("dump_partition", "p.txt"), ("export_mesh", "m.txt")):
+        data = (tmp_path / name).read_bytes()
+        assert hashlib.sha256(data).hexdigest() == gold[key]["sha256"], key
