@@ -2,6 +2,7 @@
 on this repo's config-4 H-matrix, for comparison with the GPU solves.
 
   python tests/diagnostics/oracle_solve.py <out.json> <scheme> [<scheme> ...]
+  (HMX_CONFIG=<n> selects another BASELINE config; default 4)
 
 Test/diagnostic tool (imports the oracle as the checker); ~5-10 min per
 scheme at config 4.
@@ -23,7 +24,8 @@ from oracle import hmx_oracle as orc  # noqa: E402
 
 def main():
     out, schemes = sys.argv[1], sys.argv[2:]
-    mesh, h, x, b, _ = bench.build_workload(4)
+    import os
+    mesh, h, x, b, _ = bench.build_workload(int(os.environ.get("HMX_CONFIG", "4")))
     sh64 = hx.prepare_scheme(h, "m1-double")
     res = json.loads(Path(out).read_text()) if Path(out).exists() else {}
     for s in schemes:
