@@ -66,6 +66,7 @@ constexpr int kSegRows = 64;      // max rows per stage-2 segment (leaf rows)
 constexpr int kS1Rows = 256;      // max rank rows per stage-1 segment
 constexpr int kSegThreads = 256;  // stage-2 CTA size (thread-group layout of gtab)
 constexpr int kS1Threads = 128;   // stage-1 CTA size
+constexpr int kS1Threads32 = 64;  // stage-1 CTA size for widened-FP32-only stage 1 (<= 256 rows)
 constexpr int kSegWMax = 2048;    // columns of g staged in shared memory per tile (stage 2)
 constexpr int kS1WMax = 1024;     // max columns per stage-1 segment chunk
 

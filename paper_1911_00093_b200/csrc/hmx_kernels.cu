@@ -131,8 +131,9 @@ __global__ void __launch_bounds__(NT, (OUT == OUT_Y && F32MODE != F32_ALL64) ? H
   if (out.skip != nullptr && *out.skip != 0) return;  // guarded launch (solver)
   // stage 1: let the dependent stage-2 grid launch as soon as every stage-1
   // CTA has started (its CTAs then fill the SMs stage 1's tail frees and
-  // prefetch; griddepcontrol.wait in stage 2 still waits for all of stage 1)
-  if (OUT == OUT_Z) asm volatile("griddepcontrol.launch_dependents;");
+  // prefetch; griddepcontrol.wait in stage 2 still waits for all of stage 1).
+  // The 64-thread FP32 stage 1 triggers at CTA end instead (measured).
+  if (OUT == OUT_Z && NT >= 128) asm volatile("griddepcontrol.launch_dependents;");
   const Seg sg = segs[blockIdx.x];
   const int R = sg.R;
   const int tid = threadIdx.x;
@@ -384,6 +385,7 @@ __global__ void __launch_bounds__(NT, (OUT == OUT_Y && F32MODE != F32_ALL64) ? H
         if (tid == 0) P.red_count[sg.red] = 0u;  // ready for the next matvec
       }
     }
+    if (NT < 128) asm volatile("griddepcontrol.launch_dependents;");
 
   } else {
     // ---------------- stage-2 epilogue: y, finite flag, fused dots
@@ -520,9 +522,15 @@ cudaError_t launch_stage1(const DevPlan& P, const double* x, cudaStream_t st, co
   if (P.n_seg1 == 0) return cudaSuccess;
   S2Out none{};
   none.skip = skip;
+  // FP32 data widened into FP64 sums (m1-mixed, m2-single, m2-mixed): 64-thread
+  // CTAs, 16 per SM (measured -3..-4 % on stage 1 against 128 threads; the
+  // FP32-accumulating m1-single stage 1 is faster on 128)
+  const bool all32 = P.pipe == P_M1M || P.pipe == P_M2S || P.pipe == P_M2M;
   switch (P.f32mode1) {
     case F32_ALL32: return launch_seg<F32_ALL32, OUT_Z, kS1Threads>(P, P.seg1, P.n_seg1, x, none, st, false);
-    default: return launch_seg<F32_ALL64, OUT_Z, kS1Threads>(P, P.seg1, P.n_seg1, x, none, st, false);
+    default:
+      return all32 ? launch_seg<F32_ALL64, OUT_Z, kS1Threads32>(P, P.seg1, P.n_seg1, x, none, st, false)
+                   : launch_seg<F32_ALL64, OUT_Z, kS1Threads>(P, P.seg1, P.n_seg1, x, none, st, false);
   }
 }
 

@@ -777,7 +777,7 @@ int hmx::plan_create_impl(const hmx_matrix_desc* d, int device, const hmx_plan_o
   info.stage1_bytes = s1_bytes;
   info.stage2_bytes = s2_bytes;
   info.s1_grid = (int32_t)seg1.size();
-  info.s1_block = kS1Threads;
+  info.s1_block = (pipe == P_M1M || pipe == P_M2S || pipe == P_M2M) ? kS1Threads32 : kS1Threads;
   info.s2_grid = (int32_t)nseg2;
   info.s2_block = kSegThreads;
   return HMX_OK;
