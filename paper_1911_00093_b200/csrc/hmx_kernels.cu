@@ -522,15 +522,15 @@ cudaError_t launch_stage1(const DevPlan& P, const double* x, cudaStream_t st, co
   if (P.n_seg1 == 0) return cudaSuccess;
   S2Out none{};
   none.skip = skip;
-  // FP32 data widened into FP64 sums (m1-mixed, m2-single, m2-mixed): 64-thread
-  // CTAs, 16 per SM (measured -3..-4 % on stage 1 against 128 threads; the
-  // FP32-accumulating m1-single stage 1 is faster on 128)
-  const bool all32 = P.pipe == P_M1M || P.pipe == P_M2S || P.pipe == P_M2M;
+  // every stage-1 segment FP32 data widened into FP64 sums (m1-mixed, m2-single,
+  // m2-mixed, m3 with an all-FP32 class): 64-thread CTAs, 16 per SM (measured
+  // -3..-4 % on stage 1 against 128 threads; the FP32-accumulating m1-single
+  // stage 1 is faster on 128)
   switch (P.f32mode1) {
     case F32_ALL32: return launch_seg<F32_ALL32, OUT_Z, kS1Threads>(P, P.seg1, P.n_seg1, x, none, st, false);
     default:
-      return all32 ? launch_seg<F32_ALL64, OUT_Z, kS1Threads32>(P, P.seg1, P.n_seg1, x, none, st, false)
-                   : launch_seg<F32_ALL64, OUT_Z, kS1Threads>(P, P.seg1, P.n_seg1, x, none, st, false);
+      return P.s1_narrow ? launch_seg<F32_ALL64, OUT_Z, kS1Threads32>(P, P.seg1, P.n_seg1, x, none, st, false)
+                         : launch_seg<F32_ALL64, OUT_Z, kS1Threads>(P, P.seg1, P.n_seg1, x, none, st, false);
   }
 }
 

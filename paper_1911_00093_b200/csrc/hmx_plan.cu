@@ -735,6 +735,8 @@ int hmx::plan_create_impl(const hmx_matrix_desc* d, int device, const hmx_plan_o
   dp.blob64 = d_b64;
   dp.blob32 = d_b32;
   dp.f32mode1 = pipe == P_M1S ? F32_ALL32 : F32_ALL64;
+  dp.s1_narrow = pipe != P_M1S && !seg1.empty() &&
+                 std::all_of(seg1.begin(), seg1.end(), [](const Seg& a) { return a.W64 == 0; });
   dp.f32mode2 = f32mode2;
   dp.zepi = pipe == P_M1D ? Z_NONE : (pipe == P_M1S || pipe == P_M1M) ? Z_ROUND32 : Z_SCALE;
   dp.zscale = d_zs;
@@ -777,7 +779,7 @@ int hmx::plan_create_impl(const hmx_matrix_desc* d, int device, const hmx_plan_o
   info.stage1_bytes = s1_bytes;
   info.stage2_bytes = s2_bytes;
   info.s1_grid = (int32_t)seg1.size();
-  info.s1_block = (pipe == P_M1M || pipe == P_M2S || pipe == P_M2M) ? kS1Threads32 : kS1Threads;
+  info.s1_block = dp.s1_narrow ? kS1Threads32 : kS1Threads;
   info.s2_grid = (int32_t)nseg2;
   info.s2_block = kSegThreads;
   return HMX_OK;
