@@ -216,20 +216,25 @@ int hmx::plan_create_impl(const hmx_matrix_desc* d, int device, const hmx_plan_o
     return HMX_ERR_ARG;
   }
 
-  // Small problems: a 256 KB chunk streams for ~15 us on one CTA (128
-  // threads x 8 loads in flight), the whole of stage 1 at N = 20,480.  Aim
-  // for about one chunk per resident CTA slot, between 64 KB and 256 KB
-  // (measured: config 2 best at 64 KB, configs 3-4 at 256 KB).
-  if (!(opt && opt->s1_chunk_bytes > 0)) {
-    int64_t s1_total = 0;
-    for (auto& g : groups) {
-      const int cls = std::get<0>(g.first);
-      const int64_t ncol = std::get<2>(g.first) - std::get<1>(g.first);
-      const int64_t es = (cls == 2 || d->hi32) ? 4 : 8;
-      for (int32_t k : g.second) s1_total += (cls == 1 ? d->khi[k] : d->klo[k]) * ncol * es;
-    }
-    int sms = 148;
-    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device) != cudaSuccess) sms = 148;
+  // Stage-1 CTA shape.  A chunk of C bytes streams for about C / (NT x 8 x
+  // 16 B) memory latencies on one CTA, so small problems want small chunks
+  // (about one per resident CTA slot, 64-256 KB: config 2 is best at 64 KB,
+  // configs 3-4 at 256 KB).  When every stage-1 row is widened FP32 and the
+  // stage holds several waves of 256 KB chunks (config 4 and up), 64-thread
+  // CTAs, 16 per SM, are faster (measured -3..-4 %); below that they lose.
+  int64_t s1_total = 0;
+  bool fp32_only = pipe != P_M1S && !groups.empty();
+  for (auto& g : groups) {
+    const int cls = std::get<0>(g.first);
+    const int64_t ncol = std::get<2>(g.first) - std::get<1>(g.first);
+    const bool is32 = cls == 2 || d->hi32;
+    if (!is32) fp32_only = false;
+    for (int32_t k : g.second) s1_total += (cls == 1 ? d->khi[k] : d->klo[k]) * ncol * (is32 ? 4 : 8);
+  }
+  int sms = 148;
+  if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device) != cudaSuccess) sms = 148;
+  const bool s1_narrow = fp32_only && s1_total >= (int64_t)sms * (1024 / kS1Threads32) * (256 << 10);
+  if (!(opt && opt->s1_chunk_bytes > 0) && !s1_narrow) {
     const int64_t slots = (int64_t)std::max(sms, 1) * (1024 / kS1Threads);
     s1_target = std::min<int64_t>(s1_target, std::max<int64_t>(64 * 1024, s1_total / slots));
   }
@@ -735,8 +740,7 @@ int hmx::plan_create_impl(const hmx_matrix_desc* d, int device, const hmx_plan_o
   dp.blob64 = d_b64;
   dp.blob32 = d_b32;
   dp.f32mode1 = pipe == P_M1S ? F32_ALL32 : F32_ALL64;
-  dp.s1_narrow = pipe != P_M1S && !seg1.empty() &&
-                 std::all_of(seg1.begin(), seg1.end(), [](const Seg& a) { return a.W64 == 0; });
+  dp.s1_narrow = s1_narrow ? 1 : 0;
   dp.f32mode2 = f32mode2;
   dp.zepi = pipe == P_M1D ? Z_NONE : (pipe == P_M1S || pipe == P_M1M) ? Z_ROUND32 : Z_SCALE;
   dp.zscale = d_zs;
