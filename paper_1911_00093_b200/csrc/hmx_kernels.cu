@@ -115,11 +115,15 @@ __device__ __forceinline__ double z_epilogue(const DevPlan& P, double s, int zi)
 }
 
 // One CTA = one segment: rows [row0, row0+R) of a column-major item stream.
-template <int F32MODE, int OUT, int NT>
-__global__ void __launch_bounds__(NT, (OUT == OUT_Y && F32MODE != F32_ALL64) ? HMX_MIXED_MINB : 1024 / NT) seg_kernel(DevPlan P, const Seg* __restrict__ segs,
+// DEEP: stage 2 with an FP64 part, 12 FP64 columns in flight per thread at 3
+// CTAs per SM (80 registers) instead of 8 at 4 (A/B on config 4: m1-double
+// stage 2 -1.1 %, m2-double -2.4 %; FP32-only stage 2 prefers 8 at 4)
+template <int F32MODE, int OUT, int NT, bool DEEP = false>
+__global__ void __launch_bounds__(NT, DEEP ? 3 : (OUT == OUT_Y && F32MODE != F32_ALL64) ? HMX_MIXED_MINB : 1024 / NT) seg_kernel(DevPlan P, const Seg* __restrict__ segs,
                                                           const double* __restrict__ x, S2Out out) {
   // stage 1 segments have a single run (no index expansion) and <= 1024 columns
   constexpr int WMAX = OUT == OUT_Z ? kS1WMax : kSegWMax;
+  constexpr int D64 = DEEP ? 12 : 8;
   __shared__ double gs[WMAX];
   __shared__ uint8_t fl[WMAX];
   __shared__ int32_t sidx[OUT == OUT_Z ? 1 : kSegWMax];
@@ -151,42 +155,43 @@ __global__ void __launch_bounds__(NT, (OUT == OUT_Y && F32MODE != F32_ALL64) ? H
     const int cb = act ? (int)((int64_t)tw * q64 / g64) : 0;
     const int ce = act ? (int)((int64_t)tw * (q64 + 1) / g64) : 0;
     const double* __restrict__ col = P.blob64 + sg.off64 + (int64_t)tc0 * rp64 + 2 * p64;
-    // batches of 8 columns, predicated at the end of the range (a short
+    // D64 columns in flight per thread (stage 2, FP64-only kernels: deeper,
+    // at fewer resident CTAs), predicated at the end of the range (a short
     // range -- small segments -- is still one batch, never a serial chain).
     // The first batch is independent of g: it is issued before the gather
     // (and, in stage 2, before waiting on stage 1) to hide one latency.
-    double2 m[8];
+    double2 m[D64];
     int c = cb;
 #pragma unroll
-    for (int u = 0; u < 8; ++u)
+    for (int u = 0; u < D64; ++u)
       if (c + u < ce) m[u] = ld_stream(col + (int64_t)(c + u) * rp64, pol);
     if (OUT == OUT_Y && tc0 == 0) asm volatile("griddepcontrol.wait;" ::: "memory");
     __syncthreads();
     gather_g<false, NT, WMAX>(P, P.runs + sg.run0, sg.nrun64, tc0, tw, x, gs, fl, sidx);
     __syncthreads();
-    // rolling: each register is refilled with the column 8 ahead right after
-    // it is consumed (8 loads stay in flight); the tail is predicated
+    // rolling: each register is refilled with the column D64 ahead right
+    // after it is consumed (D64 loads stay in flight); the tail is predicated
     for (;;) {
-      if (c + 16 <= ce) {
+      if (c + 2 * D64 <= ce) {
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
+        for (int u = 0; u < D64; ++u) {
           const double g = gs[c + u];
           a0 = fma(m[u].x, g, a0);
           a1 = fma(m[u].y, g, a1);
-          m[u] = ld_stream(col + (int64_t)(c + 8 + u) * rp64, pol);
+          m[u] = ld_stream(col + (int64_t)(c + D64 + u) * rp64, pol);
         }
       } else {
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
+        for (int u = 0; u < D64; ++u) {
           if (c + u < ce) {
             const double g = gs[c + u];
             a0 = fma(m[u].x, g, a0);
             a1 = fma(m[u].y, g, a1);
           }
-          if (c + 8 + u < ce) m[u] = ld_stream(col + (int64_t)(c + 8 + u) * rp64, pol);
+          if (c + D64 + u < ce) m[u] = ld_stream(col + (int64_t)(c + D64 + u) * rp64, pol);
         }
       }
-      c += 8;
+      c += D64;
       if (c >= ce) break;
     }
   }
@@ -502,7 +507,7 @@ __global__ void probe_kernel(DevPlan P, const double* __restrict__ x, unsigned l
 // ------------------------------------------------------------------------------
 // launchers
 
-template <int M, int O, int NT = kSegThreads>
+template <int M, int O, int NT = kSegThreads, bool DEEP = false>
 static cudaError_t launch_seg(const DevPlan& P, const Seg* segs, int nseg, const double* x,
                               const S2Out& out, cudaStream_t st, bool pdl) {
   cudaLaunchConfig_t cfg = {};
@@ -515,7 +520,7 @@ static cudaError_t launch_seg(const DevPlan& P, const Seg* segs, int nseg, const
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = pdl ? 1 : 0;
-  return cudaLaunchKernelEx(&cfg, seg_kernel<M, O, NT>, P, segs, x, out);
+  return cudaLaunchKernelEx(&cfg, seg_kernel<M, O, NT, DEEP>, P, segs, x, out);
 }
 
 cudaError_t launch_stage1(const DevPlan& P, const double* x, cudaStream_t st, const int* skip) {
@@ -540,7 +545,9 @@ cudaError_t launch_stage2(const DevPlan& P, const double* x, const S2Out& out, c
   switch (P.f32mode2) {
     case F32_ALL32: return launch_seg<F32_ALL32, OUT_Y>(P, P.seg2, P.n_seg2, x, out, st, pdl);
     case F32_MIXED: return launch_seg<F32_MIXED, OUT_Y>(P, P.seg2, P.n_seg2, x, out, st, pdl);
-    default: return launch_seg<F32_ALL64, OUT_Y>(P, P.seg2, P.n_seg2, x, out, st, pdl);
+    default:
+      return P.s2_deep ? launch_seg<F32_ALL64, OUT_Y, kSegThreads, true>(P, P.seg2, P.n_seg2, x, out, st, pdl)
+                       : launch_seg<F32_ALL64, OUT_Y>(P, P.seg2, P.n_seg2, x, out, st, pdl);
   }
 }
 

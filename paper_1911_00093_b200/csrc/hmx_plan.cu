@@ -741,6 +741,15 @@ int hmx::plan_create_impl(const hmx_matrix_desc* d, int device, const hmx_plan_o
   dp.blob32 = d_b32;
   dp.f32mode1 = pipe == P_M1S ? F32_ALL32 : F32_ALL64;
   dp.s1_narrow = s1_narrow ? 1 : 0;
+  {
+    // deep FP64 pipeline when the FP64 part carries most of stage 2's bytes
+    int64_t b64 = 0, b32 = 0;
+    for (const Seg& a : seg2) {
+      b64 += (int64_t)a.W64 * a.R * 8;
+      b32 += (int64_t)a.W32 * a.R * 4;
+    }
+    dp.s2_deep = (f32mode2 == F32_ALL64 && b64 > 0 && b64 >= b32) ? 1 : 0;
+  }
   dp.f32mode2 = f32mode2;
   dp.zepi = pipe == P_M1D ? Z_NONE : (pipe == P_M1S || pipe == P_M1M) ? Z_ROUND32 : Z_SCALE;
   dp.zscale = d_zs;
