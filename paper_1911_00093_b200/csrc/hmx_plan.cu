@@ -233,7 +233,12 @@ int hmx::plan_create_impl(const hmx_matrix_desc* d, int device, const hmx_plan_o
   }
   int sms = 148;
   if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device) != cudaSuccess) sms = 148;
-  const bool s1_narrow = fp32_only && s1_total >= (int64_t)sms * (1024 / kS1Threads32) * (256 << 10);
+  // (Method 3 with FP64-class rows too: 64-thread CTAs with <= 128-row
+  // segments, measured -5 % on m3:c=3's stage 1; neutral-to-worse for the
+  // all-FP64 schemes, which keep 128 threads)
+  const bool s1_big = s1_total >= (int64_t)sms * (1024 / kS1Threads32) * (256 << 10);
+  const bool s1_narrow = s1_big && (fp32_only || pipe == P_M3);
+  const int64_t s1_rows = (s1_narrow && !fp32_only) ? 2 * kS1Threads32 : kS1Rows;
   if (!(opt && opt->s1_chunk_bytes > 0) && !s1_narrow) {
     const int64_t slots = (int64_t)std::max(sms, 1) * (1024 / kS1Threads);
     s1_target = std::min<int64_t>(s1_target, std::max<int64_t>(64 * 1024, s1_total / slots));
@@ -278,7 +283,7 @@ int hmx::plan_create_impl(const hmx_matrix_desc* d, int device, const hmx_plan_o
     const bool is32 = cls == 2 || d->hi32;
     const int64_t es = is32 ? 4 : 8;
     const int64_t rg = (int64_t)rows.size();
-    const int64_t pieces = (rg + kS1Rows - 1) / kS1Rows;
+    const int64_t pieces = (rg + s1_rows - 1) / s1_rows;
     for (int64_t pc = 0; pc < pieces; ++pc) {
       const int64_t r0 = rg * pc / pieces, r1 = rg * (pc + 1) / pieces, R = r1 - r0;
       const int64_t rp = round_up(R, is32 ? 4 : 2);
