@@ -222,6 +222,14 @@ int hmx_plan_create_prepared(hmx_master* master, int scheme, double split_factor
  * stage-2 ms, out_ms[3] = min matvec ms. */
 int hmx_bench_matvec(hmx_plan* plan, int warmup, int iters, int64_t flush_l2, double* out_ms);
 
+/* Page-locked host memory for matvec results (no reference counterpart: the
+ * reference returns a fresh numpy array, matvec.py:145-147, and the Python
+ * layer hands out fresh arrays backed by a pool of these buffers so the
+ * device->host copy of y is one DMA instead of a driver-staged pageable
+ * copy).  hmx_host_free accepts NULL. */
+int hmx_host_alloc(int64_t bytes, void** out);
+void hmx_host_free(void* ptr);
+
 #ifdef __cplusplus
 }
 #endif

@@ -101,6 +101,8 @@ SIGNATURES = {
                                                 ctypes.POINTER(PlanOptions),
                                                 ctypes.POINTER(ctypes.c_void_p),
                                                 ctypes.POINTER(PrepareInfo)]),
+    "hmx_host_alloc": (ctypes.c_int, [ctypes.c_int64, ctypes.POINTER(ctypes.c_void_p)]),
+    "hmx_host_free": (None, [ctypes.c_void_p]),
 }
 
 _lib = None
@@ -244,7 +246,7 @@ class Plan:
 
     def matvec(self, x: np.ndarray, permuted: bool = False) -> tuple[np.ndarray, int]:
         x = np.ascontiguousarray(x, dtype=np.float64)
-        y = np.empty(self.n, dtype=np.float64)
+        y = result_array(self.n)
         rc = self._lib.hmx_matvec(self.handle, x.ctypes.data, y.ctypes.data,
                                   HMX_PERMUTED if permuted else 0)
         if rc not in (HMX_OK, HMX_ERR_NONFINITE):
@@ -295,6 +297,72 @@ class Plan:
             self.close()
         except Exception:
             pass
+
+
+class _PinnedLease:
+    """Owner of one pooled page-locked buffer; numpy arrays made from it keep
+    it alive (ndarray.base) and it returns to the pool when the last one dies."""
+
+    __slots__ = ("ptr", "nbytes", "__array_interface__")
+
+    def __init__(self, ptr: int, nbytes: int):
+        self.ptr = ptr
+        self.nbytes = nbytes
+        self.__array_interface__ = {"shape": (nbytes // 8,), "typestr": "<f8",
+                                    "data": (ptr, False), "version": 3}
+
+    def __del__(self):
+        try:
+            _host_pool.release(self.ptr, self.nbytes)
+        except Exception:
+            pass
+
+
+class _HostPool:
+    """Page-locked buffers for matvec results.  The reference returns a fresh
+    array per call (matvec.py:145-147); so does this pool - each buffer backs
+    at most one live array - but the device->host copy into it is one DMA
+    instead of the driver's staged pageable copy.  Live plus cached pinned
+    bytes are capped (HMX_PINNED_POOL_MB, default 1024); past the cap,
+    results are ordinary pageable arrays."""
+
+    def __init__(self):
+        self.lock = threading.Lock()
+        self.free: dict[int, list[int]] = {}
+        self.held = 0
+        self.cap = int(os.environ.get("HMX_PINNED_POOL_MB", "1024")) << 20
+
+    def array(self, n: int):
+        nbytes = 8 * int(n)
+        with self.lock:
+            bucket = self.free.get(nbytes)
+            ptr = bucket.pop() if bucket else None
+            if ptr is None:
+                if self.held + nbytes > self.cap:
+                    return None
+                out = ctypes.c_void_p()
+                if load_library().hmx_host_alloc(nbytes, ctypes.byref(out)) != HMX_OK:
+                    return None
+                ptr = out.value
+                self.held += nbytes
+        return np.asarray(_PinnedLease(ptr, nbytes))
+
+    def release(self, ptr: int, nbytes: int) -> None:
+        with self.lock:
+            self.free.setdefault(nbytes, []).append(ptr)
+
+
+_host_pool = _HostPool()
+
+
+def result_array(n: int) -> np.ndarray:
+    """A fresh, uninitialised float64 array of length n for a matvec result
+    (page-locked when the pool allows)."""
+    if n > 0:
+        y = _host_pool.array(n)
+        if y is not None:
+            return y
+    return np.empty(n, dtype=np.float64)
 
 
 class Master:

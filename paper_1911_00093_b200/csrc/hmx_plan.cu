@@ -110,6 +110,21 @@ int hmx_plan_get_info(const hmx_plan* p, hmx_plan_info* info) {
   return HMX_OK;
 }
 
+int hmx_host_alloc(int64_t bytes, void** out) {
+  if (!out || bytes <= 0) {
+    set_error("hmx_host_alloc: bad size or null output");
+    return HMX_ERR_ARG;
+  }
+  *out = nullptr;
+  // portable: the buffer serves copies on any device's stream
+  HMX_CUDA(cudaHostAlloc(out, (size_t)bytes, cudaHostAllocPortable));
+  return HMX_OK;
+}
+
+void hmx_host_free(void* ptr) {
+  if (ptr) cudaFreeHost(ptr);
+}
+
 }  // extern "C"
 
 int hmx::plan_create_impl(const hmx_matrix_desc* d, int device, const hmx_plan_options* opt,
