@@ -136,6 +136,25 @@ def test_repeat_and_thread_counts_bitwise(hx, prob240):
     assert np.array_equal(y, hx.matvec(sh, hx.SourceVector(x)))
 
 
+def test_results_are_fresh_arrays(hx, prob240):
+    """matvec.py:145-147 returns a new array per call; the pinned result pool
+    must never hand a live array's buffer to another result."""
+    _, h, x = prob240
+    sh = hx.prepare_scheme(h, "m1-double")
+    ys = [hx.matvec(sh, x) for _ in range(4)]
+    ptrs = {y.ctypes.data for y in ys}
+    assert len(ptrs) == 4
+    ref = ys[0].copy()
+    for y in ys:
+        assert y.dtype == np.float64 and y.flags.writeable and y.flags.c_contiguous
+        assert np.array_equal(y, ref)
+    ys[1][:] = 0.0                        # writing one result leaves the others alone
+    assert np.array_equal(ys[2], ref)
+    del ys
+    for _ in range(8):                    # recycled buffers are fully overwritten
+        assert np.array_equal(hx.matvec(sh, x), ref)
+
+
 def test_single_and_mixed_differ_only_at_fp32_level(hx, prob240):
     _, h, x = prob240
     ys = hx.matvec(hx.prepare_scheme(h, "m1-single"), x)
