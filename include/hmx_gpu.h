@@ -41,7 +41,8 @@ typedef enum {
   HMX_ERR_CUDA = 2,       /* CUDA runtime failure (no device, OOM, ...) */
   HMX_ERR_NONFINITE = 3,  /* matvec result not finite: FloatingPointError */
   HMX_ERR_SHAPE = 4,      /* vector length does not match the matrix: ValueError */
-  HMX_ERR_OVERFLOW = 5    /* FP32 cast overflow while preparing a scheme: OverflowError */
+  HMX_ERR_OVERFLOW = 5,   /* FP32 cast overflow while preparing a scheme: OverflowError */
+  HMX_ERR_COMM = 6        /* NCCL failure in the multi-GPU entry points */
 } hmx_status;
 
 /* Precision schemes of the reference (precision.py:46-104). */
@@ -221,6 +222,44 @@ int hmx_plan_create_prepared(hmx_master* master, int scheme, double split_factor
  * out_ms[0] = mean matvec ms, out_ms[1] = mean stage-1 ms, out_ms[2] = mean
  * stage-2 ms, out_ms[3] = min matvec ms. */
 int hmx_bench_matvec(hmx_plan* plan, int warmup, int iters, int64_t flush_l2, double* out_ms);
+
+/*
+ * Multi-GPU mode: rows of the permuted index space are cut into
+ * contiguous slices [cuts[k], cuts[k+1]), one per rank (one process per GPU);
+ * each rank holds a row-restricted plan of its slice (hmx_plan_options).
+ * Per operator application there is exactly one exchange, the allgather of
+ * the iterate's slices over NCCL (grouped send/recv straight into the full
+ * permuted vector, no padding); solver dot products are local partials fused
+ * into the kernels plus one small NCCL allreduce per reduction point.  The
+ * reference has no multi-process mode; its single-process semantics
+ * (solver.py:68-168) are kept on every rank.
+ */
+typedef struct hmx_comm hmx_comm;
+
+/* NCCL unique id (128 bytes) for hmx_comm_create; made on rank 0 and passed
+ * to every rank by the caller (e.g. torch.distributed.broadcast_object_list). */
+int hmx_comm_unique_id(uint8_t id[128]);
+/* Joins the NCCL communicator (blocks until every rank has joined).  cuts has
+ * world + 1 entries, cuts[0] = 0, cuts[world] = n. */
+int hmx_comm_create(const uint8_t id[128], int world, int rank, int device, const int64_t* cuts,
+                    hmx_comm** out);
+void hmx_comm_destroy(hmx_comm* comm);
+
+/* y_local = rows [cuts[rank], cuts[rank+1]) of A x (permuted order, device
+ * pointers): x_local, this rank's slice of x, is allgathered into the full
+ * iterate, then the local two-stage product runs.  Enqueued on `stream`
+ * (UINT64_MAX = the plan's stream) without synchronising.  `nonfinite`
+ * (device int, may be NULL) is set when a local y entry is not finite. */
+int hmx_dist_matvec(hmx_plan* plan, hmx_comm* comm, const double* x_local, double* y_local,
+                    int* nonfinite, uint64_t stream);
+
+/* BiCG-STAB over row slices (solver.py:68-168, from x0 = 0), every rank
+ * calling with its own slice: b_local / x_local are this rank's rows of b / x
+ * in permuted order (host).  Same report on every rank; decisions are taken
+ * on the device from allreduced scalars, so all ranks stop together. */
+int hmx_bicgstab_dist(hmx_plan* plan, hmx_plan* plan64, hmx_comm* comm, const double* b_local,
+                      double tol, int max_iter, double* x_local, double* history,
+                      hmx_solve_report* report);
 
 /* Page-locked host memory for matvec results (no reference counterpart: the
  * reference returns a fresh numpy array, matvec.py:145-147, and the Python

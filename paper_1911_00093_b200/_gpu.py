@@ -16,6 +16,7 @@ import numpy as np
 from . import _native
 
 HMX_OK, HMX_ERR_ARG, HMX_ERR_CUDA, HMX_ERR_NONFINITE, HMX_ERR_SHAPE, HMX_ERR_OVERFLOW = 0, 1, 2, 3, 4, 5
+HMX_ERR_COMM = 6
 HMX_DEVICE_PTRS, HMX_PERMUTED = 1, 2
 
 SCHEME_CODES = {"m1-double": 0, "m1-single": 1, "m1-mixed": 2, "m2-double": 3,
@@ -102,6 +103,16 @@ SIGNATURES = {
                                                 ctypes.POINTER(ctypes.c_void_p),
                                                 ctypes.POINTER(PrepareInfo)]),
     "hmx_host_alloc": (ctypes.c_int, [ctypes.c_int64, ctypes.POINTER(ctypes.c_void_p)]),
+    "hmx_comm_unique_id": (ctypes.c_int, [ctypes.c_char_p]),
+    "hmx_comm_create": (ctypes.c_int, [ctypes.c_char_p, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                       _i64p, ctypes.POINTER(ctypes.c_void_p)]),
+    "hmx_comm_destroy": (None, [ctypes.c_void_p]),
+    "hmx_dist_matvec": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                       ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint64]),
+    "hmx_bicgstab_dist": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                         ctypes.c_void_p, ctypes.c_double, ctypes.c_int,
+                                         ctypes.c_void_p, ctypes.c_void_p,
+                                         ctypes.POINTER(SolveReport)]),
     "hmx_host_free": (None, [ctypes.c_void_p]),
 }
 
@@ -363,6 +374,83 @@ def result_array(n: int) -> np.ndarray:
         if y is not None:
             return y
     return np.empty(n, dtype=np.float64)
+
+
+def _nccl_first():
+    """Load torch (and with it torch's NCCL) before libhmx_gpu resolves NCCL
+    at run time, so the process holds one NCCL: libhmx_gpu's dlopen of
+    libnccl.so.2 then returns torch's copy."""
+    import torch  # noqa: F401
+
+
+class Comm:
+    """This rank's NCCL communicator and multi-GPU solver workspace
+    (hmx_comm_create).  `cuts` are the world + 1 row-slice boundaries of the
+    permuted index space; `uid` is Comm.unique_id() made on rank 0 and
+    passed to every rank."""
+
+    def __init__(self, uid: bytes, world: int, rank: int, device: int, cuts):
+        _nccl_first()
+        lib = load_library()
+        self._cuts = np.ascontiguousarray(cuts, dtype=np.int64)
+        if self._cuts.shape != (world + 1,):
+            raise ValueError("cuts must have world + 1 entries")
+        h = ctypes.c_void_p()
+        check(lib.hmx_comm_create(bytes(uid), int(world), int(rank), int(device),
+                                  _p(self._cuts, ctypes.c_int64), ctypes.byref(h)),
+              "hmx_comm_create")
+        self.handle = h
+        self.world, self.rank, self.device = int(world), int(rank), int(device)
+        self.r0, self.r1 = int(self._cuts[rank]), int(self._cuts[rank + 1])
+        self._lib = lib
+
+    @staticmethod
+    def unique_id() -> bytes:
+        _nccl_first()
+        buf = ctypes.create_string_buffer(128)
+        check(load_library().hmx_comm_unique_id(buf), "hmx_comm_unique_id")
+        return buf.raw
+
+    def matvec(self, plan: "Plan", x_local_ptr: int, y_local_ptr: int, nonfinite_ptr: int = 0,
+               stream: int | None = None) -> None:
+        """Enqueue y_local = (A x)[r0:r1] (device pointers, permuted order):
+        allgather of the x slices, then the local product."""
+        stream = (1 << 64) - 1 if stream is None else stream
+        check(self._lib.hmx_dist_matvec(plan.handle, self.handle, ctypes.c_void_p(x_local_ptr),
+                                        ctypes.c_void_p(y_local_ptr),
+                                        ctypes.c_void_p(nonfinite_ptr or None), int(stream)),
+              "hmx_dist_matvec")
+
+    def bicgstab(self, plan: "Plan", plan64: "Plan", b_local, tol: float, max_iter: int):
+        """BiCG-STAB on this rank's rows: returns (x_local, SolveReport,
+        history array, rc)."""
+        b = np.ascontiguousarray(b_local, dtype=np.float64)
+        if b.shape != (self.r1 - self.r0,):
+            raise ValueError(f"local right-hand side shape {b.shape} != ({self.r1 - self.r0},)")
+        x = np.zeros_like(b)
+        hist = np.zeros(int(max_iter) + 2, dtype=np.float64)
+        rep = SolveReport()
+        rc = self._lib.hmx_bicgstab_dist(plan.handle, plan64.handle if plan64 else None,
+                                         self.handle, b.ctypes.data, float(tol), int(max_iter),
+                                         x.ctypes.data, hist.ctypes.data, ctypes.byref(rep))
+        if rc not in (HMX_OK, HMX_ERR_NONFINITE):
+            check(rc, "hmx_bicgstab_dist")
+        return x, rep, hist, rc
+
+    @property
+    def closed(self) -> bool:
+        return not getattr(self, "handle", None)
+
+    def close(self):
+        if getattr(self, "handle", None):
+            self._lib.hmx_comm_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 class Master:

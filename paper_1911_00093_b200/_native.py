@@ -81,7 +81,7 @@ def build_gpu(force: bool = False, verbose: bool = False) -> Path:
             print(out)
         objs.append(str(o))
     tmp = GPU_LIB.with_suffix(".so.tmp%d" % os.getpid())
-    _run([NVCC, GENCODE, "-shared", "-o", str(tmp)] + objs + ["-lcudart"])
+    _run([NVCC, GENCODE, "-shared", "-o", str(tmp)] + objs + ["-lcudart", "-ldl"])
     os.replace(tmp, GPU_LIB)
     return GPU_LIB
 

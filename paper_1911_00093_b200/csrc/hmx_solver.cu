@@ -16,8 +16,14 @@
 // breakdown report).  Per iteration: p-update, v = A p (fused r^.v),
 // s-update (fused |s|^2), t = A s (fused t.s, t.t), x/r-update (fused |r|^2,
 // r^.r).
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <type_traits>
+
 #include <cmath>
 #include <cstdlib>
+#include <cstring>
 #include <mutex>
 
 #include "hmx_plan_impl.cuh"
@@ -189,7 +195,7 @@ __global__ void __launch_bounds__(kVecThreads) s_update_kernel(const double* r, 
                                                                 double* s, int n, double* sc,
                                                                 VecRed R, const int* ictl,
                                                                 double* hist, int* stop,
-                                                                const int* nonfin) {
+                                                                const int* nonfin, int dist = 0) {
   if (*(volatile int*)stop) return;
   const int it = ictl[0];
   const int rho_slot = rho_slot_of(it);
@@ -211,7 +217,9 @@ __global__ void __launch_bounds__(kVecThreads) s_update_kernel(const double* r, 
     s[i] = si;
     u += si * si;
   }
-  if (grid_reduce2(u, 0.0, R)) {  // last CTA, thread 0: the reduced |s|^2
+  // last CTA, thread 0: the reduced |s|^2 (multi-GPU: a local partial,
+  // decided on by decide_s_kernel after the allreduce)
+  if (grid_reduce2(u, 0.0, R) && !dist) {
     const double s_rel = __ddiv_rn(sqrt(R.out[0]), sc[SC_NB]);
     if (s_rel < tol) {
       hist[it] = s_rel;
@@ -237,7 +245,8 @@ __global__ void __launch_bounds__(kVecThreads) xr_update_kernel(double* x, doubl
                                                                  const double* rhat, int n,
                                                                  double* sc, VecRed R,
                                                                  const int* ictl, double* hist,
-                                                                 int* stop, const int* nonfin) {
+                                                                 int* stop, const int* nonfin,
+                                                                 int dist = 0) {
   if (*(volatile int*)stop) return;
   const int it = ictl[0];
   const int next_slot = rho_slot_of(it + 1);
@@ -263,13 +272,36 @@ __global__ void __launch_bounds__(kVecThreads) xr_update_kernel(double* x, doubl
     u += ri * ri;
     w += rhat[i] * ri;
   }
-  if (grid_reduce2(u, w, R)) {
+  if (grid_reduce2(u, w, R) && !dist) {
     const double rel = __ddiv_rn(sqrt(R.out[0]), sc[SC_NB]);
     hist[it] = rel;
     sc[next_slot] = R.out[1];  // rho of the next iteration
     if (rel < tol) set_stop(stop, R_CONV, it, sc, rel);
     else if (fabs(omega) < kBreakdownEps) set_stop(stop, R_OMEGA, it, sc, omega);
   }
+}
+
+// Multi-GPU: the decisions s_update / xr_update take in their last CTA,
+// taken instead on the allreduced sums (identical on every rank, so every
+// rank records the same decision at the same point).
+__global__ void decide_s_kernel(double* sc, const int* ictl, double* hist, int* stop) {
+  if (*(volatile int*)stop) return;
+  const int it = ictl[0];
+  const double s_rel = __ddiv_rn(sqrt(sc[SC_SS]), sc[SC_NB]);
+  if (s_rel < sc[SC_TOL]) {
+    hist[it] = s_rel;
+    set_stop(stop, R_SEXIT, it, sc, s_rel);
+  }
+}
+
+__global__ void decide_r_kernel(double* sc, const int* ictl, double* hist, int* stop) {
+  if (*(volatile int*)stop) return;
+  const int it = ictl[0];
+  const double rel = __ddiv_rn(sqrt(sc[SC_TMP]), sc[SC_NB]);
+  hist[it] = rel;
+  sc[rho_slot_of(it + 1)] = sc[SC_TMP + 1];
+  if (rel < sc[SC_TOL]) set_stop(stop, R_CONV, it, sc, rel);
+  else if (fabs(sc[SC_OMEGA]) < kBreakdownEps) set_stop(stop, R_OMEGA, it, sc, sc[SC_OMEGA]);
 }
 
 // out = [|b - y|^2, |b|^2]   (solver.py:60-62)
@@ -340,6 +372,29 @@ int alloc_ws(hmx_plan* p, Workspace& w, int64_t n, int grid) {
   HMX_CUDA(cudaMemset(w.sc, 0, SC_N * sizeof(double)));
   HMX_CUDA(cudaMallocHost(&w.h_sc, (SC_N + 8) * sizeof(double)));
   p->pinned.push_back(w.h_sc);
+  return HMX_OK;
+}
+
+// y = A xp on stream st (y: the plan's rows), fused dots into sc[slot..slot+1]
+int apply_sc(hmx_plan* A, double* sc, cudaStream_t st, const double* xp, double* y,
+             const double* w1, int yy, int slot, int* flag, const int* skip = nullptr) {
+  if ((w1 || yy) && A->dp.n_seg2 == 0)  // no local rows: the dots are zero
+    HMX_CUDA(cudaMemsetAsync(sc + slot, 0, 2 * sizeof(double), st));
+  S2Out out{};
+  out.skip = skip;
+  out.y = y;
+  out.permute_out = 0;
+  out.w1 = w1;
+  out.yy = yy;
+  if (w1 || yy) {
+    out.seg_dots = A->d_seg_dots;
+    out.done = A->d_done;
+    out.dots_out = sc + slot;
+  }
+  out.nonfinite = flag;
+  HMX_CUDA(launch_stage1(A->dp, xp, st, skip));
+  HMX_CUDA(launch_stage2(A->dp, xp, out, st, /*pdl=*/true));
+  A->last_xp = xp;
   return HMX_OK;
 }
 
@@ -448,6 +503,34 @@ int true_residual_dev(SolveCtx& c, double* out) {
   if (nb == 0.0) *out = nr == 0.0 ? 0.0 : INFINITY;
   else *out = nr / nb;
   return HMX_OK;
+}
+
+// Iterations completed and operator applications run for a recorded
+// decision (or none: max_iter reached); returns the completed count.
+int account_iterations(int reason, int stop_it, int max_iter, hmx_solve_report* rep) {
+  int completed;
+  if (reason == R_NONE) completed = max_iter;
+  else if (reason == R_RHO || reason == R_DENOM || reason == R_TT || reason == R_NONFINITE)
+    completed = stop_it - 1;
+  else completed = stop_it;  // R_SEXIT, R_CONV, R_OMEGA complete their iteration
+  rep->iterations = completed;
+  rep->matvecs += 2 * completed;
+  if (reason == R_DENOM) rep->matvecs += 1;
+  if (reason == R_SEXIT) rep->matvecs -= 1;  // t = A s skipped on the early exit
+  if (reason == R_TT) rep->matvecs += 2;
+  return completed;
+}
+
+void report_breakdown(int reason, int stop_it, double bval, hmx_solve_report* rep) {
+  if (reason == R_TT) {  // solver.py:139-142
+    rep->breakdown = 3;
+    rep->breakdown_iteration = stop_it;
+    return;
+  }
+  // rho (solver.py:113-115), shadow projection (:123-125), omega (:155-157)
+  rep->breakdown = reason == R_RHO ? 1 : reason == R_DENOM ? 2 : 4;
+  rep->breakdown_value = bval;
+  rep->breakdown_iteration = stop_it;
 }
 
 int workspace_for(hmx_plan* p, Workspace& out, int grid) {
@@ -637,17 +720,7 @@ int hmx_bicgstab(hmx_plan* A, hmx_plan* A64, const double* b, double tol, int ma
       stop_it = sw[2];
     }
   }
-  // iterations completed, matvecs actually run
-  int completed;
-  if (reason == R_NONE) completed = max_iter;
-  else if (reason == R_RHO || reason == R_DENOM || reason == R_TT || reason == R_NONFINITE)
-    completed = stop_it - 1;
-  else completed = stop_it;  // R_SEXIT, R_CONV, R_OMEGA complete their iteration
-  rep->iterations = completed;
-  rep->matvecs += 2 * completed;
-  if (reason == R_RHO || reason == R_DENOM) rep->matvecs += (reason == R_DENOM) ? 1 : 0;
-  if (reason == R_SEXIT) rep->matvecs -= 1;  // t = A s skipped on the early exit
-  if (reason == R_TT) rep->matvecs += 2;
+  const int completed = account_iterations(reason, stop_it, max_iter, rep);
   if (completed > 0) {
     HMX_CUDA(cudaMemcpyAsync(history + 1, w.hist + 1, (size_t)completed * sizeof(double),
                              cudaMemcpyDeviceToHost, st));
@@ -662,16 +735,11 @@ int hmx_bicgstab(hmx_plan* A, hmx_plan* A64, const double* b, double tol, int ma
       set_error("non-finite matvec result");
       return finish(HMX_ERR_NONFINITE);
     }
-    case R_RHO:    // solver.py:113-115
-    case R_DENOM:  // solver.py:123-125
-    case R_OMEGA:  // solver.py:155-157
-      rep->breakdown = reason == R_RHO ? 1 : reason == R_DENOM ? 2 : 4;
-      rep->breakdown_value = bval;
-      rep->breakdown_iteration = stop_it;
-      break;
-    case R_TT:     // solver.py:139-142
-      rep->breakdown = 3;
-      rep->breakdown_iteration = stop_it;
+    case R_RHO:
+    case R_DENOM:
+    case R_OMEGA:
+    case R_TT:
+      report_breakdown(reason, stop_it, bval, rep);
       break;
     case R_SEXIT:  // solver.py:130-136: x = x + alpha p, then confirm
       x_alpha_p_kernel<<<c.grid, kVecThreads, 0, st>>>(w.x, w.p, n32, w.sc);
@@ -680,6 +748,496 @@ int hmx_bicgstab(hmx_plan* A, hmx_plan* A64, const double* b, double tol, int ma
     case R_CONV: {  // solver.py:151-154
       double tr = 0.0;
       if ((rc = true_residual_dev(c, &tr))) return finish(rc);
+      rep->matvecs++;
+      rep->has_true_residual = 1;
+      rep->true_residual = tr;
+      rep->converged = tr < tol;
+      break;
+    }
+    default:
+      break;
+  }
+  return finish(HMX_OK);
+}
+
+}  // extern "C"
+
+// ==============================================================================
+// Multi-GPU mode: row slices, one NCCL allgather of the iterate
+// per operator application, small NCCL allreduces for the dot products.  The
+// iteration is the single-GPU one (same kernels, same IEEE scalar
+// arithmetic, same stop word); the kernels' grid reductions produce local
+// partials and the decisions move to decide_s/decide_r after the allreduce.
+// Iterations are enqueued in speculative batches guarded by the stop word
+// (one host synchronisation per batch); collectives are always enqueued, so
+// every rank issues the same sequence.
+
+struct hmx_comm {
+  std::mutex mu;
+  ncclComm_t nc = nullptr;
+  int world = 1, rank = 0, device = 0;
+  std::vector<int64_t> cuts;
+  int64_t n = 0, r0 = 0, r1 = 0;
+  std::vector<void*> allocs;
+  // full permuted vectors (allgather targets)
+  double *x_full = nullptr, *p_full = nullptr, *s_full = nullptr;
+  // local rows
+  double *b = nullptr, *x = nullptr, *r = nullptr, *rhat = nullptr, *v = nullptr, *t = nullptr,
+         *y = nullptr;
+  double* sc = nullptr;
+  double* h_sc = nullptr;  // pinned mirror: scalars, flags, stop word
+  int* flags = nullptr;
+  int* stop = nullptr;
+  int* ictl = nullptr;
+  double* partials = nullptr;
+  uint32_t* done = nullptr;
+  double* hist = nullptr;
+  int hist_cap = 0;
+  int grid = 0;
+  cudaEvent_t ev[2] = {};
+
+  template <typename T>
+  T* alloc(size_t count) {
+    void* p = nullptr;
+    if (count == 0) count = 1;
+    if (cudaMalloc(&p, count * sizeof(T)) != cudaSuccess) return nullptr;
+    allocs.push_back(p);
+    return static_cast<T*>(p);
+  }
+};
+
+// NCCL is resolved at run time (first hmx_comm_* call) rather than linked:
+// dlopen("libnccl.so.2") returns the NCCL the process already holds -- the
+// one torch loaded -- so a single NCCL serves torch.distributed and this
+// library (linking it would put the system libnccl in the process first,
+// and torch's libtorch_cuda needs symbols of its own, newer copy).
+// HMX_NCCL_LIB names a specific library instead.
+struct NcclApi {
+  bool ok = false;
+  std::string error;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
+  ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+};
+
+static NcclApi& nccl_api() {
+  static NcclApi api = [] {
+    NcclApi a;
+    const char* env = std::getenv("HMX_NCCL_LIB");
+    void* h = dlopen(env ? env : "libnccl.so.2", RTLD_NOW | RTLD_LOCAL);
+    if (!h && !env) h = dlopen("libnccl.so", RTLD_NOW | RTLD_LOCAL);
+    if (!h) {
+      a.error = std::string("cannot load NCCL: ") + dlerror();
+      return a;
+    }
+    bool all = true;
+    auto get = [&](auto& fn, const char* name) {
+      fn = reinterpret_cast<std::remove_reference_t<decltype(fn)>>(dlsym(h, name));
+      if (!fn) {
+        all = false;
+        a.error += std::string(" missing ") + name;
+      }
+    };
+    get(a.GetUniqueId, "ncclGetUniqueId");
+    get(a.CommInitRank, "ncclCommInitRank");
+    get(a.CommDestroy, "ncclCommDestroy");
+    get(a.GetErrorString, "ncclGetErrorString");
+    get(a.GroupStart, "ncclGroupStart");
+    get(a.GroupEnd, "ncclGroupEnd");
+    get(a.Send, "ncclSend");
+    get(a.Recv, "ncclRecv");
+    get(a.AllReduce, "ncclAllReduce");
+    a.ok = all;
+    return a;
+  }();
+  return api;
+}
+
+#define HMX_NCCL(call)                                                                    \
+  do {                                                                                    \
+    ncclResult_t _r = (call);                                                             \
+    if (_r != ncclSuccess) {                                                              \
+      hmx::set_error(std::string("NCCL error in " #call ": ") + nccl_api().GetErrorString(_r));    \
+      return HMX_ERR_COMM;                                                                \
+    }                                                                                     \
+  } while (0)
+
+namespace {
+
+// The one exchange per operator application: every rank's slice of `full`
+// (its rows [cuts[q], cuts[q+1])) to every other rank, grouped NCCL
+// send/recv straight into place (uneven slices, no padding, no copies).
+int allgather_rows(hmx_comm* c, double* full, cudaStream_t st) {
+  if (c->world == 1) return HMX_OK;
+  const int64_t m = c->r1 - c->r0;
+  HMX_NCCL(nccl_api().GroupStart());
+  for (int q = 0; q < c->world; ++q) {
+    if (q == c->rank) continue;
+    const int64_t mq = c->cuts[(size_t)q + 1] - c->cuts[(size_t)q];
+    if (m > 0) HMX_NCCL(nccl_api().Send(full + c->r0, (size_t)m, ncclFloat64, q, c->nc, st));
+    if (mq > 0) HMX_NCCL(nccl_api().Recv(full + c->cuts[(size_t)q], (size_t)mq, ncclFloat64, q, c->nc, st));
+  }
+  HMX_NCCL(nccl_api().GroupEnd());
+  return HMX_OK;
+}
+
+int allreduce_sum(hmx_comm* c, double* v, int count, cudaStream_t st) {
+  HMX_NCCL(nccl_api().AllReduce(v, v, (size_t)count, ncclFloat64, ncclSum, c->nc, st));
+  return HMX_OK;
+}
+
+// dot partials (sum) and a non-finite flag (max) in one NCCL group
+int allreduce_dots_flag(hmx_comm* c, double* dots, int count, int* flag, cudaStream_t st) {
+  HMX_NCCL(nccl_api().GroupStart());
+  if (count > 0) HMX_NCCL(nccl_api().AllReduce(dots, dots, (size_t)count, ncclFloat64, ncclSum, c->nc, st));
+  HMX_NCCL(nccl_api().AllReduce(flag, flag, 1, ncclInt32, ncclMax, c->nc, st));
+  HMX_NCCL(nccl_api().GroupEnd());
+  return HMX_OK;
+}
+
+struct DistCtx {
+  hmx_plan* A;
+  hmx_plan* A64;
+  hmx_comm* c;
+  cudaStream_t st;
+  int grid;
+  int nl;
+  VecRed red(int slot) const { return VecRed{c->partials, c->done, c->sc + slot}; }
+};
+
+int dist_sync(const DistCtx& d) {
+  hmx_comm* c = d.c;
+  HMX_CUDA(cudaMemcpyAsync(c->h_sc, c->sc, SC_N * sizeof(double), cudaMemcpyDeviceToHost, d.st));
+  HMX_CUDA(cudaMemcpyAsync(c->h_sc + SC_N, c->flags, 4 * sizeof(int), cudaMemcpyDeviceToHost, d.st));
+  HMX_CUDA(cudaMemcpyAsync(c->h_sc + SC_N + 2, c->stop, 4 * sizeof(int), cudaMemcpyDeviceToHost, d.st));
+  HMX_CUDA(cudaStreamSynchronize(d.st));
+  return HMX_OK;
+}
+
+const int* dist_host_stop(const DistCtx& d) { return reinterpret_cast<const int*>(d.c->h_sc + SC_N + 2); }
+const int* dist_host_flags(const DistCtx& d) { return reinterpret_cast<const int*>(d.c->h_sc + SC_N); }
+
+// one iteration on the local rows (the single-GPU enqueue_iteration with the
+// collectives between its kernels)
+int enqueue_iteration_dist(const DistCtx& d) {
+  hmx_comm* c = d.c;
+  cudaStream_t st = d.st;
+  double* pl = c->p_full + c->r0;
+  double* sl = c->s_full + c->r0;
+  int rc;
+  p_update_kernel<<<d.grid, kVecThreads, 0, st>>>(c->r, c->v, pl, d.nl, c->ictl, c->sc, c->stop);
+  if ((rc = allgather_rows(c, c->p_full, st))) return rc;
+  if ((rc = apply_sc(d.A, c->sc, st, c->p_full, c->v, c->rhat, 0, SC_DV, c->flags, c->stop))) return rc;
+  if ((rc = allreduce_dots_flag(c, c->sc + SC_DV, 1, c->flags, st))) return rc;
+  s_update_kernel<<<d.grid, kVecThreads, 0, st>>>(c->r, c->v, sl, d.nl, c->sc, d.red(SC_SS), c->ictl,
+                                                    c->hist, c->stop, c->flags, 1);
+  if ((rc = allreduce_sum(c, c->sc + SC_SS, 1, st))) return rc;
+  decide_s_kernel<<<1, 1, 0, st>>>(c->sc, c->ictl, c->hist, c->stop);
+  if ((rc = allgather_rows(c, c->s_full, st))) return rc;
+  if ((rc = apply_sc(d.A, c->sc, st, c->s_full, c->t, sl, 1, SC_DT, c->flags + 1, c->stop))) return rc;
+  if ((rc = allreduce_dots_flag(c, c->sc + SC_DT, 2, c->flags + 1, st))) return rc;
+  xr_update_kernel<<<d.grid, kVecThreads, 0, st>>>(c->x, c->r, pl, sl, c->t, c->rhat, d.nl, c->sc,
+                                                     d.red(SC_TMP), c->ictl, c->hist, c->stop,
+                                                     c->flags + 1, 1);
+  if ((rc = allreduce_sum(c, c->sc + SC_TMP, 2, st))) return rc;
+  decide_r_kernel<<<1, 1, 0, st>>>(c->sc, c->ictl, c->hist, c->stop);
+  advance_kernel<<<1, 1, 0, st>>>(c->ictl, c->stop, 0, 0);
+  HMX_CUDA(cudaGetLastError());
+  return HMX_OK;
+}
+
+// |b - A64 x| / |b| over all ranks (solver.py:56-65)
+int true_residual_dist(const DistCtx& d, double* out) {
+  hmx_comm* c = d.c;
+  cudaStream_t st = d.st;
+  int rc;
+  if (d.nl > 0)
+    HMX_CUDA(cudaMemcpyAsync(c->x_full + c->r0, c->x, (size_t)d.nl * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  if ((rc = allgather_rows(c, c->x_full, st))) return rc;
+  if ((rc = apply_sc(d.A64, c->sc, st, c->x_full, c->y, nullptr, 0, 0, c->flags + 2))) return rc;
+  resid_kernel<<<d.grid, kVecThreads, 0, st>>>(c->b, c->y, d.nl, d.red(SC_RES));
+  HMX_CUDA(cudaGetLastError());
+  if ((rc = allreduce_dots_flag(c, c->sc + SC_RES, 2, c->flags + 2, st))) return rc;
+  if ((rc = dist_sync(d))) return rc;
+  if (dist_host_flags(d)[2]) {
+    set_error("non-finite matvec result");
+    return HMX_ERR_NONFINITE;
+  }
+  const double nr = std::sqrt(c->h_sc[SC_RES]), nb = std::sqrt(c->h_sc[SC_RES + 1]);
+  if (nb == 0.0) *out = nr == 0.0 ? 0.0 : INFINITY;
+  else *out = nr / nb;
+  return HMX_OK;
+}
+
+bool plan_matches(const hmx_plan* p, const hmx_comm* c) {
+  return p->n == c->n && p->dp.row_begin == c->r0 && p->dp.row_end == c->r1 && p->device == c->device;
+}
+
+}  // namespace
+
+extern "C" {
+
+int hmx_comm_unique_id(uint8_t id[128]) {
+  if (!id) return HMX_ERR_ARG;
+  if (!nccl_api().ok) {
+    set_error(nccl_api().error);
+    return HMX_ERR_COMM;
+  }
+  static_assert(sizeof(ncclUniqueId) == 128, "NCCL unique id size");
+  ncclUniqueId u;
+  HMX_NCCL(nccl_api().GetUniqueId(&u));
+  std::memcpy(id, &u, sizeof(u));
+  return HMX_OK;
+}
+
+void hmx_comm_destroy(hmx_comm* c) {
+  if (!c) return;
+  {
+    DeviceGuard g(c->device);
+    cudaDeviceSynchronize();
+    if (c->nc) nccl_api().CommDestroy(c->nc);
+    for (void* a : c->allocs) cudaFree(a);
+    if (c->h_sc) cudaFreeHost(c->h_sc);
+    for (auto& e : c->ev)
+      if (e) cudaEventDestroy(e);
+  }
+  delete c;
+}
+
+int hmx_comm_create(const uint8_t id[128], int world, int rank, int device, const int64_t* cuts,
+                    hmx_comm** out) {
+  if (!id || !cuts || !out || world < 1 || rank < 0 || rank >= world) {
+    set_error("hmx_comm_create: bad arguments");
+    return HMX_ERR_ARG;
+  }
+  *out = nullptr;
+  if (!nccl_api().ok) {
+    set_error(nccl_api().error);
+    return HMX_ERR_COMM;
+  }
+  if (cuts[0] != 0) {
+    set_error("hmx_comm_create: cuts[0] must be 0");
+    return HMX_ERR_ARG;
+  }
+  for (int q = 0; q < world; ++q)
+    if (cuts[q + 1] < cuts[q]) {
+      set_error("hmx_comm_create: cuts must be non-decreasing");
+      return HMX_ERR_ARG;
+    }
+  if (cuts[world] > INT32_MAX || cuts[world] < 1) {
+    set_error("hmx_comm_create: n out of range");
+    return HMX_ERR_ARG;
+  }
+  DeviceGuard guard(device);
+  HMX_CUDA(cudaSetDevice(device));
+  auto* c = new hmx_comm();
+  c->world = world;
+  c->rank = rank;
+  c->device = device;
+  c->cuts.assign(cuts, cuts + world + 1);
+  c->n = cuts[world];
+  c->r0 = cuts[rank];
+  c->r1 = cuts[rank + 1];
+  ncclUniqueId u;
+  std::memcpy(&u, id, sizeof(u));
+  const ncclResult_t r = nccl_api().CommInitRank(&c->nc, world, u, rank);
+  if (r != ncclSuccess) {
+    set_error(std::string("ncclCommInitRank: ") + nccl_api().GetErrorString(r));
+    c->nc = nullptr;
+    hmx_comm_destroy(c);
+    return HMX_ERR_COMM;
+  }
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+  c->grid = 2 * sms;
+  const size_t n = (size_t)c->n, nl = (size_t)(c->r1 - c->r0);
+  c->x_full = c->alloc<double>(n);
+  c->p_full = c->alloc<double>(n);
+  c->s_full = c->alloc<double>(n);
+  double** loc[] = {&c->b, &c->x, &c->r, &c->rhat, &c->v, &c->t, &c->y};
+  bool ok = c->x_full && c->p_full && c->s_full;
+  for (double** v : loc) ok = ok && (*v = c->alloc<double>(nl)) != nullptr;
+  c->sc = c->alloc<double>(SC_N);
+  c->flags = c->alloc<int>(4);
+  c->stop = c->alloc<int>(4);
+  c->ictl = c->alloc<int>(4);
+  c->partials = c->alloc<double>((size_t)2 * c->grid);
+  c->done = c->alloc<uint32_t>(1);
+  ok = ok && c->sc && c->flags && c->stop && c->ictl && c->partials && c->done;
+  if (!ok || cudaMallocHost(&c->h_sc, (SC_N + 8) * sizeof(double)) != cudaSuccess ||
+      cudaMemset(c->done, 0, sizeof(uint32_t)) != cudaSuccess ||
+      cudaMemset(c->sc, 0, SC_N * sizeof(double)) != cudaSuccess ||
+      cudaMemset(c->x_full, 0, n * sizeof(double)) != cudaSuccess ||
+      cudaEventCreate(&c->ev[0]) != cudaSuccess || cudaEventCreate(&c->ev[1]) != cudaSuccess) {
+    set_error("hmx_comm_create: device allocation failed");
+    hmx_comm_destroy(c);
+    return HMX_ERR_CUDA;
+  }
+  *out = c;
+  return HMX_OK;
+}
+
+int hmx_dist_matvec(hmx_plan* p, hmx_comm* c, const double* x_local, double* y_local, int* nonfinite,
+                    uint64_t stream) {
+  if (!p || !c || (!x_local && c->r1 > c->r0) || (!y_local && c->r1 > c->r0)) {
+    set_error("null argument");
+    return HMX_ERR_ARG;
+  }
+  if (!plan_matches(p, c)) {
+    set_error("plan rows / device do not match this rank's slice");
+    return HMX_ERR_ARG;
+  }
+  std::scoped_lock lock(c->mu, p->mu);
+  DeviceGuard guard(p->device);
+  cudaStream_t st = stream == UINT64_MAX ? p->stream : reinterpret_cast<cudaStream_t>(stream);
+  const int64_t nl = c->r1 - c->r0;
+  if (nl > 0 && x_local != c->x_full + c->r0)
+    HMX_CUDA(cudaMemcpyAsync(c->x_full + c->r0, x_local, (size_t)nl * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  int rc = allgather_rows(c, c->x_full, st);
+  if (rc) return rc;
+  S2Out out{};
+  out.y = y_local;
+  out.permute_out = 0;
+  out.nonfinite = nonfinite ? nonfinite : p->d_nonfinite;
+  HMX_CUDA(launch_stage1(p->dp, c->x_full, st));
+  HMX_CUDA(launch_stage2(p->dp, c->x_full, out, st, /*pdl=*/true));
+  p->last_xp = c->x_full;
+  return HMX_OK;
+}
+
+int hmx_bicgstab_dist(hmx_plan* A, hmx_plan* A64, hmx_comm* c, const double* b_local, double tol,
+                      int max_iter, double* x_local, double* history, hmx_solve_report* rep) {
+  if (!A || !c || !history || !rep || ((!b_local || !x_local) && c->r1 > c->r0)) {
+    set_error("null argument");
+    return HMX_ERR_ARG;
+  }
+  if (!A64) A64 = A;
+  if (!plan_matches(A, c) || !plan_matches(A64, c)) {
+    set_error("plan rows / device do not match this rank's slice");
+    return HMX_ERR_ARG;
+  }
+  if (!(tol > 0.0) || max_iter < 1) {
+    set_error("tol must be positive and max_iter >= 1");
+    return HMX_ERR_ARG;
+  }
+  std::unique_lock<std::mutex> l0(c->mu, std::defer_lock), l1(A->mu, std::defer_lock),
+      l2(A64->mu, std::defer_lock);
+  if (A == A64) std::lock(l0, l1);
+  else std::lock(l0, l1, l2);
+  DeviceGuard guard(A->device);
+  *rep = hmx_solve_report{};
+  DistCtx d{A, A64, c, A->stream, c->grid, (int)(c->r1 - c->r0)};
+  cudaStream_t st = d.st;
+  const size_t nlb = (size_t)d.nl * sizeof(double);
+  int rc;
+
+  HMX_CUDA(cudaEventRecord(c->ev[0], st));
+  if (d.nl > 0) HMX_CUDA(cudaMemcpyAsync(c->b, b_local, nlb, cudaMemcpyHostToDevice, st));
+  HMX_CUDA(cudaMemsetAsync(c->flags, 0, 4 * sizeof(int), st));
+  HMX_CUDA(cudaMemsetAsync(c->stop, 0, 4 * sizeof(int), st));
+  // |b| (solver.py:91)
+  dot2_kernel<<<d.grid, kVecThreads, 0, st>>>(c->b, c->b, nullptr, nullptr, d.nl, d.red(SC_BB));
+  HMX_CUDA(cudaGetLastError());
+  if ((rc = allreduce_sum(c, c->sc + SC_BB, 1, st))) return rc;
+  if ((rc = dist_sync(d))) return rc;
+  const double nb = std::sqrt(c->h_sc[SC_BB]);
+  int hlen = 0;
+  auto finish = [&](int status) -> int {
+    rep->history_len = hlen;
+    if (status == HMX_OK && d.nl > 0) HMX_CUDA(cudaMemcpyAsync(x_local, c->x, nlb, cudaMemcpyDeviceToHost, st));
+    HMX_CUDA(cudaEventRecord(c->ev[1], st));
+    HMX_CUDA(cudaStreamSynchronize(st));
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, c->ev[0], c->ev[1]);
+    rep->device_ms = ms;
+    return status;
+  };
+  if (nb == 0.0) {  // zero data: x = 0 is exact (solver.py:92-97)
+    if (d.nl > 0) HMX_CUDA(cudaMemsetAsync(c->x, 0, nlb, st));
+    history[hlen++] = 0.0;
+    rep->converged = 1;
+    rep->has_true_residual = 1;
+    rep->true_residual = 0.0;
+    return finish(HMX_OK);
+  }
+  if (c->hist_cap < max_iter + 2) {
+    double* hd = c->alloc<double>((size_t)max_iter + 2);
+    if (!hd) {
+      set_error("cudaMalloc failed for the residual history");
+      return HMX_ERR_CUDA;
+    }
+    c->hist = hd;
+    c->hist_cap = max_iter + 2;
+  }
+  // x = 0 ; r = b - A x ; r_hat = r   (solver.py:99-102)
+  HMX_CUDA(cudaMemsetAsync(c->p_full, 0, (size_t)c->n * sizeof(double), st));
+  if ((rc = apply_sc(A, c->sc, st, c->p_full, c->t, nullptr, 0, 0, c->flags))) return rc;
+  rep->matvecs++;
+  if ((rc = allreduce_dots_flag(c, nullptr, 0, c->flags, st))) return rc;
+  init_kernel<<<d.grid, kVecThreads, 0, st>>>(c->b, c->t, c->r, c->rhat, c->x, d.nl, d.red(SC_RHO1));
+  HMX_CUDA(cudaGetLastError());
+  if ((rc = allreduce_sum(c, c->sc + SC_RHO1, 1, st))) return rc;
+  HMX_CUDA(cudaMemcpyAsync(c->sc + SC_NB, &nb, sizeof(double), cudaMemcpyHostToDevice, st));
+  if ((rc = dist_sync(d))) return rc;
+  if (dist_host_flags(d)[0]) {
+    set_error("non-finite matvec result");
+    return finish(HMX_ERR_NONFINITE);
+  }
+  history[hlen++] = std::sqrt(c->h_sc[SC_RHO1]) / nb;
+  {
+    const int ctl[4] = {1, max_iter, 0, 0};
+    HMX_CUDA(cudaMemcpyAsync(c->ictl, ctl, sizeof(ctl), cudaMemcpyHostToDevice, st));
+    HMX_CUDA(cudaMemcpyAsync(c->sc + SC_TOL, &tol, sizeof(double), cudaMemcpyHostToDevice, st));
+  }
+  // speculative batches (identical on every rank: the stop word is)
+  int done_through = 0, batch = 2;
+  while (done_through < max_iter) {
+    const int last = std::min(max_iter, done_through + batch);
+    for (int i = done_through + 1; i <= last; ++i)
+      if ((rc = enqueue_iteration_dist(d))) return rc;
+    done_through = last;
+    if ((rc = dist_sync(d))) return rc;
+    if (dist_host_stop(d)[0]) break;
+    batch = std::min(batch * 2, 16);
+  }
+  int reason = R_NONE, stop_it = 0;
+  if (dist_host_stop(d)[0]) {
+    reason = dist_host_stop(d)[1];
+    stop_it = dist_host_stop(d)[2];
+  }
+  const int completed = account_iterations(reason, stop_it, max_iter, rep);
+  if (completed > 0) {
+    HMX_CUDA(cudaMemcpyAsync(history + 1, c->hist + 1, (size_t)completed * sizeof(double),
+                             cudaMemcpyDeviceToHost, st));
+    HMX_CUDA(cudaStreamSynchronize(st));
+    hlen += completed;
+  }
+  const double bval = c->h_sc[SC_BVAL];
+  switch (reason) {
+    case R_NONFINITE:
+      A->last_xp = dist_host_flags(d)[0] ? c->p_full : c->s_full;
+      set_error("non-finite matvec result");
+      return finish(HMX_ERR_NONFINITE);
+    case R_RHO:
+    case R_DENOM:
+    case R_OMEGA:
+    case R_TT:
+      report_breakdown(reason, stop_it, bval, rep);
+      break;
+    case R_SEXIT:  // solver.py:130-136
+      x_alpha_p_kernel<<<d.grid, kVecThreads, 0, st>>>(c->x, c->p_full + c->r0, d.nl, c->sc);
+      HMX_CUDA(cudaGetLastError());
+      /* fallthrough */
+    case R_CONV: {  // solver.py:151-154
+      double tr = 0.0;
+      if ((rc = true_residual_dist(d, &tr))) return finish(rc);
       rep->matvecs++;
       rep->has_true_residual = 1;
       rep->true_residual = tr;

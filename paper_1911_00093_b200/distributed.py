@@ -7,16 +7,26 @@ builds only the blocks meeting its rows (compress.build_hmatrix(rows=...)),
 and holds a row-restricted device plan (hmx_plan_options / hmx_apply_local).
 
 Per matvec there is exactly one collective: an allgather of the iterate's
-slices (padded to equal length, NCCL over NVLink) into the full permuted
-vector every rank's stage 1 reads.  BiCG-STAB dot products are local partial
-sums (fused into the stage-2 epilogue on the GPU) finished by one small
-allreduce per reduction point.  Control flow mirrors reference
-pkg/src/hmx/solver.py:68-168 on every rank (identical scalars after the
-allreduces), so all ranks take the same decisions.
+slices into the full permuted vector every rank's stage 1 reads.  BiCG-STAB
+dot products are local partial sums (fused into the stage-2 epilogue on the
+GPU) finished by one small allreduce per reduction point.  Control flow
+mirrors reference pkg/src/hmx/solver.py:68-168 on every rank (identical
+scalars after the allreduces), so all ranks take the same decisions.
 
-The torch.distributed process group carries the collectives: NCCL on GPUs,
-gloo for the CPU tests (tests/test_distributed_gloo.py), where the local
-product is a CPU stand-in injected by the test.
+Two implementations of that protocol:
+
+* the GPU product path (`make_comm`, `bicgstab_gpu`, `bench_main`):
+  libhmx_gpu.so's own NCCL communicator (hmx_comm_create), the allgather as
+  grouped NCCL send/recv straight into the full vector (uneven slices, no
+  padding or copies; hmx_dist_matvec), and the whole BiCG-STAB iteration in
+  C++/CUDA (hmx_bicgstab_dist): the single-GPU fused vector kernels on local
+  rows, scalars and every decision on the device, iterations enqueued in
+  guarded batches -- no host synchronisation per matvec;
+* `DistributedOperator` / `bicgstab_distributed`: the same protocol written
+  with torch.distributed collectives and torch vector arithmetic, whose
+  local product is injectable.  It runs the multi-process tests on CPU
+  (gloo, world 2, tests/test_distributed_gloo.py) with a CPU stand-in for
+  the local product.
 """
 
 from __future__ import annotations
@@ -268,6 +278,42 @@ def bicgstab_distributed(op: DistributedOperator, op64: DistributedOperator, b_l
 # ---------------------------------------------------------------------------
 # GPU setup and benchmark (torchrun, one rank per GPU)
 
+def make_comm(slices: RowSlices, rank: int, device, group=None):
+    """This rank's libhmx_gpu NCCL communicator over the row slices.  The
+    NCCL unique id is made on rank 0 and broadcast through the
+    torch.distributed group (any backend) when world > 1."""
+    from . import _gpu
+
+    uid = _gpu.Comm.unique_id() if rank == 0 else None
+    if slices.world > 1:
+        import torch.distributed as dist
+        box = [uid]
+        dist.broadcast_object_list(box, src=0, group=group)
+        uid = box[0]
+    index = device.index if hasattr(device, "index") else int(device)
+    return _gpu.Comm(uid, slices.world, rank, index or 0, slices.cuts)
+
+
+def bicgstab_gpu(comm, plan, plan64, b_local, tol=1e-6, max_iter=1000, scheme_label=""):
+    """BiCG-STAB on this rank's rows through hmx_bicgstab_dist.  b_local is
+    this rank's slice of b in permuted order (host array); returns
+    (x_local, SolverReport), the report identical on every rank."""
+    from . import _gpu
+
+    t0 = time.perf_counter()
+    x, rep, hist, rc = comm.bicgstab(plan, plan64, b_local, tol, max_iter)
+    wall = time.perf_counter() - t0
+    if rc == _gpu.HMX_ERR_NONFINITE:
+        raise FloatingPointError("non-finite matvec result")
+    return x, SolverReport(
+        scheme=scheme_label, converged=bool(rep.converged), iterations=int(rep.iterations),
+        residual_history=[float(v) for v in hist[:rep.history_len]],
+        true_residual=float(rep.true_residual) if rep.has_true_residual else None,
+        wall_time_s=wall,
+        breakdown=_breakdown_message(rep.breakdown, rep.breakdown_value, rep.breakdown_iteration),
+        device_time_s=rep.device_ms / 1e3, matvecs=int(rep.matvecs))
+
+
 def make_gpu_operator(h, scheme: str, slices: RowSlices, rank: int, device, group=None):
     """Row-restricted device plan of `scheme` for this rank."""
     from . import _gpu
@@ -293,7 +339,7 @@ def bench_main(args, build_workload, workload_name, metric):
     import bench as bench_mod
     from .compress import build_hmatrix
     from .partition import build_block_partition, build_cluster_tree
-    from .problem import jittered_sphere_mesh
+    from .problem import jittered_sphere_mesh, right_hand_side
 
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -318,13 +364,21 @@ def bench_main(args, build_workload, workload_name, metric):
     peak, peak_src = bench_mod.measured_peak()
     a, b_ = slices.span(rank)
     x_np = np.random.default_rng(42).uniform(-1.0, 1.0, mesh.n)
-    x_host = torch.from_numpy(np.ascontiguousarray(x_np[np.asarray(h.permutation)[a:b_]])).pin_memory()
+    perm = np.asarray(h.permutation)
+    x_host = torch.from_numpy(np.ascontiguousarray(x_np[perm[a:b_]])).pin_memory()
     y_host = torch.empty(b_ - a, dtype=torch.float64).pin_memory()
+    b_full = right_hand_side(mesh) if c.get("voltages") else mesh.centroids[:, 2].copy()
+    b_local = np.ascontiguousarray(b_full[perm[a:b_]])
+    comm = make_comm(slices, rank, device)
+    y_dev = torch.empty(b_ - a, dtype=torch.float64, device=device)
     results, clocks, headline = {}, None, None
+    op64 = None
 
     def step(op, x_local):
-        op.gather(x_local)
-        return op.local_apply(op._full, None, False)[0]
+        # the one allgather (NCCL send/recv into the full vector) + local product
+        comm.matvec(op.plan, x_local.data_ptr(), y_dev.data_ptr(),
+                    stream=torch.cuda.current_stream(device).cuda_stream)
+        return y_dev
 
     def timed(fn, k):
         dist.barrier()
@@ -358,6 +412,19 @@ def bench_main(args, build_workload, workload_name, metric):
         entry = {"ms": ms, "matvec_per_s": 1e3 / ms, "payload_bytes_all_ranks": float(local_bytes),
                  "local_ms_rank0": r["ms"], "stage1_ms_rank0": r["stage1_ms"],
                  "stage2_ms_rank0": r["stage2_ms"], "rows_rank0": b_ - a}
+        if not args.no_solve:
+            if op64 is None:
+                op64 = op if name == bench_mod.HEADLINE else make_gpu_operator(
+                    h, bench_mod.HEADLINE, slices, rank, device)[0]
+            dist.barrier()
+            _, srep = bicgstab_gpu(comm, op.plan, op64.plan, b_local, tol=1e-8, max_iter=1000,
+                                   scheme_label=name)
+            t_solve = torch.tensor([srep.device_time_s], device=device)
+            dist.all_reduce(t_solve, op=dist.ReduceOp.MAX)
+            entry["solve"] = {"iterations": srep.iterations, "converged": srep.converged,
+                              "true_residual": srep.true_residual,
+                              "device_s_max_over_ranks": float(t_solve),
+                              "matvecs": srep.matvecs, "breakdown": srep.breakdown}
         if name == bench_mod.HEADLINE:
             # end to end: this rank's x slice from pinned host memory, the
             # allgather, the local product, its y slice back to the host
@@ -370,7 +437,11 @@ def bench_main(args, build_workload, workload_name, metric):
             s2_bytes = info["stage2_bytes"] + 8 * (b_ - a)
             headline = (entry, s2_bytes, r, info)
         results[name] = entry
-        op.plan.close()
+        if op is not op64:
+            op.plan.close()
+    if op64 is not None:
+        op64.plan.close()
+    comm.close()
     dist.barrier()
     if rank == 0:
         entry, s2_bytes, r, info = headline
@@ -393,7 +464,8 @@ def bench_main(args, build_workload, workload_name, metric):
             "e2e": {"value": 1e3 / entry["e2e_ms"], "unit": "matvec/s",
                     "h2d_bytes_per_step": 8 * int(mesh.n), "d2h_bytes_per_step": 8 * int(mesh.n)},
             "gpu_launches": 2 * args.steps, "clocks": clocks, "variants": results,
-            "note": "each step = one NCCL allgather of the iterate + the local two-stage product; "
+            "note": "each step = one NCCL allgather of the iterate (grouped send/recv into the "
+                    "full vector) + the local two-stage product; solves: hmx_bicgstab_dist; "
                     "cpu_baseline is reported by the N=1 run",
         }), flush=True)
     dist.destroy_process_group()

@@ -100,3 +100,77 @@ def test_distributed_solver_nccl_world1(hx, cfg):
                                                                              ref.true_residual)
     finally:
         dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("scheme", ["m1-double", "m1-mixed", "m2-mixed", "m3:c=1"])
+def test_cxx_dist_path_world1_is_the_single_gpu_path(hx, cfg, scheme):
+    """hmx_dist_matvec and hmx_bicgstab_dist (libhmx_gpu's own NCCL
+    communicator, device-side decisions, batched iterations) at world 1 run
+    the single-GPU kernels in the same order: bitwise the single-GPU matvec
+    and graph-resident solver (solution, history, report)."""
+    import torch
+
+    from paper_1911_00093_b200 import _gpu
+    from paper_1911_00093_b200 import distributed as D
+
+    mesh, h, x = cfg
+    n = h.n
+    perm = np.asarray(h.permutation)
+    slices = D.RowSlices([0, n])
+    dev = torch.device("cuda", 0)
+    comm = D.make_comm(slices, 0, dev)
+    sh = hx.prepare_scheme(h, scheme)
+    sh64 = hx.prepare_scheme(h, "m1-double")
+    plan = _gpu.Plan(sh.packed, h.partition.table, perm, sh.scheme.label, n, row_range=(0, n))
+    plan64 = _gpu.Plan(sh64.packed, h.partition.table, perm, "m1-double", n, row_range=(0, n))
+    try:
+        xp = torch.from_numpy(np.ascontiguousarray(x[perm])).to(dev)
+        y = torch.empty(n, dtype=torch.float64, device=dev)
+        comm.matvec(plan, xp.data_ptr(), y.data_ptr(),
+                    stream=torch.cuda.current_stream().cuda_stream)
+        torch.cuda.synchronize()
+        assert np.array_equal(y.cpu().numpy(), hx.matvec(sh, x)[perm])
+
+        b = mesh.centroids[:, 2].copy()
+        xl, rep = D.bicgstab_gpu(comm, plan, plan64, b[perm], tol=1e-8, max_iter=1000,
+                                 scheme_label=scheme)
+        x_ref, ref = hx.bicgstab(sh, h, b, hx.SolverConfig(tol=1e-8))
+        assert (rep.iterations, rep.converged, rep.matvecs, rep.breakdown) == \
+            (ref.iterations, ref.converged, ref.matvecs, ref.breakdown)
+        assert rep.residual_history == ref.residual_history
+        assert rep.true_residual == ref.true_residual
+        xs = np.empty(n)
+        xs[perm] = xl
+        assert np.array_equal(xs, x_ref)
+    finally:
+        plan.close()
+        plan64.close()
+        comm.close()
+
+
+def test_cxx_dist_solver_edge_cases_world1(hx, cfg):
+    """Zero right-hand side and max_iter exhaustion through hmx_bicgstab_dist
+    report like the single-GPU solver (solver.py:92-97, :160-168)."""
+    import torch
+
+    from paper_1911_00093_b200 import _gpu
+    from paper_1911_00093_b200 import distributed as D
+
+    mesh, h, _ = cfg
+    n = h.n
+    perm = np.asarray(h.permutation)
+    comm = D.make_comm(D.RowSlices([0, n]), 0, torch.device("cuda", 0))
+    sh = hx.prepare_scheme(h, "m2-mixed")
+    plan = _gpu.Plan(sh.packed, h.partition.table, perm, sh.scheme.label, n, row_range=(0, n))
+    try:
+        x0, r0 = D.bicgstab_gpu(comm, plan, None, np.zeros(n), tol=1e-8)
+        assert r0.converged and r0.iterations == 0 and r0.true_residual == 0.0
+        assert np.array_equal(x0, np.zeros(n))
+        b = mesh.centroids[:, 2].copy()
+        _, rk = D.bicgstab_gpu(comm, plan, None, b[perm], tol=1e-14, max_iter=3)
+        _, ref = hx.bicgstab(sh, h, b, hx.SolverConfig(tol=1e-14, max_iter=3))
+        assert rk.iterations == ref.iterations == 3 and not rk.converged
+        assert rk.residual_history == ref.residual_history
+    finally:
+        plan.close()
+        comm.close()
