@@ -37,7 +37,8 @@ struct Seg {             // 64 bytes; one CTA
   int32_t run0;          // first run; FP64 runs then FP32 runs
   int32_t nrun64, nrun32;
   int32_t red;           // stage 1: reduction group of a column-chunked segment, or -1
-  int32_t chunk, nchunks;
+  int32_t chunk, nchunks;  // stage 1: column chunk / count; stage 2: chunk = wb, the first
+                           // thread of the FP32-accumulated groups of a mixed FP32 part (0: none)
   int32_t part_off;      // partial slots (nchunks * R doubles)
   int32_t gtab;          // FP32 part: group cuts gtab[gtab..gtab+G] then the first FP32-
                          // accumulated column; <= -2: that column alone at gtab[-2-gtab]; -1: none

@@ -206,8 +206,26 @@ __global__ void __launch_bounds__(NT, DEEP ? 3 : (OUT == OUT_Y && F32MODE != F32
   // ---------------- FP32 part: 4 rows x 16 bytes per thread
   const int rp32 = (R + 3) & ~3;
   const int tpg32 = rp32 >> 2;
-  const int g32 = NT / tpg32;
-  const int q32 = tid / tpg32, p32 = tid - q32 * tpg32;
+  int g32 = NT / tpg32;
+  int q32 = tid / tpg32, p32 = tid - q32 * tpg32;
+  if constexpr (F32MODE == F32_MIXED && OUT == OUT_Y) {
+    // warp-aligned split (plan: sg.chunk = wb): groups of the FP64-accumulated
+    // columns on threads [0, wb), of the FP32-accumulated ones from wb on, so
+    // no warp runs both loops
+    const int wb = sg.chunk;
+    if (wb > 0 && sg.gtab >= 0) {
+      const int ga = wb / tpg32, gb = (NT - wb) / tpg32;
+      g32 = ga + gb;
+      if (tid < wb) {
+        if (q32 >= ga) q32 = g32;  // idle
+      } else {
+        const int u = tid - wb;
+        const int qb = u / tpg32;
+        p32 = u - qb * tpg32;
+        q32 = qb < gb ? ga + qb : g32;
+      }
+    }
+  }
   double b[4] = {0.0, 0.0, 0.0, 0.0};
   float b32[4] = {0.f, 0.f, 0.f, 0.f};
   // the part holds FP64-accumulated items first, then FP32-accumulated ones

@@ -369,8 +369,11 @@ int hmx::plan_create_impl(const hmx_matrix_desc* d, int device, const hmx_plan_o
     const int64_t* t = d->table + 5 * it.block;
     return it.cls == 0 ? t[3] - t[2] : it.cls == 1 ? d->khi[it.block] : d->klo[it.block];
   };
-  const char* dw_env = std::getenv("HMX_DENSE_WEIGHT");
-  const double dense_weight = dw_env ? std::atof(dw_env) : 1.8;
+  // cost of an FP64-accumulated (widened) column relative to an FP32-chain
+  // column in a mixed FP32 part (A/B on config 4 with the warp-aligned split:
+  // m1-mixed best at 0.8-1.0, m2-single at 1/1.0-1/1.2)
+  const char* aw_env = std::getenv("HMX_ACC64_WEIGHT");
+  const double acc64_weight = aw_env ? std::atof(aw_env) : 0.85;
   const bool dense_single = pipe == P_M1S || pipe == P_M2S;  // A32 . x32 in FP32
   const bool u_acc32 = pipe == P_M1S || pipe == P_M1M;       // U32 . z32 in FP32
   bool any_acc32 = false, any_acc64_in32 = false;
@@ -429,28 +432,26 @@ int hmx::plan_create_impl(const hmx_matrix_desc* d, int device, const hmx_plan_o
     // reference's FP32 GEMV; FP64-accumulated items may be cut anywhere.
     // Targets are re-spread over the remaining groups after every cut.
     sg.gtab = -1;
+    sg.chunk = 0;  // stage 2: wb, the first thread of the FP32-accumulated groups
     if (sg.W32 > 0 && sg.W32 <= kSegWMax && (dense_single || u_acc32)) {
-      const int64_t tpg = round_up(sg.R, 4) / 4, G = kSegThreads / tpg;
+      const int64_t tpg = round_up(sg.R, 4) / 4;
       struct Span { int64_t a, b; };
       std::vector<Span> acc;  // FP32-accumulated items of the part
       for (int32_t j = 0; j < sg.nrun32; ++j) {
         const Run& r = runs[(size_t)(sg.run0 + sg.nrun64 + j)];
         if (r.flags & RUN_ACC32) acc.push_back({r.col0, (int64_t)r.col0 + r.width});
       }
-      sg.gtab = (int32_t)gtab.size();
-      gtab.push_back(0);
-      int64_t prev = 0;
-      size_t k = 0;
       // balance estimated cost, not columns: when the part mixes FP64- and
-      // FP32-accumulated items, a dense-block column costs dense_weight
-      // relative to a low-rank slab column (measured on config 4: m1-mixed
-      // and m2-single stage 2 -4..-7 %; pure FP32 parts balance by columns)
-      const bool mixed_part = !acc.empty() && acc.front().a > 0;
+      // FP32-accumulated items, a widened FP64-accumulated column costs
+      // acc64_weight relative to an FP32-chain column (pure parts balance
+      // by columns)
+      const int64_t c32 = acc.empty() ? sg.W32 : acc.front().a;  // first FP32-accumulated column
+      const bool mixed_part = !acc.empty() && c32 > 0;
       std::vector<double> wcol(1, 0.0);  // cost prefix at every item boundary
       std::vector<int64_t> ccol(1, 0);
       for (int32_t j = 0; j < sg.nrun32; ++j) {
         const Run& r = runs[(size_t)(sg.run0 + sg.nrun64 + j)];
-        const double w = (mixed_part && !(r.flags & RUN_Z)) ? dense_weight : 1.0;
+        const double w = (mixed_part && !(r.flags & RUN_ACC32)) ? acc64_weight : 1.0;
         ccol.push_back(ccol.back() + r.width);
         wcol.push_back(wcol.back() + w * r.width);
       }
@@ -466,22 +467,61 @@ int hmx::plan_create_impl(const hmx_matrix_desc* d, int device, const hmx_plan_o
         const double w = (wcol[i + 1] - wcol[i]) / (double)(ccol[i + 1] - ccol[i]);
         return (double)ccol[i] + (t - wcol[i]) / w;
       };
-      const double total = wcol.back();
-      for (int64_t q = 1; q < G; ++q) {
-        const double pc = cost_at(prev);
-        const double share = (total - pc) / (double)(G - q + 1);
-        int64_t cut = (int64_t)std::llround(col_at(pc + share));
-        while (k < acc.size() && acc[k].b <= cut) ++k;
-        if (k < acc.size() && acc[k].a < cut && cut < acc[k].b) {
-          // inside an FP32 item: move to its nearer end
-          cut = (cut - acc[k].a <= acc[k].b - cut) ? acc[k].a : acc[k].b;
+      // cuts of [lo, hi) among G groups (targets re-spread after every cut);
+      // a cut never falls strictly inside an FP32-accumulated item
+      // (RUN_ACC32), so each (row, block) is one FP32 chain as in the
+      // reference's FP32 GEMV; FP64-accumulated items may be cut anywhere
+      auto cut_range = [&](int64_t lo, int64_t hi, int64_t G) {
+        int64_t prev = lo;
+        size_t k = 0;
+        const double total = cost_at(hi);
+        for (int64_t q = 1; q < G; ++q) {
+          const double pc = cost_at(prev);
+          const double share = (total - pc) / (double)(G - q + 1);
+          int64_t cut = (int64_t)std::llround(col_at(pc + share));
+          while (k < acc.size() && acc[k].b <= cut) ++k;
+          if (k < acc.size() && acc[k].a < cut && cut < acc[k].b) {
+            // inside an FP32 item: move to its nearer end
+            cut = (cut - acc[k].a <= acc[k].b - cut) ? acc[k].a : acc[k].b;
+          }
+          cut = std::min<int64_t>(std::max(cut, prev), hi);
+          gtab.push_back((int32_t)cut);
+          prev = cut;
         }
-        cut = std::min<int64_t>(std::max(cut, prev), sg.W32);
-        gtab.push_back((int32_t)cut);
-        prev = cut;
+        gtab.push_back((int32_t)hi);
+      };
+      sg.gtab = (int32_t)gtab.size();
+      gtab.push_back(0);
+      if (mixed_part) {
+        // FP64- and FP32-accumulated columns run different loops: give each
+        // its own warps (a warp holding groups of both kinds would execute
+        // both loops one after the other).  wb, a multiple of 32, splits the
+        // threads: groups of the FP64-accumulated range [0, c32) below it,
+        // of the FP32-accumulated range [c32, W32) from it on; wb balances
+        // the estimated cost per group.
+        const double ca = cost_at(c32), cb = wcol.back() - ca;
+        int64_t best_wb = 0;
+        double best = 1e300;
+        for (int64_t wb = 32; wb < kSegThreads; wb += 32) {
+          const int64_t ga = wb / tpg, gb = (kSegThreads - wb) / tpg;
+          if (ga < 1 || gb < 1) continue;
+          const double t = std::max(ca / (double)ga, cb / (double)gb);
+          if (t < best) {
+            best = t;
+            best_wb = wb;
+          }
+        }
+        if (best_wb > 0) {
+          sg.chunk = (int32_t)best_wb;
+          cut_range(0, c32, best_wb / tpg);
+          cut_range(c32, sg.W32, (kSegThreads - best_wb) / tpg);
+        } else {
+          cut_range(0, sg.W32, kSegThreads / tpg);
+        }
+      } else {
+        cut_range(0, sg.W32, kSegThreads / tpg);
       }
-      gtab.push_back(sg.W32);
-      gtab.push_back((int32_t)(acc.empty() ? sg.W32 : acc.front().a));  // first FP32-accumulated column
+      gtab.push_back((int32_t)c32);  // first FP32-accumulated column
     } else if (sg.W32 > kSegWMax && (dense_single || u_acc32)) {
       // wide part (tiled, no group cuts): only the first FP32-accumulated column
       int32_t first = sg.W32;
