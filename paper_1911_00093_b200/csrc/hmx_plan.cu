@@ -387,6 +387,91 @@ int hmx::plan_create_impl(const hmx_matrix_desc* d, int device, const hmx_plan_o
     std::stable_sort(lst.begin(), lst.end(), [&](const ItemRef& a, const ItemRef& b) {
       return (int)item_acc32(a) < (int)item_acc32(b);
     });
+
+  // Thread groups of a stage-2 FP32 part that holds FP32-accumulated
+  // (chain) items, i.e. the schemes whose reference GEMV accumulates in FP32
+  // (matvec.py:57, :73).  Each (row, chain item) stays ONE FP32 chain, so a
+  // chain item is never split between groups: chain items are dealt to
+  // groups by LPT (widest first, to the least-loaded group) and laid out
+  // group by group (partition order inside a group), which balances far
+  // better than cutting the partition-order stream at item boundaries (a
+  // 40-column dense item against ~66-column group shares).  FP64-accumulated
+  // (widened) items come first and are cut anywhere.  When the part has
+  // both kinds, the two run different loops, so each kind gets its own
+  // warps: threads [0, wb) for the widened columns, [wb, 256) for the
+  // chains, wb (a multiple of 32) minimising the larger estimated group
+  // cost, a widened column costing acc64_weight of a chain column.
+  struct FP32Groups {
+    std::vector<int64_t> cuts;  // G + 1 column boundaries; empty: no group table
+    int64_t c32 = 0;            // first chain column
+    int64_t wb = 0;
+  };
+  auto lpt = [](const std::vector<int64_t>& w, int64_t G, std::vector<int32_t>* owner) {
+    std::vector<int32_t> order(w.size());
+    for (size_t i = 0; i < w.size(); ++i) order[i] = (int32_t)i;
+    std::stable_sort(order.begin(), order.end(), [&](int32_t a, int32_t b) { return w[(size_t)a] > w[(size_t)b]; });
+    std::vector<int64_t> load((size_t)G, 0);
+    if (owner) owner->assign(w.size(), 0);
+    for (int32_t i : order) {
+      const size_t g = (size_t)(std::min_element(load.begin(), load.end()) - load.begin());
+      load[g] += w[(size_t)i];
+      if (owner) (*owner)[(size_t)i] = (int32_t)g;
+    }
+    return *std::max_element(load.begin(), load.end());
+  };
+  auto plan_fp32_groups = [&](std::vector<ItemRef>& lst, int64_t R) {
+    FP32Groups fg;
+    if (!(dense_single || u_acc32) || lst.empty()) return fg;
+    int64_t W = 0;
+    for (const ItemRef& it : lst) W += item_width(it);
+    if (W > kSegWMax) return fg;  // tiled part: no group table
+    const int64_t tpg = round_up(R, 4) / 4, G = kSegThreads / tpg;
+    size_t nA = 0;
+    while (nA < lst.size() && !item_acc32(lst[nA])) ++nA;
+    int64_t colsA = 0;
+    for (size_t i = 0; i < nA; ++i) colsA += item_width(lst[i]);
+    std::vector<int64_t> wB;
+    for (size_t i = nA; i < lst.size(); ++i) wB.push_back(item_width(lst[i]));
+    fg.c32 = colsA;
+    int64_t gA = 0, gB = G;
+    if (nA > 0 && !wB.empty()) {
+      double best = 1e300;
+      for (int64_t wb = 32; wb < kSegThreads; wb += 32) {
+        const int64_t ga = wb / tpg, gb = (kSegThreads - wb) / tpg;
+        if (ga < 1 || gb < 1) continue;
+        const double t = std::max(acc64_weight * (double)colsA / (double)ga, (double)lpt(wB, gb, nullptr));
+        if (t < best) {
+          best = t;
+          fg.wb = wb;
+          gA = ga;
+          gB = gb;
+        }
+      }
+    } else if (nA > 0) {
+      gA = G;
+      gB = 0;
+    }
+    // widened range [0, colsA): even cuts over gA groups (or all G groups
+    // when there are no chains)
+    fg.cuts.push_back(0);
+    for (int64_t q = 1; q <= gA; ++q) fg.cuts.push_back(colsA * q / gA);
+    if (gB > 0) {
+      std::vector<int32_t> owner;
+      lpt(wB, gB, &owner);
+      std::vector<ItemRef> chains(lst.begin() + (ptrdiff_t)nA, lst.end());
+      std::vector<int64_t> load((size_t)gB, 0);
+      size_t k = nA;
+      for (int64_t g = 0; g < gB; ++g) {
+        for (size_t i = 0; i < chains.size(); ++i)
+          if (owner[i] == g) {
+            lst[k++] = chains[i];
+            load[(size_t)g] += wB[i];
+          }
+        fg.cuts.push_back(fg.cuts.back() + load[(size_t)g]);
+      }
+    }
+    return fg;
+  };
   for (int64_t s = 0; s < nseg2; ++s) {
     Seg& sg = seg2[(size_t)s];
     sg.row0 = (int32_t)seg_start[(size_t)s];
@@ -395,6 +480,7 @@ int hmx::plan_create_impl(const hmx_matrix_desc* d, int device, const hmx_plan_o
     sg.red = -1;
     sg.nchunks = 1;
     sg.part_off = -1;
+    const FP32Groups fg = plan_fp32_groups(items32[(size_t)s], sg.R);  // may reorder chain items
     for (int part = 0; part < 2; ++part) {
       const auto& lst = part == 0 ? items64[(size_t)s] : items32[(size_t)s];
       int64_t col = 0;
@@ -426,102 +512,15 @@ int hmx::plan_create_impl(const hmx_matrix_desc* d, int device, const hmx_plan_o
         sg.nrun32 = (int32_t)lst.size();
       }
     }
-    // item-aligned group boundaries for FP32-accumulated parts: a group
-    // boundary never falls strictly inside an FP32-accumulated item
-    // (RUN_ACC32), so each (row, block) is one FP32 chain as in the
-    // reference's FP32 GEMV; FP64-accumulated items may be cut anywhere.
-    // Targets are re-spread over the remaining groups after every cut.
+    // group boundaries of the FP32 part (plan_fp32_groups): gtab[0..G] then
+    // the first FP32-accumulated column; sg.chunk = wb of a warp-split part
     sg.gtab = -1;
-    sg.chunk = 0;  // stage 2: wb, the first thread of the FP32-accumulated groups
-    if (sg.W32 > 0 && sg.W32 <= kSegWMax && (dense_single || u_acc32)) {
-      const int64_t tpg = round_up(sg.R, 4) / 4;
-      struct Span { int64_t a, b; };
-      std::vector<Span> acc;  // FP32-accumulated items of the part
-      for (int32_t j = 0; j < sg.nrun32; ++j) {
-        const Run& r = runs[(size_t)(sg.run0 + sg.nrun64 + j)];
-        if (r.flags & RUN_ACC32) acc.push_back({r.col0, (int64_t)r.col0 + r.width});
-      }
-      // balance estimated cost, not columns: when the part mixes FP64- and
-      // FP32-accumulated items, a widened FP64-accumulated column costs
-      // acc64_weight relative to an FP32-chain column (pure parts balance
-      // by columns)
-      const int64_t c32 = acc.empty() ? sg.W32 : acc.front().a;  // first FP32-accumulated column
-      const bool mixed_part = !acc.empty() && c32 > 0;
-      std::vector<double> wcol(1, 0.0);  // cost prefix at every item boundary
-      std::vector<int64_t> ccol(1, 0);
-      for (int32_t j = 0; j < sg.nrun32; ++j) {
-        const Run& r = runs[(size_t)(sg.run0 + sg.nrun64 + j)];
-        const double w = (mixed_part && !(r.flags & RUN_ACC32)) ? acc64_weight : 1.0;
-        ccol.push_back(ccol.back() + r.width);
-        wcol.push_back(wcol.back() + w * r.width);
-      }
-      auto cost_at = [&](int64_t c) {
-        const size_t i = (size_t)(std::upper_bound(ccol.begin(), ccol.end(), c) - ccol.begin()) - 1;
-        if (i + 1 >= ccol.size()) return wcol.back();
-        const double w = (wcol[i + 1] - wcol[i]) / (double)(ccol[i + 1] - ccol[i]);
-        return wcol[i] + w * (double)(c - ccol[i]);
-      };
-      auto col_at = [&](double t) {
-        const size_t i = (size_t)(std::upper_bound(wcol.begin(), wcol.end(), t) - wcol.begin()) - 1;
-        if (i + 1 >= wcol.size()) return (double)ccol.back();
-        const double w = (wcol[i + 1] - wcol[i]) / (double)(ccol[i + 1] - ccol[i]);
-        return (double)ccol[i] + (t - wcol[i]) / w;
-      };
-      // cuts of [lo, hi) among G groups (targets re-spread after every cut);
-      // a cut never falls strictly inside an FP32-accumulated item
-      // (RUN_ACC32), so each (row, block) is one FP32 chain as in the
-      // reference's FP32 GEMV; FP64-accumulated items may be cut anywhere
-      auto cut_range = [&](int64_t lo, int64_t hi, int64_t G) {
-        int64_t prev = lo;
-        size_t k = 0;
-        const double total = cost_at(hi);
-        for (int64_t q = 1; q < G; ++q) {
-          const double pc = cost_at(prev);
-          const double share = (total - pc) / (double)(G - q + 1);
-          int64_t cut = (int64_t)std::llround(col_at(pc + share));
-          while (k < acc.size() && acc[k].b <= cut) ++k;
-          if (k < acc.size() && acc[k].a < cut && cut < acc[k].b) {
-            // inside an FP32 item: move to its nearer end
-            cut = (cut - acc[k].a <= acc[k].b - cut) ? acc[k].a : acc[k].b;
-          }
-          cut = std::min<int64_t>(std::max(cut, prev), hi);
-          gtab.push_back((int32_t)cut);
-          prev = cut;
-        }
-        gtab.push_back((int32_t)hi);
-      };
+    sg.chunk = 0;
+    if (!fg.cuts.empty()) {
       sg.gtab = (int32_t)gtab.size();
-      gtab.push_back(0);
-      if (mixed_part) {
-        // FP64- and FP32-accumulated columns run different loops: give each
-        // its own warps (a warp holding groups of both kinds would execute
-        // both loops one after the other).  wb, a multiple of 32, splits the
-        // threads: groups of the FP64-accumulated range [0, c32) below it,
-        // of the FP32-accumulated range [c32, W32) from it on; wb balances
-        // the estimated cost per group.
-        const double ca = cost_at(c32), cb = wcol.back() - ca;
-        int64_t best_wb = 0;
-        double best = 1e300;
-        for (int64_t wb = 32; wb < kSegThreads; wb += 32) {
-          const int64_t ga = wb / tpg, gb = (kSegThreads - wb) / tpg;
-          if (ga < 1 || gb < 1) continue;
-          const double t = std::max(ca / (double)ga, cb / (double)gb);
-          if (t < best) {
-            best = t;
-            best_wb = wb;
-          }
-        }
-        if (best_wb > 0) {
-          sg.chunk = (int32_t)best_wb;
-          cut_range(0, c32, best_wb / tpg);
-          cut_range(c32, sg.W32, (kSegThreads - best_wb) / tpg);
-        } else {
-          cut_range(0, sg.W32, kSegThreads / tpg);
-        }
-      } else {
-        cut_range(0, sg.W32, kSegThreads / tpg);
-      }
-      gtab.push_back((int32_t)c32);  // first FP32-accumulated column
+      for (int64_t c : fg.cuts) gtab.push_back((int32_t)c);
+      gtab.push_back((int32_t)fg.c32);
+      sg.chunk = (int32_t)fg.wb;
     } else if (sg.W32 > kSegWMax && (dense_single || u_acc32)) {
       // wide part (tiled, no group cuts): only the first FP32-accumulated column
       int32_t first = sg.W32;
