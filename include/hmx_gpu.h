@@ -199,6 +199,33 @@ int hmx_bicgstab(hmx_plan* plan, hmx_plan* plan64, const double* b, double tol, 
 int hmx_apply_local(hmx_plan* plan, const double* xp, double* y, const double* w1, int yy,
                     double* dots, int* nonfinite, uint64_t stream);
 
+/*
+ * Build the FP64 masters of one H-matrix on the device (reference
+ * compress.py:285-342: ACA of the admissible blocks, compress.py:79-207,
+ * kernel-entry assembly of the near field, :256-282), bit-identical to the
+ * host builder; the result serves hmx_plan_create_prepared like an uploaded
+ * master.  Fills kinds / ranks / offsets (n_blocks each, the host builder's
+ * packed layout: 0 dense m*n, 1 low rank U m x r then Vt r x n, 2 not built),
+ * n_data (float64 elements) and fallbacks (ACA blocks stored dense).
+ */
+typedef struct {
+  int64_t n;
+  int64_t n_blocks;
+  const double* pcent;   /* n x 3 panel centroids, permuted order */
+  const double* parea;   /* n panel areas, permuted order */
+  const int64_t* perm;   /* permuted -> original */
+  const int64_t* table;  /* n_blocks x 5: rs, re, cs, ce, admissible */
+  double tol;            /* ACA tolerance */
+  int64_t max_rank;      /* 0: min(m, n) */
+  int64_t row_lo;        /* build only blocks meeting rows [row_lo, row_hi) */
+  int64_t row_hi;        /* 0: n */
+} hmx_build_desc;
+
+int hmx_master_build(const hmx_build_desc* desc, int device, hmx_master** out, int32_t* kinds,
+                     int64_t* ranks, int64_t* offsets, int64_t* n_data, int64_t* fallbacks);
+/* Copies the packed master data (n_data float64) to the host. */
+int hmx_master_download(hmx_master* master, double* data);
+
 /* Upload the FP64 masters of one H-matrix once (device-resident). */
 int hmx_master_create(const hmx_master_desc* desc, int device, hmx_master** out);
 void hmx_master_destroy(hmx_master* master);

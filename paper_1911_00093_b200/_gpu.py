@@ -68,6 +68,13 @@ class MasterDesc(ctypes.Structure):
                 ("n_data", ctypes.c_int64)]
 
 
+class BuildDesc(ctypes.Structure):
+    _fields_ = [("n", ctypes.c_int64), ("n_blocks", ctypes.c_int64),
+                ("pcent", ctypes.POINTER(ctypes.c_double)), ("parea", ctypes.POINTER(ctypes.c_double)),
+                ("perm", _i64p), ("table", _i64p), ("tol", ctypes.c_double),
+                ("max_rank", ctypes.c_int64), ("row_lo", ctypes.c_int64), ("row_hi", ctypes.c_int64)]
+
+
 class PrepareInfo(ctypes.Structure):
     _fields_ = [("payload_bytes", ctypes.c_int64), ("underflow_count", ctypes.c_int64),
                 ("overflow_block", ctypes.c_int64), ("fp32_ranks", ctypes.c_int64)]
@@ -98,6 +105,10 @@ SIGNATURES = {
     "hmx_master_create": (ctypes.c_int, [ctypes.POINTER(MasterDesc), ctypes.c_int,
                                          ctypes.POINTER(ctypes.c_void_p)]),
     "hmx_master_destroy": (None, [ctypes.c_void_p]),
+    "hmx_master_build": (ctypes.c_int, [ctypes.POINTER(BuildDesc), ctypes.c_int,
+                                        ctypes.POINTER(ctypes.c_void_p), _i32p, _i64p, _i64p,
+                                        _i64p, _i64p]),
+    "hmx_master_download": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p]),
     "hmx_plan_create_prepared": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_double,
                                                 ctypes.POINTER(PlanOptions),
                                                 ctypes.POINTER(ctypes.c_void_p),
@@ -482,6 +493,49 @@ class Master:
         self.n = int(n)
         self.device = int(device)
         self._lib = lib
+
+    @classmethod
+    def build(cls, pcent, parea, perm, table, tol: float, max_rank: int = 0, rows=None,
+              device: int = 0):
+        """Build the masters on the device (hmx_master_build): returns
+        (Master, kinds, ranks, offsets, n_data, fallbacks)."""
+        lib = load_library()
+        keep = [np.ascontiguousarray(pcent, dtype=np.float64),
+                np.ascontiguousarray(parea, dtype=np.float64),
+                np.ascontiguousarray(perm, dtype=np.int64),
+                np.ascontiguousarray(table, dtype=np.int64)]
+        nb = keep[3].shape[0]
+        d = BuildDesc()
+        d.n = keep[1].shape[0]
+        d.n_blocks = nb
+        d.pcent = _p(keep[0], ctypes.c_double)
+        d.parea = _p(keep[1], ctypes.c_double)
+        d.perm = _p(keep[2], ctypes.c_int64)
+        d.table = _p(keep[3], ctypes.c_int64)
+        d.tol = float(tol)
+        d.max_rank = int(max_rank or 0)
+        d.row_lo, d.row_hi = (int(rows[0]), int(rows[1])) if rows else (0, 0)
+        kinds = np.empty(nb, dtype=np.int32)
+        ranks = np.empty(nb, dtype=np.int64)
+        offsets = np.empty(nb, dtype=np.int64)
+        n_data, fallbacks = ctypes.c_int64(0), ctypes.c_int64(0)
+        h = ctypes.c_void_p()
+        check(lib.hmx_master_build(ctypes.byref(d), int(device), ctypes.byref(h),
+                                   _p(kinds, ctypes.c_int32), _p(ranks, ctypes.c_int64),
+                                   _p(offsets, ctypes.c_int64), ctypes.byref(n_data),
+                                   ctypes.byref(fallbacks)), "hmx_master_build")
+        self = cls.__new__(cls)
+        self.handle = h
+        self.n = int(d.n)
+        self.device = int(device)
+        self._lib = lib
+        return self, kinds, ranks, offsets, int(n_data.value), int(fallbacks.value)
+
+    def download(self, n_data: int) -> np.ndarray:
+        """The packed master data (float64) on the host."""
+        out = np.empty(n_data, dtype=np.float64)
+        check(self._lib.hmx_master_download(self.handle, out.ctypes.data), "hmx_master_download")
+        return out
 
     @property
     def closed(self) -> bool:

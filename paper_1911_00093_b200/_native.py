@@ -31,7 +31,7 @@ GPU_LIB = LIB_DIR / "libhmx_gpu.so"
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 GENCODE = "-gencode=arch=compute_100a,code=sm_100a"
 
-GPU_SOURCES = ["hmx_plan.cu", "hmx_kernels.cu", "hmx_solver.cu", "hmx_prepare.cu"]
+GPU_SOURCES = ["hmx_plan.cu", "hmx_kernels.cu", "hmx_solver.cu", "hmx_prepare.cu", "hmx_build.cu"]
 
 _lock = threading.Lock()
 _host = None

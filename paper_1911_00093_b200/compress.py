@@ -180,12 +180,18 @@ class HMatrixF64:
 def build_hmatrix(mesh, partition: BlockPartition | None = None,
                   aca_tol: float = DEFAULT_ACA_TOL, max_rank: int | None = None,
                   leaf_size: int = DEFAULT_LEAF_SIZE, eta: float = DEFAULT_ETA,
-                  threads: int | None = None, rows: tuple | None = None) -> HMatrixF64:
+                  threads: int | None = None, rows: tuple | None = None,
+                  device: int | None = None) -> HMatrixF64:
     """Compress the kernel matrix of `mesh` (reference compress.py:285-342).
 
     `rows=(lo, hi)` (permuted indices) builds only the blocks whose rows meet
     [lo, hi); the others are kept as kind 2 (not built, no payload).  Used by
     the multi-GPU mode, where each rank owns a row slice.
+
+    `device=k` compresses on CUDA device k (hmx_master_build: GPU ACA and
+    kernel-entry assembly, bit-identical to the host build); the masters stay
+    resident there for prepare_scheme_device / device plans, and a host copy
+    backs the returned object like a host build's.
     """
     if partition is None:
         tree = build_cluster_tree(mesh, leaf_size=leaf_size)
@@ -201,10 +207,12 @@ def build_hmatrix(mesh, partition: BlockPartition | None = None,
     if np.any(np.all(pcent[order[1:]] == pcent[order[:-1]], axis=1)):
         raise ValueError("mesh has coincident panel centroids")
 
-    lib = _native.host()
-    nthreads = threads or _native.host_threads()
     table = partition.table
     nb = table.shape[0]
+    if device is not None:
+        return _build_on_device(partition, pcent, parea, table, aca_tol, max_rank, rows, device)
+    lib = _native.host()
+    nthreads = threads or _native.host_threads()
     err = ctypes.create_string_buffer(256)
     handle = lib.hb_build(_native.ptr(pcent, _native.c_f64p), _native.ptr(parea, _native.c_f64p),
                           pcent.shape[0], _native.ptr(table, _native.c_i64p), nb, float(aca_tol),
@@ -237,6 +245,29 @@ def build_hmatrix(mesh, partition: BlockPartition | None = None,
         stored_scalars=total, compression_ratio=float(total) / float(n * n), aca_tol=aca_tol)
     return HMatrixF64(partition, report=report,
                       packed=PackedMaster(data, kinds, ranks, offsets))
+
+
+def _report(n, kinds, ranks, total, fallbacks, aca_tol) -> BuildReport:
+    low = kinds == 1
+    hist_r, hist_c = np.unique(ranks[low], return_counts=True)
+    return BuildReport(
+        n=n, dense_blocks=int(np.count_nonzero(kinds == 0)), lowrank_blocks=int(np.count_nonzero(low)),
+        fallback_blocks=fallbacks,
+        rank_histogram={int(r): int(c) for r, c in zip(hist_r, hist_c)},
+        stored_scalars=total, compression_ratio=float(total) / float(n * n), aca_tol=aca_tol)
+
+
+def _build_on_device(partition, pcent, parea, table, aca_tol, max_rank, rows, device) -> HMatrixF64:
+    from . import _gpu
+
+    master, kinds, ranks, offsets, total, fallbacks = _gpu.Master.build(
+        pcent, parea, partition.tree.permutation, table, aca_tol, max_rank or 0, rows,
+        device=int(device))
+    data = master.download(total)
+    h = HMatrixF64(partition, report=_report(partition.n, kinds, ranks, total, fallbacks, aca_tol),
+                   packed=PackedMaster(data, kinds, ranks, offsets))
+    object.__setattr__(h, "_hmx_gpu_master", master)  # device_prepare.get_master reuses it
+    return h
 
 
 def densify(h: HMatrixF64, cap: int = DENSIFY_CAP) -> np.ndarray:

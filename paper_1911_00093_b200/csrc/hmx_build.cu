@@ -1,0 +1,612 @@
+// H-matrix compression on the GPU ("GPU ACA +
+// kernel-entry assembly"): the FP64 masters of one H-matrix are built straight
+// into device memory -- dense near-field blocks by kernel-entry assembly,
+// admissible blocks by adaptive cross approximation -- ready for
+// hmx_plan_create_prepared, with no payload crossing the host link.
+//
+// Arithmetic restates reference pkg/src/hmx/compress.py:79-207 (ACA with
+// partial pivoting) and :256-282 (kernel entries) exactly as the host
+// builder does (csrc/aca_core.h): every floating-point operation is an
+// explicit IEEE intrinsic in the host's order (no FMA contraction; the
+// norm/cross dot products are the host's FMA chains, each run sequentially
+// by one lane), pivots are first-index argmax like the host loops, so the
+// device masters are BIT-IDENTICAL to the host builder's
+// (tests/test_gpu_build.py).
+//
+// One warp per admissible block (grid-stride over blocks sorted by size):
+// lanes evaluate residual rows/columns entry-parallel, warp shuffles find
+// the max and the pivots, lanes run the 2 + 2 rank dot-product chains in
+// parallel.  Two passes: pass 1 finds every rank (factors in bounded,
+// batched scratch of kAcaCap columns), pass 2 recomputes and writes the
+// factors straight into the packed master layout.  Blocks that need more
+// than kAcaCap ranks, or that take the reference's "ran out of pivot rows"
+// path (exact remainder, possible dense fallback), are completed on the host
+// with the host builder's aca_block -- the same arithmetic.
+#include <algorithm>
+#include <atomic>
+#include <cstring>
+#include <numeric>
+#include <thread>
+#include <vector>
+
+#include "aca_core.h"
+#include "hmx_plan_impl.cuh"
+
+namespace hmx {
+namespace {
+
+constexpr int kAcaCap = 48;              // ranks per block in pass-1 scratch
+constexpr int kAcaWarps = 8;             // warps per CTA
+constexpr double kPiD = 3.141592653589793;
+constexpr double kFourPiD = 4.0 * kPiD;  // compress.py:38
+constexpr double kEpsD = 2.220446049250313e-16;
+
+struct AcaTask {
+  int64_t r0, c0;
+  int64_t u_off;     // U element (i, k) at base[u_off + i * cap + k]
+  int64_t vt_off;    // Vt element (k, j) at base[vt_off + k * n + j]
+  int64_t flag_off;  // byte flags: rows [0, m), columns [m, m + n)
+  int32_t m, n, budget, cap;
+};
+
+enum : int32_t { ACA_OK = 0, ACA_HOST = 1 };
+
+__device__ __forceinline__ double kentry_dev(const double* __restrict__ pc, const double* __restrict__ pa,
+                                             int64_t gi, int64_t gj) {
+  if (gi == gj) return __dmul_rn(0.5, __dsqrt_rn(__ddiv_rn(pa[gi], kPiD)));
+  const double* a = pc + 3 * gi;
+  const double* b = pc + 3 * gj;
+  const double dx = __dsub_rn(a[0], b[0]), dy = __dsub_rn(a[1], b[1]), dz = __dsub_rn(a[2], b[2]);
+  const double d = __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz)));
+  return __ddiv_rn(pa[gj], __dmul_rn(kFourPiD, d));
+}
+
+// (value, index) argmax over the warp: larger value, then smaller index
+__device__ __forceinline__ void warp_argmax(double& v, int& idx) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const double v2 = __shfl_xor_sync(0xffffffffu, v, o);
+    const int i2 = __shfl_xor_sync(0xffffffffu, idx, o);
+    if (v2 > v || (v2 == v && i2 < idx)) {
+      v = v2;
+      idx = i2;
+    }
+  }
+}
+
+// One warp per task.  out_rank/out_status per task.
+__global__ void __launch_bounds__(32 * kAcaWarps) aca_kernel(const AcaTask* __restrict__ tasks, int ntask,
+                                                             const double* __restrict__ pc,
+                                                             const double* __restrict__ pa, double tol,
+                                                             double* base, uint8_t* flags, int32_t* out_rank,
+                                                             int32_t* out_status) {
+  __shared__ double sab[kAcaWarps][2 * kAcaCap + 2];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  double* ab = sab[wid];
+  for (int t = blockIdx.x * kAcaWarps + wid; t < ntask; t += gridDim.x * kAcaWarps) {
+    const AcaTask T = tasks[t];
+    const int m = T.m, n = T.n, cap = T.cap;
+    double* U = base + T.u_off;
+    double* Vt = base + T.vt_off;
+    uint8_t* rowu = flags + T.flag_off;
+    uint8_t* colu = rowu + m;
+    for (int i = lane; i < m + n; i += 32) rowu[i] = 0;
+    __syncwarp();
+    double frob_sq = 0.0, max_seen = 0.0;
+    int rank = 0, i_star = 0, status = ACA_OK;
+    bool converged = false;
+    while (rank < T.budget && i_star >= 0) {
+      if (rank == cap) {
+        status = ACA_HOST;
+        break;
+      }
+      // residual row i_star, written into the next Vt row
+      double* row = Vt + (int64_t)rank * n;
+      const double* urow = U + (int64_t)i_star * cap;
+      double rmax = 0.0, best = -1.0;
+      int jbest = 0;
+      for (int j = lane; j < n; j += 32) {
+        double v = kentry_dev(pc, pa, T.r0 + i_star, T.c0 + j);
+        if (rank) {
+          double s = 0.0;
+          for (int k = 0; k < rank; ++k) s = __dadd_rn(s, __dmul_rn(urow[k], Vt[(int64_t)k * n + j]));
+          v = __dsub_rn(v, s);
+        }
+        row[j] = v;
+        const double a = fabs(v);
+        rmax = (rmax < a) ? a : rmax;
+        const double mv = colu[j] ? 0.0 : a;
+        if (mv > best) {
+          best = mv;
+          jbest = j;
+        }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double r2 = __shfl_xor_sync(0xffffffffu, rmax, o);
+        rmax = (rmax < r2) ? r2 : rmax;
+      }
+      warp_argmax(best, jbest);
+      __syncwarp();
+      if (lane == 0) rowu[i_star] = 1;
+      max_seen = (max_seen < rmax) ? rmax : max_seen;
+      const double pivot = colu[jbest] ? 0.0 : row[jbest];
+      __syncwarp();
+      if (fabs(pivot) <= __dmul_rn(kEpsD, max_seen)) {
+        // vanished pivot: next unused row (compress.py:155-158)
+        int first = m;
+        for (int i = lane; i < m; i += 32)
+          if (!rowu[i]) {
+            first = i;
+            break;
+          }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) first = min(first, __shfl_xor_sync(0xffffffffu, first, o));
+        i_star = first < m ? first : -1;
+        __syncwarp();
+        continue;
+      }
+      for (int j = lane; j < n; j += 32) row[j] = __ddiv_rn(row[j], pivot);
+      // residual column j_star, written into U column `rank`
+      for (int i = lane; i < m; i += 32) {
+        double v = kentry_dev(pc, pa, T.r0 + i, T.c0 + jbest);
+        if (rank) {
+          const double* ui = U + (int64_t)i * cap;
+          double s = 0.0;
+          for (int k = 0; k < rank; ++k) s = __dadd_rn(s, __dmul_rn(ui[k], Vt[(int64_t)k * n + jbest]));
+          v = __dsub_rn(v, s);
+        }
+        U[(int64_t)i * cap + rank] = v;
+      }
+      __syncwarp();
+      if (lane == 0) colu[jbest] = 1;
+      // the host's FMA chains, one per lane: |u|, |v|, a_k = U_k . u, b_k = Vt_k . v
+      const int nch = 2 + 2 * rank;
+      for (int c = lane; c < nch; c += 32) {
+        double s = 0.0;
+        if (c == 0) {
+          for (int i = 0; i < m; ++i) {
+            const double u = U[(int64_t)i * cap + rank];
+            s = fma(u, u, s);
+          }
+        } else if (c == 1) {
+          for (int j = 0; j < n; ++j) s = fma(row[j], row[j], s);
+        } else if (c < 2 + rank) {
+          const int k = c - 2;
+          for (int i = 0; i < m; ++i) s = fma(U[(int64_t)i * cap + k], U[(int64_t)i * cap + rank], s);
+        } else {
+          const int k = c - 2 - rank;
+          const double* vk = Vt + (int64_t)k * n;
+          for (int j = 0; j < n; ++j) s = fma(vk[j], row[j], s);
+        }
+        ab[c] = s;
+      }
+      __syncwarp();
+      const double u_norm = __dsqrt_rn(ab[0]), v_norm = __dsqrt_rn(ab[1]);
+      double cross = 0.0;
+      if (rank) {
+        double s = 0.0;
+        for (int k = 0; k < rank; ++k) s = fma(ab[2 + k], ab[2 + rank + k], s);
+        cross = __dmul_rn(2.0, s);
+      }
+      __syncwarp();
+      const double uv = __dmul_rn(u_norm, v_norm);
+      const double f = __dadd_rn(__dadd_rn(frob_sq, __dmul_rn(uv, uv)), cross);
+      frob_sq = (f < 0.0) ? 0.0 : f;
+      ++rank;
+      if (uv <= __dmul_rn(tol, __dsqrt_rn(frob_sq))) {
+        converged = true;
+        break;
+      }
+      // next pivot row: largest |u_new| among unused rows (first index)
+      double cb = -1.0;
+      int ib = 0;
+      for (int i = lane; i < m; i += 32) {
+        const double cv = rowu[i] ? -1.0 : fabs(U[(int64_t)i * cap + rank - 1]);
+        if (cv > cb) {
+          cb = cv;
+          ib = i;
+        }
+      }
+      warp_argmax(cb, ib);
+      i_star = cb < 0.0 ? -1 : ib;
+      __syncwarp();
+    }
+    // "ran out of pivot rows" (compress.py:191-205): the host measures the
+    // remainder and decides between these factors and the dense fallback
+    if (status == ACA_OK && !converged && rank < T.budget) status = ACA_HOST;
+    if (lane == 0) {
+      out_rank[t] = rank;
+      out_status[t] = status;
+    }
+    __syncwarp();
+  }
+}
+
+// Dense near-field blocks (and ACA dense fallbacks): compress.py:272-282.
+struct DenseTask {
+  int64_t r0, c0, off;
+  int32_t m, n;
+};
+
+__global__ void dense_fill_kernel(const DenseTask* __restrict__ tasks, const double* __restrict__ pc,
+                                  const double* __restrict__ pa, double* base) {
+  const DenseTask T = tasks[blockIdx.x];
+  const int64_t total = (int64_t)T.m * T.n;
+  for (int64_t e = threadIdx.x; e < total; e += blockDim.x) {
+    const int64_t i = e / T.n, j = e - i * T.n;
+    base[T.off + e] = kentry_dev(pc, pa, T.r0 + i, T.c0 + j);
+  }
+}
+
+int run_aca(const std::vector<AcaTask>& tasks, const double* d_pc, const double* d_pa, double tol,
+            double* base, uint8_t* d_flags, int32_t* d_rank, int32_t* d_status, cudaStream_t st, int sms) {
+  if (tasks.empty()) return HMX_OK;
+  AcaTask* d_tasks = nullptr;
+  HMX_CUDA(cudaMalloc(&d_tasks, tasks.size() * sizeof(AcaTask)));
+  cudaError_t e = cudaMemcpyAsync(d_tasks, tasks.data(), tasks.size() * sizeof(AcaTask),
+                                  cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess) {
+    const int64_t want = ((int64_t)tasks.size() + kAcaWarps - 1) / kAcaWarps;
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)sms * 8));
+    aca_kernel<<<grid, 32 * kAcaWarps, 0, st>>>(d_tasks, (int)tasks.size(), d_pc, d_pa, tol, base, d_flags,
+                                                d_rank, d_status);
+    e = cudaGetLastError();
+  }
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  cudaFree(d_tasks);
+  if (e != cudaSuccess) return cuda_fail(e, "aca_kernel");
+  return HMX_OK;
+}
+
+}  // namespace
+}  // namespace hmx
+
+using namespace hmx;
+
+extern "C" {
+
+int hmx_master_build(const hmx_build_desc* d, int device, hmx_master** out, int32_t* kinds, int64_t* ranks,
+                     int64_t* offsets, int64_t* n_data, int64_t* fallbacks) {
+  if (!d || !out || !kinds || !ranks || !offsets || !n_data || !d->pcent || !d->parea || !d->perm ||
+      !d->table) {
+    set_error("null argument");
+    return HMX_ERR_ARG;
+  }
+  *out = nullptr;
+  const int64_t N = d->n, nb = d->n_blocks;
+  if (N < 1 || nb < 1 || !(d->tol > 0.0) || d->max_rank < 0) {
+    set_error("invalid build descriptor (n, n_blocks >= 1, tol > 0, max_rank >= 0)");
+    return HMX_ERR_ARG;
+  }
+  int count = 0;
+  if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0) {
+    set_error("no CUDA device is available");
+    return HMX_ERR_CUDA;
+  }
+  if (device < 0 || device >= count) {
+    set_error("device index out of range");
+    return HMX_ERR_ARG;
+  }
+  DeviceGuard guard(device);
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+  const int64_t row_lo = d->row_lo, row_hi = d->row_hi > 0 ? d->row_hi : N;
+
+  auto* M = new hmx_master();
+  auto fail = [&](int rc) {
+    hmx_master_destroy(M);
+    return rc;
+  };
+  M->device = device;
+  M->n = N;
+  M->nb = nb;
+  M->perm.assign(d->perm, d->perm + N);
+  M->table.assign(d->table, d->table + 5 * nb);
+  cudaError_t e = cudaStreamCreateWithFlags(&M->stream, cudaStreamNonBlocking);
+  if (e != cudaSuccess) return fail(cuda_fail(e, "cudaStreamCreate"));
+  cudaStream_t st = M->stream;
+
+  // geometry on the device
+  double* d_pc = M->alloc<double>((size_t)(3 * N));
+  double* d_pa = M->alloc<double>((size_t)N);
+  if (!d_pc || !d_pa) {
+    set_error("cudaMalloc failed for the mesh geometry");
+    return fail(HMX_ERR_CUDA);
+  }
+  if ((e = cudaMemcpyAsync(d_pc, d->pcent, (size_t)(3 * N) * 8, cudaMemcpyHostToDevice, st)) != cudaSuccess ||
+      (e = cudaMemcpyAsync(d_pa, d->parea, (size_t)N * 8, cudaMemcpyHostToDevice, st)) != cudaSuccess)
+    return fail(cuda_fail(e, "geometry upload"));
+
+  // block classes: 0 dense, 1 ACA, 2 not built (outside the row range)
+  std::vector<int32_t> kind((size_t)nb), rank((size_t)nb, 0);
+  std::vector<int64_t> aca_blocks;
+  for (int64_t k = 0; k < nb; ++k) {
+    const int64_t* t = d->table + 5 * k;
+    if (t[1] <= t[0] || t[3] <= t[2] || t[0] < 0 || t[1] > N || t[2] < 0 || t[3] > N) {
+      set_error("block " + std::to_string(k) + " is outside the matrix");
+      return fail(HMX_ERR_ARG);
+    }
+    if (t[1] <= row_lo || t[0] >= row_hi) kind[(size_t)k] = 2;
+    else if (t[4]) {
+      kind[(size_t)k] = 1;
+      aca_blocks.push_back(k);
+    } else {
+      kind[(size_t)k] = 0;
+    }
+  }
+  // largest blocks first (their sequential chains are the longest)
+  std::stable_sort(aca_blocks.begin(), aca_blocks.end(), [&](int64_t a, int64_t b) {
+    const int64_t* ta = d->table + 5 * a;
+    const int64_t* tb = d->table + 5 * b;
+    return (ta[1] - ta[0]) + (ta[3] - ta[2]) > (tb[1] - tb[0]) + (tb[3] - tb[2]);
+  });
+  auto budget_of = [&](int64_t k) {
+    const int64_t* t = d->table + 5 * k;
+    int64_t b = std::min(t[1] - t[0], t[3] - t[2]);
+    if (d->max_rank > 0) b = std::min(b, d->max_rank);
+    return b;
+  };
+  const size_t na = aca_blocks.size();
+  int32_t *d_rank = nullptr, *d_status = nullptr;
+  d_rank = M->alloc<int32_t>(std::max<size_t>(na, 1));
+  d_status = M->alloc<int32_t>(std::max<size_t>(na, 1));
+  if (!d_rank || !d_status) {
+    set_error("cudaMalloc failed for the ACA results");
+    return fail(HMX_ERR_CUDA);
+  }
+
+  // ---- pass 1: ranks, in batches of bounded scratch
+  const int64_t kScratch = (int64_t)1 << 28;  // doubles (2 GiB) per batch
+  std::vector<int32_t> h_rank(na, 0), h_status(na, 0);
+  {
+    double* scratch = nullptr;
+    uint8_t* fl = nullptr;
+    int64_t sc_cap = 0, fl_cap = 0;
+    size_t b0 = 0;
+    int rc = HMX_OK;
+    while (b0 < na && rc == HMX_OK) {
+      std::vector<AcaTask> batch;
+      int64_t used = 0, fused = 0;
+      size_t b1 = b0;
+      for (; b1 < na; ++b1) {
+        const int64_t k = aca_blocks[b1];
+        const int64_t* t = d->table + 5 * k;
+        const int64_t m = t[1] - t[0], n = t[3] - t[2];
+        const int64_t cap = std::min<int64_t>(budget_of(k), kAcaCap);
+        const int64_t need = cap * (m + n);
+        if (!batch.empty() && used + need > kScratch) break;
+        AcaTask T{};
+        T.r0 = t[0];
+        T.c0 = t[2];
+        T.m = (int32_t)m;
+        T.n = (int32_t)n;
+        T.budget = (int32_t)budget_of(k);
+        T.cap = (int32_t)cap;
+        T.u_off = used;
+        T.vt_off = used + m * cap;
+        T.flag_off = fused;
+        used += need;
+        fused += m + n;
+        batch.push_back(T);
+      }
+      if (used > sc_cap) {
+        cudaFree(scratch);
+        scratch = nullptr;
+        if (cudaMalloc(&scratch, (size_t)used * 8) != cudaSuccess) {
+          set_error("cudaMalloc failed for the ACA scratch");
+          rc = HMX_ERR_CUDA;
+          break;
+        }
+        sc_cap = used;
+      }
+      if (fused > fl_cap) {
+        cudaFree(fl);
+        fl = nullptr;
+        if (cudaMalloc(&fl, (size_t)fused) != cudaSuccess) {
+          set_error("cudaMalloc failed for the ACA flags");
+          rc = HMX_ERR_CUDA;
+          break;
+        }
+        fl_cap = fused;
+      }
+      rc = run_aca(batch, d_pc, d_pa, d->tol, scratch, fl, d_rank + b0, d_status + b0, st, sms);
+      b0 = b1;
+    }
+    cudaFree(scratch);
+    cudaFree(fl);
+    if (rc) return fail(rc);
+    if (na) {
+      if ((e = cudaMemcpy(h_rank.data(), d_rank, na * 4, cudaMemcpyDeviceToHost)) != cudaSuccess ||
+          (e = cudaMemcpy(h_status.data(), d_status, na * 4, cudaMemcpyDeviceToHost)) != cudaSuccess)
+        return fail(cuda_fail(e, "ACA ranks"));
+    }
+  }
+
+  // ---- host completion of the rare blocks (same arithmetic: aca_core.h)
+  std::vector<size_t> host_idx;
+  for (size_t q = 0; q < na; ++q)
+    if (h_status[q] == ACA_HOST) host_idx.push_back(q);
+  std::vector<hmx_aca::BlockResult> host_res(host_idx.size());
+  int64_t nfall = 0;
+  {
+    hmx_aca::Geom G{d->pcent, d->parea};
+    std::vector<char> fb(host_idx.size(), 0);
+    std::atomic<size_t> next{0};
+    const unsigned nt = std::max(1u, std::min<unsigned>(std::thread::hardware_concurrency(),
+                                                        (unsigned)std::max<size_t>(host_idx.size(), 1)));
+    std::vector<std::thread> pool;
+    for (unsigned w = 0; w < nt; ++w)
+      pool.emplace_back([&]() {
+        for (;;) {
+          const size_t h = next.fetch_add(1);
+          if (h >= host_idx.size()) break;
+          const int64_t k = aca_blocks[host_idx[h]];
+          const int64_t* t = d->table + 5 * k;
+          bool f = false;
+          hmx_aca::aca_block(G, t[0], t[1] - t[0], t[2], t[3] - t[2], d->tol, d->max_rank, host_res[h], f);
+          fb[h] = f ? 1 : 0;
+        }
+      });
+    for (auto& th : pool) th.join();
+    for (size_t h = 0; h < host_idx.size(); ++h) {
+      const size_t q = host_idx[h];
+      const int64_t k = aca_blocks[q];
+      if (fb[h]) {
+        kind[(size_t)k] = 0;  // dense fallback (the host builder stores it dense too)
+        ++nfall;
+      } else {
+        h_rank[q] = (int32_t)host_res[h].rank;
+      }
+    }
+  }
+  for (size_t q = 0; q < na; ++q)
+    if (kind[(size_t)aca_blocks[q]] == 1) rank[(size_t)aca_blocks[q]] = h_rank[q];
+
+  // ---- layout (hb_build_layout's): dense m*n, low rank r*(m+n), skipped 0
+  int64_t off = 0;
+  M->kind.resize((size_t)nb);
+  M->offset.resize((size_t)nb);
+  M->rank.resize((size_t)nb);
+  M->roff.resize((size_t)nb);
+  for (int64_t k = 0; k < nb; ++k) {
+    const int64_t* t = d->table + 5 * k;
+    const int64_t m = t[1] - t[0], n = t[3] - t[2];
+    const int32_t kd = kind[(size_t)k];
+    const int64_t r = kd == 1 ? rank[(size_t)k] : 0;
+    kinds[k] = kd;
+    ranks[k] = r;
+    offsets[k] = off;
+    M->kind[(size_t)k] = kd;
+    M->rank[(size_t)k] = r;
+    M->offset[(size_t)k] = off;
+    M->roff[(size_t)k] = M->rank_sum;
+    M->rank_sum += r;
+    M->max_rank = std::max(M->max_rank, r);
+    off += kd == 0 ? m * n : kd == 1 ? r * (m + n) : 0;
+  }
+  *n_data = off;
+  M->n_data = off;
+  if (fallbacks) *fallbacks = nfall;
+  M->data = M->alloc<double>((size_t)std::max<int64_t>(off, 1));
+  if (!M->data) {
+    set_error("cudaMalloc failed for the masters (out of device memory?)");
+    return fail(HMX_ERR_CUDA);
+  }
+
+  // ---- dense blocks: kernel-entry assembly
+  {
+    std::vector<DenseTask> dt;
+    for (int64_t k = 0; k < nb; ++k)
+      if (kind[(size_t)k] == 0) {
+        const int64_t* t = d->table + 5 * k;
+        dt.push_back({t[0], t[2], offsets[k], (int32_t)(t[1] - t[0]), (int32_t)(t[3] - t[2])});
+      }
+    for (size_t b0 = 0; b0 < dt.size(); b0 += 1 << 20) {  // grid.x limit headroom
+      const size_t cnt = std::min<size_t>(dt.size() - b0, (size_t)1 << 20);
+      DenseTask* d_dt = nullptr;
+      if ((e = cudaMalloc(&d_dt, cnt * sizeof(DenseTask))) != cudaSuccess) return fail(cuda_fail(e, "dense tasks"));
+      e = cudaMemcpyAsync(d_dt, dt.data() + b0, cnt * sizeof(DenseTask), cudaMemcpyHostToDevice, st);
+      if (e == cudaSuccess) {
+        dense_fill_kernel<<<(unsigned)cnt, 256, 0, st>>>(d_dt, d_pc, d_pa, M->data);
+        e = cudaGetLastError();
+      }
+      if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+      cudaFree(d_dt);
+      if (e != cudaSuccess) return fail(cuda_fail(e, "dense_fill_kernel"));
+    }
+  }
+
+  // ---- pass 2: the factors straight into the packed layout (U m x r
+  // row-major, then Vt r x n), recomputed with the ranks known
+  {
+    std::vector<AcaTask> tasks;
+    std::vector<size_t> which;
+    int64_t fused = 0;
+    for (size_t q = 0; q < na; ++q) {
+      const int64_t k = aca_blocks[q];
+      if (kind[(size_t)k] != 1 || h_status[q] == ACA_HOST) continue;
+      const int64_t* t = d->table + 5 * k;
+      const int64_t m = t[1] - t[0], n = t[3] - t[2], r = rank[(size_t)k];
+      AcaTask T{};
+      T.r0 = t[0];
+      T.c0 = t[2];
+      T.m = (int32_t)m;
+      T.n = (int32_t)n;
+      T.budget = (int32_t)budget_of(k);
+      T.cap = (int32_t)r;
+      T.u_off = offsets[k];
+      T.vt_off = offsets[k] + m * r;
+      T.flag_off = fused;
+      fused += m + n;
+      tasks.push_back(T);
+      which.push_back(q);
+    }
+    uint8_t* fl = nullptr;
+    if (!tasks.empty() && cudaMalloc(&fl, (size_t)std::max<int64_t>(fused, 1)) != cudaSuccess) {
+      set_error("cudaMalloc failed for the ACA flags");
+      return fail(HMX_ERR_CUDA);
+    }
+    int rc = run_aca(tasks, d_pc, d_pa, d->tol, M->data, fl, d_rank, d_status, st, sms);
+    cudaFree(fl);
+    if (rc) return fail(rc);
+    if (!tasks.empty()) {
+      // pass 2 must reproduce pass 1 (same arithmetic): check the ranks
+      std::vector<int32_t> r2(tasks.size()), s2(tasks.size());
+      if ((e = cudaMemcpy(r2.data(), d_rank, tasks.size() * 4, cudaMemcpyDeviceToHost)) != cudaSuccess ||
+          (e = cudaMemcpy(s2.data(), d_status, tasks.size() * 4, cudaMemcpyDeviceToHost)) != cudaSuccess)
+        return fail(cuda_fail(e, "ACA pass-2 ranks"));
+      for (size_t i = 0; i < tasks.size(); ++i)
+        if (r2[i] != tasks[i].cap || s2[i] != ACA_OK) {
+          set_error("ACA pass 2 diverged from pass 1");
+          return fail(HMX_ERR_CUDA);
+        }
+    }
+  }
+  // host-completed low-rank blocks
+  for (size_t h = 0; h < host_idx.size(); ++h) {
+    const int64_t k = aca_blocks[host_idx[h]];
+    if (kind[(size_t)k] != 1) continue;
+    const hmx_aca::BlockResult& R = host_res[h];
+    const int64_t* t = d->table + 5 * k;
+    const int64_t m = t[1] - t[0];
+    if (R.rank > 0) {
+      if ((e = cudaMemcpy(M->data + offsets[k], R.u.data(), R.u.size() * 8, cudaMemcpyHostToDevice)) != cudaSuccess ||
+          (e = cudaMemcpy(M->data + offsets[k] + m * R.rank, R.vt.data(), R.vt.size() * 8,
+                          cudaMemcpyHostToDevice)) != cudaSuccess)
+        return fail(cuda_fail(e, "host ACA upload"));
+    }
+  }
+
+  // ---- device tables (as hmx_master_create)
+  auto up = [&](auto** dst, const auto* src, size_t cnt) -> int {
+    using T = typename std::remove_pointer<typename std::remove_reference<decltype(*dst)>::type>::type;
+    *dst = M->alloc<T>(cnt);
+    if (!*dst) {
+      set_error("cudaMalloc failed for the master tables");
+      return HMX_ERR_CUDA;
+    }
+    if (cnt) HMX_CUDA(cudaMemcpy(*dst, src, cnt * sizeof(T), cudaMemcpyHostToDevice));
+    return HMX_OK;
+  };
+  int rc = up(&M->d_table, M->table.data(), (size_t)(5 * nb));
+  if (!rc) rc = up(&M->d_kind, M->kind.data(), (size_t)nb);
+  if (!rc) rc = up(&M->d_offset, M->offset.data(), (size_t)nb);
+  if (!rc) rc = up(&M->d_rank, M->rank.data(), (size_t)nb);
+  if (!rc) rc = up(&M->d_roff, M->roff.data(), (size_t)nb);
+  if (rc) return fail(rc);
+  *out = M;
+  return HMX_OK;
+}
+
+int hmx_master_download(hmx_master* m, double* data) {
+  if (!m || (!data && m->n_data > 0)) {
+    set_error("null argument");
+    return HMX_ERR_ARG;
+  }
+  DeviceGuard guard(m->device);
+  if (m->n_data > 0) HMX_CUDA(cudaMemcpy(data, m->data, (size_t)m->n_data * 8, cudaMemcpyDeviceToHost));
+  return HMX_OK;
+}
+
+}  // extern "C"

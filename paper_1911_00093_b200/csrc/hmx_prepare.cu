@@ -24,31 +24,6 @@
 
 #include "hmx_plan_impl.cuh"
 
-struct hmx_master {
-  int device = 0;
-  int64_t n = 0, nb = 0, n_data = 0, rank_sum = 0, max_rank = 0;
-  cudaStream_t stream = nullptr;
-  // host copies for the flattener
-  std::vector<int64_t> perm, table, offset, rank, roff;
-  std::vector<int32_t> kind;
-  // device
-  double* data = nullptr;
-  int64_t* d_table = nullptr;
-  int64_t* d_offset = nullptr;
-  int64_t* d_rank = nullptr;
-  int64_t* d_roff = nullptr;
-  int32_t* d_kind = nullptr;
-  std::vector<void*> allocs;
-
-  template <typename T>
-  T* alloc(size_t count) {
-    void* p = nullptr;
-    if (cudaMalloc(&p, std::max<size_t>(count, 1) * sizeof(T)) != cudaSuccess) return nullptr;
-    allocs.push_back(p);
-    return static_cast<T*>(p);
-  }
-};
-
 namespace hmx {
 
 // max of non-negative doubles through their bit patterns (order independent)
