@@ -140,6 +140,27 @@ class PackedMaster:
                                self.data[o + m * r:o + r * (m + n)].reshape(r, n))
 
 
+class DevicePackedMaster(PackedMaster):
+    """Packed masters built on a device (hmx_master_build): `kinds`, `ranks`,
+    `offsets` on the host, `data` copied from the device on first use (the
+    device-side consumers -- prepare_scheme_device, device plans -- never
+    need it)."""
+
+    def __init__(self, master, n_data: int, kinds, ranks, offsets):
+        self._master = master
+        self._n_data = int(n_data)
+        self._data = None
+        self.kinds = kinds
+        self.ranks = ranks
+        self.offsets = offsets
+
+    @property
+    def data(self) -> np.ndarray:
+        if self._data is None:
+            self._data = self._master.download(self._n_data)
+        return self._data
+
+
 class HMatrixF64:
     """FP64 master H-matrix: partition plus one payload per block."""
 
@@ -263,9 +284,8 @@ def _build_on_device(partition, pcent, parea, table, aca_tol, max_rank, rows, de
     master, kinds, ranks, offsets, total, fallbacks = _gpu.Master.build(
         pcent, parea, partition.tree.permutation, table, aca_tol, max_rank or 0, rows,
         device=int(device))
-    data = master.download(total)
     h = HMatrixF64(partition, report=_report(partition.n, kinds, ranks, total, fallbacks, aca_tol),
-                   packed=PackedMaster(data, kinds, ranks, offsets))
+                   packed=DevicePackedMaster(master, total, kinds, ranks, offsets))
     object.__setattr__(h, "_hmx_gpu_master", master)  # device_prepare.get_master reuses it
     return h
 

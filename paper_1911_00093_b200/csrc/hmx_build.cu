@@ -24,7 +24,11 @@
 // with the host builder's aca_block -- the same arithmetic.
 #include <algorithm>
 #include <atomic>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <numeric>
 #include <thread>
 #include <vector>
@@ -35,7 +39,8 @@
 namespace hmx {
 namespace {
 
-constexpr int kAcaCap = 48;              // ranks per block in pass-1 scratch
+constexpr int kCap1 = 24;   // ranks per block in pass-1 scratch (config 4: max rank 19)
+constexpr int kCap2 = 96;   // retry round for the blocks that exhaust kCap1
 constexpr int kAcaWarps = 8;             // warps per CTA
 constexpr double kPiD = 3.141592653589793;
 constexpr double kFourPiD = 4.0 * kPiD;  // compress.py:38
@@ -43,13 +48,13 @@ constexpr double kEpsD = 2.220446049250313e-16;
 
 struct AcaTask {
   int64_t r0, c0;
-  int64_t u_off;     // U element (i, k) at base[u_off + i * cap + k]
+  int64_t u_off;     // U element (i, k) at base[u_off + k * m + i] (column-major: the chains stream)
   int64_t vt_off;    // Vt element (k, j) at base[vt_off + k * n + j]
   int64_t flag_off;  // byte flags: rows [0, m), columns [m, m + n)
   int32_t m, n, budget, cap;
 };
 
-enum : int32_t { ACA_OK = 0, ACA_HOST = 1 };
+enum : int32_t { ACA_OK = 0, ACA_HOST = 1, ACA_CAP = 2 };
 
 __device__ __forceinline__ double kentry_dev(const double* __restrict__ pc, const double* __restrict__ pa,
                                              int64_t gi, int64_t gj) {
@@ -80,7 +85,7 @@ __global__ void __launch_bounds__(32 * kAcaWarps) aca_kernel(const AcaTask* __re
                                                              const double* __restrict__ pa, double tol,
                                                              double* base, uint8_t* flags, int32_t* out_rank,
                                                              int32_t* out_status) {
-  __shared__ double sab[kAcaWarps][2 * kAcaCap + 2];
+  __shared__ double sab[kAcaWarps][2 * kCap2 + 2];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   double* ab = sab[wid];
   for (int t = blockIdx.x * kAcaWarps + wid; t < ntask; t += gridDim.x * kAcaWarps) {
@@ -96,20 +101,20 @@ __global__ void __launch_bounds__(32 * kAcaWarps) aca_kernel(const AcaTask* __re
     int rank = 0, i_star = 0, status = ACA_OK;
     bool converged = false;
     while (rank < T.budget && i_star >= 0) {
-      if (rank == cap) {
-        status = ACA_HOST;
+      if (rank == cap) {  // scratch columns exhausted: retried with more
+        status = ACA_CAP;
         break;
       }
       // residual row i_star, written into the next Vt row
       double* row = Vt + (int64_t)rank * n;
-      const double* urow = U + (int64_t)i_star * cap;
+      const double* urow = U + i_star;  // U(i_star, k) at urow[k * m]
       double rmax = 0.0, best = -1.0;
       int jbest = 0;
       for (int j = lane; j < n; j += 32) {
         double v = kentry_dev(pc, pa, T.r0 + i_star, T.c0 + j);
         if (rank) {
           double s = 0.0;
-          for (int k = 0; k < rank; ++k) s = __dadd_rn(s, __dmul_rn(urow[k], Vt[(int64_t)k * n + j]));
+          for (int k = 0; k < rank; ++k) s = __dadd_rn(s, __dmul_rn(urow[(int64_t)k * m], Vt[(int64_t)k * n + j]));
           v = __dsub_rn(v, s);
         }
         row[j] = v;
@@ -151,34 +156,50 @@ __global__ void __launch_bounds__(32 * kAcaWarps) aca_kernel(const AcaTask* __re
       for (int i = lane; i < m; i += 32) {
         double v = kentry_dev(pc, pa, T.r0 + i, T.c0 + jbest);
         if (rank) {
-          const double* ui = U + (int64_t)i * cap;
+          const double* ui = U + i;
           double s = 0.0;
-          for (int k = 0; k < rank; ++k) s = __dadd_rn(s, __dmul_rn(ui[k], Vt[(int64_t)k * n + jbest]));
+          for (int k = 0; k < rank; ++k) s = __dadd_rn(s, __dmul_rn(ui[(int64_t)k * m], Vt[(int64_t)k * n + jbest]));
           v = __dsub_rn(v, s);
         }
-        U[(int64_t)i * cap + rank] = v;
+        U[(int64_t)rank * m + i] = v;
       }
       __syncwarp();
       if (lane == 0) colu[jbest] = 1;
       // the host's FMA chains, one per lane: |u|, |v|, a_k = U_k . u, b_k = Vt_k . v
       const int nch = 2 + 2 * rank;
       for (int c = lane; c < nch; c += 32) {
-        double s = 0.0;
+        // one loop for every chain (lanes stay converged), loads batched
+        // ahead of the sequential FMA chain
+        const double *pa_, *pb_;
+        int len;
         if (c == 0) {
-          for (int i = 0; i < m; ++i) {
-            const double u = U[(int64_t)i * cap + rank];
-            s = fma(u, u, s);
-          }
+          pa_ = pb_ = U + (int64_t)rank * m;
+          len = m;
         } else if (c == 1) {
-          for (int j = 0; j < n; ++j) s = fma(row[j], row[j], s);
+          pa_ = pb_ = row;
+          len = n;
         } else if (c < 2 + rank) {
-          const int k = c - 2;
-          for (int i = 0; i < m; ++i) s = fma(U[(int64_t)i * cap + k], U[(int64_t)i * cap + rank], s);
+          pa_ = U + (int64_t)(c - 2) * m;
+          pb_ = U + (int64_t)rank * m;
+          len = m;
         } else {
-          const int k = c - 2 - rank;
-          const double* vk = Vt + (int64_t)k * n;
-          for (int j = 0; j < n; ++j) s = fma(vk[j], row[j], s);
+          pa_ = Vt + (int64_t)(c - 2 - rank) * n;
+          pb_ = row;
+          len = n;
         }
+        double s = 0.0;
+        int i = 0;
+        for (; i + 16 <= len; i += 16) {
+          double a[16], b[16];
+#pragma unroll
+          for (int u = 0; u < 16; ++u) {
+            a[u] = pa_[i + u];
+            b[u] = pb_[i + u];
+          }
+#pragma unroll
+          for (int u = 0; u < 16; ++u) s = fma(a[u], b[u], s);
+        }
+        for (; i < len; ++i) s = fma(pa_[i], pb_[i], s);
         ab[c] = s;
       }
       __syncwarp();
@@ -202,7 +223,7 @@ __global__ void __launch_bounds__(32 * kAcaWarps) aca_kernel(const AcaTask* __re
       double cb = -1.0;
       int ib = 0;
       for (int i = lane; i < m; i += 32) {
-        const double cv = rowu[i] ? -1.0 : fabs(U[(int64_t)i * cap + rank - 1]);
+        const double cv = rowu[i] ? -1.0 : fabs(U[(int64_t)(rank - 1) * m + i]);
         if (cv > cb) {
           cb = cv;
           ib = i;
@@ -237,6 +258,42 @@ __global__ void dense_fill_kernel(const DenseTask* __restrict__ tasks, const dou
     const int64_t i = e / T.n, j = e - i * T.n;
     base[T.off + e] = kentry_dev(pc, pa, T.r0 + i, T.c0 + j);
   }
+}
+
+// Scratch factors (U m x cap column-major, Vt cap x n) into the packed layout
+// (U m x r, then Vt r x n).
+struct CopyTask {
+  int64_t src_u, src_vt, dst;
+  int32_t m, n, cap, r;
+};
+
+__global__ void compact_kernel(const CopyTask* __restrict__ tasks, const double* __restrict__ src,
+                               double* dst) {
+  const CopyTask T = tasks[blockIdx.x];
+  const int64_t nu = (int64_t)T.m * T.r, nv = (int64_t)T.r * T.n;
+  for (int64_t e = threadIdx.x; e < nu; e += blockDim.x) {
+    const int64_t i = e / T.r, k = e - i * T.r;
+    dst[T.dst + e] = src[T.src_u + k * T.m + i];
+  }
+  for (int64_t e = threadIdx.x; e < nv; e += blockDim.x) dst[T.dst + nu + e] = src[T.src_vt + e];
+}
+
+template <typename T, typename F>
+int launch_tasks(const std::vector<T>& v, cudaStream_t st, F&& launch) {
+  for (size_t b0 = 0; b0 < v.size(); b0 += (size_t)1 << 20) {
+    const size_t cnt = std::min<size_t>(v.size() - b0, (size_t)1 << 20);
+    T* d = nullptr;
+    HMX_CUDA(cudaMalloc(&d, cnt * sizeof(T)));
+    cudaError_t e = cudaMemcpyAsync(d, v.data() + b0, cnt * sizeof(T), cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess) {
+      launch(d, (unsigned)cnt);
+      e = cudaGetLastError();
+    }
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    cudaFree(d);
+    if (e != cudaSuccess) return cuda_fail(e, "build kernel");
+  }
+  return HMX_OK;
 }
 
 int run_aca(const std::vector<AcaTask>& tasks, const double* d_pc, const double* d_pa, double tol,
@@ -291,6 +348,15 @@ int hmx_master_build(const hmx_build_desc* d, int device, hmx_master** out, int3
   DeviceGuard guard(device);
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+  const bool timing = std::getenv("HMX_BUILD_TIMING") != nullptr;
+  auto t_start = std::chrono::steady_clock::now();
+  auto lap = [&](const char* what) {
+    if (!timing) return;
+    const auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[hmx_master_build] %-28s %8.1f ms\n", what,
+                 std::chrono::duration<double, std::milli>(now - t_start).count());
+    t_start = now;
+  };
   const int64_t row_lo = d->row_lo, row_hi = d->row_hi > 0 ? d->row_hi : N;
 
   auto* M = new hmx_master();
@@ -356,26 +422,39 @@ int hmx_master_build(const hmx_build_desc* d, int device, hmx_master** out, int3
     return fail(HMX_ERR_CUDA);
   }
 
-  // ---- pass 1: ranks, in batches of bounded scratch
-  const int64_t kScratch = (int64_t)1 << 28;  // doubles (2 GiB) per batch
+  // ---- ACA rounds.  A round runs the ACA of a set of blocks in batches of
+  // bounded scratch (U m x cap column-major, then Vt cap x n per block) and
+  // hands every finished batch to `done`.  Pass 1: ranks with kCap1 columns;
+  // when one batch holds every block (config 4: 14 GB) its scratch is kept
+  // and compacted into the masters.  Retry: the blocks that exhausted kCap1,
+  // with kCap2.  Pass 2: the blocks whose factors were not kept, recomputed
+  // with their final rank as cap and compacted batch by batch.
+  size_t free_b = 0, total_b = 0;
+  cudaMemGetInfo(&free_b, &total_b);
+  const int64_t scratch_budget =
+      std::max<int64_t>((int64_t)1 << 27, std::min<int64_t>((int64_t)(free_b / 8) * 4 / 10, (int64_t)4 << 30));
   std::vector<int32_t> h_rank(na, 0), h_status(na, 0);
-  {
-    double* scratch = nullptr;
+  auto aca_round = [&](const std::vector<size_t>& idx, const std::function<int64_t(size_t)>& cap_of,
+                       const std::function<int(const std::vector<AcaTask>&, const std::vector<int32_t>&,
+                                               const std::vector<int32_t>&, size_t, double*, bool)>& done)
+      -> int {
     uint8_t* fl = nullptr;
+    double* sc = nullptr;
     int64_t sc_cap = 0, fl_cap = 0;
     size_t b0 = 0;
     int rc = HMX_OK;
-    while (b0 < na && rc == HMX_OK) {
+    bool kept = false;
+    while (b0 < idx.size() && rc == HMX_OK) {
       std::vector<AcaTask> batch;
       int64_t used = 0, fused = 0;
       size_t b1 = b0;
-      for (; b1 < na; ++b1) {
-        const int64_t k = aca_blocks[b1];
+      for (; b1 < idx.size(); ++b1) {
+        const int64_t k = aca_blocks[idx[b1]];
         const int64_t* t = d->table + 5 * k;
         const int64_t m = t[1] - t[0], n = t[3] - t[2];
-        const int64_t cap = std::min<int64_t>(budget_of(k), kAcaCap);
+        const int64_t cap = cap_of(idx[b1]);
         const int64_t need = cap * (m + n);
-        if (!batch.empty() && used + need > kScratch) break;
+        if (!batch.empty() && used + need > scratch_budget) break;
         AcaTask T{};
         T.r0 = t[0];
         T.c0 = t[2];
@@ -390,10 +469,11 @@ int hmx_master_build(const hmx_build_desc* d, int device, hmx_master** out, int3
         fused += m + n;
         batch.push_back(T);
       }
+      const bool only = b0 == 0 && b1 == idx.size();
       if (used > sc_cap) {
-        cudaFree(scratch);
-        scratch = nullptr;
-        if (cudaMalloc(&scratch, (size_t)used * 8) != cudaSuccess) {
+        cudaFree(sc);
+        sc = nullptr;
+        if (cudaMalloc(&sc, (size_t)std::max<int64_t>(used, 1) * 8) != cudaSuccess) {
           set_error("cudaMalloc failed for the ACA scratch");
           rc = HMX_ERR_CUDA;
           break;
@@ -410,23 +490,84 @@ int hmx_master_build(const hmx_build_desc* d, int device, hmx_master** out, int3
         }
         fl_cap = fused;
       }
-      rc = run_aca(batch, d_pc, d_pa, d->tol, scratch, fl, d_rank + b0, d_status + b0, st, sms);
+      rc = run_aca(batch, d_pc, d_pa, d->tol, sc, fl, d_rank, d_status, st, sms);
+      if (rc) break;
+      std::vector<int32_t> r(batch.size()), q(batch.size());
+      if ((e = cudaMemcpy(r.data(), d_rank, batch.size() * 4, cudaMemcpyDeviceToHost)) != cudaSuccess ||
+          (e = cudaMemcpy(q.data(), d_status, batch.size() * 4, cudaMemcpyDeviceToHost)) != cudaSuccess) {
+        rc = cuda_fail(e, "ACA ranks");
+        break;
+      }
+      rc = done(batch, r, q, b0, sc, only);
+      if (rc == -1) {  // the callback keeps the scratch
+        kept = true;
+        rc = HMX_OK;
+      }
       b0 = b1;
     }
-    cudaFree(scratch);
     cudaFree(fl);
+    if (!kept) cudaFree(sc);
+    return rc;
+  };
+  // pass 1
+  double* kept_scratch = nullptr;
+  std::vector<AcaTask> kept_tasks;
+  {
+    std::vector<size_t> all(na);
+    std::iota(all.begin(), all.end(), (size_t)0);
+    const int rc = aca_round(
+        all, [&](size_t q) { return std::min<int64_t>(budget_of(aca_blocks[q]), kCap1); },
+        [&](const std::vector<AcaTask>& b, const std::vector<int32_t>& r, const std::vector<int32_t>& q,
+            size_t b0, double* sc, bool only) -> int {
+          for (size_t i = 0; i < b.size(); ++i) {
+            h_rank[b0 + i] = r[i];
+            h_status[b0 + i] = q[i];
+          }
+          if (!only) return HMX_OK;
+          kept_scratch = sc;
+          kept_tasks = b;
+          return -1;
+        });
     if (rc) return fail(rc);
-    if (na) {
-      if ((e = cudaMemcpy(h_rank.data(), d_rank, na * 4, cudaMemcpyDeviceToHost)) != cudaSuccess ||
-          (e = cudaMemcpy(h_status.data(), d_status, na * 4, cudaMemcpyDeviceToHost)) != cudaSuccess)
-        return fail(cuda_fail(e, "ACA ranks"));
+  }
+  struct FreeOnExit {
+    double** p;
+    ~FreeOnExit() { cudaFree(*p); }
+  } scratch_guard{&kept_scratch};
+  lap("pass 1 (ranks)");
+  // retry round for the blocks that exhausted kCap1
+  {
+    std::vector<size_t> retry;
+    for (size_t q = 0; q < na; ++q)
+      if (h_status[q] == ACA_CAP) retry.push_back(q);
+    if (timing && na) {
+      const int64_t* t = d->table + 5 * aca_blocks[0];
+      std::fprintf(stderr, "[hmx_master_build] %zu ACA blocks, largest %lld x %lld (rank %d), %zu retried with %d columns, "
+                   "pass-1 scratch %s\n", na, (long long)(t[1] - t[0]), (long long)(t[3] - t[2]), h_rank[0],
+                   retry.size(), kCap2, kept_scratch ? "kept" : "batched");
+    }
+    if (!retry.empty()) {
+      const int rc = aca_round(
+          retry, [&](size_t q) { return std::min<int64_t>(budget_of(aca_blocks[q]), kCap2); },
+          [&](const std::vector<AcaTask>& b, const std::vector<int32_t>& r, const std::vector<int32_t>& q,
+              size_t b0, double*, bool) -> int {
+            for (size_t i = 0; i < b.size(); ++i) {
+              h_rank[retry[b0 + i]] = r[i];
+              h_status[retry[b0 + i]] = q[i];
+            }
+            return HMX_OK;
+          });
+      if (rc) return fail(rc);
     }
   }
-
+  // pass-1 blocks whose factors are in the kept scratch
+  std::vector<char> in_kept(na, 0);
+  if (kept_scratch)
+    for (size_t q = 0; q < na; ++q) in_kept[q] = h_status[q] == ACA_OK && h_rank[q] <= kept_tasks[q].cap;
   // ---- host completion of the rare blocks (same arithmetic: aca_core.h)
   std::vector<size_t> host_idx;
   for (size_t q = 0; q < na; ++q)
-    if (h_status[q] == ACA_HOST) host_idx.push_back(q);
+    if (h_status[q] != ACA_OK) host_idx.push_back(q);  // remainder path, or beyond kCap2 ranks
   std::vector<hmx_aca::BlockResult> host_res(host_idx.size());
   int64_t nfall = 0;
   {
@@ -462,6 +603,9 @@ int hmx_master_build(const hmx_build_desc* d, int device, hmx_master** out, int3
   }
   for (size_t q = 0; q < na; ++q)
     if (kind[(size_t)aca_blocks[q]] == 1) rank[(size_t)aca_blocks[q]] = h_rank[q];
+  if (timing) std::fprintf(stderr, "[hmx_master_build] %zu of %zu ACA blocks completed on the host\n",
+                           host_idx.size(), na);
+  lap("host completion");
 
   // ---- layout (hb_build_layout's): dense m*n, low rank r*(m+n), skipped 0
   int64_t off = 0;
@@ -502,67 +646,65 @@ int hmx_master_build(const hmx_build_desc* d, int device, hmx_master** out, int3
         const int64_t* t = d->table + 5 * k;
         dt.push_back({t[0], t[2], offsets[k], (int32_t)(t[1] - t[0]), (int32_t)(t[3] - t[2])});
       }
-    for (size_t b0 = 0; b0 < dt.size(); b0 += 1 << 20) {  // grid.x limit headroom
-      const size_t cnt = std::min<size_t>(dt.size() - b0, (size_t)1 << 20);
-      DenseTask* d_dt = nullptr;
-      if ((e = cudaMalloc(&d_dt, cnt * sizeof(DenseTask))) != cudaSuccess) return fail(cuda_fail(e, "dense tasks"));
-      e = cudaMemcpyAsync(d_dt, dt.data() + b0, cnt * sizeof(DenseTask), cudaMemcpyHostToDevice, st);
-      if (e == cudaSuccess) {
-        dense_fill_kernel<<<(unsigned)cnt, 256, 0, st>>>(d_dt, d_pc, d_pa, M->data);
-        e = cudaGetLastError();
-      }
-      if (e == cudaSuccess) e = cudaStreamSynchronize(st);
-      cudaFree(d_dt);
-      if (e != cudaSuccess) return fail(cuda_fail(e, "dense_fill_kernel"));
-    }
-  }
-
-  // ---- pass 2: the factors straight into the packed layout (U m x r
-  // row-major, then Vt r x n), recomputed with the ranks known
-  {
-    std::vector<AcaTask> tasks;
-    std::vector<size_t> which;
-    int64_t fused = 0;
-    for (size_t q = 0; q < na; ++q) {
-      const int64_t k = aca_blocks[q];
-      if (kind[(size_t)k] != 1 || h_status[q] == ACA_HOST) continue;
-      const int64_t* t = d->table + 5 * k;
-      const int64_t m = t[1] - t[0], n = t[3] - t[2], r = rank[(size_t)k];
-      AcaTask T{};
-      T.r0 = t[0];
-      T.c0 = t[2];
-      T.m = (int32_t)m;
-      T.n = (int32_t)n;
-      T.budget = (int32_t)budget_of(k);
-      T.cap = (int32_t)r;
-      T.u_off = offsets[k];
-      T.vt_off = offsets[k] + m * r;
-      T.flag_off = fused;
-      fused += m + n;
-      tasks.push_back(T);
-      which.push_back(q);
-    }
-    uint8_t* fl = nullptr;
-    if (!tasks.empty() && cudaMalloc(&fl, (size_t)std::max<int64_t>(fused, 1)) != cudaSuccess) {
-      set_error("cudaMalloc failed for the ACA flags");
-      return fail(HMX_ERR_CUDA);
-    }
-    int rc = run_aca(tasks, d_pc, d_pa, d->tol, M->data, fl, d_rank, d_status, st, sms);
-    cudaFree(fl);
+    const int rc = launch_tasks(dt, st, [&](const DenseTask* t, unsigned cnt) {
+      dense_fill_kernel<<<cnt, 256, 0, st>>>(t, d_pc, d_pa, M->data);
+    });
     if (rc) return fail(rc);
-    if (!tasks.empty()) {
-      // pass 2 must reproduce pass 1 (same arithmetic): check the ranks
-      std::vector<int32_t> r2(tasks.size()), s2(tasks.size());
-      if ((e = cudaMemcpy(r2.data(), d_rank, tasks.size() * 4, cudaMemcpyDeviceToHost)) != cudaSuccess ||
-          (e = cudaMemcpy(s2.data(), d_status, tasks.size() * 4, cudaMemcpyDeviceToHost)) != cudaSuccess)
-        return fail(cuda_fail(e, "ACA pass-2 ranks"));
-      for (size_t i = 0; i < tasks.size(); ++i)
-        if (r2[i] != tasks[i].cap || s2[i] != ACA_OK) {
-          set_error("ACA pass 2 diverged from pass 1");
-          return fail(HMX_ERR_CUDA);
-        }
+  }
+  // ---- factors into the packed layout (U m x r row-major, then Vt r x n)
+  auto compact = [&](const std::vector<AcaTask>& b, const std::vector<size_t>& qs, const double* sc) -> int {
+    std::vector<CopyTask> ct;
+    for (size_t i = 0; i < b.size(); ++i) {
+      const size_t q = qs[i];
+      const int64_t k = aca_blocks[q];
+      if (kind[(size_t)k] != 1 || h_status[q] != ACA_OK) continue;
+      ct.push_back({b[i].u_off, b[i].vt_off, offsets[k], b[i].m, b[i].n, b[i].cap, (int32_t)rank[(size_t)k]});
+    }
+    return launch_tasks(ct, st, [&](const CopyTask* dt, unsigned cnt) {
+      compact_kernel<<<cnt, 256, 0, st>>>(dt, sc, M->data);
+    });
+  };
+  if (kept_scratch) {
+    std::vector<size_t> qs(na);
+    std::iota(qs.begin(), qs.end(), (size_t)0);
+    std::vector<AcaTask> b;
+    std::vector<size_t> bq;
+    for (size_t q = 0; q < na; ++q)
+      if (in_kept[q]) {
+        b.push_back(kept_tasks[q]);
+        bq.push_back(q);
+      }
+    const int rc = compact(b, bq, kept_scratch);
+    if (rc) return fail(rc);
+    cudaFree(kept_scratch);
+    kept_scratch = nullptr;
+  }
+  lap("layout + dense + compaction");
+  // pass 2: the GPU-finished blocks whose factors were not kept, recomputed
+  // with their rank as cap (same arithmetic: the ranks must reproduce)
+  {
+    std::vector<size_t> redo;
+    for (size_t q = 0; q < na; ++q)
+      if (h_status[q] == ACA_OK && !in_kept[q] && kind[(size_t)aca_blocks[q]] == 1) redo.push_back(q);
+    if (!redo.empty()) {
+      const int rc = aca_round(
+          redo, [&](size_t q) { return std::max<int64_t>(h_rank[q], 1); },
+          [&](const std::vector<AcaTask>& b, const std::vector<int32_t>& r, const std::vector<int32_t>& q,
+              size_t b0, double* sc, bool) -> int {
+            std::vector<size_t> qs(b.size());
+            for (size_t i = 0; i < b.size(); ++i) {
+              qs[i] = redo[b0 + i];
+              if (r[i] != h_rank[qs[i]] || q[i] != ACA_OK) {
+                set_error("ACA pass 2 diverged from pass 1");
+                return HMX_ERR_CUDA;
+              }
+            }
+            return compact(b, qs, sc);
+          });
+      if (rc) return fail(rc);
     }
   }
+  lap("pass 2 (factors)");
   // host-completed low-rank blocks
   for (size_t h = 0; h < host_idx.size(); ++h) {
     const int64_t k = aca_blocks[host_idx[h]];
