@@ -98,8 +98,14 @@ typedef struct {
   int64_t row_begin;
   int64_t row_end;
   int32_t s1_chunk_bytes; /* stage-1 column-chunk target; 0 = adaptive (64-256 KB) */
-  int32_t reserved;       /* must be 0 */
+  int32_t flags;          /* HMX_PLAN_* bits, 0 = none */
 } hmx_plan_options;
+
+/* hmx_plan_options.flags: order the stage-1 work so the part that reads
+ * only x[row_begin, row_end) -- this rank's own slice of the iterate in the
+ * multi-GPU mode -- can run while the allgather brings the other slices
+ * (hmx_dist_matvec, hmx_bicgstab_dist). */
+#define HMX_PLAN_LOCAL_FIRST 1
 
 typedef struct hmx_plan hmx_plan;
 

@@ -39,7 +39,10 @@ class MatrixDesc(ctypes.Structure):
 
 class PlanOptions(ctypes.Structure):
     _fields_ = [("row_begin", ctypes.c_int64), ("row_end", ctypes.c_int64),
-                ("s1_chunk_bytes", ctypes.c_int32), ("reserved", ctypes.c_int32)]
+                ("s1_chunk_bytes", ctypes.c_int32), ("flags", ctypes.c_int32)]
+
+
+HMX_PLAN_LOCAL_FIRST = 1
 
 
 class PlanInfo(ctypes.Structure):
@@ -186,7 +189,7 @@ class Plan:
     """A device-resident flattened H-matrix for one scheme (owns a C plan)."""
 
     def __init__(self, packed, table, perm, scheme_label: str, n: int, device: int = 0,
-                 row_range=None, s1_chunk_bytes: int = 0):
+                 row_range=None, s1_chunk_bytes: int = 0, local_first: bool = False):
         lib = load_library()
         code = SCHEME_CODES.get(scheme_label, 6 if scheme_label.startswith("m3") else None)
         if code is None:
@@ -220,6 +223,7 @@ class Plan:
         if row_range is not None:
             opt.row_begin, opt.row_end = int(row_range[0]), int(row_range[1])
         opt.s1_chunk_bytes = int(s1_chunk_bytes)
+        opt.flags = HMX_PLAN_LOCAL_FIRST if local_first else 0
         h = ctypes.c_void_p()
         rc = lib.hmx_plan_create(ctypes.byref(d), int(device), ctypes.byref(opt), ctypes.byref(h))
         self._keep = []  # the plan holds device copies; host arrays may go

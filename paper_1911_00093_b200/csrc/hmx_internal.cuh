@@ -86,7 +86,7 @@ struct DevPlan {
   int32_t zepi;
   int32_t s1_narrow;              // every stage-1 segment is widened FP32: 64-thread CTAs
   int32_t s2_deep;                // FP64-accumulating stage 2 with an FP64 part: deep pipeline
-  int32_t pad3;
+  int32_t n_seg1_local;           // leading stage-1 segments reading only x[row_begin, row_end)
   const int32_t* gtab;            // item-aligned FP32 group boundaries (stage 2)
   const double* zscale;           // d per z entry (methods 2, 3)
   double* z;

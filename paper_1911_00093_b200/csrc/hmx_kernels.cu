@@ -12,6 +12,7 @@
 //   m3    hi f64 / lo f32 widened, z *= d      dense f64; U_hi f64; U_lo widened f64
 //
 // Every f32-accumulated partial is widened once and added in f64.
+#include <algorithm>
 #include <type_traits>
 
 #include "hmx_kernels.cuh"
@@ -541,8 +542,11 @@ static cudaError_t launch_seg(const DevPlan& P, const Seg* segs, int nseg, const
   return cudaLaunchKernelEx(&cfg, seg_kernel<M, O, NT, DEEP>, P, segs, x, out);
 }
 
-cudaError_t launch_stage1(const DevPlan& P, const double* x, cudaStream_t st, const int* skip) {
-  if (P.n_seg1 == 0) return cudaSuccess;
+cudaError_t launch_stage1(const DevPlan& P, const double* x, cudaStream_t st, const int* skip,
+                          int seg_begin, int seg_count) {
+  const int nseg = seg_count < 0 ? P.n_seg1 - seg_begin : std::min(seg_count, P.n_seg1 - seg_begin);
+  if (nseg <= 0) return cudaSuccess;
+  const Seg* segs = P.seg1 + seg_begin;
   S2Out none{};
   none.skip = skip;
   // every stage-1 segment FP32 data widened into FP64 sums (m1-mixed, m2-single,
@@ -550,10 +554,10 @@ cudaError_t launch_stage1(const DevPlan& P, const double* x, cudaStream_t st, co
   // -3..-4 % on stage 1 against 128 threads; the FP32-accumulating m1-single
   // stage 1 is faster on 128)
   switch (P.f32mode1) {
-    case F32_ALL32: return launch_seg<F32_ALL32, OUT_Z, kS1Threads>(P, P.seg1, P.n_seg1, x, none, st, false);
+    case F32_ALL32: return launch_seg<F32_ALL32, OUT_Z, kS1Threads>(P, segs, nseg, x, none, st, false);
     default:
-      return P.s1_narrow ? launch_seg<F32_ALL64, OUT_Z, kS1Threads32>(P, P.seg1, P.n_seg1, x, none, st, false)
-                         : launch_seg<F32_ALL64, OUT_Z, kS1Threads>(P, P.seg1, P.n_seg1, x, none, st, false);
+      return P.s1_narrow ? launch_seg<F32_ALL64, OUT_Z, kS1Threads32>(P, segs, nseg, x, none, st, false)
+                         : launch_seg<F32_ALL64, OUT_Z, kS1Threads>(P, segs, nseg, x, none, st, false);
   }
 }
 

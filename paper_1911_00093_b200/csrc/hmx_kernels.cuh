@@ -5,8 +5,9 @@
 
 namespace hmx {
 
+// stage-1 segments [seg_begin, seg_begin + seg_count) (count < 0: to the end)
 cudaError_t launch_stage1(const DevPlan& P, const double* x, cudaStream_t st,
-                          const int* skip = nullptr);
+                          const int* skip = nullptr, int seg_begin = 0, int seg_count = -1);
 cudaError_t launch_stage2(const DevPlan& P, const double* x, const S2Out& out, cudaStream_t st,
                           bool pdl);
 cudaError_t launch_gather_perm(const double* x, const int32_t* perm, double* xp, int n,

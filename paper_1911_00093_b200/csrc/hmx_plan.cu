@@ -634,9 +634,23 @@ int hmx::plan_create_impl(const hmx_matrix_desc* d, int device, const hmx_plan_o
   }
   // stage-1 CTAs in decreasing size: chunked (long) segments start first and
   // the many small ones fill the tail
-  std::stable_sort(seg1.begin(), seg1.end(), [](const Seg& a, const Seg& b) {
+  // (HMX_PLAN_LOCAL_FIRST: the segments that read only this plan's own x
+  // slice first, so the multi-GPU mode can run them during the allgather)
+  const bool local_first = opt && (opt->flags & HMX_PLAN_LOCAL_FIRST);
+  auto s1_local = [&](const Seg& sg) {
+    const Run& r = runs[(size_t)sg.run0];
+    return local_first && r.src >= rb && (int64_t)r.src + r.width <= re;
+  };
+  std::stable_sort(seg1.begin(), seg1.end(), [&](const Seg& a, const Seg& b) {
+    const bool la = s1_local(a), lb = s1_local(b);
+    if (la != lb) return la;
     return (int64_t)a.R * (a.W64 * 2 + a.W32) > (int64_t)b.R * (b.W64 * 2 + b.W32);
   });
+  int32_t n_seg1_local = 0;
+  for (const Seg& sg : seg1) n_seg1_local += s1_local(sg) ? 1 : 0;
+  // test hook: split the stage-1 launch in two at world 1 too (where every
+  // segment is local), to exercise the two-stream path
+  if (local_first && std::getenv("HMX_TEST_SPLIT_STAGE1")) n_seg1_local = (int32_t)seg1.size() / 2;
 
   DevPlan& dp = p->dp;
   dp.n = (int32_t)n;
@@ -794,6 +808,7 @@ int hmx::plan_create_impl(const hmx_matrix_desc* d, int device, const hmx_plan_o
   dp.seg1 = d_seg1;
   dp.seg2 = d_seg2;
   dp.n_seg1 = (int32_t)seg1.size();
+  dp.n_seg1_local = n_seg1_local;
   dp.n_seg2 = (int32_t)nseg2;
   dp.runs = d_runs;
   dp.blob64 = d_b64;

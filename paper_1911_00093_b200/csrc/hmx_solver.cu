@@ -795,6 +795,10 @@ struct hmx_comm {
   int hist_cap = 0;
   int grid = 0;
   cudaEvent_t ev[2] = {};
+  // overlap of the allgather with the stage-1 work on the local x slice
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_x = nullptr, ev_local = nullptr;
+  bool overlap = false;
 
   template <typename T>
   T* alloc(size_t count) {
@@ -902,6 +906,45 @@ int allreduce_dots_flag(hmx_comm* c, double* dots, int count, int* flag, cudaStr
   return HMX_OK;
 }
 
+// y_local = rows of A full, with the one exchange: `full` holds this rank's
+// slice (written on st); the allgather of the other slices runs on st while
+// the plan's leading stage-1 segments that read only the local slice
+// (HMX_PLAN_LOCAL_FIRST) run on the side stream; then the rest of stage 1
+// and stage 2 (dots fused as in apply_sc).  Without local-first segments
+// this is allgather + apply_sc.
+int dist_apply(hmx_comm* c, hmx_plan* A, double* sc, cudaStream_t st, double* full, double* y,
+               const double* w1, int yy, int slot, int* flag, const int* skip = nullptr) {
+  // (one rank has nothing to gather: a single stream is cheaper, except
+  // under the test hook that exercises the two-stream path)
+  const int nloc = c->overlap ? A->dp.n_seg1_local : 0;
+  if (nloc > 0) {
+    HMX_CUDA(cudaEventRecord(c->ev_x, st));
+    HMX_CUDA(cudaStreamWaitEvent(c->side, c->ev_x, 0));
+    HMX_CUDA(launch_stage1(A->dp, full, c->side, skip, 0, nloc));
+    HMX_CUDA(cudaEventRecord(c->ev_local, c->side));
+  }
+  int rc = allgather_rows(c, full, st);
+  if (rc) return rc;
+  if ((w1 || yy) && A->dp.n_seg2 == 0) HMX_CUDA(cudaMemsetAsync(sc + slot, 0, 2 * sizeof(double), st));
+  S2Out out{};
+  out.skip = skip;
+  out.y = y;
+  out.permute_out = 0;
+  out.w1 = w1;
+  out.yy = yy;
+  if (w1 || yy) {
+    out.seg_dots = A->d_seg_dots;
+    out.done = A->d_done;
+    out.dots_out = sc + slot;
+  }
+  out.nonfinite = flag;
+  HMX_CUDA(launch_stage1(A->dp, full, st, skip, nloc, -1));
+  if (nloc > 0) HMX_CUDA(cudaStreamWaitEvent(st, c->ev_local, 0));
+  HMX_CUDA(launch_stage2(A->dp, full, out, st, /*pdl=*/true));
+  A->last_xp = full;
+  return HMX_OK;
+}
+
 struct DistCtx {
   hmx_plan* A;
   hmx_plan* A64;
@@ -933,15 +976,13 @@ int enqueue_iteration_dist(const DistCtx& d) {
   double* sl = c->s_full + c->r0;
   int rc;
   p_update_kernel<<<d.grid, kVecThreads, 0, st>>>(c->r, c->v, pl, d.nl, c->ictl, c->sc, c->stop);
-  if ((rc = allgather_rows(c, c->p_full, st))) return rc;
-  if ((rc = apply_sc(d.A, c->sc, st, c->p_full, c->v, c->rhat, 0, SC_DV, c->flags, c->stop))) return rc;
+  if ((rc = dist_apply(c, d.A, c->sc, st, c->p_full, c->v, c->rhat, 0, SC_DV, c->flags, c->stop))) return rc;
   if ((rc = allreduce_dots_flag(c, c->sc + SC_DV, 1, c->flags, st))) return rc;
   s_update_kernel<<<d.grid, kVecThreads, 0, st>>>(c->r, c->v, sl, d.nl, c->sc, d.red(SC_SS), c->ictl,
                                                     c->hist, c->stop, c->flags, 1);
   if ((rc = allreduce_sum(c, c->sc + SC_SS, 1, st))) return rc;
   decide_s_kernel<<<1, 1, 0, st>>>(c->sc, c->ictl, c->hist, c->stop);
-  if ((rc = allgather_rows(c, c->s_full, st))) return rc;
-  if ((rc = apply_sc(d.A, c->sc, st, c->s_full, c->t, sl, 1, SC_DT, c->flags + 1, c->stop))) return rc;
+  if ((rc = dist_apply(c, d.A, c->sc, st, c->s_full, c->t, sl, 1, SC_DT, c->flags + 1, c->stop))) return rc;
   if ((rc = allreduce_dots_flag(c, c->sc + SC_DT, 2, c->flags + 1, st))) return rc;
   xr_update_kernel<<<d.grid, kVecThreads, 0, st>>>(c->x, c->r, pl, sl, c->t, c->rhat, d.nl, c->sc,
                                                      d.red(SC_TMP), c->ictl, c->hist, c->stop,
@@ -960,8 +1001,7 @@ int true_residual_dist(const DistCtx& d, double* out) {
   int rc;
   if (d.nl > 0)
     HMX_CUDA(cudaMemcpyAsync(c->x_full + c->r0, c->x, (size_t)d.nl * sizeof(double), cudaMemcpyDeviceToDevice, st));
-  if ((rc = allgather_rows(c, c->x_full, st))) return rc;
-  if ((rc = apply_sc(d.A64, c->sc, st, c->x_full, c->y, nullptr, 0, 0, c->flags + 2))) return rc;
+  if ((rc = dist_apply(c, d.A64, c->sc, st, c->x_full, c->y, nullptr, 0, 0, c->flags + 2))) return rc;
   resid_kernel<<<d.grid, kVecThreads, 0, st>>>(c->b, c->y, d.nl, d.red(SC_RES));
   HMX_CUDA(cudaGetLastError());
   if ((rc = allreduce_dots_flag(c, c->sc + SC_RES, 2, c->flags + 2, st))) return rc;
@@ -1007,6 +1047,9 @@ void hmx_comm_destroy(hmx_comm* c) {
     if (c->h_sc) cudaFreeHost(c->h_sc);
     for (auto& e : c->ev)
       if (e) cudaEventDestroy(e);
+    if (c->ev_x) cudaEventDestroy(c->ev_x);
+    if (c->ev_local) cudaEventDestroy(c->ev_local);
+    if (c->side) cudaStreamDestroy(c->side);
   }
   delete c;
 }
@@ -1045,6 +1088,7 @@ int hmx_comm_create(const uint8_t id[128], int world, int rank, int device, cons
   c->n = cuts[world];
   c->r0 = cuts[rank];
   c->r1 = cuts[rank + 1];
+  c->overlap = world > 1 || std::getenv("HMX_TEST_SPLIT_STAGE1") != nullptr;
   ncclUniqueId u;
   std::memcpy(&u, id, sizeof(u));
   const ncclResult_t r = nccl_api().CommInitRank(&c->nc, world, u, rank);
@@ -1075,7 +1119,10 @@ int hmx_comm_create(const uint8_t id[128], int world, int rank, int device, cons
       cudaMemset(c->done, 0, sizeof(uint32_t)) != cudaSuccess ||
       cudaMemset(c->sc, 0, SC_N * sizeof(double)) != cudaSuccess ||
       cudaMemset(c->x_full, 0, n * sizeof(double)) != cudaSuccess ||
-      cudaEventCreate(&c->ev[0]) != cudaSuccess || cudaEventCreate(&c->ev[1]) != cudaSuccess) {
+      cudaEventCreate(&c->ev[0]) != cudaSuccess || cudaEventCreate(&c->ev[1]) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->ev_x, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->ev_local, cudaEventDisableTiming) != cudaSuccess) {
     set_error("hmx_comm_create: device allocation failed");
     hmx_comm_destroy(c);
     return HMX_ERR_CUDA;
@@ -1100,16 +1147,8 @@ int hmx_dist_matvec(hmx_plan* p, hmx_comm* c, const double* x_local, double* y_l
   const int64_t nl = c->r1 - c->r0;
   if (nl > 0 && x_local != c->x_full + c->r0)
     HMX_CUDA(cudaMemcpyAsync(c->x_full + c->r0, x_local, (size_t)nl * sizeof(double), cudaMemcpyDeviceToDevice, st));
-  int rc = allgather_rows(c, c->x_full, st);
-  if (rc) return rc;
-  S2Out out{};
-  out.y = y_local;
-  out.permute_out = 0;
-  out.nonfinite = nonfinite ? nonfinite : p->d_nonfinite;
-  HMX_CUDA(launch_stage1(p->dp, c->x_full, st));
-  HMX_CUDA(launch_stage2(p->dp, c->x_full, out, st, /*pdl=*/true));
-  p->last_xp = c->x_full;
-  return HMX_OK;
+  return dist_apply(c, p, c->sc, st, c->x_full, y_local, nullptr, 0, 0,
+                    nonfinite ? nonfinite : p->d_nonfinite);
 }
 
 int hmx_bicgstab_dist(hmx_plan* A, hmx_plan* A64, hmx_comm* c, const double* b_local, double tol,

@@ -321,7 +321,7 @@ def make_gpu_operator(h, scheme: str, slices: RowSlices, rank: int, device, grou
 
     sh = prepare_scheme(h, scheme)
     plan = _gpu.Plan(sh.packed, h.partition.table, np.asarray(h.permutation), sh.scheme.label,
-                     h.n, device=device.index or 0, row_range=slices.span(rank))
+                     h.n, device=device.index or 0, row_range=slices.span(rank), local_first=True)
     return DistributedOperator(slices, rank, group=group, device=device, plan=plan), sh
 
 

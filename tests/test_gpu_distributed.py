@@ -102,13 +102,20 @@ def test_distributed_solver_nccl_world1(hx, cfg):
         dist.destroy_process_group()
 
 
+@pytest.mark.parametrize("local_first", [False, True, "split"])
 @pytest.mark.parametrize("scheme", ["m1-double", "m1-mixed", "m2-mixed", "m3:c=1"])
-def test_cxx_dist_path_world1_is_the_single_gpu_path(hx, cfg, scheme):
+def test_cxx_dist_path_world1_is_the_single_gpu_path(hx, cfg, scheme, local_first, monkeypatch):
     """hmx_dist_matvec and hmx_bicgstab_dist (libhmx_gpu's own NCCL
     communicator, device-side decisions, batched iterations) at world 1 run
     the single-GPU kernels in the same order: bitwise the single-GPU matvec
-    and graph-resident solver (solution, history, report)."""
+    and graph-resident solver (solution, history, report).  local_first:
+    the plans order stage 1 local-slice first and the stage-1 work on the
+    local slice runs on a side stream during the allgather ("split": half of
+    stage 1 on each stream, the test hook that exercises both launches)."""
     import torch
+
+    if local_first == "split":
+        monkeypatch.setenv("HMX_TEST_SPLIT_STAGE1", "1")
 
     from paper_1911_00093_b200 import _gpu
     from paper_1911_00093_b200 import distributed as D
@@ -121,8 +128,11 @@ def test_cxx_dist_path_world1_is_the_single_gpu_path(hx, cfg, scheme):
     comm = D.make_comm(slices, 0, dev)
     sh = hx.prepare_scheme(h, scheme)
     sh64 = hx.prepare_scheme(h, "m1-double")
-    plan = _gpu.Plan(sh.packed, h.partition.table, perm, sh.scheme.label, n, row_range=(0, n))
-    plan64 = _gpu.Plan(sh64.packed, h.partition.table, perm, "m1-double", n, row_range=(0, n))
+    lf = bool(local_first)
+    plan = _gpu.Plan(sh.packed, h.partition.table, perm, sh.scheme.label, n, row_range=(0, n),
+                     local_first=lf)
+    plan64 = _gpu.Plan(sh64.packed, h.partition.table, perm, "m1-double", n, row_range=(0, n),
+                       local_first=lf)
     try:
         xp = torch.from_numpy(np.ascontiguousarray(x[perm])).to(dev)
         y = torch.empty(n, dtype=torch.float64, device=dev)
