@@ -431,13 +431,30 @@ int hmx_master_build(const hmx_build_desc* d, int device, hmx_master** out, int3
   // with their final rank as cap and compacted batch by batch.
   size_t free_b = 0, total_b = 0;
   cudaMemGetInfo(&free_b, &total_b);
-  const int64_t scratch_budget =
-      std::max<int64_t>((int64_t)1 << 27, std::min<int64_t>((int64_t)(free_b / 8) * 4 / 10, (int64_t)4 << 30));
+  const int64_t scratch_budget = std::max<int64_t>((int64_t)1 << 27, (int64_t)(free_b / 8) * 45 / 100);
   std::vector<int32_t> h_rank(na, 0), h_status(na, 0);
-  auto aca_round = [&](const std::vector<size_t>& idx, const std::function<int64_t(size_t)>& cap_of,
+  auto aca_round = [&](const std::vector<size_t>& idx_in, const std::function<int64_t(size_t)>& cap_of,
                        const std::function<int(const std::vector<AcaTask>&, const std::vector<int32_t>&,
-                                               const std::vector<int32_t>&, size_t, double*, bool)>& done)
+                                               const std::vector<int32_t>&, const std::vector<size_t>&,
+                                               double*, bool)>& done)
       -> int {
+    // more than one batch: deal the (size-sorted) blocks round-robin so
+    // every batch mixes large and small blocks (a batch of only the largest
+    // leaves most warps idle behind their long sequential chains)
+    std::vector<size_t> idx = idx_in;
+    {
+      int64_t total = 0;
+      for (size_t q : idx_in) {
+        const int64_t* t = d->table + 5 * aca_blocks[q];
+        total += cap_of(q) * ((t[1] - t[0]) + (t[3] - t[2]));
+      }
+      const int64_t nbat = (total + scratch_budget - 1) / scratch_budget;
+      if (nbat > 1) {
+        idx.clear();
+        for (int64_t b = 0; b < nbat; ++b)
+          for (size_t i = (size_t)b; i < idx_in.size(); i += (size_t)nbat) idx.push_back(idx_in[i]);
+      }
+    }
     uint8_t* fl = nullptr;
     double* sc = nullptr;
     int64_t sc_cap = 0, fl_cap = 0;
@@ -498,7 +515,8 @@ int hmx_master_build(const hmx_build_desc* d, int device, hmx_master** out, int3
         rc = cuda_fail(e, "ACA ranks");
         break;
       }
-      rc = done(batch, r, q, b0, sc, only);
+      rc = done(batch, r, q, std::vector<size_t>(idx.begin() + (ptrdiff_t)b0, idx.begin() + (ptrdiff_t)b1), sc,
+                only);
       if (rc == -1) {  // the callback keeps the scratch
         kept = true;
         rc = HMX_OK;
@@ -518,10 +536,10 @@ int hmx_master_build(const hmx_build_desc* d, int device, hmx_master** out, int3
     const int rc = aca_round(
         all, [&](size_t q) { return std::min<int64_t>(budget_of(aca_blocks[q]), kCap1); },
         [&](const std::vector<AcaTask>& b, const std::vector<int32_t>& r, const std::vector<int32_t>& q,
-            size_t b0, double* sc, bool only) -> int {
+            const std::vector<size_t>& qs, double* sc, bool only) -> int {
           for (size_t i = 0; i < b.size(); ++i) {
-            h_rank[b0 + i] = r[i];
-            h_status[b0 + i] = q[i];
+            h_rank[qs[i]] = r[i];
+            h_status[qs[i]] = q[i];
           }
           if (!only) return HMX_OK;
           kept_scratch = sc;
@@ -550,10 +568,10 @@ int hmx_master_build(const hmx_build_desc* d, int device, hmx_master** out, int3
       const int rc = aca_round(
           retry, [&](size_t q) { return std::min<int64_t>(budget_of(aca_blocks[q]), kCap2); },
           [&](const std::vector<AcaTask>& b, const std::vector<int32_t>& r, const std::vector<int32_t>& q,
-              size_t b0, double*, bool) -> int {
+              const std::vector<size_t>& qs, double*, bool) -> int {
             for (size_t i = 0; i < b.size(); ++i) {
-              h_rank[retry[b0 + i]] = r[i];
-              h_status[retry[b0 + i]] = q[i];
+              h_rank[qs[i]] = r[i];
+              h_status[qs[i]] = q[i];
             }
             return HMX_OK;
           });
@@ -633,6 +651,14 @@ int hmx_master_build(const hmx_build_desc* d, int device, hmx_master** out, int3
   M->n_data = off;
   if (fallbacks) *fallbacks = nfall;
   M->data = M->alloc<double>((size_t)std::max<int64_t>(off, 1));
+  if (!M->data && kept_scratch) {
+    // no room next to the kept pass-1 scratch: drop it, recompute in pass 2
+    cudaFree(kept_scratch);
+    kept_scratch = nullptr;
+    std::fill(in_kept.begin(), in_kept.end(), 0);
+    cudaGetLastError();
+    M->data = M->alloc<double>((size_t)std::max<int64_t>(off, 1));
+  }
   if (!M->data) {
     set_error("cudaMalloc failed for the masters (out of device memory?)");
     return fail(HMX_ERR_CUDA);
@@ -690,10 +716,8 @@ int hmx_master_build(const hmx_build_desc* d, int device, hmx_master** out, int3
       const int rc = aca_round(
           redo, [&](size_t q) { return std::max<int64_t>(h_rank[q], 1); },
           [&](const std::vector<AcaTask>& b, const std::vector<int32_t>& r, const std::vector<int32_t>& q,
-              size_t b0, double* sc, bool) -> int {
-            std::vector<size_t> qs(b.size());
+              const std::vector<size_t>& qs, double* sc, bool) -> int {
             for (size_t i = 0; i < b.size(); ++i) {
-              qs[i] = redo[b0 + i];
               if (r[i] != h_rank[qs[i]] || q[i] != ACA_OK) {
                 set_error("ACA pass 2 diverged from pass 1");
                 return HMX_ERR_CUDA;
