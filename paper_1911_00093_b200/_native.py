@@ -74,6 +74,7 @@ def build_gpu(force: bool = False, verbose: bool = False) -> Path:
         cmd = [NVCC, GENCODE, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
                "-Xcompiler", "-ffp-contract=off", "--fmad=true",
                "-I", str(INCLUDE_DIR), "-I", str(CSRC), "-c", str(s), "-o", str(o)]
+        cmd[1:1] = os.environ.get("HMX_NVCC_EXTRA", "").split()  # A/B builds (tools/ab_build.sh)
         if verbose:
             cmd.insert(1, "-Xptxas=-v")
         out = _run(cmd)
