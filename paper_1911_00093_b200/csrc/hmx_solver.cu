@@ -375,11 +375,10 @@ int alloc_ws(hmx_plan* p, Workspace& w, int64_t n, int grid) {
   return HMX_OK;
 }
 
-// y = A xp on stream st (y: the plan's rows), fused dots into sc[slot..slot+1]
-int apply_sc(hmx_plan* A, double* sc, cudaStream_t st, const double* xp, double* y,
-             const double* w1, int yy, int slot, int* flag, const int* skip = nullptr) {
-  if ((w1 || yy) && A->dp.n_seg2 == 0)  // no local rows: the dots are zero
-    HMX_CUDA(cudaMemsetAsync(sc + slot, 0, 2 * sizeof(double), st));
+// Stage-2 epilogue options: y (the plan's rows), dots y.w1 / y.y fused into
+// sc[slot..slot+1], the non-finite flag, the stop word as launch guard.
+S2Out solver_out(hmx_plan* A, double* sc, double* y, const double* w1, int yy, int slot, int* flag,
+                 const int* skip) {
   S2Out out{};
   out.skip = skip;
   out.y = y;
@@ -392,31 +391,23 @@ int apply_sc(hmx_plan* A, double* sc, cudaStream_t st, const double* xp, double*
     out.dots_out = sc + slot;
   }
   out.nonfinite = flag;
+  return out;
+}
+
+// y = A xp on stream st, fused dots into sc[slot..slot+1]
+int apply_sc(hmx_plan* A, double* sc, cudaStream_t st, const double* xp, double* y,
+             const double* w1, int yy, int slot, int* flag, const int* skip = nullptr) {
+  if ((w1 || yy) && A->dp.n_seg2 == 0)  // no local rows: the dots are zero
+    HMX_CUDA(cudaMemsetAsync(sc + slot, 0, 2 * sizeof(double), st));
   HMX_CUDA(launch_stage1(A->dp, xp, st, skip));
-  HMX_CUDA(launch_stage2(A->dp, xp, out, st, /*pdl=*/true));
+  HMX_CUDA(launch_stage2(A->dp, xp, solver_out(A, sc, y, w1, yy, slot, flag, skip), st, /*pdl=*/true));
   A->last_xp = xp;
   return HMX_OK;
 }
 
-// y = A xp on stream st, fused dots into sc[slot..slot+1]
 int apply(hmx_plan* A, const Workspace& w, cudaStream_t st, const double* xp, double* y,
           const double* w1, int yy, int slot, int* flag, const int* skip = nullptr) {
-  S2Out out{};
-  out.skip = skip;
-  out.y = y;
-  out.permute_out = 0;
-  out.w1 = w1;
-  out.yy = yy;
-  if (w1 || yy) {
-    out.seg_dots = A->d_seg_dots;
-    out.done = A->d_done;
-    out.dots_out = w.sc + slot;
-  }
-  out.nonfinite = flag;
-  HMX_CUDA(launch_stage1(A->dp, xp, st, skip));
-  HMX_CUDA(launch_stage2(A->dp, xp, out, st, /*pdl=*/true));
-  A->last_xp = xp;
-  return HMX_OK;
+  return apply_sc(A, w.sc, st, xp, y, w1, yy, slot, flag, skip);
 }
 
 // scalars, non-finite flags and the stop word in one pinned mirror
@@ -926,18 +917,7 @@ int dist_apply(hmx_comm* c, hmx_plan* A, double* sc, cudaStream_t st, double* fu
   int rc = allgather_rows(c, full, st);
   if (rc) return rc;
   if ((w1 || yy) && A->dp.n_seg2 == 0) HMX_CUDA(cudaMemsetAsync(sc + slot, 0, 2 * sizeof(double), st));
-  S2Out out{};
-  out.skip = skip;
-  out.y = y;
-  out.permute_out = 0;
-  out.w1 = w1;
-  out.yy = yy;
-  if (w1 || yy) {
-    out.seg_dots = A->d_seg_dots;
-    out.done = A->d_done;
-    out.dots_out = sc + slot;
-  }
-  out.nonfinite = flag;
+  const S2Out out = solver_out(A, sc, y, w1, yy, slot, flag, skip);
   HMX_CUDA(launch_stage1(A->dp, full, st, skip, nloc, -1));
   if (nloc > 0) HMX_CUDA(cudaStreamWaitEvent(st, c->ev_local, 0));
   HMX_CUDA(launch_stage2(A->dp, full, out, st, /*pdl=*/true));
