@@ -80,7 +80,8 @@ __device__ __forceinline__ void warp_argmax(double& v, int& idx) {
 }
 
 // One warp per task.  out_rank/out_status per task.
-__global__ void __launch_bounds__(32 * kAcaWarps) aca_kernel(const AcaTask* __restrict__ tasks, int ntask,
+__global__ void __launch_bounds__(32 * kAcaWarps) aca_kernel(const AcaTask* __restrict__ tasks,
+                                                             const int32_t* __restrict__ which, int ntask,
                                                              const double* __restrict__ pc,
                                                              const double* __restrict__ pa, double tol,
                                                              double* base, uint8_t* flags, int32_t* out_rank,
@@ -88,7 +89,8 @@ __global__ void __launch_bounds__(32 * kAcaWarps) aca_kernel(const AcaTask* __re
   __shared__ double sab[kAcaWarps][2 * kCap2 + 2];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   double* ab = sab[wid];
-  for (int t = blockIdx.x * kAcaWarps + wid; t < ntask; t += gridDim.x * kAcaWarps) {
+  for (int tt = blockIdx.x * kAcaWarps + wid; tt < ntask; tt += gridDim.x * kAcaWarps) {
+    const int t = which[tt];
     const AcaTask T = tasks[t];
     const int m = T.m, n = T.n, cap = T.cap;
     double* U = base + T.u_off;
@@ -244,6 +246,215 @@ __global__ void __launch_bounds__(32 * kAcaWarps) aca_kernel(const AcaTask* __re
   }
 }
 
+// ---- one CTA per large block (m + n >= kBigMN, cap <= kCtaCap): the same
+// arithmetic as aca_kernel (bitwise), with 256 threads on the residual row /
+// column and the dot-product chains fed through shared memory in chunks
+// loaded by the whole CTA (one lane streaming a 10^5-10^6-long chain from
+// global memory is bound by its own few loads in flight).
+constexpr int kCtaThreads = 256;
+constexpr int kCtaCap = 32;
+constexpr int kCtaArrays = 2 * kCtaCap;
+constexpr int kCtaChunk = 128;
+constexpr int64_t kBigMN = 8192;
+constexpr size_t kCtaSmem = (size_t)kCtaArrays * kCtaChunk * sizeof(double);
+
+__device__ __forceinline__ void cta_argmax(double& v, int& idx, double* sv, int* si) {
+  warp_argmax(v, idx);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  __syncthreads();
+  if (lane == 0) {
+    sv[w] = v;
+    si[w] = idx;
+  }
+  __syncthreads();
+  v = sv[0];
+  idx = si[0];
+  for (int q = 1; q < kCtaThreads / 32; ++q)
+    if (sv[q] > v || (sv[q] == v && si[q] < idx)) {
+      v = sv[q];
+      idx = si[q];
+    }
+}
+
+__device__ __forceinline__ double cta_max(double v, double* sv) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const double r2 = __shfl_xor_sync(0xffffffffu, v, o);
+    v = (v < r2) ? r2 : v;
+  }
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) sv[threadIdx.x >> 5] = v;
+  __syncthreads();
+  v = sv[0];
+  for (int q = 1; q < kCtaThreads / 32; ++q) v = (v < sv[q]) ? sv[q] : v;
+  return v;
+}
+
+__device__ __forceinline__ int cta_min(int v, int* si) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = min(v, __shfl_xor_sync(0xffffffffu, v, o));
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) si[threadIdx.x >> 5] = v;
+  __syncthreads();
+  v = si[0];
+  for (int q = 1; q < kCtaThreads / 32; ++q) v = min(v, si[q]);
+  return v;
+}
+
+__global__ void __launch_bounds__(kCtaThreads) aca_cta_kernel(const AcaTask* __restrict__ tasks,
+                                                              const int32_t* __restrict__ which,
+                                                              const double* __restrict__ pc,
+                                                              const double* __restrict__ pa, double tol,
+                                                              double* base, uint8_t* flags, int32_t* out_rank,
+                                                              int32_t* out_status) {
+  extern __shared__ double chunk[];  // [kCtaArrays][kCtaChunk]
+  __shared__ double sv[kCtaThreads / 32];
+  __shared__ int si[kCtaThreads / 32];
+  __shared__ double ab[kCtaArrays + 2];
+  const int tid = threadIdx.x;
+  const int t = which[blockIdx.x];
+  const AcaTask T = tasks[t];
+  const int m = T.m, n = T.n, cap = T.cap;
+  double* U = base + T.u_off;
+  double* Vt = base + T.vt_off;
+  uint8_t* rowu = flags + T.flag_off;
+  uint8_t* colu = rowu + m;
+  for (int i = tid; i < m + n; i += kCtaThreads) rowu[i] = 0;
+  __syncthreads();
+  double frob_sq = 0.0, max_seen = 0.0;
+  int rank = 0, i_star = 0, status = ACA_OK;
+  bool converged = false;
+  while (rank < T.budget && i_star >= 0) {
+    if (rank == cap) {
+      status = ACA_CAP;
+      break;
+    }
+    double* row = Vt + (int64_t)rank * n;
+    const double* urow = U + i_star;
+    double rmax = 0.0, best = -1.0;
+    int jbest = 0;
+    for (int j = tid; j < n; j += kCtaThreads) {
+      double v = kentry_dev(pc, pa, T.r0 + i_star, T.c0 + j);
+      if (rank) {
+        double s = 0.0;
+        for (int k = 0; k < rank; ++k) s = __dadd_rn(s, __dmul_rn(urow[(int64_t)k * m], Vt[(int64_t)k * n + j]));
+        v = __dsub_rn(v, s);
+      }
+      row[j] = v;
+      const double a = fabs(v);
+      rmax = (rmax < a) ? a : rmax;
+      const double mv = colu[j] ? 0.0 : a;
+      if (mv > best) {
+        best = mv;
+        jbest = j;
+      }
+    }
+    rmax = cta_max(rmax, sv);
+    cta_argmax(best, jbest, sv, si);
+    max_seen = (max_seen < rmax) ? rmax : max_seen;
+    const double pivot = colu[jbest] ? 0.0 : row[jbest];
+    __syncthreads();
+    if (tid == 0) rowu[i_star] = 1;
+    __syncthreads();
+    if (fabs(pivot) <= __dmul_rn(kEpsD, max_seen)) {
+      int first = m;
+      for (int i = tid; i < m; i += kCtaThreads)
+        if (!rowu[i]) {
+          first = i;
+          break;
+        }
+      first = cta_min(first, si);
+      i_star = first < m ? first : -1;
+      __syncthreads();
+      continue;
+    }
+    for (int j = tid; j < n; j += kCtaThreads) row[j] = __ddiv_rn(row[j], pivot);
+    for (int i = tid; i < m; i += kCtaThreads) {
+      double v = kentry_dev(pc, pa, T.r0 + i, T.c0 + jbest);
+      if (rank) {
+        const double* ui = U + i;
+        double s = 0.0;
+        for (int k = 0; k < rank; ++k) s = __dadd_rn(s, __dmul_rn(ui[(int64_t)k * m], Vt[(int64_t)k * n + jbest]));
+        v = __dsub_rn(v, s);
+      }
+      U[(int64_t)rank * m + i] = v;
+    }
+    __syncthreads();
+    if (tid == 0) colu[jbest] = 1;
+    // chains (the host's FMA chains, one thread each, same order as
+    // aca_kernel): array c is chain c's first operand -- 0: U col rank,
+    // 1: v (row), 2+k: U col k, 2+rank+k: Vt row k; the second operand is
+    // array 0 (chains 0 and 2+k) or array 1 (chains 1 and 2+rank+k)
+    const int nch = 2 + 2 * rank;
+    double s = 0.0;
+    const int maxlen = max(m, n);
+    for (int i0 = 0; i0 < maxlen; i0 += kCtaChunk) {
+      for (int idx = tid; idx < nch * kCtaChunk; idx += kCtaThreads) {
+        const int a = idx / kCtaChunk, e = idx - a * kCtaChunk, i = i0 + e;
+        const double* p;
+        int len;
+        if (a == 0) {
+          p = U + (int64_t)rank * m;
+          len = m;
+        } else if (a == 1) {
+          p = row;
+          len = n;
+        } else if (a < 2 + rank) {
+          p = U + (int64_t)(a - 2) * m;
+          len = m;
+        } else {
+          p = Vt + (int64_t)(a - 2 - rank) * n;
+          len = n;
+        }
+        chunk[idx] = i < len ? p[i] : 0.0;
+      }
+      __syncthreads();
+      if (tid < nch) {
+        const int len = (tid == 0 || (tid >= 2 && tid < 2 + rank)) ? m : n;
+        const double* A = chunk + tid * kCtaChunk;
+        const double* B = chunk + ((tid == 0 || (tid >= 2 && tid < 2 + rank)) ? 0 : kCtaChunk);
+        const int e1 = min(kCtaChunk, len - i0);
+        for (int e = 0; e < e1; ++e) s = fma(A[e], B[e], s);
+      }
+      __syncthreads();
+    }
+    if (tid < nch) ab[tid] = s;
+    __syncthreads();
+    const double u_norm = __dsqrt_rn(ab[0]), v_norm = __dsqrt_rn(ab[1]);
+    double cross = 0.0;
+    if (rank) {
+      double c2 = 0.0;
+      for (int k = 0; k < rank; ++k) c2 = fma(ab[2 + k], ab[2 + rank + k], c2);
+      cross = __dmul_rn(2.0, c2);
+    }
+    const double uv = __dmul_rn(u_norm, v_norm);
+    const double f = __dadd_rn(__dadd_rn(frob_sq, __dmul_rn(uv, uv)), cross);
+    frob_sq = (f < 0.0) ? 0.0 : f;
+    ++rank;
+    if (uv <= __dmul_rn(tol, __dsqrt_rn(frob_sq))) {
+      converged = true;
+      break;
+    }
+    double cb = -1.0;
+    int ib = 0;
+    for (int i = tid; i < m; i += kCtaThreads) {
+      const double cv = rowu[i] ? -1.0 : fabs(U[(int64_t)(rank - 1) * m + i]);
+      if (cv > cb) {
+        cb = cv;
+        ib = i;
+      }
+    }
+    cta_argmax(cb, ib, sv, si);
+    i_star = cb < 0.0 ? -1 : ib;
+    __syncthreads();
+  }
+  if (status == ACA_OK && !converged && rank < T.budget) status = ACA_HOST;
+  if (tid == 0) {
+    out_rank[t] = rank;
+    out_status[t] = status;
+  }
+}
+
 // Dense near-field blocks (and ACA dense fallbacks): compress.py:272-282.
 struct DenseTask {
   int64_t r0, c0, off;
@@ -299,20 +510,51 @@ int launch_tasks(const std::vector<T>& v, cudaStream_t st, F&& launch) {
 int run_aca(const std::vector<AcaTask>& tasks, const double* d_pc, const double* d_pa, double tol,
             double* base, uint8_t* d_flags, int32_t* d_rank, int32_t* d_status, cudaStream_t st, int sms) {
   if (tasks.empty()) return HMX_OK;
+  // large blocks: a CTA each, on a side stream, concurrently with the
+  // warp-per-block kernel over the rest
+  std::vector<int32_t> big, small;
+  for (size_t i = 0; i < tasks.size(); ++i) {
+    const AcaTask& T = tasks[i];
+    ((int64_t)T.m + T.n >= kBigMN && T.cap <= kCtaCap ? big : small).push_back((int32_t)i);
+  }
   AcaTask* d_tasks = nullptr;
-  HMX_CUDA(cudaMalloc(&d_tasks, tasks.size() * sizeof(AcaTask)));
-  cudaError_t e = cudaMemcpyAsync(d_tasks, tasks.data(), tasks.size() * sizeof(AcaTask),
-                                  cudaMemcpyHostToDevice, st);
-  if (e == cudaSuccess) {
-    const int64_t want = ((int64_t)tasks.size() + kAcaWarps - 1) / kAcaWarps;
+  int32_t* d_which = nullptr;
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev = nullptr;
+  cudaError_t e = cudaMalloc(&d_tasks, tasks.size() * sizeof(AcaTask));
+  if (e == cudaSuccess) e = cudaMalloc(&d_which, tasks.size() * sizeof(int32_t));
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(d_tasks, tasks.data(), tasks.size() * sizeof(AcaTask), cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess && !small.empty())
+    e = cudaMemcpyAsync(d_which, small.data(), small.size() * 4, cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess && !big.empty())
+    e = cudaMemcpyAsync(d_which + small.size(), big.data(), big.size() * 4, cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess && !big.empty()) {
+    e = cudaFuncSetAttribute(aca_cta_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kCtaSmem);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventRecord(ev, st);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(side, ev, 0);
+    if (e == cudaSuccess) {
+      aca_cta_kernel<<<(unsigned)big.size(), kCtaThreads, kCtaSmem, side>>>(
+          d_tasks, d_which + small.size(), d_pc, d_pa, tol, base, d_flags, d_rank, d_status);
+      e = cudaGetLastError();
+    }
+  }
+  if (e == cudaSuccess && !small.empty()) {
+    const int64_t want = ((int64_t)small.size() + kAcaWarps - 1) / kAcaWarps;
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)sms * 8));
-    aca_kernel<<<grid, 32 * kAcaWarps, 0, st>>>(d_tasks, (int)tasks.size(), d_pc, d_pa, tol, base, d_flags,
-                                                d_rank, d_status);
+    aca_kernel<<<grid, 32 * kAcaWarps, 0, st>>>(d_tasks, d_which, (int)small.size(), d_pc, d_pa, tol, base,
+                                                d_flags, d_rank, d_status);
     e = cudaGetLastError();
   }
   if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (e == cudaSuccess && side) e = cudaStreamSynchronize(side);
+  if (ev) cudaEventDestroy(ev);
+  if (side) cudaStreamDestroy(side);
+  cudaFree(d_which);
   cudaFree(d_tasks);
-  if (e != cudaSuccess) return cuda_fail(e, "aca_kernel");
+  if (e != cudaSuccess) return cuda_fail(e, "aca kernels");
   return HMX_OK;
 }
 

@@ -24,7 +24,8 @@ def _same(h_gpu, h_cpu):
 
 
 @pytest.mark.parametrize("level,leaf,tol", [(2, 32, 1e-4), (3, 32, 1e-4), (4, 64, 1e-5),
-                                            (3, 32, 1e-10), (4, 32, 1e-13)])
+                                            (3, 32, 1e-10), (4, 32, 1e-13),
+                                            (6, 64, 1e-5)])   # 5120 x 5120 blocks: CTA path
 def test_device_build_is_bitwise_the_host_build(hx, level, leaf, tol):
     mesh = hx.jittered_sphere_mesh(level, seed=42)
     _same(hx.build_hmatrix(mesh, aca_tol=tol, leaf_size=leaf, device=0),
