@@ -40,6 +40,7 @@ namespace hmx {
 namespace {
 
 constexpr int kCap1 = 24;   // ranks per block in pass-1 scratch (config 4: max rank 19)
+constexpr int kCap1Small = 16;  // ... when 24 would not fit in one batch (config 5: max rank 14)
 constexpr int kCap2 = 96;   // retry round for the blocks that exhaust kCap1
 constexpr int kAcaWarps = 8;             // warps per CTA
 constexpr double kPiD = 3.141592653589793;
@@ -673,7 +674,21 @@ int hmx_master_build(const hmx_build_desc* d, int device, hmx_master** out, int3
   // with their final rank as cap and compacted batch by batch.
   size_t free_b = 0, total_b = 0;
   cudaMemGetInfo(&free_b, &total_b);
-  const int64_t scratch_budget = std::max<int64_t>((int64_t)1 << 27, (int64_t)(free_b / 8) * 45 / 100);
+  const int64_t scratch_budget = std::max<int64_t>((int64_t)1 << 27, (int64_t)(free_b / 8) * 60 / 100);
+  // pass-1 columns per block: 24, or 16 when that keeps pass 1 in one batch
+  // (its scratch is then compacted instead of recomputed; blocks that need
+  // more are retried)
+  int64_t cap1 = kCap1;
+  {
+    int64_t need24 = 0, need16 = 0;
+    for (int64_t k : aca_blocks) {
+      const int64_t* t = d->table + 5 * k;
+      const int64_t mn = (t[1] - t[0]) + (t[3] - t[2]);
+      need24 += std::min<int64_t>(budget_of(k), kCap1) * mn;
+      need16 += std::min<int64_t>(budget_of(k), kCap1Small) * mn;
+    }
+    if (need24 > scratch_budget && need16 <= scratch_budget) cap1 = kCap1Small;
+  }
   std::vector<int32_t> h_rank(na, 0), h_status(na, 0);
   auto aca_round = [&](const std::vector<size_t>& idx_in, const std::function<int64_t(size_t)>& cap_of,
                        const std::function<int(const std::vector<AcaTask>&, const std::vector<int32_t>&,
@@ -776,7 +791,7 @@ int hmx_master_build(const hmx_build_desc* d, int device, hmx_master** out, int3
     std::vector<size_t> all(na);
     std::iota(all.begin(), all.end(), (size_t)0);
     const int rc = aca_round(
-        all, [&](size_t q) { return std::min<int64_t>(budget_of(aca_blocks[q]), kCap1); },
+        all, [&](size_t q) { return std::min<int64_t>(budget_of(aca_blocks[q]), cap1); },
         [&](const std::vector<AcaTask>& b, const std::vector<int32_t>& r, const std::vector<int32_t>& q,
             const std::vector<size_t>& qs, double* sc, bool only) -> int {
           for (size_t i = 0; i < b.size(); ++i) {
