@@ -122,8 +122,32 @@ def raise_nonfinite(plan, h) -> None:
     raise FloatingPointError("non-finite matvec result after summation")
 
 
+def _is_cuda_tensor(x) -> bool:
+    t = type(x)
+    return t.__module__.startswith("torch") and getattr(x, "is_cuda", False)
+
+
+def _matvec_cuda_tensor(sh, x):
+    """x a CUDA torch tensor: zero-copy in and out, y a new
+    float64 CUDA tensor in original order on x's device."""
+    import torch
+    if x.dim() != 1 or x.shape[0] != sh.n:
+        raise ValueError(f"vector shape {tuple(x.shape)} does not match matrix size {sh.n}")
+    x = x.to(torch.float64).contiguous()
+    plan = get_plan(sh, x.device.index)
+    y = torch.empty_like(x)
+    torch.cuda.current_stream(x.device).synchronize()  # x complete before the plan's stream reads it
+    rc = plan.matvec_device(x.data_ptr(), y.data_ptr(), permuted=False)  # synchronous
+    if rc == _gpu.HMX_ERR_NONFINITE:
+        raise_nonfinite(plan, sh.base)
+    return y
+
+
 def matvec(sh, x) -> np.ndarray:
-    """Multiply the prepared H-matrix by x on the GPU; FP64 result."""
+    """Multiply the prepared H-matrix by x on the GPU; FP64 result (a numpy
+    array, or a CUDA tensor when x is one)."""
+    if _is_cuda_tensor(x):
+        return _matvec_cuda_tensor(sh, x)
     src = _source(sh, x)
     plan = get_plan(sh)
     y, rc = plan.matvec(src)

@@ -303,3 +303,22 @@ def test_config4_solve_confirms_true_residual(hx, cfg4):
     assert abs(hx.true_residual(h, x, b) - rep.true_residual) <= 1e-12
     assert rep.converged == (rep.true_residual < 1e-8)
     assert 40 <= rep.iterations <= 80
+
+
+def test_cuda_tensor_inputs_are_zero_copy(hx, prob240):
+    """SURVEY s8b: torch CUDA tensors go in and come out without host copies;
+    the values are the host path's, bitwise."""
+    import torch
+    _, h, x = prob240
+    for scheme in ("m1-double", "m2-mixed"):
+        sh = hx.prepare_scheme(h, scheme)
+        xt = torch.from_numpy(x).cuda()
+        yt = hx.matvec(sh, xt)
+        assert yt.is_cuda and yt.dtype == torch.float64 and yt.shape == xt.shape
+        assert np.array_equal(yt.cpu().numpy(), hx.matvec(sh, x))
+    with pytest.raises(ValueError):
+        hx.matvec(sh, torch.zeros(h.n + 1, dtype=torch.float64, device="cuda"))
+    bad = torch.from_numpy(x).cuda()
+    bad[0] = float("inf")
+    with pytest.raises(FloatingPointError, match="block"):
+        hx.matvec(hx.prepare_scheme(h, "m1-double"), bad)
