@@ -222,7 +222,8 @@ def test_unusual_shapes(hx, orc, shape):
         pay = hx.LowRankBlockF64(rng.normal(size=(n, r)), rng.normal(size=(r, n)))
     h = _single_block(hx, pay, n, r > 0)
     x = rng.uniform(-1, 1, n)
-    for scheme in ("m1-double", "m1-single", "m2-mixed", "m3:c=1"):
+    for scheme in ("m1-double", "m1-single", "m1-mixed", "m2-double", "m2-single", "m2-mixed",
+                   "m3:c=1", "m3:c=-1"):
         sh = hx.prepare_scheme(h, scheme)
         assert rel(hx.matvec(sh, x), orc.matvec(sh, x)) <= tol_for(scheme) * 10
 
