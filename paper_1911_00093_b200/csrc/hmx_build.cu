@@ -568,6 +568,7 @@ extern "C" {
 
 int hmx_master_build(const hmx_build_desc* d, int device, hmx_master** out, int32_t* kinds, int64_t* ranks,
                      int64_t* offsets, int64_t* n_data, int64_t* fallbacks) {
+  NvtxRange nvtx("hmx_master_build");
   if (!d || !out || !kinds || !ranks || !offsets || !n_data || !d->pcent || !d->parea || !d->perm ||
       !d->table) {
     set_error("null argument");

@@ -129,6 +129,7 @@ void hmx_host_free(void* ptr) {
 
 int hmx::plan_create_impl(const hmx_matrix_desc* d, int device, const hmx_plan_options* opt,
                           hmx_plan* p, const DevSource* dsrc) {
+  NvtxRange nvtx("hmx plan: flatten + upload");
   const int64_t n = d->n, nb = d->n_blocks;
   if (n < 1 || n > INT32_MAX / 2 || nb < 1 || d->scheme < 0 || d->scheme > HMX_M3) {
     set_error("invalid matrix descriptor (n, n_blocks or scheme)");
@@ -910,6 +911,7 @@ int hmx_plan_create(const hmx_matrix_desc* d, int device, const hmx_plan_options
 }
 
 int hmx_matvec(hmx_plan* p, const double* x, double* y, int flags) {
+  NvtxRange nvtx("hmx_matvec");
   if (!p || !x || !y) {
     set_error("null argument");
     return HMX_ERR_ARG;

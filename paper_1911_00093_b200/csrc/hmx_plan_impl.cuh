@@ -3,6 +3,7 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <mutex>
@@ -22,6 +23,16 @@ int cuda_fail(cudaError_t e, const char* what);
     cudaError_t _e = (call);                             \
     if (_e != cudaSuccess) return cuda_fail(_e, #call);  \
   } while (0)
+
+// NVTX range for the host-side phases (plan build, matvec call, solve,
+// compression): free when no profiler is attached (nvtx3 is header-only and
+// resolves its tool at run time), visible on nsys / ncu timelines otherwise.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 // Restores the caller's current device on scope exit.
 struct DeviceGuard {

@@ -343,6 +343,7 @@ int hmx_master_create(const hmx_master_desc* d, int device, hmx_master** out) {
 
 int hmx_plan_create_prepared(hmx_master* m, int scheme, double split_factor, const hmx_plan_options* opt,
                              hmx_plan** out, hmx_prepare_info* info) {
+  NvtxRange nvtx("hmx_plan_create_prepared");
   if (!m || !out) {
     set_error("null argument");
     return HMX_ERR_ARG;

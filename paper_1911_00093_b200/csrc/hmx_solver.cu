@@ -543,6 +543,7 @@ int workspace_for(hmx_plan* p, Workspace& out, int grid) {
 extern "C" {
 
 int hmx_true_residual(hmx_plan* p64, const double* x, const double* b, double* out) {
+  NvtxRange nvtx("hmx_true_residual");
   if (!p64 || !x || !b || !out) {
     set_error("null argument");
     return HMX_ERR_ARG;
@@ -569,6 +570,7 @@ int hmx_true_residual(hmx_plan* p64, const double* x, const double* b, double* o
 
 int hmx_bicgstab(hmx_plan* A, hmx_plan* A64, const double* b, double tol, int max_iter, double* x,
                  double* history, hmx_solve_report* rep) {
+  NvtxRange nvtx("hmx_bicgstab");
   if (!A || !b || !x || !history || !rep) {
     set_error("null argument");
     return HMX_ERR_ARG;
@@ -1113,6 +1115,7 @@ int hmx_comm_create(const uint8_t id[128], int world, int rank, int device, cons
 
 int hmx_dist_matvec(hmx_plan* p, hmx_comm* c, const double* x_local, double* y_local, int* nonfinite,
                     uint64_t stream) {
+  NvtxRange nvtx("hmx_dist_matvec");
   if (!p || !c || (!x_local && c->r1 > c->r0) || (!y_local && c->r1 > c->r0)) {
     set_error("null argument");
     return HMX_ERR_ARG;
@@ -1133,6 +1136,7 @@ int hmx_dist_matvec(hmx_plan* p, hmx_comm* c, const double* x_local, double* y_l
 
 int hmx_bicgstab_dist(hmx_plan* A, hmx_plan* A64, hmx_comm* c, const double* b_local, double tol,
                       int max_iter, double* x_local, double* history, hmx_solve_report* rep) {
+  NvtxRange nvtx("hmx_bicgstab_dist");
   if (!A || !c || !history || !rep || ((!b_local || !x_local) && c->r1 > c->r0)) {
     set_error("null argument");
     return HMX_ERR_ARG;

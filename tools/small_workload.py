@@ -44,7 +44,7 @@ def main():
     D.bicgstab_gpu(comm, plan, None, b[perm], tol=1e-8)
     plan.close()
     comm.close()
-    print("sanitize workload done")
+    print("small workload done")
 
 
 if __name__ == "__main__":
