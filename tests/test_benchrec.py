@@ -68,3 +68,36 @@ def test_gpu_bench_drivers(hx):
     srec = B.run_solver_bench(cfg)
     assert all(r.iterations and r.true_residual is not None for r in srec)
     assert "achieved_GBps" in B.emit_report(recs)
+
+
+def test_cli_parser_and_no_gpu_error(capsys):
+    """`python -m paper_1911_00093_b200 bench ...` (the reference CLI's bench
+    subcommand on the GPU): flags parse like the reference's; without a GPU
+    it reports the error and exits 1 instead of computing on the CPU."""
+    from paper_1911_00093_b200 import _gpu
+    from paper_1911_00093_b200.__main__ import build_parser, main
+    args = build_parser().parse_args(["bench", "matvec", "--schemes", "m1-double,m2-mixed",
+                                      "--c-list", "1,3", "--refine", "1", "--device", "0"])
+    assert args.schemes == ("m1-double", "m2-mixed") and args.c_list == (1, 3)
+    try:
+        has_gpu = _gpu.device_count() > 0
+    except Exception:
+        has_gpu = False
+    if not has_gpu:
+        rc = main(["bench", "matvec", "--spheres", "1", "--refine", "0", "--reps", "2", "--sets", "2"])
+        assert rc == 1 and "error:" in capsys.readouterr().err
+
+
+@pytest.mark.gpu
+def test_cli_bench_writes_reference_schema(tmp_path, hx):
+    from paper_1911_00093_b200.__main__ import main
+    out = tmp_path / "r.json"
+    assert main(["bench", "matvec", "--spheres", "2", "--refine", "1", "--reps", "5", "--sets", "2",
+                 "--schemes", "m1-double,m2-mixed", "--c-list", "3", "--format", "json",
+                 "--out", str(out)]) == 0
+    recs = hx.read_report(out)
+    assert [r.scheme for r in recs] == ["m1-double", "m2-mixed", "m3:c=3"]
+    assert all(r.device == "cuda:0" and r.matvecs_per_s > 0 for r in recs)
+    assert main(["bench", "solve", "--spheres", "2", "--refine", "1", "--sets", "1",
+                 "--schemes", "m1-double", "--out", str(tmp_path / "s.csv")]) == 0
+    assert hx.read_report(tmp_path / "s.csv")[0].iterations > 0
