@@ -54,3 +54,16 @@ def test_device_built_masters_serve_device_plans(hx):
     for scheme in ("m1-double", "m2-mixed", "m3:c=2"):
         assert np.array_equal(hx.matvec(hx.prepare_scheme_device(hg, scheme), x),
                               hx.matvec(hx.prepare_scheme(hc, scheme), x))
+
+
+def test_device_build_matches_dense_assembly(hx):
+    """Reference tests/test_compress.py:122-126 on the GPU-compressed matrix:
+    relative Frobenius error against the dense kernel matrix <= 1e-6 at ACA
+    tolerance 1e-8; payload kinds follow admissibility."""
+    mesh = hx.build_sphere_mesh(hx.axis_centers(3, 3.0), refinement=1)
+    h = hx.build_hmatrix(mesh, aca_tol=1e-8, device=0)
+    a = hx.assemble_dense(mesh)
+    assert np.linalg.norm(a - hx.densify(h)) / np.linalg.norm(a) <= 1e-6
+    for blk, payload in h.items():
+        assert isinstance(payload, hx.LowRankBlockF64) == bool(blk.admissible) or \
+            isinstance(payload, hx.DenseBlockF64)
