@@ -101,3 +101,22 @@ def test_cli_bench_writes_reference_schema(tmp_path, hx):
     assert main(["bench", "solve", "--spheres", "2", "--refine", "1", "--sets", "1",
                  "--schemes", "m1-double", "--out", str(tmp_path / "s.csv")]) == 0
     assert hx.read_report(tmp_path / "s.csv")[0].iterations > 0
+
+
+def test_cli_info_on_host(tmp_path, capsys):
+    """`info` builds on the host and writes the reference's interchange files."""
+    from paper_1911_00093_b200.__main__ import main
+    part, mesh = tmp_path / "p.txt", tmp_path / "m.txt"
+    assert main(["info", "--spheres", "1", "--refine", "1", "--json",
+                 "--dump-partition", str(part), "--export-mesh", str(mesh)]) == 0
+    out = capsys.readouterr().out
+    assert '"n": 80' in out and part.exists() and mesh.exists()
+
+
+@pytest.mark.gpu
+def test_cli_solve_and_gpu_build(capsys):
+    from paper_1911_00093_b200.__main__ import main
+    assert main(["solve", "--spheres", "2", "--refine", "1", "--scheme", "m2-mixed", "--json",
+                 "--gpu-build"]) == 0
+    assert '"converged": true' in capsys.readouterr().out
+    assert main(["info", "--spheres", "2", "--refine", "1", "--gpu-build"]) == 0
