@@ -1,4 +1,4 @@
-"""The multi-GPU mode's host logic on CPU with gloo, world_size 2: byte-
+"""The multi-GPU mode's host logic on CPU with gloo, world_size 2 and 3: byte-
 balanced row partition, padded allgather of the iterate (the one collective
 per matvec), allreduced dots, and the distributed BiCG-STAB control flow.
 The local product is a CPU stand-in (the oracle restricted to the rank's
@@ -21,7 +21,7 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, out_dir):
+def _worker(rank, world, port, out_dir, shift=0):
     sys.path.insert(0, str(ROOT))
     sys.path.insert(0, str(ROOT / "tests"))
     import torch
@@ -39,7 +39,9 @@ def _worker(rank, world, port, out_dir):
     h = hmatrix_from_fixture(arr)
     perm = np.asarray(h.permutation)
     table = h.partition.table
-    slices = D.RowSlices(D.partition_rows(table, h.packed.kinds, h.packed.ranks, h.n, world))
+    cuts = D.partition_rows(table, h.packed.kinds, h.packed.ranks, h.n, world)
+    cuts[1] += shift   # uneven slices whose cut straddles blocks
+    slices = D.RowSlices(cuts)
     a, b = slices.span(rank)
 
     def stand_in(sh):
@@ -100,27 +102,31 @@ def test_row_restricted_build_matches_full(hx, orc):
     assert sh.packed.kind.tolist().count(2) == int((~meet).sum())
 
 
-def test_gloo_world2_matvec_and_bicgstab(tmp_path, hx, orc):
+@pytest.mark.parametrize("world,shift", [(2, 0), (3, 7)])
+def test_gloo_world2_matvec_and_bicgstab(tmp_path, hx, orc, world, shift):
+    """world 2 with the byte-balanced cuts; world 3 with a cut moved 7 rows
+    into a leaf (uneven, padded slices; blocks straddling the cut)."""
     import torch.multiprocessing as mp
 
     from golden_util import hmatrix_from_fixture, load
     port = _free_port()
-    mp.start_processes(_worker, args=(2, port, str(tmp_path)), nprocs=2, join=True,
+    mp.start_processes(_worker, args=(world, port, str(tmp_path), shift), nprocs=world, join=True,
                        start_method="spawn")
-    r0, r1 = (np.load(tmp_path / f"r{k}.npz") for k in (0, 1))
+    rs = [np.load(tmp_path / f"r{k}.npz") for k in range(world)]
     arr, _ = load("ref240_aca4")
     h = hmatrix_from_fixture(arr)
     perm = np.asarray(h.permutation)
     sh = hx.prepare_scheme(h, "m2-mixed")
-    y_full = np.concatenate([r0["y"], r1["y"]])
+    y_full = np.concatenate([r["y"] for r in rs])
     assert np.array_equal(y_full, orc.matvec(sh, arr["x"])[perm])
     # every rank took the same decisions
-    assert int(r0["it"]) == int(r1["it"]) and bool(r0["conv"]) == bool(r1["conv"])
-    assert np.array_equal(r0["hist"], r1["hist"])
+    for r in rs[1:]:
+        assert int(r["it"]) == int(rs[0]["it"]) and bool(r["conv"]) == bool(rs[0]["conv"])
+        assert np.array_equal(r["hist"], rs[0]["hist"])
     # and they match the single-process solve up to the dots' summation order
     xo, ref = orc.bicgstab(sh, hx.prepare_scheme(h, "m1-double"), arr["b"], tol=1e-8)
-    assert abs(int(r0["it"]) - ref["iterations"]) <= 1
-    assert bool(r0["conv"]) == ref["converged"]
+    assert abs(int(rs[0]["it"]) - ref["iterations"]) <= 1
+    assert bool(rs[0]["conv"]) == ref["converged"]
     x = np.empty(h.n)
-    x[perm] = np.concatenate([r0["x"], r1["x"]])
+    x[perm] = np.concatenate([r["x"] for r in rs])
     assert np.linalg.norm(x - xo) / np.linalg.norm(xo) <= 1e-6
