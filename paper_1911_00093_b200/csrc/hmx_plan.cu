@@ -823,7 +823,12 @@ int hmx::plan_create_impl(const hmx_matrix_desc* d, int device, const hmx_plan_o
       b64 += (int64_t)a.W64 * a.R * 8;
       b32 += (int64_t)a.W32 * a.R * 4;
     }
-    dp.s2_deep = (f32mode2 == F32_ALL64 && b64 > 0 && b64 >= b32) ? 1 : 0;
+    // ... and only with several waves of row segments (4 per SM): small
+    // plans prefer more resident CTAs (A/B: config 2 m3:c=3 65.0 -> 59.9 us,
+    // m1-double 51.8 -> 51.0 us; config 3 neutral; config 4 keeps the deep
+    // pipeline, -1.1 % / -2.4 % for m1-/m2-double)
+    const bool many = nseg2 >= (int64_t)4 * 4 * sms;
+    dp.s2_deep = (f32mode2 == F32_ALL64 && b64 > 0 && b64 >= b32 && many && !std::getenv("HMX_S2_NO_DEEP")) ? 1 : 0;
   }
   dp.f32mode2 = f32mode2;
   dp.zepi = pipe == P_M1D ? Z_NONE : (pipe == P_M1S || pipe == P_M1M) ? Z_ROUND32 : Z_SCALE;
