@@ -44,6 +44,7 @@ def _geometry_parser() -> argparse.ArgumentParser:
 
 
 def build_parser() -> argparse.ArgumentParser:
+    """Argument parser of the `info` / `solve` / `bench` subcommands (reference cli.py:160-210)."""
     geo = _geometry_parser()
     ap = argparse.ArgumentParser(prog="python -m paper_1911_00093_b200",
                                  description="B200 H-matrix matvec / BiCG-STAB (the reference "
@@ -152,6 +153,7 @@ def _cmd_bench(args) -> int:
 
 
 def main(argv=None) -> int:
+    """CLI entry point; returns the process exit code (reference cli.py:212-226: 1 on a reported error)."""
     import numpy as np
 
     args = build_parser().parse_args(argv)

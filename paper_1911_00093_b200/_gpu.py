@@ -27,6 +27,7 @@ _i32p = ctypes.POINTER(ctypes.c_int32)
 
 
 class MatrixDesc(ctypes.Structure):
+    """ctypes mirror of `hmx_matrix_desc` (include/hmx_gpu.h:72-93): the packed H-matrix handed to `hmx_plan_create`."""
     _fields_ = [("n", ctypes.c_int64), ("n_blocks", ctypes.c_int64),
                 ("scheme", ctypes.c_int32), ("a32", ctypes.c_int32), ("hi32", ctypes.c_int32),
                 ("reserved", ctypes.c_int32),
@@ -38,6 +39,7 @@ class MatrixDesc(ctypes.Structure):
 
 
 class PlanOptions(ctypes.Structure):
+    """ctypes mirror of `hmx_plan_options` (include/hmx_gpu.h:97-102)."""
     _fields_ = [("row_begin", ctypes.c_int64), ("row_end", ctypes.c_int64),
                 ("s1_chunk_bytes", ctypes.c_int32), ("flags", ctypes.c_int32)]
 
@@ -46,6 +48,7 @@ HMX_PLAN_LOCAL_FIRST = 1
 
 
 class PlanInfo(ctypes.Structure):
+    """ctypes mirror of `hmx_plan_info` (include/hmx_gpu.h:112-121): bytes streamed per matvec and the launch shape."""
     _fields_ = [("n", ctypes.c_int64), ("payload_bytes", ctypes.c_int64),
                 ("device_bytes", ctypes.c_int64), ("s1_segments", ctypes.c_int64),
                 ("s1_tasks", ctypes.c_int64), ("s2_segments", ctypes.c_int64),
@@ -56,6 +59,7 @@ class PlanInfo(ctypes.Structure):
 
 
 class SolveReport(ctypes.Structure):
+    """ctypes mirror of `hmx_solve_report` (include/hmx_gpu.h:156-168)."""
     _fields_ = [("converged", ctypes.c_int32), ("iterations", ctypes.c_int32),
                 ("has_true_residual", ctypes.c_int32), ("breakdown", ctypes.c_int32),
                 ("true_residual", ctypes.c_double), ("breakdown_value", ctypes.c_double),
@@ -65,6 +69,7 @@ class SolveReport(ctypes.Structure):
 
 
 class MasterDesc(ctypes.Structure):
+    """ctypes mirror of `hmx_master_desc` (include/hmx_gpu.h:130-140): the FP64 master copy kept on the device."""
     _fields_ = [("n", ctypes.c_int64), ("n_blocks", ctypes.c_int64),
                 ("perm", _i64p), ("table", _i64p), ("kind", _i32p), ("offset", _i64p),
                 ("rank", _i64p), ("data", ctypes.POINTER(ctypes.c_double)),
@@ -72,6 +77,7 @@ class MasterDesc(ctypes.Structure):
 
 
 class BuildDesc(ctypes.Structure):
+    """ctypes mirror of `hmx_build_desc` (include/hmx_gpu.h:217-228): inputs of the on-device ACA compression."""
     _fields_ = [("n", ctypes.c_int64), ("n_blocks", ctypes.c_int64),
                 ("pcent", ctypes.POINTER(ctypes.c_double)), ("parea", ctypes.POINTER(ctypes.c_double)),
                 ("perm", _i64p), ("table", _i64p), ("tol", ctypes.c_double),
@@ -79,6 +85,7 @@ class BuildDesc(ctypes.Structure):
 
 
 class PrepareInfo(ctypes.Structure):
+    """ctypes mirror of `hmx_prepare_info` (include/hmx_gpu.h:145-150)."""
     _fields_ = [("payload_bytes", ctypes.c_int64), ("underflow_count", ctypes.c_int64),
                 ("overflow_block", ctypes.c_int64), ("fp32_ranks", ctypes.c_int64)]
 
@@ -159,11 +166,13 @@ def load_library(build: bool = False):
 
 
 def last_error() -> str:
+    """Message of the last failed `hmx_*` call on this thread."""
     msg = load_library().hmx_last_error()
     return msg.decode() if msg else ""
 
 
 def check(rc: int, what: str):
+    """Raise the Python exception matching an `hmx_status` code (include/hmx_gpu.h:38-46); no-op on HMX_OK."""
     if rc == HMX_OK:
         return
     msg = f"{what} failed: {last_error()}"
@@ -175,6 +184,7 @@ def check(rc: int, what: str):
 
 
 def device_count() -> int:
+    """Number of CUDA devices the native library sees."""
     lib = load_library()
     c = ctypes.c_int(0)
     lib.hmx_device_count(ctypes.byref(c))

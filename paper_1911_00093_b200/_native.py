@@ -46,6 +46,7 @@ def _run(cmd):
 
 
 def build_host(force: bool = False) -> Path:
+    """Compile the host C++ library (cluster tree, partition, ACA) in-tree with g++."""
     src = CSRC / "hbuild.cpp"
     if not force and HOST_LIB.exists() and HOST_LIB.stat().st_mtime >= src.stat().st_mtime:
         return HOST_LIB
@@ -58,10 +59,12 @@ def build_host(force: bool = False) -> Path:
 
 
 def gpu_sources():
+    """CUDA sources of the GPU library, in link order."""
     return [CSRC / s for s in GPU_SOURCES]
 
 
 def build_gpu(force: bool = False, verbose: bool = False) -> Path:
+    """Compile the GPU library in-tree for sm_100a with nvcc (`-gencode arch=compute_100a,code=sm_100a -lineinfo`)."""
     srcs = gpu_sources()
     deps = srcs + list(CSRC.glob("*.cuh")) + [INCLUDE_DIR / "hmx_gpu.h"]
     if (not force and GPU_LIB.exists()
@@ -98,6 +101,7 @@ c_i8p = ctypes.POINTER(ctypes.c_int8)
 
 
 class HbNode(ctypes.Structure):
+    """ctypes mirror of one cluster-tree node of the host library (index range, bounding box, children)."""
     _fields_ = [("start", ctypes.c_int64), ("end", ctypes.c_int64),
                 ("bmin", ctypes.c_double * 3), ("bmax", ctypes.c_double * 3),
                 ("left", ctypes.c_int64), ("right", ctypes.c_int64)]
@@ -153,6 +157,7 @@ def ptr(arr, ctype):
 
 
 def host_threads() -> int:
+    """Thread count of the host builder (HMX_HOST_THREADS, else the CPU count)."""
     env = os.environ.get("HMX_HOST_THREADS")
     if env:
         return max(1, int(env))

@@ -43,6 +43,7 @@ DENSIFY_CAP = 4096       # reference compress.py:36
 
 @dataclass
 class DenseBlockF64:
+    """A dense (inadmissible) block stored in FP64 (reference compress.py:42-50)."""
     values: np.ndarray
 
     def __post_init__(self):
@@ -72,6 +73,7 @@ class LowRankBlockF64:
 
 @dataclass
 class BuildReport:
+    """Statistics of one H-matrix build (reference compress.py:211-233)."""
     n: int
     dense_blocks: int
     lowrank_blocks: int

@@ -99,6 +99,7 @@ def partition_rows(table: np.ndarray, kinds: np.ndarray, ranks: np.ndarray, n: i
 
 @dataclass
 class RowSlices:
+    """Row cuts of the permuted index space, one contiguous slice per rank (`cuts[r]:cuts[r+1]`)."""
     cuts: list
 
     @property

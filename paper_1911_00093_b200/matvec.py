@@ -52,6 +52,7 @@ class SourceVector:
 
 
 def default_device() -> int:
+    """CUDA device the matvec path uses (HMX_DEVICE, default 0)."""
     return int(os.environ.get("HMX_DEVICE", "0"))
 
 
@@ -113,6 +114,7 @@ def _source(sh, x) -> np.ndarray:
 
 
 def raise_nonfinite(plan, h) -> None:
+    """Raise the reference's FloatingPointError naming the first block with a non-finite contribution (reference matvec.py:123-135)."""
     k = plan.nonfinite_block()
     if k >= 0:
         r = _table(h)[k]

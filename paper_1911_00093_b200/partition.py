@@ -55,12 +55,14 @@ class ClusterNode:
 
 
 def node_distance(a: ClusterNode, b: ClusterNode) -> float:
+    """Euclidean distance between two cluster bounding boxes (reference partition.py:56-60)."""
     gap = np.maximum(0.0, np.maximum(a.bbox_min - b.bbox_max, b.bbox_min - a.bbox_max))
     return float(np.linalg.norm(gap))
 
 
 @dataclass
 class ClusterTree:
+    """Cluster tree over the panels and its permutation (reference partition.py:63-72)."""
     root: ClusterNode
     permutation: np.ndarray  # permuted index -> original panel index
     leaf_size: int

@@ -84,6 +84,7 @@ def _as_scheme(scheme) -> PrecisionScheme:
 
 @dataclass
 class ScaledLowRank:
+    """Low-rank factors with per-column scales (reference precision.py:107-119)."""
     u_unit: np.ndarray
     vt_unit: np.ndarray
     diag: np.ndarray
@@ -124,17 +125,20 @@ def split_indices(diag, c: int):
 
 @dataclass(slots=True)
 class DensePayload:
+    """Dense block payload of a prepared scheme (reference precision.py:169-172)."""
     values: np.ndarray
 
 
 @dataclass(slots=True)
 class FactorPayload:
+    """Low-rank factors stored in one dtype (reference precision.py:174-180)."""
     u: np.ndarray
     vt: np.ndarray
 
 
 @dataclass(slots=True)
 class ScaledPayload:
+    """Scaled low-rank factors (reference precision.py:182-189)."""
     u: np.ndarray
     vt: np.ndarray
     diag: np.ndarray
@@ -142,6 +146,7 @@ class ScaledPayload:
 
 @dataclass(slots=True)
 class SplitLowRank:
+    """Method 3 block: leading `c` ranks in FP64, the rest in FP32 (reference precision.py:191-207)."""
     idx_fp64: np.ndarray
     idx_fp32: np.ndarray
     u_hi: np.ndarray

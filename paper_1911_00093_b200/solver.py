@@ -25,6 +25,7 @@ __all__ = ["SolverConfig", "SolverReport", "bicgstab", "true_residual"]
 
 @dataclass
 class SolverConfig:
+    """BiCG-STAB stopping rule and iteration cap (reference solver.py:30-43)."""
     tol: float = 1e-6
     max_iter: int = 1000
     threads: int = 1
@@ -40,6 +41,7 @@ class SolverConfig:
 
 @dataclass
 class SolverReport:
+    """Outcome of one solve (reference solver.py:45-54) plus device timings."""
     scheme: str
     converged: bool
     iterations: int
