@@ -1,0 +1,65 @@
+"""The `bench.py` JSON-line contract, run as the driver runs it (a
+subprocess, one line on stdout): the reference arm on the host cores (CPU),
+and our arm on the GPU at BASELINE config 2 with every key the driver and the
+judge read (roofline, e2e with the copied bytes, clocks, gpu_launches)."""
+
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+from conftest import ROOT
+
+BASE_KEYS = {"metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step",
+             "higher_is_better", "scaling", "vs_baseline", "dtype", "data", "config", "e2e"}
+
+
+def _run(*args, timeout=600):
+    env = dict(os.environ, HMX_DEVICE="0")
+    p = subprocess.run([sys.executable, "bench.py", *args], cwd=ROOT, env=env, timeout=timeout,
+                       capture_output=True, text=True)
+    assert p.returncode == 0, p.stderr[-2000:]
+    lines = [ln for ln in p.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, p.stdout
+    return json.loads(lines[0])
+
+
+def test_reference_arm_line():
+    d = _run("--impl", "reference", "--config", "2", "--steps", "3", "--warmup", "3")
+    assert BASE_KEYS <= d.keys()
+    assert d["impl"] == "reference" and d["unit"] == "matvec/s" and d["higher_is_better"]
+    assert d["steps"] == 3 and d["warmup"] == 3 and d["value"] > 0
+    assert d["ms_per_step"] == pytest.approx(1e3 / d["value"])
+    cb = d["cpu_baseline"]
+    assert cb["value"] == d["value"] and cb["kind"] == "port" and cb["cores"] >= 1 and cb["sample"]
+    assert d["e2e"] == {"value": d["value"], "unit": "matvec/s", "h2d_bytes_per_step": 0,
+                        "d2h_bytes_per_step": 0}
+    assert d["config"]["n"] == 20480
+
+
+def test_warmup_floor_is_three():
+    d = _run("--impl", "reference", "--config", "2", "--steps", "3", "--warmup", "1")
+    assert d["warmup"] == 3
+
+
+@pytest.mark.gpu
+def test_our_arm_line():
+    d = _run("--config", "2", "--steps", "20", "--warmup", "3", "--variants", "m1-double",
+             "--no-solve", "--no-cpu-baseline")
+    assert BASE_KEYS <= d.keys() and "impl" not in d
+    n = d["config"]["n"]
+    assert n == 20480 and d["n_gpus"] == 1 and d["steps"] == 20 and d["dtype"] == "f64"
+    assert d["value"] == pytest.approx(1e3 / d["ms_per_step"])
+    rf = d["roofline"]
+    assert rf["bound"] == "hbm" and rf["unit"] == "GB/s" and rf["peak"] > 1000
+    assert rf["frac"] == pytest.approx(rf["achieved"] / rf["peak"])
+    assert 0.05 < rf["frac"] < 1.3
+    e = d["e2e"]
+    assert e["h2d_bytes_per_step"] == 8 * n and e["d2h_bytes_per_step"] == 8 * n
+    assert 0 < e["value"] <= d["value"] * 1.05  # host copies inside the timed region
+    assert d["gpu_launches"] == 2 * 20
+    assert {"sm_mhz", "sm_max_mhz", "reasons"} <= d["clocks"].keys()
+    v = d["variants"]["m1-double"]
+    assert v["stage1_ms"] > 0 and v["stage2_ms"] > 0
