@@ -464,7 +464,11 @@ def bench_main(args, build_workload, workload_name, metric):
             "cpu_baseline": None,
             "e2e": {"value": 1e3 / entry["e2e_ms"], "unit": "matvec/s",
                     "h2d_bytes_per_step": 8 * int(mesh.n), "d2h_bytes_per_step": 8 * int(mesh.n)},
-            "gpu_launches": 2 * args.steps, "clocks": clocks, "variants": results,
+            # our kernels per step: stage 1 (at world > 1 two launches: the
+            # local-first segments on the side stream, the rest after the
+            # allgather) and stage 2; NCCL's own kernels not counted
+            "gpu_launches": (3 if world > 1 else 2) * args.steps, "clocks": clocks,
+            "variants": results,
             "note": "each step = one NCCL allgather of the iterate (grouped send/recv into the "
                     "full vector) + the local two-stage product; solves: hmx_bicgstab_dist; "
                     "cpu_baseline is reported by the N=1 run",
