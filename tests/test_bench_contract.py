@@ -93,3 +93,13 @@ def test_distributed_arm_line_one_rank():
     assert s["converged"] and s["true_residual"] < 1e-8
     s = d["variants"]["m2-mixed"]["solve"]
     assert s["iterations"] > 0 and s["true_residual"] < 1e-7
+
+
+def test_reference_arm_other_ranks_exit_quietly():
+    """Under torchrun (N > 1) only rank 0 runs and prints the reference arm."""
+    env = dict(os.environ, RANK="1", WORLD_SIZE="2", LOCAL_RANK="1")
+    p = subprocess.run([sys.executable, "bench.py", "--impl", "reference", "--gpus", "2",
+                        "--config", "2", "--steps", "3", "--warmup", "3"], cwd=ROOT, env=env,
+                       timeout=300, capture_output=True, text=True)
+    assert p.returncode == 0, p.stderr[-2000:]
+    assert not [ln for ln in p.stdout.splitlines() if ln.startswith("{")]
