@@ -26,9 +26,10 @@ namespace hmx {
 enum Out : int { OUT_Y = 0, OUT_Z = 1 };
 
 // Shared-memory slot of an FP32-accumulated column: the FP32 source value in
-// the low word, 1 in the high word on the first column of an item.
-__device__ __forceinline__ double acc32_slot(float g, bool start) {
-  return __hiloint2double(start ? 1 : 0, __float_as_int(g));
+// the low word, the column's tree code (OB_*, hmx_internal.cuh) in the high
+// word (stage 1: OB_ITEM_CHAIN on a segment's first column, else 0).
+__device__ __forceinline__ double acc32_slot(float g, int code) {
+  return __hiloint2double(code, __float_as_int(g));
 }
 
 // 8-byte asynchronous global -> shared copies (the x / z segments of a tile)
@@ -44,11 +45,13 @@ __device__ __forceinline__ void cp_async_wait_all() {
 // Stage a tile [tc0, tc0+tw) of one part's source vector g (x segments and z
 // vectors, in item order) into shared memory with cp.async; FP32-accumulated
 // columns are then rewritten as acc32_slot and FP32-shadow columns rounded
-// (fl: scratch flags, bit 0 item start, bit 1 FP32 item).  A single run
+// (fl: scratch flags, the column's OB_* code and kFlAcc32).  RUN_OBL items
+// are stored in SGEMV lane order, so column k reads source obl_col(k).  A single run
 // (every stage-1 segment) is a contiguous copy.  Otherwise the runs are first
 // expanded into a per-column source index in shared memory, so every
 // column's copy is independent (no dependent run lookups).
 constexpr int32_t kTagZ = 1 << 30, kTagRound = 1 << 29, kIdxMask = kTagRound - 1;
+constexpr uint8_t kFlAcc32 = 16;  // fl: low 4 bits the OB_* code, bit 4 an FP32-accumulated column
 template <bool FLAGS, int NT, int WMAX>
 __device__ __forceinline__ void gather_g(const DevPlan& P, const Run* __restrict__ runs, int nrun,
                                          int tc0, int tw, const double* __restrict__ x,
@@ -56,13 +59,18 @@ __device__ __forceinline__ void gather_g(const DevPlan& P, const Run* __restrict
   constexpr int PER = WMAX / NT;  // columns per thread
   if (nrun == 1) {
     const Run r = runs[0];
-    const double* src = ((r.flags & RUN_Z) ? P.z : x) + r.src + (tc0 - r.col0);
+    const double* src = ((r.flags & RUN_Z) ? P.z : x) + r.src;
     const bool rnd = (r.flags & RUN_ROUND) != 0;
     const bool f32 = FLAGS && (r.flags & RUN_ACC32);
+    const bool obl = FLAGS && (r.flags & RUN_OBL);
+    int code[PER];
 #pragma unroll
     for (int u = 0; u < PER; ++u) {
       const int c = threadIdx.x + u * NT;
-      if (c < tw) cp_async8(gs + c, src + c);
+      const int k = tc0 + c - r.col0;
+      code[u] = k == 0 ? OB_ITEM_CHAIN : OB_NONE;
+      const int sc = obl ? obl_col(r.width, k, &code[u]) : k;
+      if (c < tw) cp_async8(gs + c, src + sc);
     }
     cp_async_wait_all();
     if (rnd || f32) {
@@ -71,7 +79,7 @@ __device__ __forceinline__ void gather_g(const DevPlan& P, const Run* __restrict
         const int c = threadIdx.x + u * NT;
         if (c < tw) {
           const double g = gs[c];
-          gs[c] = f32 ? acc32_slot((float)g, tc0 + c == r.col0) : (double)(float)g;
+          gs[c] = f32 ? acc32_slot((float)g, code[u]) : (double)(float)g;
         }
       }
     }
@@ -82,10 +90,13 @@ __device__ __forceinline__ void gather_g(const DevPlan& P, const Run* __restrict
     const Run r = runs[j];
     const int lo = max(r.col0, tc0), hi = min(r.col0 + r.width, tc0 + tw);
     const int32_t tag = ((r.flags & RUN_Z) ? kTagZ : 0) | ((r.flags & RUN_ROUND) ? kTagRound : 0);
-    const uint8_t f32 = (r.flags & RUN_ACC32) ? 2 : 0;
+    const uint8_t f32 = (r.flags & RUN_ACC32) ? kFlAcc32 : 0;
+    const bool obl = FLAGS && (r.flags & RUN_OBL);
     for (int col = lo; col < hi; ++col) {
-      sidx[col - tc0] = (r.src + (col - r.col0)) | tag;
-      if constexpr (FLAGS) fl[col - tc0] = (uint8_t)((col == r.col0 ? 1 : 0) | f32);
+      int code = col == r.col0 ? OB_ITEM_CHAIN : OB_NONE;
+      const int sc = obl ? obl_col(r.width, col - r.col0, &code) : col - r.col0;
+      sidx[col - tc0] = (r.src + sc) | tag;
+      if constexpr (FLAGS) fl[col - tc0] = (uint8_t)(code | f32);
     }
   }
   __syncthreads();
@@ -103,7 +114,7 @@ __device__ __forceinline__ void gather_g(const DevPlan& P, const Run* __restrict
     const int c = threadIdx.x + u * NT;
     if (c < tw) {
       const uint8_t f = FLAGS ? fl[c] : 0;
-      if (FLAGS && (f & 2)) gs[c] = acc32_slot((float)gs[c], f & 1);
+      if (FLAGS && (f & kFlAcc32)) gs[c] = acc32_slot((float)gs[c], f & 15);
       else if (id[u] & kTagRound) gs[c] = (double)(float)gs[c];
     }
   }
@@ -130,6 +141,9 @@ __global__ void __launch_bounds__(NT, DEEP ? 3 : (OUT == OUT_Y && F32MODE != F32
   __shared__ int32_t sidx[OUT == OUT_Z ? 1 : kSegWMax];
   __shared__ double red64[2 * NT];
   __shared__ double red32[4 * NT];
+  // pending FP32 lane-tree values of stage 2's FP32-accumulated items
+  // (consume32): dynamic shared memory, 3 x NT float4 (kTreeSmem)
+  extern __shared__ float4 tstate[];
   __shared__ double wred[2][NT / 32];
   __shared__ unsigned ticket;
 
@@ -245,18 +259,91 @@ __global__ void __launch_bounds__(NT, DEEP ? 3 : (OUT == OUT_Y && F32MODE != F32
     b[2] = fma((double)v.z, g, b[2]);
     b[3] = fma((double)v.w, g, b[3]);
   };
-  // FP32 chain per (row, item): the gathered slot holds the FP32 source in
-  // its low word and "first column of an item" in its high word
+  // FP32-accumulated items (stage 2): per row, the SGEMV lane tree of
+  // hmx_internal.cuh evaluated in storage order.  b32 is the running FMA
+  // chain; the tree's pending values live in shared memory (touched only at
+  // sub-chain starts, so they cost no registers in the streaming loop):
+  // TS_P a finished A_j waiting for B_j, TS_01 = l0 (+ l1), TS_2 = l2.  They
+  // are zero whenever tmode == 0 (0: plain chain, 1: lane tree open, 2: tail
+  // chain after the tree).
+  enum { TS_P = 0, TS_01 = 1, TS_2 = 2 };
+  int tmode = 0;
+  auto tload = [&](int k) { return tstate[k * NT + tid]; };
+  auto tstore = [&](int k, float a, float b_, float c, float d) { tstate[k * NT + tid] = make_float4(a, b_, c, d); };
+  // close the open tree: widen its value once and add it in FP64
+  auto flush32 = [&]() {
+    float v[4] = {b32[0], b32[1], b32[2], b32[3]};
+    if (OUT == OUT_Y && tmode != 0) {
+      const float4 s01 = tload(TS_01);
+      if (tmode == 1) {
+        const float4 pp = tload(TS_P), s2 = tload(TS_2);
+        v[0] = s01.x + (s2.x + (pp.x + b32[0]));
+        v[1] = s01.y + (s2.y + (pp.y + b32[1]));
+        v[2] = s01.z + (s2.z + (pp.z + b32[2]));
+        v[3] = s01.w + (s2.w + (pp.w + b32[3]));
+        tstore(TS_P, 0.f, 0.f, 0.f, 0.f);
+        tstore(TS_2, 0.f, 0.f, 0.f, 0.f);
+      } else {
+        v[0] = s01.x + b32[0];
+        v[1] = s01.y + b32[1];
+        v[2] = s01.z + b32[2];
+        v[3] = s01.w + b32[3];
+      }
+      tstore(TS_01, 0.f, 0.f, 0.f, 0.f);
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      b[i] += (double)v[i];
+      b32[i] = 0.f;
+    }
+    tmode = 0;
+  };
+  // the gathered slot holds the FP32 source in its low word and the column's
+  // OB_* code in its high word
   auto consume32 = [&](const float4& v, int cc) {
     const double e = gs[cc];
-    // item start: close the previous FP32 partial (a real branch: the
-    // compiler would otherwise predicate the flush onto every column)
-    if (OUT == OUT_Y && __double2hiint(e) != 0) {
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        b[i] += (double)b32[i];
-        b32[i] = 0.f;
+    // sub-chain start: fold the tree (a real branch: the compiler would
+    // otherwise predicate the folds onto every column)
+    if (OUT == OUT_Y && __double2hiint(e) != OB_NONE) {
+      const int code = __double2hiint(e);
+      if (code <= OB_ITEM_MAIN) {
+        flush32();
+        tmode = code == OB_ITEM_MAIN ? 1 : 0;
+      } else if (code == OB_B) {
+        tstore(TS_P, b32[0], b32[1], b32[2], b32[3]);
+        tmode = 1;
+      } else if (code < OB_TAIL1) {
+        const float4 pp = tload(TS_P);
+        const float l0 = pp.x + b32[0], l1 = pp.y + b32[1], l2 = pp.z + b32[2], l3 = pp.w + b32[3];
+        if (code == OB_A1) {
+          tstore(TS_01, l0, l1, l2, l3);
+        } else if (code == OB_A1 + 1) {
+          const float4 s01 = tload(TS_01);
+          tstore(TS_01, s01.x + l0, s01.y + l1, s01.z + l2, s01.w + l3);
+        } else {
+          tstore(TS_2, l0, l1, l2, l3);
+        }
+        tstore(TS_P, 0.f, 0.f, 0.f, 0.f);
+        tmode = 1;
+      } else {
+        const float4 pp = tload(TS_P), s01 = tload(TS_01), s2 = tload(TS_2);
+        // main = (l0 + l1) + (l2 + l3)
+        const float m0 = s01.x + (s2.x + (pp.x + b32[0])), m1 = s01.y + (s2.y + (pp.y + b32[1]));
+        const float m2 = s01.z + (s2.z + (pp.z + b32[2])), m3 = s01.w + (s2.w + (pp.w + b32[3]));
+        tstore(TS_P, 0.f, 0.f, 0.f, 0.f);
+        tstore(TS_2, 0.f, 0.f, 0.f, 0.f);
+        if (code == OB_TAIL1) {  // the one tail column is fused onto main
+          tstore(TS_01, 0.f, 0.f, 0.f, 0.f);
+          b32[0] = m0, b32[1] = m1, b32[2] = m2, b32[3] = m3;
+          tmode = 0;
+          goto fma32;
+        }
+        tstore(TS_01, m0, m1, m2, m3);
+        tmode = 2;
       }
+#pragma unroll
+      for (int i = 0; i < 4; ++i) b32[i] = 0.f;
+    fma32:
       __syncwarp(__activemask());
     }
     const float gf = __int_as_float(__double2loint(e));
@@ -366,11 +453,8 @@ __global__ void __launch_bounds__(NT, DEEP ? 3 : (OUT == OUT_Y && F32MODE != F32
     }
     if constexpr (F32MODE != F32_ALL64) {
       if (cm < ce) drain(cm, ce, consume32, std::false_type{});
+      flush32();  // (a tiled part may cut an item between tiles: each piece is closed)
     }
-  }
-  if constexpr (F32MODE != F32_ALL64) {
-#pragma unroll
-    for (int i = 0; i < 4; ++i) b[i] += (double)b32[i];
   }
 
   // ---------------- fixed-order reduction over thread groups
@@ -521,7 +605,8 @@ __global__ void probe_kernel(DevPlan P, const double* __restrict__ x, unsigned l
       double s = 0.0;
       float s32 = 0.f;
       for (int c = 0; c < r.width; ++c) {
-        double g = src[r.src + c];
+        int code;
+        double g = src[r.src + ((r.flags & RUN_OBL) ? obl_col(r.width, c, &code) : c)];
         if (r.flags & RUN_ROUND) g = (double)(float)g;
         const int64_t e = (int64_t)(r.col0 + c) * rp + row;
         if (f32part) {
@@ -541,13 +626,20 @@ __global__ void probe_kernel(DevPlan P, const double* __restrict__ x, unsigned l
 // ------------------------------------------------------------------------------
 // launchers
 
+// dynamic shared memory of a seg_kernel instantiation: the FP32 lane-tree
+// state of stage 2's FP32-accumulated items
+template <int M, int O, int NT>
+constexpr size_t tree_smem() {
+  return (O == OUT_Y && M != F32_ALL64) ? 3 * NT * sizeof(float4) : 0;
+}
+
 template <int M, int O, int NT = kSegThreads, bool DEEP = false>
 static cudaError_t launch_seg(const DevPlan& P, const Seg* segs, int nseg, const double* x,
                               const S2Out& out, cudaStream_t st, bool pdl) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)nseg);
   cfg.blockDim = dim3(NT);
-  cfg.dynamicSmemBytes = 0;
+  cfg.dynamicSmemBytes = tree_smem<M, O, NT>();
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -586,6 +678,19 @@ cudaError_t launch_stage2(const DevPlan& P, const double* x, const S2Out& out, c
       return P.s2_deep ? launch_seg<F32_ALL64, OUT_Y, kSegThreads, true>(P, P.seg2, P.n_seg2, x, out, st, pdl)
                        : launch_seg<F32_ALL64, OUT_Y>(P, P.seg2, P.n_seg2, x, out, st, pdl);
   }
+}
+
+// Opt the stage-2 FP32 kernels into > 48 KB of shared memory (static +
+// the lane-tree state); called once per plan creation, outside any capture.
+cudaError_t configure_kernels() {
+  cudaError_t e = cudaFuncSetAttribute(seg_kernel<F32_ALL32, OUT_Y, kSegThreads, false>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)tree_smem<F32_ALL32, OUT_Y, kSegThreads>());
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(seg_kernel<F32_MIXED, OUT_Y, kSegThreads, false>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)tree_smem<F32_MIXED, OUT_Y, kSegThreads>());
+  return e;
 }
 
 cudaError_t launch_gather_perm(const double* x, const int32_t* perm, double* xp, int n,

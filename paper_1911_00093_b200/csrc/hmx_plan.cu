@@ -137,6 +137,7 @@ int hmx::plan_create_impl(const hmx_matrix_desc* d, int device, const hmx_plan_o
   }
   const int pipe = d->scheme;
   const bool has_lo = pipe == P_M3;
+  HMX_CUDA(configure_kernels());
   const int64_t rb = opt && opt->row_end > 0 ? opt->row_begin : 0;
   const int64_t re = opt && opt->row_end > 0 ? opt->row_end : n;
   if (rb < 0 || re > n || rb >= re) {
@@ -492,10 +493,10 @@ int hmx::plan_create_impl(const hmx_matrix_desc* d, int device, const hmx_plan_o
         r.col0 = (int32_t)col;
         if (it.cls == 0) {
           r.src = (int32_t)t[2];
-          r.flags = (part == 1 && dense_single) ? (RUN_ROUND | RUN_ACC32) : 0;
+          r.flags = (part == 1 && dense_single) ? (RUN_ROUND | RUN_ACC32 | RUN_OBL) : 0;
         } else {
           r.src = (int32_t)(it.cls == 1 ? zoff_hi[(size_t)it.block] : zoff_lo[(size_t)it.block]);
-          r.flags = RUN_Z | ((part == 1 && it.cls == 1 && u_acc32) ? RUN_ACC32 : 0);
+          r.flags = RUN_Z | ((part == 1 && it.cls == 1 && u_acc32) ? (RUN_ACC32 | RUN_OBL) : 0);
         }
         if (part == 1) {
           if (r.flags & RUN_ACC32) any_acc32 = true;
@@ -594,12 +595,16 @@ int hmx::plan_create_impl(const hmx_matrix_desc* d, int device, const hmx_plan_o
         src_off = d->lo_off[it.block];
         src32 = true;
       }
+      // FP32-accumulated items are stored in SGEMV lane order (obl_col)
+      const bool obl = part == 1 && item_acc32(it);
       for (int64_t i = 0; i < sg.R; ++i) {
         const int64_t e0 = src_off + (r0 + i) * w;
         for (int64_t c = 0; c < w; ++c) {
+          int code;
+          const int64_t sc = obl ? obl_col((int)w, (int)c, &code) : c;
           const int64_t dst = o + (col + c) * rp + i;
-          if (part == 0) b64[(size_t)dst] = src32 ? d->buf32[e0 + c] : d->buf64[e0 + c];
-          else b32[(size_t)dst] = src32 ? d->buf32[e0 + c] : (float)d->buf64[e0 + c];
+          if (part == 0) b64[(size_t)dst] = src32 ? d->buf32[e0 + sc] : d->buf64[e0 + sc];
+          else b32[(size_t)dst] = src32 ? d->buf32[e0 + sc] : (float)d->buf64[e0 + sc];
         }
       }
       col += w;
@@ -727,7 +732,8 @@ int hmx::plan_create_impl(const hmx_matrix_desc* d, int device, const hmx_plan_o
         u.item0 = (int32_t)pit.size();
         u.nitems = (int32_t)lst.size();
         u.is32 = part;
-        for (const ItemRef& it : lst) pit.push_back({it.block, it.cls, (int32_t)item_width(it), 0});
+        for (const ItemRef& it : lst)
+          pit.push_back({it.block, it.cls, (int32_t)item_width(it), (part == 1 && item_acc32(it)) ? 1 : 0});
         ps2.push_back(u);
       }
     }

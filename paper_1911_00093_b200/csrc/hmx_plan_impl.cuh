@@ -169,7 +169,7 @@ struct PackS2 {
   int32_t R, rp, row0, item0, nitems, is32;
 };
 struct PackItem {
-  int32_t block, cls, width, pad;  // cls 0 dense, 1 hi, 2 lo
+  int32_t block, cls, width, pad;  // cls 0 dense, 1 hi, 2 lo; pad 1: store in obl_col order
 };
 struct PackRow {
   int32_t block, q;
