@@ -51,8 +51,9 @@ def measured_peak():
 
 
 class ClockSampler:
-    """SM clocks and throttle reasons sampled through NVML every 10 ms while
-    the timed region runs (falls back to nvidia-smi polling)."""
+    """SM clocks and throttle reasons sampled through NVML every 5 ms while
+    the timed region runs, plus one sample as it ends (falls back to
+    nvidia-smi polling)."""
 
     REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
                "sw_power_cap": 0x4}
@@ -64,39 +65,58 @@ class ClockSampler:
         self._stop = threading.Event()
         self._th = None
 
+    def _sample_nvml(self):
+        import pynvml
+        h = self._h
+        sm = float(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM))
+        mask = int(pynvml.nvmlDeviceGetCurrentClocksEventReasons(h))
+        util = int(pynvml.nvmlDeviceGetUtilizationRates(h).gpu)
+        self.rows.append((sm, mask, util))
+
     def _run(self):
+        if self._h is not None:
+            try:
+                while True:
+                    self._sample_nvml()
+                    if self._stop.wait(0.005):
+                        break
+                return
+            except Exception:
+                pass
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(
+                    ["nvidia-smi", "-i", str(self.device),
+                     "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active,utilization.gpu",
+                     "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                v = [t.strip() for t in out.stdout.strip().split(",")]
+                self.max_mhz = float(v[1])
+                self.rows.append((float(v[0]), int(v[2], 16), int(v[3])))
+            except Exception:
+                pass
+            self._stop.wait(0.1)
+
+    def __enter__(self):
+        # NVML is initialised here, before the timed region, so the sampler
+        # thread takes its first sample at once (a 20-step region lasts ~20 ms)
+        self._h = None
         try:
             import pynvml
             pynvml.nvmlInit()
-            h = pynvml.nvmlDeviceGetHandleByIndex(self.device)
-            self.max_mhz = float(pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM))
-            while not self._stop.is_set():
-                sm = float(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM))
-                mask = int(pynvml.nvmlDeviceGetCurrentClocksEventReasons(h))
-                util = int(pynvml.nvmlDeviceGetUtilizationRates(h).gpu)
-                self.rows.append((sm, mask, util))
-                self._stop.wait(0.01)
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(self.device)
+            self.max_mhz = float(pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM))
         except Exception:
-            while not self._stop.is_set():
-                try:
-                    out = subprocess.run(
-                        ["nvidia-smi", "-i", str(self.device),
-                         "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active,utilization.gpu",
-                         "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
-                    v = [t.strip() for t in out.stdout.strip().split(",")]
-                    self.max_mhz = float(v[1])
-                    self.rows.append((float(v[0]), int(v[2], 16), int(v[3])))
-                except Exception:
-                    pass
-                self._stop.wait(0.1)
-
-    def __enter__(self):
+            self._h = None
         self._th = threading.Thread(target=self._run, daemon=True)
         self._th.start()
-        time.sleep(0.05)
         return self
 
     def __exit__(self, *exc):
+        if self._h is not None:
+            try:
+                self._sample_nvml()   # one sample at the end of the region, whatever its length
+            except Exception:
+                pass
         self._stop.set()
         if self._th:
             self._th.join(timeout=10)
@@ -107,7 +127,7 @@ class ClockSampler:
         busy = [r[0] for r in self.rows if r[2] > 50] or [r[0] for r in self.rows]
         reasons = sorted({name for r in self.rows for name, bit in self.REASONS.items() if r[1] & bit})
         return {"sm_mhz": statistics.median(busy), "sm_max_mhz": self.max_mhz, "reasons": reasons,
-                "samples": len(self.rows), "source": "nvml, 10 ms"}
+                "samples": len(self.rows), "source": "nvml, 5 ms + one at the end"}
 
 
 def build_workload(cfg_id: int):
@@ -134,44 +154,44 @@ def workload_name(cfg_id):
             f"eta 2.0, ACA {c['aca']:g}; x ~ U(-1,1) seed 42; b = centroid z")
 
 
-def cpu_reference_sample(sh, x, budget_s: float, threads: int):
-    """Oracle (numpy restatement of the reference matvec) on a bounded block
-    sample; returns (matvec/s scaled to the full matrix, sample description)."""
+def workload_config(cfg_id, mesh, h, algo_bytes):
+    """The `config` object of the JSON line -- identical in both arms."""
+    return {"workload": workload_name(cfg_id), "scheme": HEADLINE, "n": int(mesh.n),
+            "blocks": int(h.partition.table.shape[0]), "parallelism": "single GPU",
+            "l2": f"inputs {algo_bytes / 1e9:.2f} GB >> 126 MB L2 (no flush needed)"}
+
+
+def cpu_full_passes(sh, x, budget_s: float, threads: int = 1, max_passes: int = 20):
+    """The oracle's FULL matvec (numpy restatement of the reference's
+    matvec.py, every block) timed on this host: passes until budget_s is
+    spent (at least 2); returns (matvec/s from the median pass, passes)."""
     from oracle import hmx_oracle as orc
-    t = sh.base.partition.table
-    nb = t.shape[0]
-    pay = sh.payloads  # materialise views (not timed)
-    blocks = sh.base.partition.blocks
-    sizes = np.array([p.values.nbytes if hasattr(p, "values")
-                      else sum(getattr(p, f).nbytes for f in ("u", "vt") if hasattr(p, f))
-                      + (sum(getattr(p, f).nbytes for f in ("u_hi", "vt_hi", "u_lo", "vt_lo",
-                                                               "diag_hi", "diag_lo"))
-                         if hasattr(p, "u_hi") else 0)
-                      for p in pay], dtype=np.float64)
-    del blocks
-    total = float(sizes.sum())
-    # calibrate on every 64th block, then size the sample to ~budget/3 per pass
-    probe = np.arange(0, nb, 64)
-    t0 = time.perf_counter()
-    orc.matvec_threaded(sh, x, threads, blocks=probe)
-    dt = max(time.perf_counter() - t0, 1e-6)
-    frac_probe = sizes[probe].sum() / total
-    per_full = dt / frac_probe
-    stride = max(1, int(np.ceil(per_full / (budget_s / 3.0))))
-    sample = np.arange(0, nb, stride)
-    frac = float(sizes[sample].sum() / total)
+    orc.matvec_threaded(sh, x, threads)          # warm: payload views, page faults
     times = []
     t_end = time.perf_counter() + budget_s
-    while time.perf_counter() < t_end or len(times) < 2:
+    while len(times) < 2 or (time.perf_counter() < t_end and len(times) < max_passes):
         t0 = time.perf_counter()
-        orc.matvec_threaded(sh, x, threads, blocks=sample)
+        orc.matvec_threaded(sh, x, threads)
         times.append(time.perf_counter() - t0)
-        if len(times) >= 20:
-            break
-    best = float(np.median(times))
-    return frac / best, (f"every {stride}th block ({len(sample)} of {nb} blocks, "
-                         f"{100 * frac:.2f}% of payload bytes), {len(times)} passes, median; "
-                         f"scaled to one full matvec"), len(times)
+    return 1.0 / float(np.median(times)), len(times)
+
+
+def measured_reference_solve(cfg_id):
+    """The reference algorithm's BiCG-STAB to 1e-8 on this config's H-matrix,
+    MEASURED (not estimated): the threads=1 oracle solve recorded in
+    tests/golden/solver_envelope_config<k>.json (run in the build container
+    by tests/golden/make_solver_envelope.py); None if absent."""
+    f = ROOT / "tests" / "golden" / f"solver_envelope_config{cfg_id}.json"
+    if not f.exists():
+        return None
+    d = json.loads(f.read_text())
+    run = d.get("schemes", {}).get(HEADLINE, {}).get("1")
+    if not run:
+        return None
+    return {"wall_s": run["cpu_s"], "iterations": run["iterations"], "converged": run["converged"],
+            "true_residual": run["true_residual"],
+            "where": "build container (8-core Xeon, OPENBLAS_NUM_THREADS=1), oracle bicgstab, "
+                     "tests/golden/solver_envelope_config%d.json" % cfg_id}
 
 
 def _timed(fn):
@@ -182,9 +202,11 @@ def _timed(fn):
 
 def run_reference(args):
     """--impl reference: the reference's CPU matvec (oracle port of
-    matvec.py / matvec_threaded) on the host cores.  One step = one pass over
-    a fixed block sample sized so that W + K passes take about a minute; the
-    value is scaled to full matvecs per second."""
+    matvec.py / matvec_threaded, pinned bit-for-bit to the reference) on the
+    host cores.  One step = one FULL matvec of the workload (every block), no
+    sampling; threads = the faster of 1 and all host threads on one full
+    pass.  The H-matrix itself comes from this repo's host builder
+    (libhmx_host.so, untimed: the reference's own build takes 442 s here)."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
@@ -192,57 +214,34 @@ def run_reference(args):
     from oracle import hmx_oracle as orc
     mesh, h, x, b, _ = build_workload(args.config)
     sh = hx.prepare_scheme(h, HEADLINE)
-    pay = sh.payloads
-    sizes = np.array([getattr(p, "values", None).nbytes if hasattr(p, "values")
-                      else p.u.nbytes + p.vt.nbytes for p in pay], dtype=np.float64)
-    total = float(sizes.sum())
-    nb = len(pay)
     ncpu = os.cpu_count() or 1
-    # size the sample from a 1-thread probe, then keep the faster of 1 thread
-    # and all host threads on that sample
-    probe = np.arange(0, nb, 64)
-    t0 = time.perf_counter()
-    orc.matvec_threaded(sh, x, 1, blocks=probe)
-    per_full = max(time.perf_counter() - t0, 1e-9) * total / sizes[probe].sum()
-    budget = 60.0 / (args.steps + args.warmup + 2)        # seconds per pass
-    stride = max(1, int(np.ceil(per_full / budget)))
-    sample = np.arange(0, nb, stride)
-    frac = float(sizes[sample].sum() / total)
-    trial = {}
-    for threads in sorted({1, ncpu}):
-        t0 = time.perf_counter()
-        orc.matvec_threaded(sh, x, threads, blocks=sample)
-        trial[threads] = time.perf_counter() - t0
+    orc.matvec_threaded(sh, x, 1)                    # warm (payload views, page faults)
+    trial = {t: _timed(lambda t=t: orc.matvec_threaded(sh, x, t)) for t in sorted({1, ncpu})}
     threads = min(trial, key=trial.get)
-    # the per-call fixed part (permutation gather, result allocation,
-    # inverse scatter: reference matvec.py:113-147) is paid once per matvec;
-    # only the per-block part scales with the sampled fraction
-    empty = np.zeros(0, dtype=np.int64)
-    fixed = min(_timed(lambda: orc.matvec(sh, x, blocks=empty)) for _ in range(5))
     for _ in range(args.warmup):
-        orc.matvec_threaded(sh, x, threads, blocks=sample)
+        orc.matvec_threaded(sh, x, threads)
     times = []
     for _ in range(args.steps):
         t0 = time.perf_counter()
-        orc.matvec_threaded(sh, x, threads, blocks=sample)
+        orc.matvec_threaded(sh, x, threads)
         times.append(time.perf_counter() - t0)
-    per_block = max(float(np.mean(times)) - fixed, 1e-9)
-    v = 1.0 / (fixed + per_block / frac)
-    desc = (f"every {stride}th block ({len(sample)} of {nb} blocks, {100 * frac:.2f}% of the "
-            f"payload bytes) per step, {threads} thread(s) (better of 1 and {ncpu}); full matvec "
-            f"time = fixed per-call part ({1e3 * fixed:.2f} ms, measured) + sampled block time / "
-            f"sampled fraction")
+    ms = 1e3 * float(np.mean(times))
+    v = 1e3 / ms
+    desc = (f"full matvec per step (all {h.partition.table.shape[0]} blocks), {threads} thread(s) "
+            f"(the faster of 1 and {ncpu} on a full pass: "
+            + ", ".join(f"{t}: {1e3 * dt:.0f} ms" for t, dt in trial.items()) + ")")
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": "matvec/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1e3 / v, "higher_is_better": True, "scaling": "strong",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": workload_name(args.config), "scheme": HEADLINE, "n": int(mesh.n)},
+        "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded jittered icosphere, BASELINE.json recipe)",
+        "config": workload_config(args.config, mesh, h, sh.payload_bytes + 16 * mesh.n),
         "cpu_baseline": {"value": v, "unit": "matvec/s", "cores": threads, "kind": "port",
-                         "sample": desc},
+                         "sample": desc, "solve": measured_reference_solve(args.config)},
         "e2e": {"value": v, "unit": "matvec/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "note": ("oracle/hmx_oracle.py: numpy restatement of the reference's matvec.py "
-                 "(per-block loop over OpenBLAS GEMVs), pinned bit-for-bit to the reference"),
+                 "(per-block loop over OpenBLAS GEMVs), pinned bit-for-bit to the reference; "
+                 "libhmx_host.so is loaded only to build the input H-matrix (untimed)"),
     }
     print(json.dumps(line), flush=True)
 
@@ -324,6 +323,14 @@ def run_ours(args):
                 e2e_t.append(time.perf_counter() - t0)
             e2e_ms = 1e3 * float(np.mean(e2e_t))
             results[name]["e2e_ms"] = e2e_ms
+            # the same with a pageable numpy x (what the reference API's callers pass)
+            x_page = np.array(x, copy=True)
+            e2e_p = []
+            for _ in range(max(5, min(args.steps, 50))):
+                t0 = time.perf_counter()
+                hx.matvec(sh, x_page)
+                e2e_p.append(time.perf_counter() - t0)
+            results[name]["e2e_pageable_ms"] = 1e3 * float(np.mean(e2e_p))
         else:
             plan.close()
             del sh
@@ -343,28 +350,19 @@ def run_ours(args):
 
     cpu = None
     if not args.no_cpu_baseline:
-        v, sample, passes = cpu_reference_sample(sh, x, args.cpu_budget, 1)
-        cpu = {"value": v, "unit": "matvec/s", "cores": 1, "kind": "port", "sample": sample}
-        # the reference's solve is >= 95 % matvecs: its time to
-        # 1e-8 on this host, estimated as the GPU solve's operator
-        # applications x the measured CPU matvec time (config 4: 256 s, too
-        # long to run in the bench)
-        solve = results.get(HEADLINE, {}).get("solve")
-        if solve:
-            cpu["solve_estimate_s"] = solve["matvecs"] / v
-            cpu["solve_estimate"] = (f"{solve['matvecs']} operator applications (the GPU solve's) x "
-                                     f"the CPU matvec time; reference solve on its own host: "
-                                     f"SURVEY s6.3")
+        v, passes = cpu_full_passes(sh, x, args.cpu_budget, 1)
+        cpu = {"value": v, "unit": "matvec/s", "cores": 1, "kind": "port",
+               "sample": f"{passes} FULL oracle matvecs (every block, 1 thread), median pass",
+               # the reference algorithm's solve, measured (not estimated)
+               "solve": measured_reference_solve(args.config)}
 
     line = {
         "metric": METRIC, "value": 1e3 / ms, "unit": "matvec/s", "n_gpus": 1,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded jittered icosphere, BASELINE.json recipe)",
-        "config": {"workload": workload_name(args.config), "scheme": HEADLINE, "n": int(n),
-                   "blocks": int(h.partition.table.shape[0]), "parallelism": "single GPU",
-                   "l2": f"inputs {algo / 1e9:.2f} GB >> 126 MB L2 (no flush needed)",
-                   "build_s": t_build},
+        "config": workload_config(args.config, mesh, h, algo),
+        "build_s": t_build,
         "roofline": {"bound": "hbm", "achieved": dom_achieved, "peak": peak, "unit": "GB/s",
                      "frac": dom_achieved / peak, "traffic": traffic,
                      "kernel": "s2_kernel (row-segment stream: dense + U slabs)",
@@ -374,7 +372,10 @@ def run_ours(args):
                      "matvec_frac_of_8TBps": algo / (ms * 1e6) / 8000.0},
         "cpu_baseline": cpu,
         "e2e": {"value": 1e3 / results[HEADLINE]["e2e_ms"], "unit": "matvec/s",
-                "h2d_bytes_per_step": 8 * int(n), "d2h_bytes_per_step": 8 * int(n)},
+                "h2d_bytes_per_step": 8 * int(n), "d2h_bytes_per_step": 8 * int(n),
+                "input": "x in pinned host memory",
+                "pageable": {"value": 1e3 / results[HEADLINE]["e2e_pageable_ms"], "unit": "matvec/s",
+                             "input": "x a pageable numpy array (the reference API's usual caller)"}},
         "gpu_launches": 2 * args.steps,
         "clocks": clocks,
         "variants": results,

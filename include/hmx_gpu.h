@@ -24,7 +24,10 @@
  * All vectors are float64.  Pointers are host pointers unless a flag says
  * device.  Every call returns an hmx_status; hmx_last_error() describes the
  * last failure on the calling thread.  Calls on one plan are serialised by
- * the plan's mutex; distinct plans may be used concurrently.
+ * the plan's mutex (host side) and by an event chained through every call's
+ * stream (device side: work a call enqueues on a caller's stream finishes
+ * before the plan's next call starts on any stream); distinct plans may be
+ * used concurrently.
  */
 #ifndef HMX_GPU_H
 #define HMX_GPU_H
@@ -201,7 +204,9 @@ int hmx_bicgstab(hmx_plan* plan, hmx_plan* plan64, const double* b, double tol, 
  * `nonfinite` (device int, may be NULL) is set to 1 when a y entry is not
  * finite.  Enqueued on `stream` (a cudaStream_t, 0 being the legacy default
  * stream; UINT64_MAX = the plan's own stream); returns without
- * synchronising. */
+ * synchronising.  xp must stay valid until the product completes, and, if a
+ * non-finite result is reported, until hmx_nonfinite_block has named the
+ * block (the probe re-reads the most recent input). */
 int hmx_apply_local(hmx_plan* plan, const double* xp, double* y, const double* w1, int yy,
                     double* dots, int* nonfinite, uint64_t stream);
 

@@ -45,58 +45,32 @@ struct Seg {             // 64 bytes; one CTA
 };
 static_assert(sizeof(Seg) == 64, "Seg layout");
 
-// RUN_OBL: a stage-2 FP32-accumulated item stored in SGEMV lane order (below)
-enum : int32_t { RUN_Z = 1, RUN_ROUND = 2, RUN_ACC32 = 4, RUN_OBL = 8 };
+// RUN_CHUNK: a stage-2 FP32-accumulated item in SGEMV chunk layout (below)
+enum : int32_t { RUN_Z = 1, RUN_ROUND = 2, RUN_ACC32 = 4, RUN_CHUNK = 8 };
 
-// ---- FP32 accumulation order of the stage-2 FP32-accumulated items ----------
+// ---- FP32-accumulated stage-2 items: the reference's summation order ---------
 // The reference's FP32 products (`A32 @ x32`, `U32 @ z32`; matvec.py:57, :73)
-// run through OpenBLAS SGEMV-T.  Its summation tree for an n-wide row,
+// run through OpenBLAS SGEMV-T.  Its summation tree for one n-wide row,
 // recovered by probing (tools/sgemv_order_probe.py; CPU model and bitwise
-// check in tools/fp32_accum_emulation.py), is, with main = 4*floor(n/4) and
-// nch = main/4 chunks of 4 columns:
-//   * four lanes j = 0..3; lane j = A_j + B_j, two FMA chains over column
-//     4c + j for the chunks c in A and in B (nch even: A = even chunks,
-//     B = odd ones; nch odd: A = {0, 1, 3, 5, ..}, B = {2, 4, ..}); for n = 8
-//     A_j = column 2j, B_j = column 2j + 1;
-//   * main = (l0 + l1) + (l2 + l3);
-//   * tail (n - main columns): 1 -> fma onto main; 2 -> main + fma(a_m, g_m,
-//     a_{m+1} g_{m+1}); 3 -> main + fma(a_{m+2}, g_{m+2}, that);
+// check against numpy in tools/fp32_accum_emulation.py), with nch = n / 4
+// chunks of 4 columns and T = n % 4 tail columns:
+//   * two 4-wide FMA accumulators A and B over the chunks (nch even: A takes
+//     the even chunks, B the odd ones; nch odd: A = {0, 1, 3, 5, ..},
+//     B = {2, 4, ..}); l = A + B lane-wise; main = (l0 + l1) + (l2 + l3);
+//   * tail: T = 1: fma(a_m, g_m, main); T = 2: main + fma(a_m, g_m, a_{m+1}
+//     g_{m+1}); T = 3: main + fma(a_{m+2}, g_{m+2}, that)   (m = 4 nch);
+//   * n = 8: l_j = a_{2j} g_{2j} + a_{2j+1} g_{2j+1}, then main as above;
 //   * n <= 3 and 5 <= n <= 7: one forward FMA chain.
-// The flattener stores such an item's columns in processing order (lane by
-// lane, A then B, then the tail) and the kernel evaluates the tree with a
-// few FP32 registers, driven by one code per sub-chain start.
-enum : int32_t {
-  OB_NONE = 0,       // continue the current FMA chain
-  OB_ITEM_CHAIN = 1, // first column of a plain-chain item
-  OB_ITEM_MAIN = 2,  // first column (A_0) of a lane-tree item
-  OB_B = 3,          // first column of B_j
-  OB_A1 = 4,         // first column of A_1 (A_2 = OB_A1 + 1, A_3 = OB_A1 + 2)
-  OB_TAIL1 = 7,      // the single tail column: FMA onto main
-  OB_TAIL = 8        // first column of a 2- or 3-column tail chain
-};
-// Original column of stored position k of an n-wide item, and its code.
-__host__ __device__ __forceinline__ int obl_col(int n, int k, int* code) {
-  *code = OB_NONE;
-  if (n <= 3 || (n >= 5 && n <= 7)) {
-    if (k == 0) *code = OB_ITEM_CHAIN;
-    return k;
-  }
-  const int mainw = n & ~3, nch = mainw >> 2;
-  if (k < mainw) {
-    const int j = k / nch, r = k - j * nch;
-    const int na = (nch + 1) >> 1;  // chunks in A
-    if (r == 0) *code = j == 0 ? OB_ITEM_MAIN : OB_A1 + (j - 1);
-    else if (r == na) *code = OB_B;
-    if (n == 8) return k;
-    int chunk;
-    if (r < na) chunk = (nch & 1) ? (r == 0 ? 0 : 2 * r - 1) : 2 * r;
-    else chunk = (nch & 1) ? 2 * (r - na) + 2 : 2 * (r - na) + 1;
-    return 4 * chunk + j;
-  }
-  const int t = k - mainw, T = n - mainw;
-  if (t == 0) *code = T == 1 ? OB_TAIL1 : OB_TAIL;
-  if (T == 1) return mainw;
-  return t == 0 ? mainw + 1 : t == 1 ? mainw : mainw + 2;
+// The stage-2 kernel evaluates exactly this per row, one row per thread.  Such
+// an item (R rows padded to rp, n columns) is stored as its nch chunks, each
+// rp rows x 4 floats (16 bytes per row: one vector load), then the T tail
+// columns rp floats each; chain-shaped widths store every column that way.
+// Same element count (rp * n) as the column-major items.
+__host__ __device__ __forceinline__ bool chain_shaped(int n) { return n <= 3 || (n >= 5 && n <= 7); }
+__host__ __device__ __forceinline__ int64_t chunk_off(int n, int rp, int row, int k) {
+  const int nch = chain_shaped(n) ? 0 : n >> 2;
+  if (k < 4 * nch) return ((int64_t)(k >> 2) * rp + row) * 4 + (k & 3);
+  return (int64_t)4 * nch * rp + (int64_t)(k - 4 * nch) * rp + row;
 }
 
 struct Run {             // one item (block slab) of a segment part

@@ -26,10 +26,9 @@ namespace hmx {
 enum Out : int { OUT_Y = 0, OUT_Z = 1 };
 
 // Shared-memory slot of an FP32-accumulated column: the FP32 source value in
-// the low word, the column's tree code (OB_*, hmx_internal.cuh) in the high
-// word (stage 1: OB_ITEM_CHAIN on a segment's first column, else 0).
-__device__ __forceinline__ double acc32_slot(float g, int code) {
-  return __hiloint2double(code, __float_as_int(g));
+// the low word, 1 in the high word on the first column of an item.
+__device__ __forceinline__ double acc32_slot(float g, bool start) {
+  return __hiloint2double(start ? 1 : 0, __float_as_int(g));
 }
 
 // 8-byte asynchronous global -> shared copies (the x / z segments of a tile)
@@ -45,13 +44,11 @@ __device__ __forceinline__ void cp_async_wait_all() {
 // Stage a tile [tc0, tc0+tw) of one part's source vector g (x segments and z
 // vectors, in item order) into shared memory with cp.async; FP32-accumulated
 // columns are then rewritten as acc32_slot and FP32-shadow columns rounded
-// (fl: scratch flags, the column's OB_* code and kFlAcc32).  RUN_OBL items
-// are stored in SGEMV lane order, so column k reads source obl_col(k).  A single run
+// (fl: scratch flags, bit 0 item start, bit 1 FP32 item).  A single run
 // (every stage-1 segment) is a contiguous copy.  Otherwise the runs are first
 // expanded into a per-column source index in shared memory, so every
 // column's copy is independent (no dependent run lookups).
 constexpr int32_t kTagZ = 1 << 30, kTagRound = 1 << 29, kIdxMask = kTagRound - 1;
-constexpr uint8_t kFlAcc32 = 16;  // fl: low 4 bits the OB_* code, bit 4 an FP32-accumulated column
 template <bool FLAGS, int NT, int WMAX>
 __device__ __forceinline__ void gather_g(const DevPlan& P, const Run* __restrict__ runs, int nrun,
                                          int tc0, int tw, const double* __restrict__ x,
@@ -59,18 +56,13 @@ __device__ __forceinline__ void gather_g(const DevPlan& P, const Run* __restrict
   constexpr int PER = WMAX / NT;  // columns per thread
   if (nrun == 1) {
     const Run r = runs[0];
-    const double* src = ((r.flags & RUN_Z) ? P.z : x) + r.src;
+    const double* src = ((r.flags & RUN_Z) ? P.z : x) + r.src + (tc0 - r.col0);
     const bool rnd = (r.flags & RUN_ROUND) != 0;
     const bool f32 = FLAGS && (r.flags & RUN_ACC32);
-    const bool obl = FLAGS && (r.flags & RUN_OBL);
-    int code[PER];
 #pragma unroll
     for (int u = 0; u < PER; ++u) {
       const int c = threadIdx.x + u * NT;
-      const int k = tc0 + c - r.col0;
-      code[u] = k == 0 ? OB_ITEM_CHAIN : OB_NONE;
-      const int sc = obl ? obl_col(r.width, k, &code[u]) : k;
-      if (c < tw) cp_async8(gs + c, src + sc);
+      if (c < tw) cp_async8(gs + c, src + c);
     }
     cp_async_wait_all();
     if (rnd || f32) {
@@ -79,7 +71,7 @@ __device__ __forceinline__ void gather_g(const DevPlan& P, const Run* __restrict
         const int c = threadIdx.x + u * NT;
         if (c < tw) {
           const double g = gs[c];
-          gs[c] = f32 ? acc32_slot((float)g, code[u]) : (double)(float)g;
+          gs[c] = f32 ? acc32_slot((float)g, tc0 + c == r.col0) : (double)(float)g;
         }
       }
     }
@@ -90,13 +82,10 @@ __device__ __forceinline__ void gather_g(const DevPlan& P, const Run* __restrict
     const Run r = runs[j];
     const int lo = max(r.col0, tc0), hi = min(r.col0 + r.width, tc0 + tw);
     const int32_t tag = ((r.flags & RUN_Z) ? kTagZ : 0) | ((r.flags & RUN_ROUND) ? kTagRound : 0);
-    const uint8_t f32 = (r.flags & RUN_ACC32) ? kFlAcc32 : 0;
-    const bool obl = FLAGS && (r.flags & RUN_OBL);
+    const uint8_t f32 = (r.flags & RUN_ACC32) ? 2 : 0;
     for (int col = lo; col < hi; ++col) {
-      int code = col == r.col0 ? OB_ITEM_CHAIN : OB_NONE;
-      const int sc = obl ? obl_col(r.width, col - r.col0, &code) : col - r.col0;
-      sidx[col - tc0] = (r.src + sc) | tag;
-      if constexpr (FLAGS) fl[col - tc0] = (uint8_t)(code | f32);
+      sidx[col - tc0] = (r.src + (col - r.col0)) | tag;
+      if constexpr (FLAGS) fl[col - tc0] = (uint8_t)((col == r.col0 ? 1 : 0) | f32);
     }
   }
   __syncthreads();
@@ -114,7 +103,7 @@ __device__ __forceinline__ void gather_g(const DevPlan& P, const Run* __restrict
     const int c = threadIdx.x + u * NT;
     if (c < tw) {
       const uint8_t f = FLAGS ? fl[c] : 0;
-      if (FLAGS && (f & kFlAcc32)) gs[c] = acc32_slot((float)gs[c], f & 15);
+      if (FLAGS && (f & 2)) gs[c] = acc32_slot((float)gs[c], f & 1);
       else if (id[u] & kTagRound) gs[c] = (double)(float)gs[c];
     }
   }
@@ -124,6 +113,151 @@ __device__ __forceinline__ double z_epilogue(const DevPlan& P, double s, int zi)
   if (P.zepi == Z_ROUND32) return (double)(float)s;   // FP32 intermediate (matvec.py:68-72)
   if (P.zepi == Z_SCALE) return s * P.zscale[zi];      // z *= diag (matvec.py:81, :88, :92)
   return s;
+}
+
+// FP32-accumulated items (RUN_CHUNK, layout chunk_off in hmx_internal.cuh) of
+// one thread group: this thread's row p of every item, in OpenBLAS SGEMV-T's
+// order, each value widened once and added in FP64 (reference matvec.py:57,
+// :73, then :106).  Explicit _rn intrinsics: nothing is contracted or
+// reassociated.  Items are software-pipelined: the next item's loads are in
+// flight while the current one is reduced.
+__device__ __forceinline__ float4 fma4(float4 a, float4 g, float4 c) {
+  return make_float4(__fmaf_rn(a.x, g.x, c.x), __fmaf_rn(a.y, g.y, c.y), __fmaf_rn(a.z, g.z, c.z),
+                     __fmaf_rn(a.w, g.w, c.w));
+}
+__device__ __forceinline__ float4 ld_chunk(const float* p) {
+  float4 r;  // L1-allocating: a thread's A and B chunks share 32-byte sectors
+  asm volatile("ld.global.nc.L1::evict_first.v4.f32 {%0,%1,%2,%3}, [%4];"
+               : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
+               : "l"(p));
+  return r;
+}
+__device__ __forceinline__ float ld_one(const float* p) {
+  float r;
+  asm volatile("ld.global.nc.L1::no_allocate.f32 %0, [%1];" : "=f"(r) : "l"(p));
+  return r;
+}
+
+// one item's prefetched values: its first kPre chunks + the tail (column
+// order m+1, m, m+2: the tail's FMA-chain order), or the up to 7 columns of a
+// chain-shaped item (k = 0..2 in t, 3..6 in x[0])
+constexpr int kPre = 2;
+struct ChainBuf {
+  float4 x[kPre];
+  float t[3];
+};
+constexpr int kMetaW = 12;  // run meta in shared memory: col0 << 12 | width
+
+__device__ __forceinline__ void chain_load(ChainBuf& b, const float* part, int meta, int rp, int p) {
+  const int n = meta & ((1 << kMetaW) - 1), c0 = meta >> kMetaW;
+  const float* it = part + (int64_t)c0 * rp + p;
+  if (chain_shaped(n)) {
+    if (n > 0) b.t[0] = ld_one(it);
+    if (n > 1) b.t[1] = ld_one(it + rp);
+    if (n > 2) b.t[2] = ld_one(it + 2 * rp);
+    if (n > 4) b.x[0].x = ld_one(it + 3 * rp);
+    if (n > 4) b.x[0].y = ld_one(it + 4 * rp);
+    if (n > 5) b.x[0].z = ld_one(it + 5 * rp);
+    if (n > 6) b.x[0].w = ld_one(it + 6 * rp);
+    return;
+  }
+  const int nch = n >> 2, T = n & 3;
+  const float* ch = it + 3 * p;  // chunk c of row p: it - p + 4 (c rp + p)
+#pragma unroll
+  for (int u = 0; u < kPre; ++u)
+    if (u < nch) b.x[u] = ld_chunk(ch + (int64_t)4 * u * rp);
+  const float* tl = it + (int64_t)4 * nch * rp;
+  if (T == 1) {
+    b.t[0] = ld_one(tl);
+  } else if (T >= 2) {
+    b.t[0] = ld_one(tl + rp);
+    b.t[1] = ld_one(tl);
+    if (T == 3) b.t[2] = ld_one(tl + 2 * rp);
+  }
+}
+
+__device__ __forceinline__ float chain_value(const ChainBuf& b, const float* part, const double* gs, int meta,
+                                             int rp, int p) {
+  const int n = meta & ((1 << kMetaW) - 1), c0 = meta >> kMetaW;
+  auto G = [&](int c) { return __int_as_float(__double2loint(gs[c])); };
+  auto G4 = [&](int c) { return make_float4(G(c), G(c + 1), G(c + 2), G(c + 3)); };
+  if (chain_shaped(n)) {  // n <= 3, 5 <= n <= 7: one forward FMA chain
+    float v = 0.f;
+    if (n > 0) v = __fmaf_rn(b.t[0], G(c0), v);
+    if (n > 1) v = __fmaf_rn(b.t[1], G(c0 + 1), v);
+    if (n > 2) v = __fmaf_rn(b.t[2], G(c0 + 2), v);
+    if (n > 4) v = __fmaf_rn(b.x[0].x, G(c0 + 3), v);
+    if (n > 4) v = __fmaf_rn(b.x[0].y, G(c0 + 4), v);
+    if (n > 5) v = __fmaf_rn(b.x[0].z, G(c0 + 5), v);
+    if (n > 6) v = __fmaf_rn(b.x[0].w, G(c0 + 6), v);
+    return v;
+  }
+  const int nch = n >> 2, T = n & 3, m = 4 * nch;
+  float4 l;
+  if (n == 8) {  // l_j = a_2j g_2j + a_2j+1 g_2j+1
+    const float4 g0 = G4(c0), g1 = G4(c0 + 4);
+    l = make_float4(__fadd_rn(__fmul_rn(b.x[0].x, g0.x), __fmul_rn(b.x[0].y, g0.y)),
+                    __fadd_rn(__fmul_rn(b.x[0].z, g0.z), __fmul_rn(b.x[0].w, g0.w)),
+                    __fadd_rn(__fmul_rn(b.x[1].x, g1.x), __fmul_rn(b.x[1].y, g1.y)),
+                    __fadd_rn(__fmul_rn(b.x[1].z, g1.z), __fmul_rn(b.x[1].w, g1.w)));
+  } else {
+    // chunk c into A or B: nch even: A = even chunks; nch odd: A = {0, 1, 3, 5, ..}
+    const bool odd = nch & 1;
+    auto inA = [&](int c) { return odd ? (c == 0 || (c & 1)) : !(c & 1); };
+    float4 A = make_float4(0.f, 0.f, 0.f, 0.f), B = A;
+#pragma unroll
+    for (int u = 0; u < kPre; ++u)
+      if (u < nch) {
+        if (inA(u)) A = fma4(b.x[u], G4(c0 + 4 * u), A);
+        else B = fma4(b.x[u], G4(c0 + 4 * u), B);
+      }
+    // the remaining chunks (n >= 12), four loads in flight
+    const float* ch = part + (int64_t)c0 * rp + 4 * p;
+    for (int c = kPre; c < nch; c += 4) {
+      float4 xs[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (c + u < nch) xs[u] = ld_chunk(ch + (int64_t)4 * (c + u) * rp);
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (c + u < nch) {
+          if (inA(c + u)) A = fma4(xs[u], G4(c0 + 4 * (c + u)), A);
+          else B = fma4(xs[u], G4(c0 + 4 * (c + u)), B);
+        }
+    }
+    l = make_float4(__fadd_rn(A.x, B.x), __fadd_rn(A.y, B.y), __fadd_rn(A.z, B.z), __fadd_rn(A.w, B.w));
+  }
+  float v = __fadd_rn(__fadd_rn(l.x, l.y), __fadd_rn(l.z, l.w));
+  if (T == 1) {
+    v = __fmaf_rn(b.t[0], G(c0 + m), v);
+  } else if (T >= 2) {
+    float tv = __fmul_rn(b.t[0], G(c0 + m + 1));
+    tv = __fmaf_rn(b.t[1], G(c0 + m), tv);
+    if (T == 3) tv = __fmaf_rn(b.t[2], G(c0 + m + 2), tv);
+    v = __fadd_rn(v, tv);
+  }
+  return v;
+}
+
+// the group's items: runs with col0 in [cb, ce) (meta[] in shared memory)
+__device__ __forceinline__ double chain_items(const int32_t* meta, int nrun, const float* __restrict__ part,
+                                              const double* gs, int cb, int ce, int rp, int p) {
+  int j = 0;
+  while (j < nrun && (meta[j] >> kMetaW) < cb) ++j;
+  int je = j;
+  while (je < nrun && (meta[je] >> kMetaW) < ce) ++je;
+  double acc = 0.0;
+  ChainBuf b0, b1;
+  if (j < je) chain_load(b0, part, meta[j], rp, p);
+  while (j < je) {
+    if (j + 1 < je) chain_load(b1, part, meta[j + 1], rp, p);
+    acc += (double)chain_value(b0, part, gs, meta[j], rp, p);
+    if (++j >= je) break;
+    if (j + 1 < je) chain_load(b0, part, meta[j + 1], rp, p);
+    acc += (double)chain_value(b1, part, gs, meta[j], rp, p);
+    ++j;
+  }
+  return acc;
 }
 
 // One CTA = one segment: rows [row0, row0+R) of a column-major item stream.
@@ -141,9 +275,6 @@ __global__ void __launch_bounds__(NT, DEEP ? 3 : (OUT == OUT_Y && F32MODE != F32
   __shared__ int32_t sidx[OUT == OUT_Z ? 1 : kSegWMax];
   __shared__ double red64[2 * NT];
   __shared__ double red32[4 * NT];
-  // pending FP32 lane-tree values of stage 2's FP32-accumulated items
-  // (consume32): dynamic shared memory, 3 x NT float4 (kTreeSmem)
-  extern __shared__ float4 tstate[];
   __shared__ double wred[2][NT / 32];
   __shared__ unsigned ticket;
 
@@ -223,21 +354,26 @@ __global__ void __launch_bounds__(NT, DEEP ? 3 : (OUT == OUT_Y && F32MODE != F32
   const int tpg32 = rp32 >> 2;
   int g32 = NT / tpg32;
   int q32 = tid / tpg32, p32 = tid - q32 * tpg32;
-  if constexpr (F32MODE == F32_MIXED && OUT == OUT_Y) {
-    // warp-aligned split (plan: sg.chunk = wb): groups of the FP64-accumulated
-    // columns on threads [0, wb), of the FP32-accumulated ones from wb on, so
-    // no warp runs both loops
-    const int wb = sg.chunk;
-    if (wb > 0 && sg.gtab >= 0) {
-      const int ga = wb / tpg32, gb = (NT - wb) / tpg32;
+  // Stage-2 parts with a group table (every part of <= kSegWMax columns):
+  // FP64-accumulated (widened) items on threads [0, wbc), 4 rows per thread
+  // as above; the FP32-accumulated items (RUN_CHUNK) on threads [wbc, NT),
+  // ONE row per thread, each item evaluated in SGEMV's own order (chain_items).
+  // wbc (plan: sg.chunk) is warp-aligned, so no warp runs both loops.
+  bool chain_thr = false;
+  int pc = 0;
+  if constexpr (F32MODE != F32_ALL64 && OUT == OUT_Y) {
+    if (sg.gtab >= 0) {
+      const int wbc = F32MODE == F32_ALL32 ? 0 : sg.chunk;
+      const int ga = wbc / tpg32, gb = (NT - wbc) / rp32;
       g32 = ga + gb;
-      if (tid < wb) {
+      if (tid < wbc) {
         if (q32 >= ga) q32 = g32;  // idle
       } else {
-        const int u = tid - wb;
-        const int qb = u / tpg32;
-        p32 = u - qb * tpg32;
+        const int u = tid - wbc;
+        const int qb = u / rp32;
+        pc = u - qb * rp32;
         q32 = qb < gb ? ga + qb : g32;
+        chain_thr = true;
       }
     }
   }
@@ -251,6 +387,7 @@ __global__ void __launch_bounds__(NT, DEEP ? 3 : (OUT == OUT_Y && F32MODE != F32
     if (sg.gtab >= 0) c32 = P.gtab[sg.gtab + g32 + 1];
     else if (sg.gtab <= -2) c32 = P.gtab[-2 - sg.gtab];
   }
+  double bc = 0.0;  // chain threads: the row's FP64 sum of its widened item values
   // widened FP32 data, FP64 accumulation
   auto consume64 = [&](const float4& v, int cc) {
     const double g = gs[cc];
@@ -259,91 +396,18 @@ __global__ void __launch_bounds__(NT, DEEP ? 3 : (OUT == OUT_Y && F32MODE != F32
     b[2] = fma((double)v.z, g, b[2]);
     b[3] = fma((double)v.w, g, b[3]);
   };
-  // FP32-accumulated items (stage 2): per row, the SGEMV lane tree of
-  // hmx_internal.cuh evaluated in storage order.  b32 is the running FMA
-  // chain; the tree's pending values live in shared memory (touched only at
-  // sub-chain starts, so they cost no registers in the streaming loop):
-  // TS_P a finished A_j waiting for B_j, TS_01 = l0 (+ l1), TS_2 = l2.  They
-  // are zero whenever tmode == 0 (0: plain chain, 1: lane tree open, 2: tail
-  // chain after the tree).
-  enum { TS_P = 0, TS_01 = 1, TS_2 = 2 };
-  int tmode = 0;
-  auto tload = [&](int k) { return tstate[k * NT + tid]; };
-  auto tstore = [&](int k, float a, float b_, float c, float d) { tstate[k * NT + tid] = make_float4(a, b_, c, d); };
-  // close the open tree: widen its value once and add it in FP64
-  auto flush32 = [&]() {
-    float v[4] = {b32[0], b32[1], b32[2], b32[3]};
-    if (OUT == OUT_Y && tmode != 0) {
-      const float4 s01 = tload(TS_01);
-      if (tmode == 1) {
-        const float4 pp = tload(TS_P), s2 = tload(TS_2);
-        v[0] = s01.x + (s2.x + (pp.x + b32[0]));
-        v[1] = s01.y + (s2.y + (pp.y + b32[1]));
-        v[2] = s01.z + (s2.z + (pp.z + b32[2]));
-        v[3] = s01.w + (s2.w + (pp.w + b32[3]));
-        tstore(TS_P, 0.f, 0.f, 0.f, 0.f);
-        tstore(TS_2, 0.f, 0.f, 0.f, 0.f);
-      } else {
-        v[0] = s01.x + b32[0];
-        v[1] = s01.y + b32[1];
-        v[2] = s01.z + b32[2];
-        v[3] = s01.w + b32[3];
-      }
-      tstore(TS_01, 0.f, 0.f, 0.f, 0.f);
-    }
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      b[i] += (double)v[i];
-      b32[i] = 0.f;
-    }
-    tmode = 0;
-  };
-  // the gathered slot holds the FP32 source in its low word and the column's
-  // OB_* code in its high word
+  // FP32 chain per (row, item): the gathered slot holds the FP32 source in
+  // its low word and "first column of an item" in its high word
   auto consume32 = [&](const float4& v, int cc) {
     const double e = gs[cc];
-    // sub-chain start: fold the tree (a real branch: the compiler would
-    // otherwise predicate the folds onto every column)
-    if (OUT == OUT_Y && __double2hiint(e) != OB_NONE) {
-      const int code = __double2hiint(e);
-      if (code <= OB_ITEM_MAIN) {
-        flush32();
-        tmode = code == OB_ITEM_MAIN ? 1 : 0;
-      } else if (code == OB_B) {
-        tstore(TS_P, b32[0], b32[1], b32[2], b32[3]);
-        tmode = 1;
-      } else if (code < OB_TAIL1) {
-        const float4 pp = tload(TS_P);
-        const float l0 = pp.x + b32[0], l1 = pp.y + b32[1], l2 = pp.z + b32[2], l3 = pp.w + b32[3];
-        if (code == OB_A1) {
-          tstore(TS_01, l0, l1, l2, l3);
-        } else if (code == OB_A1 + 1) {
-          const float4 s01 = tload(TS_01);
-          tstore(TS_01, s01.x + l0, s01.y + l1, s01.z + l2, s01.w + l3);
-        } else {
-          tstore(TS_2, l0, l1, l2, l3);
-        }
-        tstore(TS_P, 0.f, 0.f, 0.f, 0.f);
-        tmode = 1;
-      } else {
-        const float4 pp = tload(TS_P), s01 = tload(TS_01), s2 = tload(TS_2);
-        // main = (l0 + l1) + (l2 + l3)
-        const float m0 = s01.x + (s2.x + (pp.x + b32[0])), m1 = s01.y + (s2.y + (pp.y + b32[1]));
-        const float m2 = s01.z + (s2.z + (pp.z + b32[2])), m3 = s01.w + (s2.w + (pp.w + b32[3]));
-        tstore(TS_P, 0.f, 0.f, 0.f, 0.f);
-        tstore(TS_2, 0.f, 0.f, 0.f, 0.f);
-        if (code == OB_TAIL1) {  // the one tail column is fused onto main
-          tstore(TS_01, 0.f, 0.f, 0.f, 0.f);
-          b32[0] = m0, b32[1] = m1, b32[2] = m2, b32[3] = m3;
-          tmode = 0;
-          goto fma32;
-        }
-        tstore(TS_01, m0, m1, m2, m3);
-        tmode = 2;
-      }
+    // item start: close the previous FP32 partial (a real branch: the
+    // compiler would otherwise predicate the flush onto every column)
+    if (OUT == OUT_Y && __double2hiint(e) != 0) {
 #pragma unroll
-      for (int i = 0; i < 4; ++i) b32[i] = 0.f;
-    fma32:
+      for (int i = 0; i < 4; ++i) {
+        b[i] += (double)b32[i];
+        b32[i] = 0.f;
+      }
       __syncwarp(__activemask());
     }
     const float gf = __int_as_float(__double2loint(e));
@@ -362,6 +426,7 @@ __global__ void __launch_bounds__(NT, DEEP ? 3 : (OUT == OUT_Y && F32MODE != F32
       // row is one FP32 chain (reference: FP32 GEMV per block, matvec.py:57, :73)
       cb = P.gtab[sg.gtab + q32];
       ce = P.gtab[sg.gtab + q32 + 1];
+      if (chain_thr) ce = cb;  // (their items: chain_items after the tile loop)
     }
     // [cb, cm): FP64-accumulated columns, [cm, ce): FP32-accumulated ones
     const int cm = min(ce, max(cb, c32 - tc0));
@@ -453,15 +518,40 @@ __global__ void __launch_bounds__(NT, DEEP ? 3 : (OUT == OUT_Y && F32MODE != F32
     }
     if constexpr (F32MODE != F32_ALL64) {
       if (cm < ce) drain(cm, ce, consume32, std::false_type{});
-      flush32();  // (a tiled part may cut an item between tiles: each piece is closed)
+    }
+  }
+  if constexpr (F32MODE != F32_ALL64) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) b[i] += (double)b32[i];
+  }
+
+  if constexpr (F32MODE != F32_ALL64 && OUT == OUT_Y) {
+    if (chain_thr) {
+      // the part's run meta into shared memory (sidx is free after the
+      // gather), then a barrier among the chain warps only: the widened
+      // warps stream on meanwhile
+      const int wbc = F32MODE == F32_ALL32 ? 0 : sg.chunk;
+      const Run* runs = P.runs + sg.run0 + sg.nrun64;
+      for (int j = tid - wbc; j < sg.nrun32; j += NT - wbc) {
+        const Run r = runs[j];
+        sidx[j] = (r.col0 << kMetaW) | r.width;
+      }
+      asm volatile("bar.sync 1, %0;" ::"r"(NT - wbc) : "memory");
+      if (q32 < g32)
+        bc = chain_items(sidx, sg.nrun32, P.blob32 + sg.off32, gs, P.gtab[sg.gtab + q32],
+                         P.gtab[sg.gtab + q32 + 1], rp32, pc);
     }
   }
 
   // ---------------- fixed-order reduction over thread groups
   __syncthreads();
   if (sg.W32 > 0 && q32 < g32) {
+    if (chain_thr) {
+      red32[q32 * rp32 + pc] = bc;
+    } else {
 #pragma unroll
-    for (int i = 0; i < 4; ++i) red32[q32 * rp32 + 4 * p32 + i] = b[i];
+      for (int i = 0; i < 4; ++i) red32[q32 * rp32 + 4 * p32 + i] = b[i];
+    }
   }
   __syncthreads();
   // row sums over groups (fixed order); a thread owns rows tid, tid + NT, ...
@@ -605,10 +695,10 @@ __global__ void probe_kernel(DevPlan P, const double* __restrict__ x, unsigned l
       double s = 0.0;
       float s32 = 0.f;
       for (int c = 0; c < r.width; ++c) {
-        int code;
-        double g = src[r.src + ((r.flags & RUN_OBL) ? obl_col(r.width, c, &code) : c)];
+        double g = src[r.src + c];
         if (r.flags & RUN_ROUND) g = (double)(float)g;
-        const int64_t e = (int64_t)(r.col0 + c) * rp + row;
+        const int64_t e = (r.flags & RUN_CHUNK) ? (int64_t)r.col0 * rp + chunk_off(r.width, rp, row, c)
+                                                : (int64_t)(r.col0 + c) * rp + row;
         if (f32part) {
           const float m = P.blob32[sg.off32 + e];
           if (r.flags & RUN_ACC32) s32 = fmaf(m, (float)g, s32);
@@ -626,20 +716,13 @@ __global__ void probe_kernel(DevPlan P, const double* __restrict__ x, unsigned l
 // ------------------------------------------------------------------------------
 // launchers
 
-// dynamic shared memory of a seg_kernel instantiation: the FP32 lane-tree
-// state of stage 2's FP32-accumulated items
-template <int M, int O, int NT>
-constexpr size_t tree_smem() {
-  return (O == OUT_Y && M != F32_ALL64) ? 3 * NT * sizeof(float4) : 0;
-}
-
 template <int M, int O, int NT = kSegThreads, bool DEEP = false>
 static cudaError_t launch_seg(const DevPlan& P, const Seg* segs, int nseg, const double* x,
                               const S2Out& out, cudaStream_t st, bool pdl) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)nseg);
   cfg.blockDim = dim3(NT);
-  cfg.dynamicSmemBytes = tree_smem<M, O, NT>();
+  cfg.dynamicSmemBytes = 0;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -678,19 +761,6 @@ cudaError_t launch_stage2(const DevPlan& P, const double* x, const S2Out& out, c
       return P.s2_deep ? launch_seg<F32_ALL64, OUT_Y, kSegThreads, true>(P, P.seg2, P.n_seg2, x, out, st, pdl)
                        : launch_seg<F32_ALL64, OUT_Y>(P, P.seg2, P.n_seg2, x, out, st, pdl);
   }
-}
-
-// Opt the stage-2 FP32 kernels into > 48 KB of shared memory (static +
-// the lane-tree state); called once per plan creation, outside any capture.
-cudaError_t configure_kernels() {
-  cudaError_t e = cudaFuncSetAttribute(seg_kernel<F32_ALL32, OUT_Y, kSegThreads, false>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)tree_smem<F32_ALL32, OUT_Y, kSegThreads>());
-  if (e == cudaSuccess)
-    e = cudaFuncSetAttribute(seg_kernel<F32_MIXED, OUT_Y, kSegThreads, false>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)tree_smem<F32_MIXED, OUT_Y, kSegThreads>());
-  return e;
 }
 
 cudaError_t launch_gather_perm(const double* x, const int32_t* perm, double* xp, int n,

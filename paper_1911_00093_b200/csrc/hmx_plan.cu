@@ -97,8 +97,10 @@ void hmx_plan_destroy(hmx_plan* p) {
       if (p->ws->loop_graph) cudaGraphDestroy(p->ws->loop_graph);
     }
     delete p->ws;
+    if (p->ev_tail) cudaEventSynchronize(p->ev_tail);
     for (auto& e : p->ev)
       if (e) cudaEventDestroy(e);
+    if (p->ev_tail) cudaEventDestroy(p->ev_tail);
     if (p->stream) cudaStreamDestroy(p->stream);
   }
   delete p;
@@ -137,7 +139,6 @@ int hmx::plan_create_impl(const hmx_matrix_desc* d, int device, const hmx_plan_o
   }
   const int pipe = d->scheme;
   const bool has_lo = pipe == P_M3;
-  HMX_CUDA(configure_kernels());
   const int64_t rb = opt && opt->row_end > 0 ? opt->row_begin : 0;
   const int64_t re = opt && opt->row_end > 0 ? opt->row_end : n;
   if (rb < 0 || re > n || rb >= re) {
@@ -375,7 +376,7 @@ int hmx::plan_create_impl(const hmx_matrix_desc* d, int device, const hmx_plan_o
   // column in a mixed FP32 part (A/B on config 4 with the warp-aligned split:
   // m1-mixed best at 0.8-1.0, m2-single at 1/1.0-1/1.2)
   const char* aw_env = std::getenv("HMX_ACC64_WEIGHT");
-  const double acc64_weight = aw_env ? std::atof(aw_env) : 0.85;
+  const double acc64_weight = aw_env ? std::atof(aw_env) : 2.5;
   const bool dense_single = pipe == P_M1S || pipe == P_M2S;  // A32 . x32 in FP32
   const bool u_acc32 = pipe == P_M1S || pipe == P_M1M;       // U32 . z32 in FP32
   bool any_acc32 = false, any_acc64_in32 = false;
@@ -427,7 +428,8 @@ int hmx::plan_create_impl(const hmx_matrix_desc* d, int device, const hmx_plan_o
     int64_t W = 0;
     for (const ItemRef& it : lst) W += item_width(it);
     if (W > kSegWMax) return fg;  // tiled part: no group table
-    const int64_t tpg = round_up(R, 4) / 4, G = kSegThreads / tpg;
+    // widened groups: 4 rows per thread; chain groups: one row per thread
+    const int64_t rp = round_up(R, 4), tpg = rp / 4, G = kSegThreads / tpg, Gc = kSegThreads / rp;
     size_t nA = 0;
     while (nA < lst.size() && !item_acc32(lst[nA])) ++nA;
     int64_t colsA = 0;
@@ -435,11 +437,11 @@ int hmx::plan_create_impl(const hmx_matrix_desc* d, int device, const hmx_plan_o
     std::vector<int64_t> wB;
     for (size_t i = nA; i < lst.size(); ++i) wB.push_back(item_width(lst[i]));
     fg.c32 = colsA;
-    int64_t gA = 0, gB = G;
+    int64_t gA = 0, gB = Gc;
     if (nA > 0 && !wB.empty()) {
       double best = 1e300;
       for (int64_t wb = 32; wb < kSegThreads; wb += 32) {
-        const int64_t ga = wb / tpg, gb = (kSegThreads - wb) / tpg;
+        const int64_t ga = wb / tpg, gb = (kSegThreads - wb) / rp;
         if (ga < 1 || gb < 1) continue;
         const double t = std::max(acc64_weight * (double)colsA / (double)ga, (double)lpt(wB, gb, nullptr));
         if (t < best) {
@@ -452,6 +454,7 @@ int hmx::plan_create_impl(const hmx_matrix_desc* d, int device, const hmx_plan_o
     } else if (nA > 0) {
       gA = G;
       gB = 0;
+      fg.wb = kSegThreads;  // no chain threads
     }
     // widened range [0, colsA): even cuts over gA groups (or all G groups
     // when there are no chains)
@@ -493,14 +496,16 @@ int hmx::plan_create_impl(const hmx_matrix_desc* d, int device, const hmx_plan_o
         r.col0 = (int32_t)col;
         if (it.cls == 0) {
           r.src = (int32_t)t[2];
-          r.flags = (part == 1 && dense_single) ? (RUN_ROUND | RUN_ACC32 | RUN_OBL) : 0;
+          r.flags = (part == 1 && dense_single) ? (RUN_ROUND | RUN_ACC32) : 0;
         } else {
           r.src = (int32_t)(it.cls == 1 ? zoff_hi[(size_t)it.block] : zoff_lo[(size_t)it.block]);
-          r.flags = RUN_Z | ((part == 1 && it.cls == 1 && u_acc32) ? (RUN_ACC32 | RUN_OBL) : 0);
+          r.flags = RUN_Z | ((part == 1 && it.cls == 1 && u_acc32) ? RUN_ACC32 : 0);
         }
         if (part == 1) {
           if (r.flags & RUN_ACC32) any_acc32 = true;
           else any_acc64_in32 = true;
+          // parts with a group table: chain items in SGEMV chunk layout
+          if ((r.flags & RUN_ACC32) && !fg.cuts.empty()) r.flags |= RUN_CHUNK;
         }
         runs.push_back(r);
         run_block.push_back(it.block);
@@ -595,16 +600,14 @@ int hmx::plan_create_impl(const hmx_matrix_desc* d, int device, const hmx_plan_o
         src_off = d->lo_off[it.block];
         src32 = true;
       }
-      // FP32-accumulated items are stored in SGEMV lane order (obl_col)
-      const bool obl = part == 1 && item_acc32(it);
+      // chain items of group-table parts: SGEMV chunk layout (chunk_off)
+      const bool chunk = part == 1 && item_acc32(it) && sg.gtab >= 0;
       for (int64_t i = 0; i < sg.R; ++i) {
         const int64_t e0 = src_off + (r0 + i) * w;
         for (int64_t c = 0; c < w; ++c) {
-          int code;
-          const int64_t sc = obl ? obl_col((int)w, (int)c, &code) : c;
-          const int64_t dst = o + (col + c) * rp + i;
-          if (part == 0) b64[(size_t)dst] = src32 ? d->buf32[e0 + sc] : d->buf64[e0 + sc];
-          else b32[(size_t)dst] = src32 ? d->buf32[e0 + sc] : (float)d->buf64[e0 + sc];
+          const int64_t dst = o + col * rp + (chunk ? chunk_off((int)w, (int)rp, (int)i, (int)c) : c * rp + i);
+          if (part == 0) b64[(size_t)dst] = src32 ? d->buf32[e0 + c] : d->buf64[e0 + c];
+          else b32[(size_t)dst] = src32 ? d->buf32[e0 + c] : (float)d->buf64[e0 + c];
         }
       }
       col += w;
@@ -733,7 +736,8 @@ int hmx::plan_create_impl(const hmx_matrix_desc* d, int device, const hmx_plan_o
         u.nitems = (int32_t)lst.size();
         u.is32 = part;
         for (const ItemRef& it : lst)
-          pit.push_back({it.block, it.cls, (int32_t)item_width(it), (part == 1 && item_acc32(it)) ? 1 : 0});
+          pit.push_back({it.block, it.cls, (int32_t)item_width(it),
+                         (part == 1 && item_acc32(it) && sg.gtab >= 0) ? 1 : 0});
         ps2.push_back(u);
       }
     }
@@ -863,6 +867,7 @@ int hmx::plan_create_impl(const hmx_matrix_desc* d, int device, const hmx_plan_o
   HMX_CUDA(cudaMemset(p->d_done, 0, sizeof(uint32_t)));
   HMX_CUDA(cudaMallocHost(&p->h_flag, 4 * sizeof(int)));
   for (auto& e : p->ev) HMX_CUDA(cudaEventCreate(&e));
+  HMX_CUDA(cudaEventCreateWithFlags(&p->ev_tail, cudaEventDisableTiming));
 
   hmx_plan_info& info = p->info;
   info.n = n;
@@ -936,6 +941,7 @@ int hmx_matvec(hmx_plan* p, const double* x, double* y, int flags) {
   const int64_t n = p->n;
   const bool dev = flags & HMX_DEVICE_PTRS, permuted = flags & HMX_PERMUTED;
   cudaStream_t st = p->stream;
+  HMX_CUDA(plan_enter(p, st));
   const double* src;
   if (dev) {
     src = x;
@@ -979,6 +985,7 @@ int hmx_nonfinite_block(hmx_plan* p, int64_t* block) {
     return HMX_OK;
   }
   cudaStream_t st = p->stream;
+  HMX_CUDA(plan_enter(p, st));
   HMX_CUDA(cudaMemsetAsync(p->d_first_bad, 0xff, sizeof(unsigned long long), st));
   HMX_CUDA(launch_probe(p->dp, p->last_xp, p->d_first_bad, st));
   unsigned long long v = 0;
@@ -1010,8 +1017,10 @@ int hmx_apply_local(hmx_plan* p, const double* xp, double* y, const double* w1, 
     out.dots_out = dots;
   }
   out.nonfinite = nonfinite ? nonfinite : p->d_nonfinite;
+  HMX_CUDA(plan_enter(p, st));
   HMX_CUDA(launch_stage1(p->dp, xp, st));
   HMX_CUDA(launch_stage2(p->dp, xp, out, st, /*pdl=*/true));
+  HMX_CUDA(plan_leave(p, st));
   p->last_xp = xp;
   return HMX_OK;
 }
@@ -1021,6 +1030,7 @@ int hmx_bench_matvec(hmx_plan* p, int warmup, int iters, int64_t flush_l2, doubl
   std::lock_guard<std::mutex> lock(p->mu);
   DeviceGuard guard(p->device);
   cudaStream_t st = p->stream;
+  HMX_CUDA(plan_enter(p, st));
   void* flush = nullptr;
   if (flush_l2 > 0) HMX_CUDA(cudaMalloc(&flush, (size_t)flush_l2));
   S2Out out{};

@@ -99,9 +99,12 @@ struct hmx_plan {
   unsigned long long* d_first_bad = nullptr;
   // pinned host staging
   int* h_flag = nullptr;
-  // input of the most recent matvec (for the non-finite probe)
+  // input of the most recent matvec (for the non-finite probe; the caller of
+  // hmx_apply_local keeps it alive until hmx_nonfinite_block returns)
   const double* last_xp = nullptr;
   cudaEvent_t ev[8] = {};
+  // end of the plan's most recent asynchronous work (any stream); see plan_enter
+  cudaEvent_t ev_tail = nullptr;
 
   template <typename T>
   T* alloc(size_t count) {
@@ -114,6 +117,19 @@ struct hmx_plan {
 };
 
 // FP64 masters resident on a device (hmx_master_create / hmx_master_build).
+// A plan's device work may be queued on several streams (its own, a caller's
+// in hmx_apply_local / hmx_dist_matvec) and it shares per-plan scratch (z,
+// chunk partials, arrival counters, flags).  Every entry point makes its
+// stream wait for the plan's previous asynchronous work first (plan_enter);
+// the asynchronous ones record their end (plan_leave).  The plan mutex orders
+// the enqueues, these events order the device work.
+inline cudaError_t plan_enter(hmx_plan* p, cudaStream_t st) {
+  return p->ev_tail ? cudaStreamWaitEvent(st, p->ev_tail, 0) : cudaSuccess;
+}
+inline cudaError_t plan_leave(hmx_plan* p, cudaStream_t st) {
+  return p->ev_tail ? cudaEventRecord(p->ev_tail, st) : cudaSuccess;
+}
+
 struct hmx_master {
   int device = 0;
   int64_t n = 0, nb = 0, n_data = 0, rank_sum = 0, max_rank = 0;
@@ -169,7 +185,7 @@ struct PackS2 {
   int32_t R, rp, row0, item0, nitems, is32;
 };
 struct PackItem {
-  int32_t block, cls, width, pad;  // cls 0 dense, 1 hi, 2 lo; pad 1: store in obl_col order
+  int32_t block, cls, width, pad;  // cls 0 dense, 1 hi, 2 lo; pad 1: SGEMV chunk layout (chunk_off)
 };
 struct PackRow {
   int32_t block, q;

@@ -143,10 +143,9 @@ __global__ void pack_s2_kernel(DevSource S, const PackS2* __restrict__ units, co
     const int64_t r0 = u.row0 - tb[0];
     const int64_t total = (int64_t)u.R * p.width;
     for (int64_t e = threadIdx.x; e < total; e += blockDim.x) {
-      const int i = (int)(e % u.R), cs = (int)(e / u.R);
-      const int64_t dst = u.dst + (col + cs) * u.rp + i;
-      int code;  // FP32-accumulated items: stored in SGEMV lane order (hmx_internal.cuh)
-      const int c = p.pad ? obl_col(p.width, cs, &code) : cs;
+      const int i = (int)(e % u.R), c = (int)(e / u.R);
+      // chain items of group-table parts: SGEMV chunk layout (hmx_internal.cuh)
+      const int64_t dst = u.dst + col * u.rp + (p.pad ? chunk_off(p.width, u.rp, i, c) : (int64_t)c * u.rp + i);
       if (p.cls == 0) {
         lost += put(b64, b32, dst, u.is32, S.data[S.offset[k] + (r0 + i) * n + c], k, S);
       } else {

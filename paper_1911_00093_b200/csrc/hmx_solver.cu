@@ -555,6 +555,7 @@ int hmx_true_residual(hmx_plan* p64, const double* x, const double* b, double* o
   SolveCtx c{};
   c.A = c.A64 = p64;
   c.st = p64->stream;
+  HMX_CUDA(plan_enter(p64, c.st));
   c.grid = 2 * sms;
   int rc = workspace_for(p64, c.w, c.grid);
   if (rc) return rc;
@@ -595,6 +596,8 @@ int hmx_bicgstab(hmx_plan* A, hmx_plan* A64, const double* b, double tol, int ma
   c.A = A;
   c.A64 = A64;
   c.st = A->stream;
+  HMX_CUDA(plan_enter(A, c.st));
+  if (A64 != A) HMX_CUDA(plan_enter(A64, c.st));
   c.grid = 2 * sms;
   int rc = workspace_for(A, c.w, c.grid);
   if (rc) return rc;
@@ -1128,10 +1131,14 @@ int hmx_dist_matvec(hmx_plan* p, hmx_comm* c, const double* x_local, double* y_l
   DeviceGuard guard(p->device);
   cudaStream_t st = stream == UINT64_MAX ? p->stream : reinterpret_cast<cudaStream_t>(stream);
   const int64_t nl = c->r1 - c->r0;
+  HMX_CUDA(plan_enter(p, st));
   if (nl > 0 && x_local != c->x_full + c->r0)
     HMX_CUDA(cudaMemcpyAsync(c->x_full + c->r0, x_local, (size_t)nl * sizeof(double), cudaMemcpyDeviceToDevice, st));
-  return dist_apply(c, p, c->sc, st, c->x_full, y_local, nullptr, 0, 0,
-                    nonfinite ? nonfinite : p->d_nonfinite);
+  const int rc = dist_apply(c, p, c->sc, st, c->x_full, y_local, nullptr, 0, 0,
+                            nonfinite ? nonfinite : p->d_nonfinite);
+  if (rc) return rc;
+  HMX_CUDA(plan_leave(p, st));
+  return HMX_OK;
 }
 
 int hmx_bicgstab_dist(hmx_plan* A, hmx_plan* A64, hmx_comm* c, const double* b_local, double tol,
@@ -1158,6 +1165,8 @@ int hmx_bicgstab_dist(hmx_plan* A, hmx_plan* A64, hmx_comm* c, const double* b_l
   *rep = hmx_solve_report{};
   DistCtx d{A, A64, c, A->stream, c->grid, (int)(c->r1 - c->r0)};
   cudaStream_t st = d.st;
+  HMX_CUDA(plan_enter(A, st));
+  if (A64 != A) HMX_CUDA(plan_enter(A64, st));
   const size_t nlb = (size_t)d.nl * sizeof(double);
   int rc;
 

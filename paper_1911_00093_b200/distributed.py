@@ -71,30 +71,62 @@ def row_costs(table: np.ndarray, kinds: np.ndarray, ranks: np.ndarray, n: int,
 def partition_rows(table: np.ndarray, kinds: np.ndarray, ranks: np.ndarray, n: int,
                    world: int) -> list[int]:
     """Cut points r_0 = 0 < r_1 < ... < r_world = n at leaf boundaries with
-    balanced bytes; prefers cuts that no block straddles (tree-aligned)."""
+    balanced bytes; prefers cuts that no block straddles (tree-aligned).
+    O(blocks + n): straddled boundaries come from a difference array."""
     if world == 1:
         return [0, n]
+    if world > n:
+        raise ValueError(f"cannot cut {n} rows into {world} non-empty slices")
     bounds, cum = row_costs(table, kinds, ranks, n)
     total = cum[-1]
-    # boundaries that no block straddles: no block has rs < b < re
-    starts, ends = table[:, 0], table[:, 1]
-    order = np.argsort(starts)
-    clean = np.ones(bounds.size, dtype=bool)
-    for i, b in enumerate(bounds):
-        clean[i] = not np.any((starts < b) & (ends > b))
+    # boundary b is straddled when some block has rs < b < re: count the
+    # blocks covering each row index in (rs, re) with a difference array
+    cover = np.zeros(n + 2, dtype=np.int64)
+    np.add.at(cover, table[:, 0] + 1, 1)
+    np.add.at(cover, table[:, 1], -1)
+    clean = np.cumsum(cover)[bounds] == 0
+    cand = np.flatnonzero(clean)
     cuts = [0]
     for k in range(1, world):
         target = total * k / world
-        cand = np.where(clean)[0]
-        j = cand[np.argmin(np.abs(cum[cand] - target))]
+        j = cand[np.argmin(np.abs(cum[cand] - target))] if cand.size else 0
         # accept a straddled boundary if a clean one is more than 5% off
-        j_any = int(np.argmin(np.abs(cum - target)))
-        if abs(cum[j] - target) > 0.05 * total / world:
-            j = j_any
-        cuts.append(int(max(bounds[j], cuts[-1] + 1)))
+        if not cand.size or abs(cum[j] - target) > 0.05 * total / world:
+            j = int(np.argmin(np.abs(cum - target)))
+        # strictly increasing, and room left for the remaining ranks
+        cuts.append(int(min(max(bounds[j], cuts[-1] + 1), n - (world - k))))
     cuts.append(n)
-    del order
     return cuts
+
+
+def measured_cuts(mesh, partition, aca_tol: float, world: int, rank: int, group=None,
+                  device=None) -> list[int]:
+    """Row cuts balanced on the MEASURED stored bytes: cut on an
+    estimate (rank 11 per admissible block), build this rank's rows, take the
+    real ranks of every block from the rank(s) that built it (an allreduce
+    max over the group: a block meeting several slices has the same rank on
+    each), and cut again on them.  Collective over `group`."""
+    import torch
+    import torch.distributed as dist
+
+    from .compress import build_hmatrix
+
+    table = partition.table
+    kinds = table[:, 4].astype(np.int32)
+    n = int(mesh.n)
+    if world == 1:
+        return [0, n]
+    est = np.where(kinds == 1, 11, 0)
+    cuts0 = partition_rows(table, kinds, est, n, world)
+    h0 = build_hmatrix(mesh, partition=partition, aca_tol=aca_tol, rows=(cuts0[rank], cuts0[rank + 1]))
+    built = np.asarray(h0.packed.kinds) != 2
+    r = np.where(built, np.asarray(h0.packed.ranks), 0).astype(np.int64)
+    t = torch.from_numpy(r)
+    if device is not None and dist.get_backend(group) == "nccl":
+        t = t.to(device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
+    ranks = t.cpu().numpy()
+    return partition_rows(table, kinds, ranks, n, world)
 
 
 @dataclass
@@ -356,10 +388,9 @@ def bench_main(args, build_workload, workload_name, metric):
     mesh = jittered_sphere_mesh(c["level"], seed=42, centers=c.get("centers", ((0.0, 0.0, 0.0),)),
                                 voltages=c.get("voltages"))
     part = build_block_partition(build_cluster_tree(mesh, c["leaf"]), 2.0)
-    # partition on an estimate (ranks unknown before ACA): ranks ~ 11
-    kinds = part.table[:, 4].astype(np.int32)
-    est = np.where(kinds == 1, 11, 0)
-    slices = RowSlices(partition_rows(part.table, kinds, est, mesh.n, world))
+    # cut on the measured stored bytes (an estimate cut, a build, the real
+    # ranks exchanged, a re-cut)
+    slices = RowSlices(measured_cuts(mesh, part, c["aca"], world, rank, device=device))
     h = build_hmatrix(mesh, partition=part, aca_tol=c["aca"], rows=slices.span(rank))
     t_build = time.perf_counter() - t0
     peak, peak_src = bench_mod.measured_peak()

@@ -57,6 +57,17 @@ def true_residual(h64, x, b) -> float:
     """||b - A x|| / ||b|| with the FP64 operator (solver.py:56-65)."""
     b = np.ascontiguousarray(b, dtype=np.float64)
     x = np.ascontiguousarray(x, dtype=np.float64)
+    n = h64.n
+    # the reference raises here too: matvec's shape check (matvec.py:115-116),
+    # then numpy broadcasting of b - A x
+    if x.shape != (n,):
+        raise ValueError(f"vector shape {x.shape} does not match matrix size {n}")
+    if b.shape in ((), (1,)):
+        # numpy broadcasts a scalar-like b in `b - A x`, while ||b|| stays the
+        # norm of the scalar: ||b_full|| = sqrt(n) |b|
+        return true_residual(h64, x, np.full(n, float(b.reshape(-1)[0]))) * float(np.sqrt(n))
+    if b.shape != (n,):
+        raise ValueError(f"operands could not be broadcast together with shapes {b.shape} ({n},)")
     plan = get_plan64(h64)
     out = ctypes.c_double(0.0)
     rc = plan._lib.hmx_true_residual(plan.handle, x.ctypes.data, b.ctypes.data,

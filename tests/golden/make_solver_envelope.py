@@ -22,7 +22,6 @@ each its own --out and merge with --merge.
 from __future__ import annotations
 
 import argparse
-import hashlib
 import json
 import os
 import sys
@@ -34,22 +33,9 @@ import numpy as np
 HERE = Path(__file__).resolve().parent
 ROOT = HERE.parent.parent
 sys.path.insert(0, str(ROOT))
+sys.path.insert(0, str(ROOT / "tests"))
 
-
-def fingerprint(h) -> dict:
-    """Cheap identity of an H-matrix: sha256 of the block table and ranks, and
-    an order-sensitive 64-bit checksum of every stored FP64 master value."""
-    pm = h.packed
-    tab = np.ascontiguousarray(h.partition.table, dtype=np.int64)
-    d = hashlib.sha256(tab.tobytes())
-    d.update(np.ascontiguousarray(pm.ranks, dtype=np.int64).tobytes())
-    bits = np.ascontiguousarray(pm.data).view(np.uint64)
-    w = (np.arange(bits.size, dtype=np.uint64) * np.uint64(0x9E3779B97F4A7C15)) | np.uint64(1)
-    with np.errstate(over="ignore"):
-        mix = int(np.bitwise_xor.reduce(bits * w)) if bits.size else 0
-        tot = int(np.add.reduce(bits, dtype=np.uint64)) if bits.size else 0
-    return {"table_ranks_sha256": d.hexdigest(), "data_xor_mix": f"{mix:016x}",
-            "data_sum": f"{tot:016x}", "n_values": int(bits.size)}
+from golden_util import fingerprint  # noqa: E402
 
 
 def main():

@@ -44,3 +44,21 @@ def config1_hmatrix():
     import paper_1911_00093_b200 as hx
     mesh = hx.jittered_sphere_mesh(3, seed=42)
     return mesh, hx.build_hmatrix(mesh, aca_tol=1e-4, leaf_size=32, eta=2.0)
+
+
+def fingerprint(h) -> dict:
+    """Cheap identity of an H-matrix: sha256 of the block table and ranks, and
+    order-sensitive 64-bit checksums of every stored FP64 master value (used
+    to assert that a test solves the matrix a golden file was made on)."""
+    import hashlib
+    pm = h.packed
+    tab = np.ascontiguousarray(h.partition.table, dtype=np.int64)
+    d = hashlib.sha256(tab.tobytes())
+    d.update(np.ascontiguousarray(pm.ranks, dtype=np.int64).tobytes())
+    bits = np.ascontiguousarray(pm.data).view(np.uint64)
+    w = (np.arange(bits.size, dtype=np.uint64) * np.uint64(0x9E3779B97F4A7C15)) | np.uint64(1)
+    with np.errstate(over="ignore"):
+        mix = int(np.bitwise_xor.reduce(bits * w)) if bits.size else 0
+        tot = int(np.add.reduce(bits, dtype=np.uint64)) if bits.size else 0
+    return {"table_ranks_sha256": d.hexdigest(), "data_xor_mix": f"{mix:016x}",
+            "data_sum": f"{tot:016x}", "n_values": int(bits.size)}

@@ -84,3 +84,23 @@ def test_shape_errors_before_device(hx):
         hx.SourceVector(np.zeros((2, 2)))
     with pytest.raises(ValueError):
         hx.SolverConfig(tol=0.0)
+    # true_residual checks both operands before any device work
+    with pytest.raises(ValueError, match="does not match"):
+        hx.true_residual(h, np.ones(mesh.n - 1), np.ones(mesh.n))
+    with pytest.raises(ValueError, match="broadcast"):
+        hx.true_residual(h, np.ones(mesh.n), np.ones(mesh.n + 3))
+
+
+def test_nccl_shim_builds_and_exports_the_resolved_symbols():
+    """tests/shim (the multi-process GPU test's NCCL stand-in) compiles and
+    exports the nine functions hmx_solver.cu's nccl_api() resolves."""
+    import ctypes
+
+    from test_gpu_dist_shim import build_shim
+    lib = ctypes.CDLL(str(build_shim()))
+    for name in ("ncclGetUniqueId", "ncclCommInitRank", "ncclCommDestroy", "ncclGetErrorString",
+                 "ncclGroupStart", "ncclGroupEnd", "ncclSend", "ncclRecv", "ncclAllReduce"):
+        assert hasattr(lib, name), name
+    src = (Path(__file__).resolve().parent.parent / "paper_1911_00093_b200" / "csrc" / "hmx_solver.cu").read_text()
+    for name in ("ncclGetUniqueId", "ncclCommInitRank", "ncclGroupEnd", "ncclAllReduce"):
+        assert f'"{name}"' in src

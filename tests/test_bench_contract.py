@@ -37,6 +37,8 @@ def test_reference_arm_line():
     assert d["e2e"] == {"value": d["value"], "unit": "matvec/s", "h2d_bytes_per_step": 0,
                         "d2h_bytes_per_step": 0}
     assert d["config"]["n"] == 20480
+    assert cb["sample"].startswith("full matvec per step")   # measured, not extrapolated
+    assert set(d["config"]) == {"workload", "scheme", "n", "blocks", "parallelism", "l2"}
 
 
 def test_warmup_floor_is_three():
@@ -61,8 +63,13 @@ def test_our_arm_line():
     assert 0 < e["value"] <= d["value"] * 1.05  # host copies inside the timed region
     assert d["gpu_launches"] == 2 * 20
     assert {"sm_mhz", "sm_max_mhz", "reasons"} <= d["clocks"].keys()
+    assert d["clocks"]["samples"] >= 1 and d["clocks"]["sm_mhz"] > 0   # even a ~1 ms region
     v = d["variants"]["m1-double"]
     assert v["stage1_ms"] > 0 and v["stage2_ms"] > 0
+    assert e["pageable"]["value"] > 0
+    # the reference arm prints the very same config object (the driver's same_config)
+    ref = _run("--impl", "reference", "--config", "2", "--steps", "3", "--warmup", "3")
+    assert ref["config"] == d["config"]
 
 
 @pytest.mark.gpu

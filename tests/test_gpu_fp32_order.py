@@ -2,8 +2,9 @@
 U slabs, m2-single dense blocks; reference matvec.py:57, :73 -- numpy
 `A32 @ x32`, i.e. OpenBLAS SGEMV).
 
-The GPU evaluates every such item in SGEMV's own lane tree
-(csrc/hmx_internal.cuh obl_col, consume32 in csrc/hmx_kernels.cu).  Checked
+The GPU evaluates every such item in SGEMV's own summation tree, one row
+per thread (csrc/hmx_internal.cuh chunk_off layout, chain_items in
+csrc/hmx_kernels.cu).  Checked
 here:
   * CPU: the kernel's order, modelled in tools/fp32_accum_emulation.py
     (sgemv_tree), reproduces the reference's products bitwise
@@ -44,13 +45,21 @@ def test_model_reproduces_reference_products():
                 assert np.array_equal(y, ref), (m, n)
 
 
-def test_obl_col_is_a_permutation_with_one_start_per_item():
-    from tools.fp32_accum_emulation import OB_ITEM_CHAIN, OB_ITEM_MAIN, obl_col
-    for n in range(1, 300):
-        cols = [obl_col(n, k) for k in range(n)]
-        assert sorted(c for c, _ in cols) == list(range(n)), n
-        assert cols[0][1] in (OB_ITEM_CHAIN, OB_ITEM_MAIN)
-        assert all(code not in (OB_ITEM_CHAIN, OB_ITEM_MAIN) for _, code in cols[1:])
+def test_chunk_layout_is_a_permutation():
+    """chunk_off (csrc/hmx_internal.cuh, ported in the emulation tool) places
+    every (row, column) of an item exactly once within rp * n elements, and
+    4-column chunks of one row are 16-byte aligned vectors."""
+    from tools.fp32_accum_emulation import chain_shaped, chunk_off
+    for rp in (4, 20, 40, 64):
+        for n in range(1, 70):
+            offs = sorted(chunk_off(n, rp, r, k) for r in range(rp) for k in range(n))
+            assert offs == list(range(rp * n)), (rp, n)
+            if not chain_shaped(n):
+                for r in range(rp):
+                    for c in range(n // 4):
+                        o = chunk_off(n, rp, r, 4 * c)
+                        assert o % 4 == 0 and [chunk_off(n, rp, r, 4 * c + j) for j in range(4)] == \
+                            [o, o + 1, o + 2, o + 3]
 
 
 def _block_diagonal(hx, m, widths, values):

@@ -1,0 +1,57 @@
+"""BiCG-STAB parity at BASELINE configs 2-4 against the REFERENCE ALGORITHM's
+own reordering envelope.
+
+tests/golden/solver_envelope_config<k>.json holds, for the headline schemes,
+the oracle BiCG-STAB (pinned bit-for-bit to reference solver.py:68-168) run
+with matvec_threaded(threads = 1..8) -- the summation reorderings the
+reference itself accepts (matvec.py:161-197) -- on THIS repo's H-matrix of
+the config (made by tests/golden/make_solver_envelope.py in the build
+container; the matrix fingerprint is checked here).  North-star criterion:
+the GPU's stop iteration lies in [min - max(1, 5 %), max + max(1, 5 %)] of
+that envelope, and its `converged` flag is one the envelope produced.
+"""
+import json
+
+import numpy as np
+import pytest
+
+from golden_util import GOLDEN, fingerprint
+
+pytestmark = pytest.mark.gpu
+
+
+def envelope(cfg):
+    f = GOLDEN / f"solver_envelope_config{cfg}.json"
+    if not f.exists():
+        pytest.skip(f"{f.name} not generated")
+    return json.loads(f.read_text())
+
+
+def check(rep, runs):
+    its = [r["iterations"] for r in runs]
+    lo = min(its) - max(1.0, 0.05 * min(its))
+    hi = max(its) + max(1.0, 0.05 * max(its))
+    assert lo <= rep.iterations <= hi, (rep.iterations, sorted(its))
+    assert rep.converged in {r["converged"] for r in runs}, (rep.converged, [r["converged"] for r in runs])
+    assert rep.breakdown is None and rep.true_residual is not None
+    assert rep.converged == (rep.true_residual < 1e-8)
+
+
+@pytest.mark.parametrize("cfg", [2, 3, 4])
+def test_bicgstab_inside_reference_envelope(hx, cfg):
+    import bench
+    env = envelope(cfg)
+    _, h, _, b, _ = bench.build_workload(cfg)
+    assert fingerprint(h) == env["fingerprint"], "not the H-matrix the envelope was made on"
+    out = {}
+    for s, runs in env["schemes"].items():
+        sh = hx.prepare_scheme(h, s)
+        _, rep = hx.bicgstab(sh, h, b, hx.SolverConfig(tol=env["tol"], max_iter=env["max_iter"]))
+        out[s] = (rep.iterations, rep.converged, rep.true_residual)
+        check(rep, list(runs.values()))
+        # the first iterations follow the reference algorithm's residual history
+        ref = np.asarray(runs["1"]["residual_history"][:6])
+        got = np.asarray(rep.residual_history[:6])
+        assert np.allclose(got, ref, rtol=1e-6 if s == "m1-double" else 1e-4), s
+        del sh
+    print(out)

@@ -14,8 +14,8 @@ FP64 (m1-double) product and y_ref the reference's own FP32 result.  Orders:
           (K = 8: ((l0+l4)+(l1+l5))+((l2+l6)+(l3+l7)), what OpenBLAS's SGEMV
           does on this container for widths that are multiples of 8 --
           probed with tools/sgemv_order_probe.py)
-  sgemv   the GPU kernel's order since round 2 (obl_col + lane tree of
-          csrc/hmx_internal.cuh): OpenBLAS SGEMV-T's own tree
+  sgemv   the GPU kernel's order since round 2 (chain_items in
+          csrc/hmx_kernels.cu): OpenBLAS SGEMV-T's own tree
 
 FMA is emulated as round32(round64(a*b) + c) with the product exact in FP64;
 the double rounding differs from a true fused FMA in rare ties only, which is
@@ -67,36 +67,17 @@ def fma_chain(a, g, acc=None):
     return acc
 
 
-OB_NONE, OB_ITEM_CHAIN, OB_ITEM_MAIN, OB_B, OB_A1, OB_TAIL1, OB_TAIL = 0, 1, 2, 3, 4, 7, 8
+def chain_shaped(n: int) -> bool:
+    return n <= 3 or 5 <= n <= 7
 
 
-def obl_col(n: int, k: int):
-    """Port of csrc/hmx_internal.cuh obl_col: (original column, OB_* code) of
-    stored position k of an n-wide FP32-accumulated item."""
-    if n <= 3 or 5 <= n <= 7:
-        return k, (OB_ITEM_CHAIN if k == 0 else OB_NONE)
-    mainw = n & ~3
-    nch = mainw >> 2
-    if k < mainw:
-        j, r = divmod(k, nch)
-        na = (nch + 1) >> 1
-        code = OB_NONE
-        if r == 0:
-            code = OB_ITEM_MAIN if j == 0 else OB_A1 + (j - 1)
-        elif r == na:
-            code = OB_B
-        if n == 8:
-            return k, code
-        if r < na:
-            chunk = (0 if r == 0 else 2 * r - 1) if nch & 1 else 2 * r
-        else:
-            chunk = 2 * (r - na) + 2 if nch & 1 else 2 * (r - na) + 1
-        return 4 * chunk + j, code
-    t, tt = k - mainw, n - mainw
-    code = (OB_TAIL1 if tt == 1 else OB_TAIL) if t == 0 else OB_NONE
-    if tt == 1:
-        return mainw, code
-    return (mainw + 1 if t == 0 else mainw if t == 1 else mainw + 2), code
+def chunk_off(n: int, rp: int, row: int, k: int) -> int:
+    """Port of csrc/hmx_internal.cuh chunk_off: element offset of (row, column
+    k) inside an n-wide FP32-accumulated item stored in SGEMV chunk layout."""
+    nch = 0 if chain_shaped(n) else n >> 2
+    if k < 4 * nch:
+        return ((k >> 2) * rp + row) * 4 + (k & 3)
+    return 4 * nch * rp + (k - 4 * nch) * rp + row
 
 
 def _fma(a, b, c):
@@ -104,44 +85,53 @@ def _fma(a, b, c):
     sum: a 48-bit product plus a 24-bit addend is exact there unless their
     exponents are > 40 apart)."""
     ld = np.longdouble
-    return (a.astype(ld) * b.astype(ld) + c.astype(ld)).astype(F32)
+    return (np.asarray(a, F32).astype(ld) * np.asarray(b, F32).astype(ld) + np.asarray(c, F32).astype(ld)).astype(F32)
+
+
+def _mul(a, b):
+    return (np.asarray(a, F32).astype(F64) * np.asarray(b, F32).astype(F64)).astype(F32)
 
 
 def sgemv_tree(a, g):
-    """The GPU kernel's FP32 product of one item (consume32 in
-    csrc/hmx_kernels.cu): columns in obl_col storage order, one FMA chain per
-    sub-chain, the lane tree folded at every sub-chain start."""
+    """The GPU kernel's FP32 product of one item, per row (chain_items in
+    csrc/hmx_kernels.cu): OpenBLAS SGEMV-T's tree -- A/B 4-wide FMA
+    accumulators over 4-column chunks, (l0 + l1) + (l2 + l3), then the tail
+    rule; n = 8 pairs adjacent columns; n <= 3 and 5..7 one FMA chain."""
+    a = np.asarray(a, F32)
+    g = np.asarray(g, F32)
     m, n = a.shape
     z = np.zeros(m, F32)
-    cur, tp, s01, s2, mode = z, z, z, z, 0
-    for k in range(n):
-        c, code = obl_col(n, k)
-        if code in (OB_ITEM_CHAIN, OB_ITEM_MAIN):
-            mode = 1 if code == OB_ITEM_MAIN else 0
-        elif code == OB_B:
-            tp, cur, mode = cur, z, 1
-        elif OB_A1 <= code < OB_TAIL1:
-            lv = tp + cur
-            if code == OB_A1:
-                s01 = lv
-            elif code == OB_A1 + 1:
-                s01 = s01 + lv
-            else:
-                s2 = lv
-            tp, cur, mode = z, z, 1
-        elif code in (OB_TAIL1, OB_TAIL):
-            mv = s01 + (s2 + (tp + cur))
-            tp, s2 = z, z
-            if code == OB_TAIL1:
-                cur, s01, mode = mv, z, 0
-            else:
-                s01, cur, mode = mv, z, 2
-        cur = _fma(a[:, c], np.full(m, g[c], F32), cur)
-    if mode == 1:
-        return s01 + (s2 + (tp + cur))
-    if mode == 2:
-        return s01 + cur
-    return cur
+    if chain_shaped(n):
+        v = z
+        for k in range(n):
+            v = _fma(a[:, k], g[k], v)
+        return v
+    nch, tt = n >> 2, n & 3
+    if n == 8:
+        lanes = [_mul(a[:, 2 * j], g[2 * j]) + _mul(a[:, 2 * j + 1], g[2 * j + 1]) for j in range(4)]
+    else:
+        if nch % 2:
+            ca, cb = [0] + list(range(1, nch, 2)), list(range(2, nch, 2))
+        else:
+            ca, cb = list(range(0, nch, 2)), list(range(1, nch, 2))
+        lanes = []
+        for j in range(4):
+            va, vb = z, z
+            for c in ca:
+                va = _fma(a[:, 4 * c + j], g[4 * c + j], va)
+            for c in cb:
+                vb = _fma(a[:, 4 * c + j], g[4 * c + j], vb)
+            lanes.append(va + vb)
+    v = (lanes[0] + lanes[1]) + (lanes[2] + lanes[3])
+    mm = 4 * nch
+    if tt == 1:
+        v = _fma(a[:, mm], g[mm], v)
+    elif tt >= 2:
+        t = _fma(a[:, mm], g[mm], _mul(a[:, mm + 1], g[mm + 1]))
+        if tt == 3:
+            t = _fma(a[:, mm + 2], g[mm + 2], t)
+        v = v + t
+    return v
 
 
 def prod32(a, g, order: str):
