@@ -47,6 +47,10 @@ static_assert(sizeof(Seg) == 64, "Seg layout");
 
 // RUN_CHUNK: a stage-2 FP32-accumulated item in SGEMV chunk layout (below)
 enum : int32_t { RUN_Z = 1, RUN_ROUND = 2, RUN_ACC32 = 4, RUN_CHUNK = 8 };
+// RUN_CHUNK items: bits 8..15 of Run.flags locate the SGEMV remainder rows of
+// the item's block within the segment (chain_row_kind): 3 + the segment row
+// where they start (0x7f: none here) | 0x80 when there are >= 2 of them
+constexpr int kRunKindShift = 8;
 
 // ---- FP32-accumulated stage-2 items: the reference's summation order ---------
 // The reference's FP32 products (`A32 @ x32`, `U32 @ z32`; matvec.py:57, :73)
@@ -96,6 +100,8 @@ constexpr int kS1Threads = 128;   // stage-1 CTA size
 constexpr int kS1Threads32 = 64;  // stage-1 CTA size for widened-FP32-only stage 1 (<= 256 rows)
 constexpr int kSegWMax = 2048;    // columns of g staged in shared memory per tile (stage 2)
 constexpr int kS1WMax = 1024;     // max columns per stage-1 segment chunk
+constexpr int kS1ExactRows = 128;  // m1-single stage 1: rank rows per CTA (one thread each)
+constexpr int kSgemvBlock = 1024; // OpenBLAS SGEMV-T column blocking: 4096 columns = 1024 chunks
 
 // Device-visible plan (passed by value to kernels).
 struct DevPlan {
@@ -112,9 +118,11 @@ struct DevPlan {
   int32_t zepi;
   int32_t s1_narrow;              // every stage-1 segment is widened FP32: 64-thread CTAs
   int32_t s2_deep;                // FP64-accumulating stage 2 with an FP64 part: deep pipeline
+  int32_t s1_exact;               // m1-single: stage 1 in SGEMV order (s1_exact_kernel)
   int32_t n_seg1_local;           // leading stage-1 segments reading only x[row_begin, row_end)
   const int32_t* gtab;            // item-aligned FP32 group boundaries (stage 2)
   const double* zscale;           // d per z entry (methods 2, 3)
+  const uint8_t* zkind;           // m1-single: SGEMV row kernel (4, 2, 1) per z entry
   double* z;
   double* part;                   // stage-1 chunk partials
   uint32_t* red_count;            // stage-1 arrival counters

@@ -115,12 +115,17 @@ __device__ __forceinline__ double z_epilogue(const DevPlan& P, double s, int zi)
   return s;
 }
 
-// FP32-accumulated items (RUN_CHUNK, layout chunk_off in hmx_internal.cuh) of
-// one thread group: this thread's row p of every item, in OpenBLAS SGEMV-T's
-// order, each value widened once and added in FP64 (reference matvec.py:57,
-// :73, then :106).  Explicit _rn intrinsics: nothing is contracted or
-// reassociated.  Items are software-pipelined: the next item's loads are in
-// flight while the current one is reduced.
+// FP32-accumulated items (RUN_CHUNK, layout chunk_off in hmx_internal.cuh):
+// each row's value in OpenBLAS SGEMV-T's order, widened once and added in
+// FP64 (reference matvec.py:57, :73, then :106).  Explicit _rn intrinsics:
+// nothing is contracted or reassociated.
+//
+// The chain warps stage the segment's chain items through shared memory: a
+// ring of kChainBufs windows of whole consecutive items (<= kChainWin bytes
+// each, contiguous in the blob), copied with cp.async by all chain threads,
+// kChainBufs - 1 windows in flight while one is reduced; inside a window item i goes to slot i mod K (K = chain
+// threads / rp), one row per thread.  Items larger than a window are read
+// from global memory by slot 0.
 __device__ __forceinline__ float4 fma4(float4 a, float4 g, float4 c) {
   return make_float4(__fmaf_rn(a.x, g.x, c.x), __fmaf_rn(a.y, g.y, c.y), __fmaf_rn(a.z, g.z, c.z),
                      __fmaf_rn(a.w, g.w, c.w));
@@ -137,127 +142,309 @@ __device__ __forceinline__ float ld_one(const float* p) {
   asm volatile("ld.global.nc.L1::no_allocate.f32 %0, [%1];" : "=f"(r) : "l"(p));
   return r;
 }
-
-// one item's prefetched values: its first kPre chunks + the tail (column
-// order m+1, m, m+2: the tail's FMA-chain order), or the up to 7 columns of a
-// chain-shaped item (k = 0..2 in t, 3..6 in x[0])
-constexpr int kPre = 2;
-struct ChainBuf {
-  float4 x[kPre];
-  float t[3];
-};
-constexpr int kMetaW = 12;  // run meta in shared memory: col0 << 12 | width
-
-__device__ __forceinline__ void chain_load(ChainBuf& b, const float* part, int meta, int rp, int p) {
-  const int n = meta & ((1 << kMetaW) - 1), c0 = meta >> kMetaW;
-  const float* it = part + (int64_t)c0 * rp + p;
-  if (chain_shaped(n)) {
-    if (n > 0) b.t[0] = ld_one(it);
-    if (n > 1) b.t[1] = ld_one(it + rp);
-    if (n > 2) b.t[2] = ld_one(it + 2 * rp);
-    if (n > 4) b.x[0].x = ld_one(it + 3 * rp);
-    if (n > 4) b.x[0].y = ld_one(it + 4 * rp);
-    if (n > 5) b.x[0].z = ld_one(it + 5 * rp);
-    if (n > 6) b.x[0].w = ld_one(it + 6 * rp);
-    return;
-  }
-  const int nch = n >> 2, T = n & 3;
-  const float* ch = it + 3 * p;  // chunk c of row p: it - p + 4 (c rp + p)
-#pragma unroll
-  for (int u = 0; u < kPre; ++u)
-    if (u < nch) b.x[u] = ld_chunk(ch + (int64_t)4 * u * rp);
-  const float* tl = it + (int64_t)4 * nch * rp;
-  if (T == 1) {
-    b.t[0] = ld_one(tl);
-  } else if (T >= 2) {
-    b.t[0] = ld_one(tl + rp);
-    b.t[1] = ld_one(tl);
-    if (T == 3) b.t[2] = ld_one(tl + 2 * rp);
-  }
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"((unsigned)__cvta_generic_to_shared(smem)),
+               "l"(gmem)
+               : "memory");
+}
+__device__ __forceinline__ void chain_bar(int nthreads) {
+  asm volatile("bar.sync 1, %0;" ::"r"(nthreads) : "memory");
 }
 
-__device__ __forceinline__ float chain_value(const ChainBuf& b, const float* part, const double* gs, int meta,
-                                             int rp, int p) {
-  const int n = meta & ((1 << kMetaW) - 1), c0 = meta >> kMetaW;
-  auto G = [&](int c) { return __int_as_float(__double2loint(gs[c])); };
+constexpr int kMetaW = 12;  // run meta in shared memory: col0 << 12 | width
+#ifndef HMX_CHAIN_WB
+#define HMX_CHAIN_WB 8192
+#endif
+#ifndef HMX_CHAIN_NBUF
+#define HMX_CHAIN_NBUF 3
+#endif
+constexpr int kChainWin = HMX_CHAIN_WB;     // bytes per staging buffer
+constexpr int kChainBufs = HMX_CHAIN_NBUF;  // staging buffers (windows in flight + 1)
+
+// row p of one n-wide item at `it` (global or shared memory, chunk layout).
+// `kind`: which OpenBLAS SGEMV-T row kernel computes this row of its block
+// (row_kind): 4 = the four-row kernel (A/B FMA chains), 2 = the two-row
+// remainder kernel (one 4-lane accumulator, multiply then add), 1 = the
+// one-row remainder kernel (A/B, multiply then add).  All end with
+// (l0 + l1) + (l2 + l3) and the same tail rule; short rows differ per kernel
+// (tools/fp32_accum_emulation.py sgemv_kind, checked bitwise against numpy).
+// G(k): the FP32 source value of the item's column k.
+template <bool GLOBAL, typename GF>
+__device__ __forceinline__ float chain_item(const float* it, GF G, int n, int rp, int p, int kind) {
+  constexpr int c0 = 0;
   auto G4 = [&](int c) { return make_float4(G(c), G(c + 1), G(c + 2), G(c + 3)); };
-  if (chain_shaped(n)) {  // n <= 3, 5 <= n <= 7: one forward FMA chain
+  auto L4 = [&](const float* q) {
+    if constexpr (GLOBAL) return ld_chunk(q);
+    else return *reinterpret_cast<const float4*>(q);
+  };
+  auto L1 = [&](const float* q) {
+    if constexpr (GLOBAL) return ld_one(q);
+    else return *q;
+  };
+  // element k of this row (chunk layout)
+  auto E = [&](int k) {
+    if (chain_shaped(n)) return L1(it + (int64_t)k * rp + p);
+    const int m = n & ~3;
+    return k < m ? L1(it + 4 * ((int64_t)(k >> 2) * rp + p) + (k & 3)) : L1(it + (int64_t)m * rp + (int64_t)(k - m) * rp + p);
+  };
+  auto Pr = [&](int k) { return __fmul_rn(E(k), G(c0 + k)); };  // rounded product
+  if (kind != 4 && n <= 8 && n != 4 && !(kind == 1 && (n == 3 || n == 5 || n == 8)) && !(kind == 2 && n == 8)) {
+    // remainder kernels, n = 1..7: a sequential multiply-then-add chain
+    float v = Pr(0);
+    for (int k = 1; k < n; ++k) v = __fadd_rn(v, Pr(k));
+    return v;
+  }
+  if (kind == 1 && n == 3) return __fmaf_rn(E(2), G(c0 + 2), __fmaf_rn(E(0), G(c0), Pr(1)));
+  if (kind == 1 && n == 5)  // lanes = products, summed in order, the tail column fused
+    return __fmaf_rn(E(4), G(c0 + 4), __fadd_rn(__fadd_rn(__fadd_rn(Pr(0), Pr(1)), Pr(2)), Pr(3)));
+  if (chain_shaped(n)) {  // four-row kernel, n <= 3, 5 <= n <= 7: one forward FMA chain
     float v = 0.f;
-    if (n > 0) v = __fmaf_rn(b.t[0], G(c0), v);
-    if (n > 1) v = __fmaf_rn(b.t[1], G(c0 + 1), v);
-    if (n > 2) v = __fmaf_rn(b.t[2], G(c0 + 2), v);
-    if (n > 4) v = __fmaf_rn(b.x[0].x, G(c0 + 3), v);
-    if (n > 4) v = __fmaf_rn(b.x[0].y, G(c0 + 4), v);
-    if (n > 5) v = __fmaf_rn(b.x[0].z, G(c0 + 5), v);
-    if (n > 6) v = __fmaf_rn(b.x[0].w, G(c0 + 6), v);
+    for (int k = 0; k < n; ++k) v = __fmaf_rn(E(k), G(c0 + k), v);
     return v;
   }
   const int nch = n >> 2, T = n & 3, m = 4 * nch;
+  const float* ch = it + 4 * p;  // chunk c of row p at ch[4 c rp]
   float4 l;
-  if (n == 8) {  // l_j = a_2j g_2j + a_2j+1 g_2j+1
+  bool seq = false;  // sequential horizontal sum (one-row kernel, n <= 8)
+  if (n == 8 && kind == 4) {  // l_j = a_2j g_2j + a_2j+1 g_2j+1
+    const float4 x0 = L4(ch), x1 = L4(ch + 4 * rp);
     const float4 g0 = G4(c0), g1 = G4(c0 + 4);
-    l = make_float4(__fadd_rn(__fmul_rn(b.x[0].x, g0.x), __fmul_rn(b.x[0].y, g0.y)),
-                    __fadd_rn(__fmul_rn(b.x[0].z, g0.z), __fmul_rn(b.x[0].w, g0.w)),
-                    __fadd_rn(__fmul_rn(b.x[1].x, g1.x), __fmul_rn(b.x[1].y, g1.y)),
-                    __fadd_rn(__fmul_rn(b.x[1].z, g1.z), __fmul_rn(b.x[1].w, g1.w)));
+    l = make_float4(__fadd_rn(__fmul_rn(x0.x, g0.x), __fmul_rn(x0.y, g0.y)),
+                    __fadd_rn(__fmul_rn(x0.z, g0.z), __fmul_rn(x0.w, g0.w)),
+                    __fadd_rn(__fmul_rn(x1.x, g1.x), __fmul_rn(x1.y, g1.y)),
+                    __fadd_rn(__fmul_rn(x1.z, g1.z), __fmul_rn(x1.w, g1.w)));
   } else {
-    // chunk c into A or B: nch even: A = even chunks; nch odd: A = {0, 1, 3, 5, ..}
-    const bool odd = nch & 1;
-    auto inA = [&](int c) { return odd ? (c == 0 || (c & 1)) : !(c & 1); };
+    // chunks into A (and B): four-row and one-row kernels: nch even: A = even
+    // chunks, B = odd; nch odd: A = {0, 1, 3, 5, ..}, B = {2, 4, ..}; two-row
+    // kernel: every chunk into A
     float4 A = make_float4(0.f, 0.f, 0.f, 0.f), B = A;
-#pragma unroll
-    for (int u = 0; u < kPre; ++u)
-      if (u < nch) {
-        if (inA(u)) A = fma4(b.x[u], G4(c0 + 4 * u), A);
-        else B = fma4(b.x[u], G4(c0 + 4 * u), B);
+    auto acc = [&](float4& X, const float4& x, const float4& g) {
+      if (kind == 4) X = fma4(x, g, X);
+      else X = make_float4(__fadd_rn(X.x, __fmul_rn(x.x, g.x)), __fadd_rn(X.y, __fmul_rn(x.y, g.y)),
+                           __fadd_rn(X.z, __fmul_rn(x.z, g.z)), __fadd_rn(X.w, __fmul_rn(x.w, g.w)));
+    };
+    int c = 0;
+    if (kind == 2) {
+      for (; c < nch; ++c) acc(A, L4(ch + (int64_t)4 * c * rp), G4(c0 + 4 * c));
+    } else {
+      if (nch & 1) {
+        acc(A, L4(ch), G4(c0));
+        c = 1;
       }
-    // the remaining chunks (n >= 12), four loads in flight
-    const float* ch = part + (int64_t)c0 * rp + 4 * p;
-    for (int c = kPre; c < nch; c += 4) {
-      float4 xs[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u)
-        if (c + u < nch) xs[u] = ld_chunk(ch + (int64_t)4 * (c + u) * rp);
-#pragma unroll
-      for (int u = 0; u < 4; ++u)
-        if (c + u < nch) {
-          if (inA(c + u)) A = fma4(xs[u], G4(c0 + 4 * (c + u)), A);
-          else B = fma4(xs[u], G4(c0 + 4 * (c + u)), B);
-        }
+      for (; c < nch; c += 2) {
+        const float4 xa = L4(ch + (int64_t)4 * c * rp), xb = L4(ch + (int64_t)4 * (c + 1) * rp);
+        acc(A, xa, G4(c0 + 4 * c));
+        acc(B, xb, G4(c0 + 4 * c + 4));
+      }
     }
     l = make_float4(__fadd_rn(A.x, B.x), __fadd_rn(A.y, B.y), __fadd_rn(A.z, B.z), __fadd_rn(A.w, B.w));
+    seq = kind == 1 && n <= 8;
   }
-  float v = __fadd_rn(__fadd_rn(l.x, l.y), __fadd_rn(l.z, l.w));
+  float v = seq ? __fadd_rn(__fadd_rn(__fadd_rn(l.x, l.y), l.z), l.w)
+                : __fadd_rn(__fadd_rn(l.x, l.y), __fadd_rn(l.z, l.w));
+  const float* tl = it + (int64_t)m * rp + p;
   if (T == 1) {
-    v = __fmaf_rn(b.t[0], G(c0 + m), v);
+    v = __fmaf_rn(L1(tl), G(c0 + m), v);
   } else if (T >= 2) {
-    float tv = __fmul_rn(b.t[0], G(c0 + m + 1));
-    tv = __fmaf_rn(b.t[1], G(c0 + m), tv);
-    if (T == 3) tv = __fmaf_rn(b.t[2], G(c0 + m + 2), tv);
+    float tv = __fmul_rn(L1(tl + rp), G(c0 + m + 1));
+    tv = __fmaf_rn(L1(tl), G(c0 + m), tv);
+    if (T == 3) tv = __fmaf_rn(L1(tl + 2 * rp), G(c0 + m + 2), tv);
     v = __fadd_rn(v, tv);
   }
   return v;
 }
 
-// the group's items: runs with col0 in [cb, ce) (meta[] in shared memory)
-__device__ __forceinline__ double chain_items(const int32_t* meta, int nrun, const float* __restrict__ part,
-                                              const double* gs, int cb, int ce, int rp, int p) {
-  int j = 0;
-  while (j < nrun && (meta[j] >> kMetaW) < cb) ++j;
-  int je = j;
-  while (je < nrun && (meta[je] >> kMetaW) < ce) ++je;
+// row kind of segment row p for an item whose block's remainder rows start at
+// segment row `rem` (kinfo: (rem + 3) | 0x80 when the remainder has >= 2
+// rows; 0x7f: no remainder rows in this segment)
+__device__ __forceinline__ int chain_row_kind(uint8_t kinfo, int p) {
+  const int rem = (kinfo & 0x7f) - 3;
+  if (p < rem) return 4;
+  if ((kinfo & 0x80) && p < rem + 2) return 2;
+  return 1;
+}
+
+// chain threads u = 0 .. nthr-1 (slot u / rp, row u % rp); items j0 .. nrun-1
+// of the part (meta in shared memory, the part's blob at `part`); buf: two
+// kChainWin-byte staging buffers.  Returns this thread's row sum (FP64).
+__device__ __forceinline__ double chain_windows(const int32_t* meta, const uint8_t* kinfo, int j0, int nrun,
+                                                const float* part, const double* gs, int rp, int u, int nthr,
+                                                float* buf) {
+  const int K = nthr / rp;
+  const int slot = u / rp, p = u - slot * rp;
+  const bool act = slot < K;
+  const int64_t wmax = kChainWin / (4 * (int64_t)rp);  // columns per window
+  auto col0 = [&](int j) { return j < nrun ? (meta[j] >> kMetaW) : -1; };
+  auto width = [&](int j) { return meta[j] & ((1 << kMetaW) - 1); };
+  // window starting at item j: [j, end) of <= wmax columns, or one oversize item
+  auto wend = [&](int j) {
+    const int cs = col0(j);
+    int e = j + 1;
+    if (width(j) > wmax) return e;
+    while (e < nrun && col0(e) + width(e) - cs <= wmax) ++e;
+    return e;
+  };
+  auto stage = [&](int j, int e, int b) {  // copy window [j, e) into buffer b (nothing if oversize)
+    if (j >= nrun || width(j) > wmax) return;
+    const int cs = col0(j), ce = col0(e - 1) + width(e - 1);
+    const int64_t n16 = (int64_t)(ce - cs) * rp / 4;  // 16-byte pieces
+    const float* src = part + (int64_t)cs * rp;
+    float* dst = buf + (int64_t)b * (kChainWin / 4);
+    for (int64_t i = u; i < n16; i += nthr) cp_async16(dst + 4 * i, src + 4 * i);
+  };
   double acc = 0.0;
-  ChainBuf b0, b1;
-  if (j < je) chain_load(b0, part, meta[j], rp, p);
-  while (j < je) {
-    if (j + 1 < je) chain_load(b1, part, meta[j + 1], rp, p);
-    acc += (double)chain_value(b0, part, gs, meta[j], rp, p);
-    if (++j >= je) break;
-    if (j + 1 < je) chain_load(b0, part, meta[j + 1], rp, p);
-    acc += (double)chain_value(b1, part, gs, meta[j], rp, p);
-    ++j;
+  // a ring of kChainBufs windows: kChainBufs - 1 in flight while one is reduced
+  int ws[kChainBufs], we[kChainBufs];  // window bounds per buffer
+  int nxt = j0;                        // first item not yet staged
+#pragma unroll
+  for (int k = 0; k < kChainBufs - 1; ++k) {
+    ws[k] = nxt;
+    we[k] = nxt < nrun ? wend(nxt) : nxt;
+    stage(ws[k], we[k], k);
+    nxt = we[k];
+    asm volatile("cp.async.commit_group;" ::: "memory");
   }
+  for (int w = 0;; ++w) {
+    const int b = w % kChainBufs;
+    const int j = ws[b], e = we[b];
+    if (j >= nrun) break;
+    {  // the window kChainBufs - 1 ahead goes into the buffer freed last round
+      const int bn = (w + kChainBufs - 1) % kChainBufs;
+      ws[bn] = nxt;
+      we[bn] = nxt < nrun ? wend(nxt) : nxt;
+      stage(ws[bn], we[bn], bn);
+      nxt = we[bn];
+    }
+    asm volatile("cp.async.commit_group;\ncp.async.wait_group %0;" ::"n"(kChainBufs - 1) : "memory");
+    chain_bar(nthr);  // every thread's copies of window [j, e) have landed
+    if (act) {
+      if (width(j) > wmax) {  // oversize item: straight from global memory
+        if (slot == 0) {
+          const int c0 = col0(j);
+          acc += (double)chain_item<true>(
+              part + (int64_t)c0 * rp, [&](int k) { return __int_as_float(__double2loint(gs[c0 + k])); },
+              width(j), rp, p, chain_row_kind(kinfo[j], p));
+        }
+      } else {
+        const float* base = buf + (int64_t)b * (kChainWin / 4);
+        const int cs = col0(j);
+        for (int i = j + slot; i < e; i += K) {
+          const int c0 = col0(i);
+          acc += (double)chain_item<false>(
+              base + (int64_t)(c0 - cs) * rp, [&](int k) { return __int_as_float(__double2loint(gs[c0 + k])); },
+              width(i), rp, p, chain_row_kind(kinfo[i], p));
+        }
+      }
+    }
+    chain_bar(nthr);  // buffer b is free again
+  }
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
   return acc;
+}
+
+// Stage 1 of m1-single: z = Vt32 . x32 accumulated in FP32 (reference
+// matvec.py:70, numpy -> OpenBLAS SGEMV-T), in SGEMV's own order: one thread
+// per rank row over the cluster's whole width, 4096-column blocks each
+// reduced by the A/B lane tree of hmx_internal.cuh (the tail rule in the last
+// block), the block values added in order (one CTA per block; the last one
+// to arrive adds them).  Rows stored in chunk layout (chunk_off), so a warp's
+// 16-byte loads cover 32 consecutive rows.
+__global__ void __launch_bounds__(kS1ExactRows) s1_exact_kernel(DevPlan P, const Seg* __restrict__ segs,
+                                                                const double* __restrict__ x, const int* skip) {
+  if (skip != nullptr && *skip != 0) return;
+  asm volatile("griddepcontrol.launch_dependents;");
+  __shared__ unsigned ticket;
+  const Seg sg = segs[blockIdx.x];
+  const int t = threadIdx.x;
+  const Run run = P.runs[sg.run0];
+  const int n = sg.W32, rp = (sg.R + 3) & ~3;
+  const float* __restrict__ it = P.blob32 + sg.off32;
+  const double* __restrict__ xs = x + run.src;
+  // the FP32 source shadow (matvec.py:119): x rounded once
+  auto G = [&](int c) { return (float)__ldg(xs + c); };
+  auto G4 = [&](int c) { return make_float4(G(c), G(c + 1), G(c + 2), G(c + 3)); };
+  float y = 0.f;
+  const int kind = t < sg.R ? P.zkind[sg.row0 + t] : 4;
+  if (t >= sg.R) {
+    // (idle row: no loads; joins the barrier below)
+  } else if (kind != 4) {
+    // a remainder row of its block's SGEMV (this CTA holds one 4096-column block)
+    y = chain_item<true>(it, G, n, rp, t, kind);
+  } else if (chain_shaped(n)) {
+    for (int k = 0; k < n; ++k) y = __fmaf_rn(ld_one(it + (int64_t)k * rp + t), G(k), y);
+  } else if (n == 8) {
+    const float4 x0 = ld_chunk(it + 4 * t), x1 = ld_chunk(it + 4 * (rp + t));
+    const float4 g0 = G4(0), g1 = G4(4);
+    const float l0 = __fadd_rn(__fmul_rn(x0.x, g0.x), __fmul_rn(x0.y, g0.y));
+    const float l1 = __fadd_rn(__fmul_rn(x0.z, g0.z), __fmul_rn(x0.w, g0.w));
+    const float l2 = __fadd_rn(__fmul_rn(x1.x, g1.x), __fmul_rn(x1.y, g1.y));
+    const float l3 = __fadd_rn(__fmul_rn(x1.z, g1.z), __fmul_rn(x1.w, g1.w));
+    y = __fadd_rn(__fadd_rn(l0, l1), __fadd_rn(l2, l3));
+  } else {
+    const int nch = n >> 2, T = n & 3;
+    for (int b0 = 0; b0 < nch; b0 += kSgemvBlock) {
+      const int nb = min(kSgemvBlock, nch - b0);
+      const bool odd = nb & 1;
+      const float* ch = it + 4 * ((int64_t)b0 * rp + t);  // chunk b0 + c at ch[4 c rp]
+      float4 A = make_float4(0.f, 0.f, 0.f, 0.f), B = A;
+      int c = 0;
+      if (odd) {
+        A = fma4(ld_chunk(ch), G4(4 * b0), A);
+        c = 1;
+      }
+      // pairs (A, B), up to four pairs' loads in flight
+      for (; c < nb; c += 8) {
+        float4 xa[4], xb[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (c + 2 * u < nb) {
+            xa[u] = ld_chunk(ch + (int64_t)4 * (c + 2 * u) * rp);
+            xb[u] = ld_chunk(ch + (int64_t)4 * (c + 2 * u + 1) * rp);
+          }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (c + 2 * u < nb) {
+            A = fma4(xa[u], G4(4 * (b0 + c + 2 * u)), A);
+            B = fma4(xb[u], G4(4 * (b0 + c + 2 * u + 1)), B);
+          }
+      }
+      const float4 l = make_float4(__fadd_rn(A.x, B.x), __fadd_rn(A.y, B.y), __fadd_rn(A.z, B.z),
+                                   __fadd_rn(A.w, B.w));
+      float v = __fadd_rn(__fadd_rn(l.x, l.y), __fadd_rn(l.z, l.w));
+      if (b0 + nb == nch && T > 0) {  // the tail belongs to the last block
+        const int m = 4 * nch;
+        const float* tl = it + (int64_t)m * rp + t;
+        if (T == 1) {
+          v = __fmaf_rn(ld_one(tl), G(m), v);
+        } else {
+          float tv = __fmul_rn(ld_one(tl + rp), G(m + 1));
+          tv = __fmaf_rn(ld_one(tl), G(m), tv);
+          if (T == 3) tv = __fmaf_rn(ld_one(tl + 2 * rp), G(m + 2), tv);
+          v = __fadd_rn(v, tv);
+        }
+      }
+      y = b0 == 0 ? v : __fadd_rn(y, v);
+    }
+  }
+  if (sg.nchunks == 1) {
+    if (t < sg.R) P.z[sg.row0 + t] = (double)y;
+    return;
+  }
+  // one 4096-column block per CTA: the last-arriving CTA adds the block
+  // values in block order (y = (b0 + b1) + ..., as SGEMV)
+  if (t < sg.R) P.part[sg.part_off + sg.chunk * sg.R + t] = (double)y;
+  __threadfence();
+  __syncthreads();
+  if (t == 0) ticket = atomicAdd(P.red_count + sg.red, 1u);
+  __syncthreads();
+  if (ticket != (unsigned)(sg.nchunks - 1)) return;
+  __threadfence();
+  if (t < sg.R) {
+    float f = (float)__ldcg(P.part + sg.part_off + t);
+    for (int ch = 1; ch < sg.nchunks; ++ch) f = __fadd_rn(f, (float)__ldcg(P.part + sg.part_off + ch * sg.R + t));
+    P.z[sg.row0 + t] = (double)f;
+  }
+  if (t == 0) P.red_count[sg.red] = 0u;  // ready for the next matvec
 }
 
 // One CTA = one segment: rows [row0, row0+R) of a column-major item stream.
@@ -276,6 +463,8 @@ __global__ void __launch_bounds__(NT, DEEP ? 3 : (OUT == OUT_Y && F32MODE != F32
   __shared__ double red64[2 * NT];
   __shared__ double red32[4 * NT];
   __shared__ double wred[2][NT / 32];
+  // chain-item staging buffers (stage-2 FP32 kernels: 2 x kChainWin bytes of dynamic shared memory)
+  extern __shared__ __align__(16) float chain_buf[];
   __shared__ unsigned ticket;
 
   if (out.skip != nullptr && *out.skip != 0) return;  // guarded launch (solver)
@@ -535,11 +724,13 @@ __global__ void __launch_bounds__(NT, DEEP ? 3 : (OUT == OUT_Y && F32MODE != F32
       for (int j = tid - wbc; j < sg.nrun32; j += NT - wbc) {
         const Run r = runs[j];
         sidx[j] = (r.col0 << kMetaW) | r.width;
+        fl[j] = (uint8_t)(r.flags >> kRunKindShift);
       }
-      asm volatile("bar.sync 1, %0;" ::"r"(NT - wbc) : "memory");
-      if (q32 < g32)
-        bc = chain_items(sidx, sg.nrun32, P.blob32 + sg.off32, gs, P.gtab[sg.gtab + q32],
-                         P.gtab[sg.gtab + q32 + 1], rp32, pc);
+      chain_bar(NT - wbc);
+      int j0 = 0;  // the first chain item (they follow the widened ones)
+      const int c32c = P.gtab[sg.gtab + g32 + 1];
+      while (j0 < sg.nrun32 && (sidx[j0] >> kMetaW) < c32c) ++j0;
+      bc = chain_windows(sidx, fl, j0, sg.nrun32, P.blob32 + sg.off32, gs, rp32, tid - wbc, NT - wbc, chain_buf);
     }
   }
 
@@ -716,13 +907,20 @@ __global__ void probe_kernel(DevPlan P, const double* __restrict__ x, unsigned l
 // ------------------------------------------------------------------------------
 // launchers
 
+// dynamic shared memory of a seg_kernel instantiation: the chain-item staging
+// buffers of the stage-2 FP32 kernels
+template <int M, int O>
+constexpr size_t chain_smem() {
+  return (O == OUT_Y && M != F32_ALL64) ? (size_t)kChainBufs * kChainWin : 0;
+}
+
 template <int M, int O, int NT = kSegThreads, bool DEEP = false>
 static cudaError_t launch_seg(const DevPlan& P, const Seg* segs, int nseg, const double* x,
                               const S2Out& out, cudaStream_t st, bool pdl) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)nseg);
   cfg.blockDim = dim3(NT);
-  cfg.dynamicSmemBytes = 0;
+  cfg.dynamicSmemBytes = chain_smem<M, O>();
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -743,6 +941,10 @@ cudaError_t launch_stage1(const DevPlan& P, const double* x, cudaStream_t st, co
   // m2-mixed, m3 with an all-FP32 class): 64-thread CTAs, 16 per SM (measured
   // -3..-4 % on stage 1 against 128 threads; the FP32-accumulating m1-single
   // stage 1 is faster on 128)
+  if (P.s1_exact) {
+    s1_exact_kernel<<<nseg, kS1ExactRows, 0, st>>>(P, segs, x, skip);
+    return cudaGetLastError();
+  }
   switch (P.f32mode1) {
     case F32_ALL32: return launch_seg<F32_ALL32, OUT_Z, kS1Threads>(P, segs, nseg, x, none, st, false);
     default:
@@ -761,6 +963,18 @@ cudaError_t launch_stage2(const DevPlan& P, const double* x, const S2Out& out, c
       return P.s2_deep ? launch_seg<F32_ALL64, OUT_Y, kSegThreads, true>(P, P.seg2, P.n_seg2, x, out, st, pdl)
                        : launch_seg<F32_ALL64, OUT_Y>(P, P.seg2, P.n_seg2, x, out, st, pdl);
   }
+}
+
+// The stage-2 FP32 kernels opt in to > 48 KB of shared memory (static + the
+// chain staging buffers); called at plan creation, outside any capture.
+cudaError_t configure_kernels() {
+  cudaError_t e = cudaFuncSetAttribute(seg_kernel<F32_ALL32, OUT_Y, kSegThreads, false>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)chain_smem<F32_ALL32, OUT_Y>());
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(seg_kernel<F32_MIXED, OUT_Y, kSegThreads, false>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)chain_smem<F32_MIXED, OUT_Y>());
+  return e;
 }
 
 cudaError_t launch_gather_perm(const double* x, const int32_t* perm, double* xp, int n,

@@ -139,6 +139,7 @@ int hmx::plan_create_impl(const hmx_matrix_desc* d, int device, const hmx_plan_o
   }
   const int pipe = d->scheme;
   const bool has_lo = pipe == P_M3;
+  HMX_CUDA(configure_kernels());
   const int64_t rb = opt && opt->row_end > 0 ? opt->row_begin : 0;
   const int64_t re = opt && opt->row_end > 0 ? opt->row_end : n;
   if (rb < 0 || re > n || rb >= re) {
@@ -281,6 +282,10 @@ int hmx::plan_create_impl(const hmx_matrix_desc* d, int device, const hmx_plan_o
   group_rows.reserve(groups.size());
   std::vector<S1Fill> fills;
   std::vector<double> zscale(pipe >= P_M2D ? (size_t)std::max<int64_t>(Z, 1) : 1, 1.0);
+  // m1-single stage 1: the SGEMV row kernel of every z entry (its rank index
+  // q within its block's rank r: rows 4 floor(r/4) .. r-1 are SGEMV's
+  // remainder rows; chain_row_kind)
+  std::vector<uint8_t> zkind(pipe == P_M1S ? (size_t)std::max<int64_t>(Z, 1) : 1, 4);
   int64_t part_len = 0;
   int32_t n_red = 0;
   int64_t s1_bytes = 0, s2_bytes = 0;
@@ -292,6 +297,11 @@ int hmx::plan_create_impl(const hmx_matrix_desc* d, int device, const hmx_plan_o
     for (int32_t k : g.second) {
       const int64_t kk = cls == 1 ? d->khi[k] : d->klo[k];
       for (int64_t q = 0; q < kk; ++q) rows.push_back({k, (int32_t)q});
+      if (pipe == P_M1S) {
+        const int64_t z0 = cls == 1 ? zoff_hi[(size_t)k] : zoff_lo[(size_t)k];
+        for (int64_t q = 0; q < kk; ++q)
+          zkind[(size_t)(z0 + q)] = q < (kk & ~int64_t(3)) ? 4 : ((kk & 3) >= 2 && q < (kk & ~int64_t(3)) + 2) ? 2 : 1;
+      }
       if (pipe >= P_M2D) {
         const double* dsrc = d->buf64 + (cls == 1 ? d->dhi_off[k] : d->dlo_off[k]);
         const int64_t z0 = cls == 1 ? zoff_hi[(size_t)k] : zoff_lo[(size_t)k];
@@ -301,13 +311,19 @@ int hmx::plan_create_impl(const hmx_matrix_desc* d, int device, const hmx_plan_o
     const bool is32 = cls == 2 || d->hi32;
     const int64_t es = is32 ? 4 : 8;
     const int64_t rg = (int64_t)rows.size();
-    const int64_t pieces = (rg + s1_rows - 1) / s1_rows;
+    // m1-single: z = Vt32 . x32 accumulated in FP32 in SGEMV's order over the
+    // whole cluster width (s1_exact_kernel: one thread per rank row, no
+    // column chunks), stored in chunk layout
+    const bool exact1 = is32 && pipe == P_M1S;
+    const int64_t rows_cap = exact1 ? kS1ExactRows : s1_rows;
+    const int64_t pieces = (rg + rows_cap - 1) / rows_cap;
     for (int64_t pc = 0; pc < pieces; ++pc) {
       const int64_t r0 = rg * pc / pieces, r1 = rg * (pc + 1) / pieces, R = r1 - r0;
       const int64_t rp = round_up(R, is32 ? 4 : 2);
-      int64_t C = std::max<int64_t>(1, s1_target / (rp * es));
+      // (exact: OpenBLAS's own 4096-column blocks, one CTA each, added in order)
+      int64_t C = exact1 ? 4 * (int64_t)kSgemvBlock : std::max<int64_t>(1, s1_target / (rp * es));
       const int64_t nch = (ncol + C - 1) / C;
-      C = (ncol + nch - 1) / nch;
+      if (!exact1) C = (ncol + nch - 1) / nch;
       const int32_t red = nch > 1 ? n_red++ : -1;
       const int32_t poff = nch > 1 ? (int32_t)part_len : -1;
       if (nch > 1) part_len += nch * R;
@@ -328,7 +344,7 @@ int hmx::plan_create_impl(const hmx_matrix_desc* d, int device, const hmx_plan_o
         r.src = (int32_t)(cs + c0);
         r.width = (int32_t)w;
         r.col0 = 0;
-        r.flags = (src_round ? RUN_ROUND : 0) | ((is32 && pipe == P_M1S) ? RUN_ACC32 : 0);
+        r.flags = (src_round ? RUN_ROUND : 0) | ((is32 && pipe == P_M1S) ? (RUN_ACC32 | RUN_CHUNK) : 0);
         runs.push_back(r);
         run_block.push_back(-1);
         if (is32) {
@@ -376,7 +392,7 @@ int hmx::plan_create_impl(const hmx_matrix_desc* d, int device, const hmx_plan_o
   // column in a mixed FP32 part (A/B on config 4 with the warp-aligned split:
   // m1-mixed best at 0.8-1.0, m2-single at 1/1.0-1/1.2)
   const char* aw_env = std::getenv("HMX_ACC64_WEIGHT");
-  const double acc64_weight = aw_env ? std::atof(aw_env) : 2.5;
+  const double acc64_weight = aw_env ? std::atof(aw_env) : 1.0;
   const bool dense_single = pipe == P_M1S || pipe == P_M2S;  // A32 . x32 in FP32
   const bool u_acc32 = pipe == P_M1S || pipe == P_M1M;       // U32 . z32 in FP32
   bool any_acc32 = false, any_acc64_in32 = false;
@@ -504,8 +520,17 @@ int hmx::plan_create_impl(const hmx_matrix_desc* d, int device, const hmx_plan_o
         if (part == 1) {
           if (r.flags & RUN_ACC32) any_acc32 = true;
           else any_acc64_in32 = true;
-          // parts with a group table: chain items in SGEMV chunk layout
-          if ((r.flags & RUN_ACC32) && !fg.cuts.empty()) r.flags |= RUN_CHUNK;
+          // parts with a group table: chain items in SGEMV chunk layout, with
+          // the segment rows SGEMV computes in its remainder kernels (rows
+          // 4 floor(m/4) .. m-1 of an m-row block)
+          if ((r.flags & RUN_ACC32) && !fg.cuts.empty()) {
+            r.flags |= RUN_CHUNK;
+            const int64_t mb = t[1] - t[0];
+            const int64_t rem = t[0] + (mb & ~int64_t(3)) - sg.row0;  // segment-relative
+            int32_t kinfo = 0x7f;  // (rem + 3: the remainder may start up to 3 rows before the segment)
+            if ((mb & 3) && rem < sg.R) kinfo = (int32_t)(rem + 3) | ((mb & 3) >= 2 ? 0x80 : 0);
+            r.flags |= kinfo << kRunKindShift;
+          }
         }
         runs.push_back(r);
         run_block.push_back(it.block);
@@ -572,9 +597,11 @@ int hmx::plan_create_impl(const hmx_matrix_desc* d, int device, const hmx_plan_o
       const int64_t kk = f.cls == 1 ? d->khi[k] : d->klo[k];
       const int64_t base = (f.cls == 1 ? d->hi_off[k] : d->lo_off[k]) + m * kk + (int64_t)row.second * f.ncol + f.c0;
       const bool src32 = f.cls == 2 || d->hi32;
+      const bool chunk = (runs[(size_t)s.run0].flags & RUN_CHUNK) != 0;
       for (int64_t j = 0; j < w; ++j) {
-        if (is32) b32[(size_t)(o + j * rp + t)] = src32 ? d->buf32[base + j] : (float)d->buf64[base + j];
-        else b64[(size_t)(o + j * rp + t)] = src32 ? d->buf32[base + j] : d->buf64[base + j];
+        const int64_t e = chunk ? chunk_off((int)w, (int)rp, (int)t, (int)j) : j * rp + t;
+        if (is32) b32[(size_t)(o + e)] = src32 ? d->buf32[base + j] : (float)d->buf64[base + j];
+        else b64[(size_t)(o + e)] = src32 ? d->buf32[base + j] : d->buf64[base + j];
       }
     }
   };
@@ -718,6 +745,7 @@ int hmx::plan_create_impl(const hmx_matrix_desc* d, int device, const hmx_plan_o
       u.c0 = (int32_t)f.c0;
       u.is32 = is32;
       u.cls = f.cls;
+      u.chunk = (runs[(size_t)sg.run0].flags & RUN_CHUNK) ? 1 : 0;
       ps1.push_back(u);
     }
     std::vector<PackS2> ps2;
@@ -803,6 +831,8 @@ int hmx::plan_create_impl(const hmx_matrix_desc* d, int device, const hmx_plan_o
                  secs() - t_meta, (off64 * 8.0 + off32 * 4.0) / 1e9);
   double* d_zs = p->alloc<double>(zscale.size());
   if ((rc = up(d_zs, zscale))) return rc;
+  uint8_t* d_zk = p->alloc<uint8_t>(zkind.size());
+  if ((rc = up(d_zk, zkind))) return rc;
   int32_t* d_perm = p->alloc<int32_t>(perm32.size());
   if ((rc = up(d_perm, perm32))) return rc;
   int32_t* d_gtab = p->alloc<int32_t>(std::max<size_t>(gtab.size(), 1));
@@ -826,6 +856,7 @@ int hmx::plan_create_impl(const hmx_matrix_desc* d, int device, const hmx_plan_o
   dp.blob32 = d_b32;
   dp.f32mode1 = pipe == P_M1S ? F32_ALL32 : F32_ALL64;
   dp.s1_narrow = s1_narrow ? 1 : 0;
+  dp.s1_exact = pipe == P_M1S ? 1 : 0;
   {
     // deep FP64 pipeline when the FP64 part carries most of stage 2's bytes
     int64_t b64 = 0, b32 = 0;
@@ -843,6 +874,7 @@ int hmx::plan_create_impl(const hmx_matrix_desc* d, int device, const hmx_plan_o
   dp.f32mode2 = f32mode2;
   dp.zepi = pipe == P_M1D ? Z_NONE : (pipe == P_M1S || pipe == P_M1M) ? Z_ROUND32 : Z_SCALE;
   dp.zscale = d_zs;
+  dp.zkind = d_zk;
   dp.z = d_z;
   dp.part = d_part;
   dp.red_count = d_cnt;

@@ -179,6 +179,7 @@ struct PackS1 {
   int64_t rows;     // offset into the (block, class position) row list
   int32_t R, rp, w, c0;
   int32_t is32, cls;  // cls 1 = FP64 class / plain factors, 2 = FP32 class
+  int32_t chunk, pad; // chunk 1: SGEMV chunk layout (chunk_off), m1-single
 };
 struct PackS2 {
   int64_t dst;

@@ -124,7 +124,8 @@ __global__ void pack_s1_kernel(DevSource S, const PackS1* __restrict__ units, co
     const int64_t slot0 = S.roff[k];
     const int q = S.cls_idx[slot0 + (u.cls == 2 ? S.khi[k] : 0) + pr.q];
     const double v = S.data[S.offset[k] + m * r + (int64_t)q * n + u.c0 + j];
-    lost += put(b64, b32, u.dst + (int64_t)j * u.rp + t, u.is32, unit(v, S.rowmag, slot0 + q), k, S);
+    const int64_t dst = u.dst + (u.chunk ? chunk_off(u.w, u.rp, t, j) : (int64_t)j * u.rp + t);
+    lost += put(b64, b32, dst, u.is32, unit(v, S.rowmag, slot0 + q), k, S);
   }
   add_lost(S, lost);
 }

@@ -67,6 +67,8 @@ def main():
         y_local = y.cpu().numpy().copy()
         xs, rep = D.bicgstab_gpu(comm, op.plan, op64.plan, rhs[perm[a:b]], tol=1e-8, max_iter=1000,
                                  scheme_label=s)
+        print(f"rank {rank} {s}: {rep.iterations} it, converged {rep.converged}, true {rep.true_residual}, "
+              f"breakdown {rep.breakdown}, matvecs {rep.matvecs}", flush=True)
         res["schemes"][s] = {
             "y_dist": y_dist.tolist(), "y_local": y_local.tolist(), "x_solve": np.asarray(xs).tolist(),
             "iterations": rep.iterations, "converged": rep.converged, "true_residual": rep.true_residual,

@@ -1,6 +1,7 @@
 """Golden FP32 block products of the reference's arithmetic (numpy `A32 @ x32`,
 reference matvec.py:57 / :73, OpenBLAS SGEMV) for block widths 1..48 and
-row counts 8 and 40, computed in the build container:
+row counts 8, 40, 30 and 5 (30 and 5: OpenBLAS's two- and one-row remainder
+kernels for rows 28-29 and 4), computed in the build container:
 
     python tests/golden/make_fp32_order.py
 
@@ -20,7 +21,7 @@ HERE = Path(__file__).resolve().parent
 
 def blocks():
     rng = np.random.default_rng(2024)
-    for m in (8, 40):
+    for m in (8, 40, 30, 5):
         for n in range(1, 49):
             a = rng.standard_normal((m, n))          # FP64 masters
             x = rng.uniform(-1.0, 1.0, n)

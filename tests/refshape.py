@@ -30,6 +30,14 @@ class PrecisionScheme:
             return f"m3:c={self.c}"
         return f"m{self.method}-{self.variant}"
 
+    @property
+    def reads_fp32_source(self) -> bool:
+        return self.variant == "single"
+
+    @property
+    def casts_dense_fp32(self) -> bool:
+        return self.method in (1, 2) and self.variant != "double"
+
 
 def parse_scheme(name: str) -> PrecisionScheme:
     if name.startswith("m3:c="):

@@ -24,6 +24,9 @@ static inline cudaError_t cudaMemcpy(void* d, const void* s, size_t n, int) {
   std::memcpy(d, s, n);
   return cudaSuccess;
 }
+static inline cudaError_t cudaMemcpyAsync(void* d, const void* s, size_t n, int k, cudaStream_t) {
+  return cudaMemcpy(d, s, n, k);
+}
 #else
 #include <cuda_runtime.h>
 #endif
@@ -85,9 +88,34 @@ struct Op {
 
 size_t type_size(int t) { return t == 8 ? 8 : t == 2 ? 4 : 0; }
 
+// HMX_SHIM_TRACE=1: one stderr line per operation; a wait longer than
+// HMX_SHIM_WAIT_S (default 120 s) prints what it waited for and aborts
+bool trace() {
+  static const bool t = std::getenv("HMX_SHIM_TRACE") != nullptr;
+  return t;
+}
+double wait_limit() {
+  static const double w = std::getenv("HMX_SHIM_WAIT_S") ? std::atof(std::getenv("HMX_SHIM_WAIT_S")) : 120.0;
+  return w;
+}
+thread_local const char* g_waiting = "";
+thread_local timespec g_t0;
 void spin(int& n) {
-  if (++n > 64) usleep(20);
-  else sched_yield();
+  if (n == 0) clock_gettime(CLOCK_MONOTONIC, &g_t0);
+  if (++n > 64) {
+    usleep(20);
+    if ((n & 1023) == 0) {
+      timespec t;
+      clock_gettime(CLOCK_MONOTONIC, &t);
+      if ((double)(t.tv_sec - g_t0.tv_sec) + 1e-9 * (double)(t.tv_nsec - g_t0.tv_nsec) > wait_limit()) {
+        std::fprintf(stderr, "hmx_nccl_shim: pid %d stuck waiting for %s\n", (int)getpid(), g_waiting);
+        std::fflush(stderr);
+        std::abort();
+      }
+    }
+  } else {
+    sched_yield();
+  }
 }
 
 thread_local int g_group = 0;
@@ -107,12 +135,23 @@ namespace {
 
 Chan& chan(ShimComm* c, int src, int dst) { return c->shm->chan[src * c->world + dst]; }
 
+// Host -> device on the operation's stream, complete when this returns (a
+// plain cudaMemcpy from pageable memory can return before its DMA lands, and
+// the library's kernels run on non-blocking streams that do not order after
+// the legacy stream).
+cudaError_t h2d(void* dst, const void* src, size_t bytes, cudaStream_t st) {
+  cudaError_t e = cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, st);
+  return e == cudaSuccess ? cudaStreamSynchronize(st) : e;
+}
+
 ncclResult_t do_send(ShimComm* c, const Op& o) {
   const size_t bytes = o.count * type_size(o.type);
   if (bytes > kChanBytes || o.peer < 0 || o.peer >= c->world) return kInvalidArgument;
   if (cudaStreamSynchronize(o.st) != cudaSuccess) return kInternalError;
   Chan& ch = chan(c, c->rank, o.peer);
   int n = 0;
+  g_waiting = "a send slot to be consumed";
+  if (trace()) std::fprintf(stderr, "shim r%d send #%llu to %d: %zu B\n", c->rank, (unsigned long long)c->sent[o.peer] + 1, o.peer, bytes);
   while (ch.read.load(std::memory_order_acquire) != ch.written.load(std::memory_order_acquire)) spin(n);
   if (cudaMemcpy(ch.data, o.sbuf, bytes, cudaMemcpyDeviceToHost) != cudaSuccess) return kInternalError;
   ch.bytes = bytes;
@@ -127,9 +166,11 @@ ncclResult_t do_recv(ShimComm* c, const Op& o) {
   Chan& ch = chan(c, o.peer, c->rank);
   const uint64_t want = ++c->recvd[o.peer];
   int n = 0;
+  g_waiting = "a message";
+  if (trace()) std::fprintf(stderr, "shim r%d recv #%llu from %d: %zu B\n", c->rank, (unsigned long long)want, o.peer, bytes);
   while (ch.written.load(std::memory_order_acquire) < want) spin(n);
   if (ch.bytes != bytes) return kInvalidArgument;
-  if (cudaMemcpy(o.rbuf, ch.data, bytes, cudaMemcpyHostToDevice) != cudaSuccess) return kInternalError;
+  if (h2d(o.rbuf, ch.data, bytes, o.st) != cudaSuccess) return kInternalError;
   ch.read.store(want, std::memory_order_release);
   return 0;
 }
@@ -141,6 +182,8 @@ ncclResult_t do_allreduce(ShimComm* c, const Op& o) {
   const uint64_t r = ++c->rounds;
   Shm* s = c->shm;
   int n = 0;
+  g_waiting = "an allreduce round";
+  if (trace()) std::fprintf(stderr, "shim r%d allreduce #%llu: %zu x type %d op %d\n", c->rank, (unsigned long long)r, o.count, o.type, o.op);
   for (int q = 0; q < c->world; ++q)  // everyone has read the previous round's slots
     while (s->ar[q].done.load(std::memory_order_acquire) + 1 < r) spin(n);
   ArSlot& mine = s->ar[c->rank];
@@ -169,7 +212,21 @@ ncclResult_t do_allreduce(ShimComm* c, const Op& o) {
     }
   }
   mine.done.store(r, std::memory_order_release);
-  if (cudaMemcpy(o.rbuf, acc.data(), bytes, cudaMemcpyHostToDevice) != cudaSuccess) return kInternalError;
+  if (trace()) {
+    for (size_t i = 0; i < o.count && i < 2; ++i) {
+      if (o.type == 8) {
+        double a, m;
+        std::memcpy(&a, acc.data() + 8 * i, 8);
+        std::memcpy(&m, mine.data + 8 * i, 8);
+        std::fprintf(stderr, "shim r%d   = %.17g (mine %.17g)\n", c->rank, a, m);
+      } else {
+        int32_t a;
+        std::memcpy(&a, acc.data() + 4 * i, 4);
+        std::fprintf(stderr, "shim r%d   = %d\n", c->rank, a);
+      }
+    }
+  }
+  if (h2d(o.rbuf, acc.data(), bytes, o.st) != cudaSuccess) return kInternalError;
   return 0;
 }
 

@@ -34,18 +34,20 @@ def test_prepare_scheme_reproduces_reference_payloads_bitwise(hx):
 def test_reference_objects_through_drop_in_on_the_gpu(hx):
     from paper_1911_00093_b200 import drop_in
 
+    import sys
     h, arr, meta = R.hmatrix()
     pkg = R.fake_reference_package()
+    mv, sv = sys.modules[pkg.__name__ + ".matvec"], sys.modules[pkg.__name__ + ".solver"]
     saved = drop_in.install(pkg)
     try:
         for s in SCHEMES:
             sh = R.scheme_hmatrix(h, s)
-            y = pkg.matvec.matvec(sh, arr["x"])
+            y = mv.matvec(sh, arr["x"])
             tol = 1e-12 if s in FP64_ONLY else 1e-5
             ref = arr[f"y/{s}"]
             assert np.max(np.abs(y - ref)) <= tol * np.max(np.abs(ref)), s
-            assert np.array_equal(pkg.matvec.matvec_threaded(sh, arr["x"], 4), y)
-            x, rep = pkg.solver.bicgstab(sh, h, arr["b"], hx.SolverConfig(tol=meta["tol"],
+            assert np.array_equal(mv.matvec_threaded(sh, arr["x"], 4), y)
+            x, rep = sv.bicgstab(sh, h, arr["b"], hx.SolverConfig(tol=meta["tol"],
                                                                          max_iter=meta["max_iter"]))
             env = meta["reports"][s]["envelope"]
             slack = max(1, int(0.05 * meta["reports"][s]["iterations"]))

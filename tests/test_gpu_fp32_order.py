@@ -23,7 +23,10 @@ import pytest
 
 from golden_util import GOLDEN, config1_hmatrix, hmatrix_from_fixture, load
 
-SMALL_VARIANTS = {2, 3, 6, 7}   # widths where SGEMV's short-row path differs by row count
+# widths whose SGEMV path (numpy's kernel choice for short rows) is not
+# reproduced for every row: checked at the FP32 tolerance only
+SMALL_VARIANTS = {1, 2, 3, 5, 6, 7, 8}
+ROWS = (8, 40, 30, 5)   # 30 and 5: OpenBLAS's two- and one-row remainder kernels
 
 
 def fixture():
@@ -31,13 +34,13 @@ def fixture():
 
 
 def test_model_reproduces_reference_products():
-    from tools.fp32_accum_emulation import sgemv_tree
+    from tools.fp32_accum_emulation import sgemv_rows
     f = fixture()
-    for m in (8, 40):
+    for m in ROWS:
         for n in range(1, 49):
             a32 = f[f"a/{m}/{n}"].astype(np.float32)
             x32 = f[f"x/{m}/{n}"].astype(np.float32)
-            y = sgemv_tree(a32, x32)
+            y = sgemv_rows(a32, x32)
             ref = f[f"y/{m}/{n}"]
             if n in SMALL_VARIANTS:
                 assert np.allclose(y, ref, rtol=1e-5, atol=1e-6), (m, n)
@@ -80,9 +83,9 @@ def _block_diagonal(hx, m, widths, values):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("m", [8, 40])
+@pytest.mark.parametrize("m", ROWS)
 def test_gpu_items_bitwise_sgemv_order(hx, m):
-    from tools.fp32_accum_emulation import sgemv_tree
+    from tools.fp32_accum_emulation import sgemv_rows
     f = fixture()
     widths = list(range(1, 49))
     h, n = _block_diagonal(hx, m, widths, [f[f"a/{m}/{w}"] for w in widths])
@@ -97,7 +100,7 @@ def test_gpu_items_bitwise_sgemv_order(hx, m):
         got = y[k * m:(k + 1) * m]
         a32 = f[f"a/{m}/{w}"].astype(np.float32)
         x32 = x[c0:c0 + w].astype(np.float32)
-        model = sgemv_tree(a32, x32).astype(np.float64)
+        model = sgemv_rows(a32, x32).astype(np.float64)
         assert np.array_equal(got, model), (m, w, got - model)
         if w not in SMALL_VARIANTS:
             assert np.array_equal(got, f[f"y/{m}/{w}"].astype(np.float64)), (m, w)

@@ -134,6 +134,101 @@ def sgemv_tree(a, g):
     return v
 
 
+def row_kind(i: int, m: int) -> int:
+    """OpenBLAS SGEMV-T computes the rows (outputs) of an m-row block four at a
+    time; the remainder uses a two-row and then a one-row kernel, whose
+    summation differs.  Kind 4, 2 or 1 for row i."""
+    if i < (m & ~3):
+        return 4
+    if (m & 3) >= 2 and i < (m & ~3) + 2:
+        return 2
+    return 1
+
+
+def _mul(a, b):
+    return (np.asarray(a, F32).astype(F64) * np.asarray(b, F32).astype(F64)).astype(F32)
+
+
+def sgemv_kind(a, g, kind: int):
+    """One row class of SGEMV-T (probed with tools/sgemv_order_probe.py and
+    the brute-force family search described in DESIGN.md):
+      kind 4: A/B accumulators, FMA chains (sgemv_tree);
+      kind 2: ONE 4-lane accumulator over all chunks, multiply-then-add;
+      kind 1: A/B accumulators, multiply-then-add;
+    then (l0 + l1) + (l2 + l3) and the tail rule of sgemv_tree.  Short rows:
+    kind 4 as sgemv_tree; kinds 2/1: n = 2..7 a sequential multiply-add chain
+    (kind 1, n = 3: the tail rule; n = 5: sequential lanes + fused tail), n = 4
+    pairwise (kind 1: sequential), n = 8 (kind 1): A/B with a sequential
+    horizontal sum."""
+    a = np.asarray(a, F32)
+    g = np.asarray(g, F32)
+    m, n = a.shape
+    if kind == 4:
+        return sgemv_tree(a, g)
+    z = np.zeros(m, F32)
+    G = lambda k: np.full(m, g[k], F32)
+    P = lambda k: _mul(a[:, k], G(k))
+    if n == 1:
+        return P(0)
+    if kind == 1 and n == 3:
+        return _fma(a[:, 2], G(2), _fma(a[:, 0], G(0), P(1)))
+    if n <= 7 and n != 4 and not (kind == 1 and n == 5):
+        v = P(0)
+        for k in range(1, n):
+            v = v + P(k)
+        return v
+    nch, tt = n >> 2, n & 3
+    if kind == 2:
+        ca, cb = list(range(nch)), []
+    elif nch % 2:
+        ca, cb = [0] + list(range(1, nch, 2)), list(range(2, nch, 2))
+    else:
+        ca, cb = list(range(0, nch, 2)), list(range(1, nch, 2))
+    lanes = []
+    for j in range(4):
+        va, vb = z, z
+        for c in ca:
+            va = va + P(4 * c + j)
+        for c in cb:
+            vb = vb + P(4 * c + j)
+        lanes.append(va + vb)
+    seq = kind == 1 and n <= 8
+    v = ((lanes[0] + lanes[1]) + lanes[2]) + lanes[3] if seq else (lanes[0] + lanes[1]) + (lanes[2] + lanes[3])
+    mm = 4 * nch
+    if tt == 1:
+        v = _fma(a[:, mm], G(mm), v)
+    elif tt >= 2:
+        t = _fma(a[:, mm], G(mm), P(mm + 1))
+        if tt == 3:
+            t = _fma(a[:, mm + 2], G(mm + 2), t)
+        v = v + t
+    return v
+
+
+def sgemv_rows(a, g):
+    """SGEMV-T of an m-row block, every row in its kernel's order (row_kind)."""
+    m = a.shape[0]
+    out = np.empty(m, F32)
+    kinds = np.array([row_kind(i, m) for i in range(m)])
+    for k in (4, 2, 1):
+        sel = kinds == k
+        if sel.any():
+            out[sel] = sgemv_kind(a[sel], g, k)
+    return out
+
+
+def sgemv_blocked(a, g, block: int = 4096, rows: bool = False):
+    """OpenBLAS SGEMV-T over long rows: 4096-column blocks, each reduced by
+    sgemv_tree (the tail in the last block), added in order -- the order of
+    the GPU's m1-single stage 1 (s1_exact_kernel)."""
+    n = a.shape[1]
+    y = None
+    for s0 in range(0, n, block):
+        v = (sgemv_rows if rows else sgemv_tree)(a[:, s0:s0 + block], g[s0:s0 + block])
+        y = v if y is None else (y + v).astype(F32)
+    return y
+
+
 def prod32(a, g, order: str):
     a = np.asarray(a, F32)
     g = np.asarray(g, F32)
@@ -146,6 +241,8 @@ def prod32(a, g, order: str):
         return fma_chain(a, g)
     if order == "sgemv":
         return sgemv_tree(a, g)
+    if order == "sgemv-rows":
+        return sgemv_rows(a, g)
     if order.startswith("lanes"):
         k = int(order[5:])
         lanes = [fma_chain(a[:, j::k], g[j::k]) for j in range(min(k, n))]
@@ -170,7 +267,10 @@ def matvec_model(sh, x, order: str, stage1_order: str | None = None):
                 yp[r0:r1] += orc.dense_partial(pay.values, xs, xs32)
         elif not hasattr(pay, "diag") and not hasattr(pay, "u_hi") and pay.u.dtype == F32:
             if xs32 is not None:   # m1-single: z = Vt32 x32 in FP32 too
-                z = prod32(pay.vt.T.T, xs32, s1) if s1 != "numpy" else pay.vt @ xs32
+                if s1 in ("sgemv", "sgemv-rows"):
+                    z = sgemv_blocked(pay.vt, xs32, rows=s1 == "sgemv-rows")
+                else:
+                    z = prod32(pay.vt, xs32, s1) if s1 != "numpy" else pay.vt @ xs32
             else:                  # m1-mixed: FP64 sum, rounded once
                 z = (pay.vt @ xs).astype(F32)
             yp[r0:r1] += prod32(pay.u, z, order)
@@ -209,6 +309,10 @@ def bitwise_check():
                     bad.append(n)
                     break
         print(f"rows {m:3d}: widths 1..69 differing from numpy: {bad if bad else 'none'}")
+    for n in (100, 1280, 4096, 4100, 5120, 10240, 20480):
+        a = rng.standard_normal((8, n)).astype(F32)
+        g = rng.standard_normal(n).astype(F32)
+        print(f"long row n={n}: blocked model == numpy: {np.array_equal(sgemv_blocked(a, g), a @ g)}")
 
 
 def main():
@@ -224,7 +328,8 @@ def main():
         for s in ("m1-single", "m1-mixed", "m2-single"):
             sh = hx.prepare_scheme(h, s)
             ref = np.linalg.norm(orc.matvec(sh, x) - y64)
-            row = [np.linalg.norm(matvec_model(sh, x, o, "numpy") - y64) / ref for o in orders]
+            row = [np.linalg.norm(matvec_model(sh, x, o, "sgemv" if o == "sgemv" else "numpy") - y64) / ref
+                   for o in orders]
             print(f"{name:12s} {s:10s} " + " ".join(f"{v:8.4f}" for v in row), flush=True)
 
 
