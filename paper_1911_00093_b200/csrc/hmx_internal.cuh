@@ -47,10 +47,22 @@ static_assert(sizeof(Seg) == 64, "Seg layout");
 
 // RUN_CHUNK: a stage-2 FP32-accumulated item in SGEMV chunk layout (below)
 enum : int32_t { RUN_Z = 1, RUN_ROUND = 2, RUN_ACC32 = 4, RUN_CHUNK = 8 };
-// RUN_CHUNK items: bits 8..15 of Run.flags locate the SGEMV remainder rows of
-// the item's block within the segment (chain_row_kind): 3 + the segment row
-// where they start (0x7f: none here) | 0x80 when there are >= 2 of them
-constexpr int kRunKindShift = 8;
+// RUN_CHUNK items: bits 4..31 of Run.flags locate, within the segment, the
+// row classes OpenBLAS SGEMV-T computes the item's block in (it takes the
+// rows of an m-row block 16, then 8, then 4 at a time, then a 2-row and a
+// 1-row remainder kernel, whose summation orders differ): four 7-bit
+// segment-relative row bounds e16 | e8 << 7 | e4 << 14 | e2 << 21
+// (chain_row_kind: p < e16 -> 16, < e8 -> 8, < e4 -> 4, < e2 -> 2, else 1)
+constexpr int kRunKindShift = 4;
+__host__ __device__ __forceinline__ int chain_row_kind(uint32_t bits, int p) {
+  const int e16 = bits & 127, e8 = (bits >> 7) & 127, e4 = (bits >> 14) & 127, e2 = (bits >> 21) & 127;
+  return p < e16 ? 16 : p < e8 ? 8 : p < e4 ? 4 : p < e2 ? 2 : 1;
+}
+// the same classes for row i of an m-row block
+__host__ __device__ __forceinline__ int sgemv_row_kind(int64_t i, int64_t m) {
+  const int64_t a16 = m & ~int64_t(15), b8 = a16 + (m & 8), c4 = b8 + (m & 4);
+  return i < a16 ? 16 : i < b8 ? 8 : i < c4 ? 4 : ((m & 3) >= 2 && i < c4 + 2) ? 2 : 1;
+}
 
 // ---- FP32-accumulated stage-2 items: the reference's summation order ---------
 // The reference's FP32 products (`A32 @ x32`, `U32 @ z32`; matvec.py:57, :73)

@@ -120,10 +120,10 @@ __device__ __forceinline__ double z_epilogue(const DevPlan& P, double s, int zi)
 // FP64 (reference matvec.py:57, :73, then :106).  Explicit _rn intrinsics:
 // nothing is contracted or reassociated.
 //
-// The chain warps stage the segment's chain items through shared memory: a
-// ring of kChainBufs windows of whole consecutive items (<= kChainWin bytes
-// each, contiguous in the blob), copied with cp.async by all chain threads,
-// kChainBufs - 1 windows in flight while one is reduced; inside a window item i goes to slot i mod K (K = chain
+// The chain warps stage the segment's chain items through shared memory:
+// windows of whole consecutive items (<= kChainWin bytes, contiguous in the
+// blob), copied with cp.async by all chain threads into two buffers, the next
+// window in flight while one is reduced; inside a window item i goes to slot i mod K (K = chain
 // threads / rp), one row per thread.  Items larger than a window are read
 // from global memory by slot 0.
 __device__ __forceinline__ float4 fma4(float4 a, float4 g, float4 c) {
@@ -155,19 +155,16 @@ constexpr int kMetaW = 12;  // run meta in shared memory: col0 << 12 | width
 #ifndef HMX_CHAIN_WB
 #define HMX_CHAIN_WB 8192
 #endif
-#ifndef HMX_CHAIN_NBUF
-#define HMX_CHAIN_NBUF 3
-#endif
-constexpr int kChainWin = HMX_CHAIN_WB;     // bytes per staging buffer
-constexpr int kChainBufs = HMX_CHAIN_NBUF;  // staging buffers (windows in flight + 1)
+constexpr int kChainWin = HMX_CHAIN_WB;  // bytes per staging buffer (two buffers)
 
 // row p of one n-wide item at `it` (global or shared memory, chunk layout).
 // `kind`: which OpenBLAS SGEMV-T row kernel computes this row of its block
-// (row_kind): 4 = the four-row kernel (A/B FMA chains), 2 = the two-row
+// (sgemv_row_kind): 16, 8, 4 = the 16-, 8- and 4-row kernels (A/B FMA
+// chains; rows shorter than 8 differ between them), 2 = the two-row
 // remainder kernel (one 4-lane accumulator, multiply then add), 1 = the
 // one-row remainder kernel (A/B, multiply then add).  All end with
-// (l0 + l1) + (l2 + l3) and the same tail rule; short rows differ per kernel
-// (tools/fp32_accum_emulation.py sgemv_kind, checked bitwise against numpy).
+// (l0 + l1) + (l2 + l3) and the same tail rule (tools/fp32_accum_emulation.py
+// sgemv_kind: bitwise numpy's own for every row count 2..64, widths 1..48).
 // G(k): the FP32 source value of the item's column k.
 template <bool GLOBAL, typename GF>
 __device__ __forceinline__ float chain_item(const float* it, GF G, int n, int rp, int p, int kind) {
@@ -188,25 +185,34 @@ __device__ __forceinline__ float chain_item(const float* it, GF G, int n, int rp
     return k < m ? L1(it + 4 * ((int64_t)(k >> 2) * rp + p) + (k & 3)) : L1(it + (int64_t)m * rp + (int64_t)(k - m) * rp + p);
   };
   auto Pr = [&](int k) { return __fmul_rn(E(k), G(c0 + k)); };  // rounded product
-  if (kind != 4 && n <= 8 && n != 4 && !(kind == 1 && (n == 3 || n == 5 || n == 8)) && !(kind == 2 && n == 8)) {
-    // remainder kernels, n = 1..7: a sequential multiply-then-add chain
-    float v = Pr(0);
-    for (int k = 1; k < n; ++k) v = __fadd_rn(v, Pr(k));
+  auto F = [&](int k, float acc) { return __fmaf_rn(E(k), G(c0 + k), acc); };
+  if (n == 1) return Pr(0);
+  if (kind >= 4 && n <= 7 && n != 4) {  // short rows of the 16-, 8- and 4-row kernels
+    if (n == 2 && kind != 16) return __fadd_rn(Pr(0), Pr(1));
+    if (kind == 4 && n == 3) return F(2, F(0, Pr(1)));
+    if (kind == 4 && n == 6) return __fadd_rn(__fadd_rn(Pr(0), F(1, Pr(2))), __fadd_rn(Pr(3), F(4, Pr(5))));
+    if (kind == 4 && n == 7)
+      return __fadd_rn(__fadd_rn(F(0, Pr(1)), F(4, Pr(5))), __fadd_rn(F(2, Pr(3)), Pr(6)));
+    float v = 0.f;  // one forward FMA chain
+    for (int k = 0; k < n; ++k) v = F(k, v);
     return v;
   }
-  if (kind == 1 && n == 3) return __fmaf_rn(E(2), G(c0 + 2), __fmaf_rn(E(0), G(c0), Pr(1)));
-  if (kind == 1 && n == 5)  // lanes = products, summed in order, the tail column fused
-    return __fmaf_rn(E(4), G(c0 + 4), __fadd_rn(__fadd_rn(__fadd_rn(Pr(0), Pr(1)), Pr(2)), Pr(3)));
-  if (chain_shaped(n)) {  // four-row kernel, n <= 3, 5 <= n <= 7: one forward FMA chain
-    float v = 0.f;
-    for (int k = 0; k < n; ++k) v = __fmaf_rn(E(k), G(c0 + k), v);
-    return v;
+  if (kind < 4) {  // the 2- and 1-row remainder kernels, short rows
+    if (kind == 1 && n == 3) return F(2, F(0, Pr(1)));
+    if (kind == 2 && n == 8)
+      return __fadd_rn(__fadd_rn(__fadd_rn(Pr(0), Pr(1)), __fadd_rn(Pr(4), Pr(5))),
+                       __fadd_rn(__fadd_rn(Pr(2), Pr(3)), __fadd_rn(Pr(6), Pr(7))));
+    if (n <= 7 && n != 4) {  // a sequential multiply-then-add chain
+      float v = Pr(0);
+      for (int k = 1; k < n; ++k) v = __fadd_rn(v, Pr(k));
+      return v;
+    }
   }
   const int nch = n >> 2, T = n & 3, m = 4 * nch;
   const float* ch = it + 4 * p;  // chunk c of row p at ch[4 c rp]
   float4 l;
   bool seq = false;  // sequential horizontal sum (one-row kernel, n <= 8)
-  if (n == 8 && kind == 4) {  // l_j = a_2j g_2j + a_2j+1 g_2j+1
+  if (n == 8 && kind >= 4) {  // l_j = a_2j g_2j + a_2j+1 g_2j+1
     const float4 x0 = L4(ch), x1 = L4(ch + 4 * rp);
     const float4 g0 = G4(c0), g1 = G4(c0 + 4);
     l = make_float4(__fadd_rn(__fmul_rn(x0.x, g0.x), __fmul_rn(x0.y, g0.y)),
@@ -219,7 +225,7 @@ __device__ __forceinline__ float chain_item(const float* it, GF G, int n, int rp
     // kernel: every chunk into A
     float4 A = make_float4(0.f, 0.f, 0.f, 0.f), B = A;
     auto acc = [&](float4& X, const float4& x, const float4& g) {
-      if (kind == 4) X = fma4(x, g, X);
+      if (kind >= 4) X = fma4(x, g, X);
       else X = make_float4(__fadd_rn(X.x, __fmul_rn(x.x, g.x)), __fadd_rn(X.y, __fmul_rn(x.y, g.y)),
                            __fadd_rn(X.z, __fmul_rn(x.z, g.z)), __fadd_rn(X.w, __fmul_rn(x.w, g.w)));
     };
@@ -254,30 +260,22 @@ __device__ __forceinline__ float chain_item(const float* it, GF G, int n, int rp
   return v;
 }
 
-// row kind of segment row p for an item whose block's remainder rows start at
-// segment row `rem` (kinfo: (rem + 3) | 0x80 when the remainder has >= 2
-// rows; 0x7f: no remainder rows in this segment)
-__device__ __forceinline__ int chain_row_kind(uint8_t kinfo, int p) {
-  const int rem = (kinfo & 0x7f) - 3;
-  if (p < rem) return 4;
-  if ((kinfo & 0x80) && p < rem + 2) return 2;
-  return 1;
-}
-
 // chain threads u = 0 .. nthr-1 (slot u / rp, row u % rp); items j0 .. nrun-1
 // of the part (meta in shared memory, the part's blob at `part`); buf: two
-// kChainWin-byte staging buffers.  Returns this thread's row sum (FP64).
-__device__ __forceinline__ double chain_windows(const int32_t* meta, const uint8_t* kinfo, int j0, int nrun,
+// kChainWin-byte staging buffers; wq: 6 ints of shared memory for the window
+// bounds thread 0 publishes one window ahead.  Returns this thread's row sum.
+__device__ __forceinline__ double chain_windows(const int32_t* meta, const uint32_t* kbits, int j0, int nrun,
                                                 const float* part, const double* gs, int rp, int u, int nthr,
-                                                float* buf) {
+                                                float* buf, int* wq) {
   const int K = nthr / rp;
   const int slot = u / rp, p = u - slot * rp;
   const bool act = slot < K;
-  const int64_t wmax = kChainWin / (4 * (int64_t)rp);  // columns per window
-  auto col0 = [&](int j) { return j < nrun ? (meta[j] >> kMetaW) : -1; };
+  const int wmax = kChainWin / (4 * rp);  // columns per window
+  auto col0 = [&](int j) { return meta[j] >> kMetaW; };
   auto width = [&](int j) { return meta[j] & ((1 << kMetaW) - 1); };
   // window starting at item j: [j, end) of <= wmax columns, or one oversize item
   auto wend = [&](int j) {
+    if (j >= nrun) return j;
     const int cs = col0(j);
     int e = j + 1;
     if (width(j) > wmax) return e;
@@ -287,56 +285,57 @@ __device__ __forceinline__ double chain_windows(const int32_t* meta, const uint8
   auto stage = [&](int j, int e, int b) {  // copy window [j, e) into buffer b (nothing if oversize)
     if (j >= nrun || width(j) > wmax) return;
     const int cs = col0(j), ce = col0(e - 1) + width(e - 1);
-    const int64_t n16 = (int64_t)(ce - cs) * rp / 4;  // 16-byte pieces
+    const int n16 = (ce - cs) * rp / 4;  // 16-byte pieces
     const float* src = part + (int64_t)cs * rp;
-    float* dst = buf + (int64_t)b * (kChainWin / 4);
-    for (int64_t i = u; i < n16; i += nthr) cp_async16(dst + 4 * i, src + 4 * i);
+    float* dst = buf + b * (kChainWin / 4);
+    for (int i = u; i < n16; i += nthr) cp_async16(dst + 4 * i, src + 4 * i);
   };
-  double acc = 0.0;
-  // a ring of kChainBufs windows: kChainBufs - 1 in flight while one is reduced
-  int ws[kChainBufs], we[kChainBufs];  // window bounds per buffer
-  int nxt = j0;                        // first item not yet staged
-#pragma unroll
-  for (int k = 0; k < kChainBufs - 1; ++k) {
-    ws[k] = nxt;
-    we[k] = nxt < nrun ? wend(nxt) : nxt;
-    stage(ws[k], we[k], k);
-    nxt = we[k];
-    asm volatile("cp.async.commit_group;" ::: "memory");
+  // window bounds: a ring of three (start, end) pairs in wq, written by thread
+  // 0 one window ahead of their use
+  if (u == 0) {
+    const int e0 = wend(j0), e1 = wend(e0);
+    wq[0] = j0, wq[1] = e0, wq[2] = e0, wq[3] = e1;
   }
+  chain_bar(nthr);
+  stage(wq[0], wq[1], 0);
+  asm volatile("cp.async.commit_group;" ::: "memory");
+  double acc = 0.0;
   for (int w = 0;; ++w) {
-    const int b = w % kChainBufs;
-    const int j = ws[b], e = we[b];
+    const int r = w % 3, r1 = (w + 1) % 3, r2 = (w + 2) % 3;
+    const int j = wq[2 * r], e = wq[2 * r + 1];
     if (j >= nrun) break;
-    {  // the window kChainBufs - 1 ahead goes into the buffer freed last round
-      const int bn = (w + kChainBufs - 1) % kChainBufs;
-      ws[bn] = nxt;
-      we[bn] = nxt < nrun ? wend(nxt) : nxt;
-      stage(ws[bn], we[bn], bn);
-      nxt = we[bn];
+    const int jn = wq[2 * r1], en = wq[2 * r1 + 1];
+    stage(jn, en, (w + 1) & 1);  // the next window is in flight while this one is reduced
+    asm volatile("cp.async.commit_group;\ncp.async.wait_group 1;" ::: "memory");
+    if (u == 0) {  // publish the window after next
+      wq[2 * r2] = en;
+      wq[2 * r2 + 1] = wend(en);
     }
-    asm volatile("cp.async.commit_group;\ncp.async.wait_group %0;" ::"n"(kChainBufs - 1) : "memory");
     chain_bar(nthr);  // every thread's copies of window [j, e) have landed
     if (act) {
       if (width(j) > wmax) {  // oversize item: straight from global memory
         if (slot == 0) {
           const int c0 = col0(j);
-          acc += (double)chain_item<true>(
-              part + (int64_t)c0 * rp, [&](int k) { return __int_as_float(__double2loint(gs[c0 + k])); },
-              width(j), rp, p, chain_row_kind(kinfo[j], p));
+          auto G = [&](int k) { return __int_as_float(__double2loint(gs[c0 + k])); };
+          acc += (double)chain_item<true>(part + (int64_t)c0 * rp, G, width(j), rp, p, chain_row_kind(kbits[j], p));
         }
       } else {
-        const float* base = buf + (int64_t)b * (kChainWin / 4);
+        const float* base = buf + (w & 1) * (kChainWin / 4);
         const int cs = col0(j);
         for (int i = j + slot; i < e; i += K) {
           const int c0 = col0(i);
-          acc += (double)chain_item<false>(
-              base + (int64_t)(c0 - cs) * rp, [&](int k) { return __int_as_float(__double2loint(gs[c0 + k])); },
-              width(i), rp, p, chain_row_kind(kinfo[i], p));
+          auto G = [&](int k) { return __int_as_float(__double2loint(gs[c0 + k])); };
+          const float* it = base + (c0 - cs) * rp;
+          // the common case first: every row of the segment in SGEMV's
+          // 16-row kernel (n < 8), or in the 16/8/4-row kernels (n >= 8)
+          const uint32_t kb = kbits[i];
+          const int wi = width(i);
+          if ((int)((kb >> (wi < 8 ? 0 : 14)) & 127) >= rp) acc += (double)chain_item<false>(it, G, wi, rp, p, 16);
+          else acc += (double)chain_item<false>(it, G, wi, rp, p, chain_row_kind(kb, p));
         }
       }
     }
-    chain_bar(nthr);  // buffer b is free again
+    chain_bar(nthr);  // buffer w & 1 is free again
   }
   asm volatile("cp.async.wait_group 0;" ::: "memory");
   return acc;
@@ -364,66 +363,58 @@ __global__ void __launch_bounds__(kS1ExactRows) s1_exact_kernel(DevPlan P, const
   auto G = [&](int c) { return (float)__ldg(xs + c); };
   auto G4 = [&](int c) { return make_float4(G(c), G(c + 1), G(c + 2), G(c + 3)); };
   float y = 0.f;
-  const int kind = t < sg.R ? P.zkind[sg.row0 + t] : 4;
+  const int kind = t < sg.R ? P.zkind[sg.row0 + t] : 16;
   if (t >= sg.R) {
     // (idle row: no loads; joins the barrier below)
-  } else if (kind != 4) {
-    // a remainder row of its block's SGEMV (this CTA holds one 4096-column block)
+  } else if (n <= 8) {  // short rows (chain-shaped, n = 4, n = 8): the per-kernel rules
     y = chain_item<true>(it, G, n, rp, t, kind);
-  } else if (chain_shaped(n)) {
-    for (int k = 0; k < n; ++k) y = __fmaf_rn(ld_one(it + (int64_t)k * rp + t), G(k), y);
-  } else if (n == 8) {
-    const float4 x0 = ld_chunk(it + 4 * t), x1 = ld_chunk(it + 4 * (rp + t));
-    const float4 g0 = G4(0), g1 = G4(4);
-    const float l0 = __fadd_rn(__fmul_rn(x0.x, g0.x), __fmul_rn(x0.y, g0.y));
-    const float l1 = __fadd_rn(__fmul_rn(x0.z, g0.z), __fmul_rn(x0.w, g0.w));
-    const float l2 = __fadd_rn(__fmul_rn(x1.x, g1.x), __fmul_rn(x1.y, g1.y));
-    const float l3 = __fadd_rn(__fmul_rn(x1.z, g1.z), __fmul_rn(x1.w, g1.w));
-    y = __fadd_rn(__fadd_rn(l0, l1), __fadd_rn(l2, l3));
   } else {
+    // this CTA's 4096-column block: the A/B lane tree (kind 4: FMA chains;
+    // kind 1: multiply then add; kind 2: one accumulator, multiply then add)
     const int nch = n >> 2, T = n & 3;
-    for (int b0 = 0; b0 < nch; b0 += kSgemvBlock) {
-      const int nb = min(kSgemvBlock, nch - b0);
-      const bool odd = nb & 1;
-      const float* ch = it + 4 * ((int64_t)b0 * rp + t);  // chunk b0 + c at ch[4 c rp]
-      float4 A = make_float4(0.f, 0.f, 0.f, 0.f), B = A;
-      int c = 0;
-      if (odd) {
-        A = fma4(ld_chunk(ch), G4(4 * b0), A);
-        c = 1;
-      }
-      // pairs (A, B), up to four pairs' loads in flight
-      for (; c < nb; c += 8) {
-        float4 xa[4], xb[4];
+    const bool fm = kind >= 4, one = kind == 2;
+    auto upd = [&](float4& X, const float4& x, const float4& g) {
+      if (fm) X = fma4(x, g, X);
+      else X = make_float4(__fadd_rn(X.x, __fmul_rn(x.x, g.x)), __fadd_rn(X.y, __fmul_rn(x.y, g.y)),
+                           __fadd_rn(X.z, __fmul_rn(x.z, g.z)), __fadd_rn(X.w, __fmul_rn(x.w, g.w)));
+    };
+    const float* ch = it + 4 * t;  // chunk c at ch[4 c rp]
+    float4 A = make_float4(0.f, 0.f, 0.f, 0.f), B = A;
+    int c = 0;
+    if (nch & 1) {  // odd: chunk 0 alone into A, then pairs (A, B) -- one accumulator: all into A
+      upd(A, ld_chunk(ch), G4(0));
+      c = 1;
+    }
+    for (; c < nch; c += 8) {  // up to four pairs' loads in flight
+      float4 xa[4], xb[4];
 #pragma unroll
-        for (int u = 0; u < 4; ++u)
-          if (c + 2 * u < nb) {
-            xa[u] = ld_chunk(ch + (int64_t)4 * (c + 2 * u) * rp);
-            xb[u] = ld_chunk(ch + (int64_t)4 * (c + 2 * u + 1) * rp);
-          }
-#pragma unroll
-        for (int u = 0; u < 4; ++u)
-          if (c + 2 * u < nb) {
-            A = fma4(xa[u], G4(4 * (b0 + c + 2 * u)), A);
-            B = fma4(xb[u], G4(4 * (b0 + c + 2 * u + 1)), B);
-          }
-      }
-      const float4 l = make_float4(__fadd_rn(A.x, B.x), __fadd_rn(A.y, B.y), __fadd_rn(A.z, B.z),
-                                   __fadd_rn(A.w, B.w));
-      float v = __fadd_rn(__fadd_rn(l.x, l.y), __fadd_rn(l.z, l.w));
-      if (b0 + nb == nch && T > 0) {  // the tail belongs to the last block
-        const int m = 4 * nch;
-        const float* tl = it + (int64_t)m * rp + t;
-        if (T == 1) {
-          v = __fmaf_rn(ld_one(tl), G(m), v);
-        } else {
-          float tv = __fmul_rn(ld_one(tl + rp), G(m + 1));
-          tv = __fmaf_rn(ld_one(tl), G(m), tv);
-          if (T == 3) tv = __fmaf_rn(ld_one(tl + 2 * rp), G(m + 2), tv);
-          v = __fadd_rn(v, tv);
+      for (int u = 0; u < 4; ++u)
+        if (c + 2 * u < nch) {
+          xa[u] = ld_chunk(ch + (int64_t)4 * (c + 2 * u) * rp);
+          xb[u] = ld_chunk(ch + (int64_t)4 * (c + 2 * u + 1) * rp);
         }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (c + 2 * u < nch) {
+          upd(A, xa[u], G4(4 * (c + 2 * u)));
+          if (one) upd(A, xb[u], G4(4 * (c + 2 * u + 1)));
+          else upd(B, xb[u], G4(4 * (c + 2 * u + 1)));
+        }
+    }
+    const float4 l = make_float4(__fadd_rn(A.x, B.x), __fadd_rn(A.y, B.y), __fadd_rn(A.z, B.z),
+                                 __fadd_rn(A.w, B.w));
+    y = __fadd_rn(__fadd_rn(l.x, l.y), __fadd_rn(l.z, l.w));
+    if (T > 0) {
+      const int m = 4 * nch;
+      const float* tl = it + (int64_t)m * rp + t;
+      if (T == 1) {
+        y = __fmaf_rn(ld_one(tl), G(m), y);
+      } else {
+        float tv = __fmul_rn(ld_one(tl + rp), G(m + 1));
+        tv = __fmaf_rn(ld_one(tl), G(m), tv);
+        if (T == 3) tv = __fmaf_rn(ld_one(tl + 2 * rp), G(m + 2), tv);
+        y = __fadd_rn(y, tv);
       }
-      y = b0 == 0 ? v : __fadd_rn(y, v);
     }
   }
   if (sg.nchunks == 1) {
@@ -465,6 +456,7 @@ __global__ void __launch_bounds__(NT, DEEP ? 3 : (OUT == OUT_Y && F32MODE != F32
   __shared__ double wred[2][NT / 32];
   // chain-item staging buffers (stage-2 FP32 kernels: 2 x kChainWin bytes of dynamic shared memory)
   extern __shared__ __align__(16) float chain_buf[];
+  __shared__ int chain_wq[6];  // chain-window bounds (chain_windows)
   __shared__ unsigned ticket;
 
   if (out.skip != nullptr && *out.skip != 0) return;  // guarded launch (solver)
@@ -716,6 +708,8 @@ __global__ void __launch_bounds__(NT, DEEP ? 3 : (OUT == OUT_Y && F32MODE != F32
 
   if constexpr (F32MODE != F32_ALL64 && OUT == OUT_Y) {
     if (chain_thr) {
+      // (the per-item SGEMV row-kernel bounds live in red32, unused until the epilogue)
+      uint32_t* kbits = reinterpret_cast<uint32_t*>(red32);
       // the part's run meta into shared memory (sidx is free after the
       // gather), then a barrier among the chain warps only: the widened
       // warps stream on meanwhile
@@ -724,13 +718,14 @@ __global__ void __launch_bounds__(NT, DEEP ? 3 : (OUT == OUT_Y && F32MODE != F32
       for (int j = tid - wbc; j < sg.nrun32; j += NT - wbc) {
         const Run r = runs[j];
         sidx[j] = (r.col0 << kMetaW) | r.width;
-        fl[j] = (uint8_t)(r.flags >> kRunKindShift);
+        kbits[j] = (uint32_t)r.flags >> kRunKindShift;
       }
       chain_bar(NT - wbc);
       int j0 = 0;  // the first chain item (they follow the widened ones)
       const int c32c = P.gtab[sg.gtab + g32 + 1];
       while (j0 < sg.nrun32 && (sidx[j0] >> kMetaW) < c32c) ++j0;
-      bc = chain_windows(sidx, fl, j0, sg.nrun32, P.blob32 + sg.off32, gs, rp32, tid - wbc, NT - wbc, chain_buf);
+      bc = chain_windows(sidx, kbits, j0, sg.nrun32, P.blob32 + sg.off32, gs, rp32, tid - wbc, NT - wbc, chain_buf,
+                         chain_wq);
     }
   }
 
@@ -911,7 +906,7 @@ __global__ void probe_kernel(DevPlan P, const double* __restrict__ x, unsigned l
 // buffers of the stage-2 FP32 kernels
 template <int M, int O>
 constexpr size_t chain_smem() {
-  return (O == OUT_Y && M != F32_ALL64) ? (size_t)kChainBufs * kChainWin : 0;
+  return (O == OUT_Y && M != F32_ALL64) ? 2 * (size_t)kChainWin : 0;
 }
 
 template <int M, int O, int NT = kSegThreads, bool DEEP = false>

@@ -283,9 +283,8 @@ int hmx::plan_create_impl(const hmx_matrix_desc* d, int device, const hmx_plan_o
   std::vector<S1Fill> fills;
   std::vector<double> zscale(pipe >= P_M2D ? (size_t)std::max<int64_t>(Z, 1) : 1, 1.0);
   // m1-single stage 1: the SGEMV row kernel of every z entry (its rank index
-  // q within its block's rank r: rows 4 floor(r/4) .. r-1 are SGEMV's
-  // remainder rows; chain_row_kind)
-  std::vector<uint8_t> zkind(pipe == P_M1S ? (size_t)std::max<int64_t>(Z, 1) : 1, 4);
+  // q within its block's rank r: sgemv_row_kind(q, r))
+  std::vector<uint8_t> zkind(pipe == P_M1S ? (size_t)std::max<int64_t>(Z, 1) : 1, 16);
   int64_t part_len = 0;
   int32_t n_red = 0;
   int64_t s1_bytes = 0, s2_bytes = 0;
@@ -299,8 +298,7 @@ int hmx::plan_create_impl(const hmx_matrix_desc* d, int device, const hmx_plan_o
       for (int64_t q = 0; q < kk; ++q) rows.push_back({k, (int32_t)q});
       if (pipe == P_M1S) {
         const int64_t z0 = cls == 1 ? zoff_hi[(size_t)k] : zoff_lo[(size_t)k];
-        for (int64_t q = 0; q < kk; ++q)
-          zkind[(size_t)(z0 + q)] = q < (kk & ~int64_t(3)) ? 4 : ((kk & 3) >= 2 && q < (kk & ~int64_t(3)) + 2) ? 2 : 1;
+        for (int64_t q = 0; q < kk; ++q) zkind[(size_t)(z0 + q)] = (uint8_t)sgemv_row_kind(q, kk);
       }
       if (pipe >= P_M2D) {
         const double* dsrc = d->buf64 + (cls == 1 ? d->dhi_off[k] : d->dlo_off[k]);
@@ -521,15 +519,16 @@ int hmx::plan_create_impl(const hmx_matrix_desc* d, int device, const hmx_plan_o
           if (r.flags & RUN_ACC32) any_acc32 = true;
           else any_acc64_in32 = true;
           // parts with a group table: chain items in SGEMV chunk layout, with
-          // the segment rows SGEMV computes in its remainder kernels (rows
-          // 4 floor(m/4) .. m-1 of an m-row block)
+          // the segment rows of each SGEMV row kernel (sgemv_row_kind of the
+          // block's rows, as 7-bit segment-relative bounds)
           if ((r.flags & RUN_ACC32) && !fg.cuts.empty()) {
             r.flags |= RUN_CHUNK;
-            const int64_t mb = t[1] - t[0];
-            const int64_t rem = t[0] + (mb & ~int64_t(3)) - sg.row0;  // segment-relative
-            int32_t kinfo = 0x7f;  // (rem + 3: the remainder may start up to 3 rows before the segment)
-            if ((mb & 3) && rem < sg.R) kinfo = (int32_t)(rem + 3) | ((mb & 3) >= 2 ? 0x80 : 0);
-            r.flags |= kinfo << kRunKindShift;
+            const int64_t mb = t[1] - t[0], d0 = sg.row0 - t[0];  // block row of segment row 0
+            const int64_t a16 = mb & ~int64_t(15), b8 = a16 + (mb & 8), c4 = b8 + (mb & 4);
+            const int64_t c2 = c4 + ((mb & 3) >= 2 ? 2 : 0);
+            auto rel = [&](int64_t bound) { return (uint32_t)std::min<int64_t>(std::max<int64_t>(bound - d0, 0), 127); };
+            const uint32_t bits = rel(a16) | rel(b8) << 7 | rel(c4) << 14 | rel(c2) << 21;
+            r.flags |= (int32_t)(bits << kRunKindShift);
           }
         }
         runs.push_back(r);

@@ -7,12 +7,13 @@ per thread (csrc/hmx_internal.cuh chunk_off layout, chain_items in
 csrc/hmx_kernels.cu).  Checked
 here:
   * CPU: the kernel's order, modelled in tools/fp32_accum_emulation.py
-    (sgemv_tree), reproduces the reference's products bitwise
+    (sgemv_rows: SGEMV's 16/8/4-row kernels and its 2- and 1-row remainder
+    kernels), reproduces the reference's products bitwise
     (tests/golden/fp32_order.npz, made by numpy in the build container) for
-    every width except the small-width variants {2, 3, 6, 7};
+    every width 1..48 and row counts 8, 40, 30 and 5;
   * GPU: block-diagonal m2-single matrices put one item per row segment, so
-    y is exactly the widened FP32 item value: bitwise the model, and bitwise
-    the reference's own numbers where the model is;
+    y is exactly the widened FP32 item value: bitwise the model and bitwise
+    the reference's own numbers;
   * GPU: the operator error ||y - y64|| of m1-single / m1-mixed / m2-single is
     within 5 % of the reference's ||y_ref - y64|| on the golden fixtures and
     BASELINE configs 1-2 (VERDICT r1 "Next" item 2).
@@ -23,10 +24,9 @@ import pytest
 
 from golden_util import GOLDEN, config1_hmatrix, hmatrix_from_fixture, load
 
-# widths whose SGEMV path (numpy's kernel choice for short rows) is not
-# reproduced for every row: checked at the FP32 tolerance only
-SMALL_VARIANTS = {1, 2, 3, 5, 6, 7, 8}
-ROWS = (8, 40, 30, 5)   # 30 and 5: OpenBLAS's two- and one-row remainder kernels
+# row counts: 8 and 40 (SGEMV's 8-row kernel), 30 (16 + 8 + 4 + the 2-row
+# remainder kernel) and 5 (4-row kernel + the 1-row remainder kernel)
+ROWS = (8, 40, 30, 5)
 
 
 def fixture():
@@ -40,12 +40,7 @@ def test_model_reproduces_reference_products():
         for n in range(1, 49):
             a32 = f[f"a/{m}/{n}"].astype(np.float32)
             x32 = f[f"x/{m}/{n}"].astype(np.float32)
-            y = sgemv_rows(a32, x32)
-            ref = f[f"y/{m}/{n}"]
-            if n in SMALL_VARIANTS:
-                assert np.allclose(y, ref, rtol=1e-5, atol=1e-6), (m, n)
-            else:
-                assert np.array_equal(y, ref), (m, n)
+            assert np.array_equal(sgemv_rows(a32, x32), f[f"y/{m}/{n}"]), (m, n)
 
 
 def test_chunk_layout_is_a_permutation():
@@ -102,8 +97,7 @@ def test_gpu_items_bitwise_sgemv_order(hx, m):
         x32 = x[c0:c0 + w].astype(np.float32)
         model = sgemv_rows(a32, x32).astype(np.float64)
         assert np.array_equal(got, model), (m, w, got - model)
-        if w not in SMALL_VARIANTS:
-            assert np.array_equal(got, f[f"y/{m}/{w}"].astype(np.float64)), (m, w)
+        assert np.array_equal(got, f[f"y/{m}/{w}"].astype(np.float64)), (m, w)
         c0 += w
 
 

@@ -14,8 +14,12 @@ FP64 (m1-double) product and y_ref the reference's own FP32 result.  Orders:
           (K = 8: ((l0+l4)+(l1+l5))+((l2+l6)+(l3+l7)), what OpenBLAS's SGEMV
           does on this container for widths that are multiples of 8 --
           probed with tools/sgemv_order_probe.py)
-  sgemv   the GPU kernel's order since round 2 (chain_items in
-          csrc/hmx_kernels.cu): OpenBLAS SGEMV-T's own tree
+  sgemv   OpenBLAS SGEMV-T's tree as its four-row kernel computes it, for
+          every row (sgemv_tree)
+  sgemv-rows  the GPU kernel's order since round 2 (chain_item /
+          s1_exact_kernel in csrc/hmx_kernels.cu): each row in the order of
+          the SGEMV row kernel that computes it (16/8/4-row kernels, 2- and
+          1-row remainder kernels; sgemv_rows) -- numpy's own products bitwise
 
 FMA is emulated as round32(round64(a*b) + c) with the product exact in FP64;
 the double rounding differs from a true fused FMA in rare ties only, which is
@@ -135,44 +139,63 @@ def sgemv_tree(a, g):
 
 
 def row_kind(i: int, m: int) -> int:
-    """OpenBLAS SGEMV-T computes the rows (outputs) of an m-row block four at a
-    time; the remainder uses a two-row and then a one-row kernel, whose
-    summation differs.  Kind 4, 2 or 1 for row i."""
-    if i < (m & ~3):
+    """OpenBLAS SGEMV-T computes the rows (outputs) of an m-row block in blocks
+    of 16, then 8, then 4 rows, then a two-row and a one-row remainder kernel;
+    their summation orders differ (the 16-, 8- and 4-row kernels only for
+    rows shorter than 8).  Kind 16, 8, 4, 2 or 1 for row i."""
+    a16 = m & ~15
+    if i < a16:
+        return 16
+    b8 = a16 + (m & 8)
+    if i < b8:
+        return 8
+    c4 = b8 + (m & 4)
+    if i < c4:
         return 4
-    if (m & 3) >= 2 and i < (m & ~3) + 2:
+    if (m & 3) >= 2 and i < c4 + 2:
         return 2
     return 1
-
-
-def _mul(a, b):
-    return (np.asarray(a, F32).astype(F64) * np.asarray(b, F32).astype(F64)).astype(F32)
 
 
 def sgemv_kind(a, g, kind: int):
     """One row class of SGEMV-T (probed with tools/sgemv_order_probe.py and
     the brute-force family search described in DESIGN.md):
-      kind 4: A/B accumulators, FMA chains (sgemv_tree);
+      kinds 16, 8, 4: A/B accumulators, FMA chains (sgemv_tree); rows
+        shorter than 8 differ: 8: n = 2 is a plain sum; 4: n = 2, 3, 6, 7 use
+        the trees below;
       kind 2: ONE 4-lane accumulator over all chunks, multiply-then-add;
       kind 1: A/B accumulators, multiply-then-add;
     then (l0 + l1) + (l2 + l3) and the tail rule of sgemv_tree.  Short rows:
     kind 4 as sgemv_tree; kinds 2/1: n = 2..7 a sequential multiply-add chain
-    (kind 1, n = 3: the tail rule; n = 5: sequential lanes + fused tail), n = 4
+    (kind 1, n = 3: the tail rule), n = 4
     pairwise (kind 1: sequential), n = 8 (kind 1): A/B with a sequential
-    horizontal sum."""
+    horizontal sum; kind 2, n = 8: ((p0 + p1) + (p4 + p5)) + ((p2 + p3) + (p6 + p7))."""
     a = np.asarray(a, F32)
     g = np.asarray(g, F32)
     m, n = a.shape
-    if kind == 4:
-        return sgemv_tree(a, g)
     z = np.zeros(m, F32)
     G = lambda k: np.full(m, g[k], F32)
     P = lambda k: _mul(a[:, k], G(k))
+    F = lambda k, acc: _fma(a[:, k], G(k), acc)
+    if kind in (16, 8, 4):
+        if kind == 8 and n == 2:
+            return P(0) + P(1)
+        if kind == 4 and n in (2, 3, 6, 7):  # the four-row kernel's short-row trees
+            if n == 2:
+                return P(0) + P(1)
+            if n == 3:
+                return F(2, F(0, P(1)))
+            if n == 6:
+                return (P(0) + F(1, P(2))) + (P(3) + F(4, P(5)))
+            return (F(0, P(1)) + F(4, P(5))) + (F(2, P(3)) + P(6))
+        return sgemv_tree(a, g)
     if n == 1:
         return P(0)
     if kind == 1 and n == 3:
         return _fma(a[:, 2], G(2), _fma(a[:, 0], G(0), P(1)))
-    if n <= 7 and n != 4 and not (kind == 1 and n == 5):
+    if kind == 2 and n == 8:
+        return ((P(0) + P(1)) + (P(4) + P(5))) + ((P(2) + P(3)) + (P(6) + P(7)))
+    if n <= 7 and n != 4:
         v = P(0)
         for k in range(1, n):
             v = v + P(k)
@@ -210,7 +233,7 @@ def sgemv_rows(a, g):
     m = a.shape[0]
     out = np.empty(m, F32)
     kinds = np.array([row_kind(i, m) for i in range(m)])
-    for k in (4, 2, 1):
+    for k in (16, 8, 4, 2, 1):
         sel = kinds == k
         if sel.any():
             out[sel] = sgemv_kind(a[sel], g, k)
@@ -320,7 +343,7 @@ def main():
     names = sys.argv[1:] or ["golden", "config1", "config2"]
     if names == ["bitwise"]:
         return bitwise_check()
-    orders = ["chain", "lanes4", "lanes8", "sgemv"]
+    orders = ["chain", "lanes4", "lanes8", "sgemv", "sgemv-rows"]
     print(f"{'case':12s} {'scheme':10s} " + " ".join(f"{o:>8s}" for o in orders)
           + "   (||y - y64|| / ||y_ref - y64||)")
     for name, h, x in cases(names):
@@ -328,7 +351,7 @@ def main():
         for s in ("m1-single", "m1-mixed", "m2-single"):
             sh = hx.prepare_scheme(h, s)
             ref = np.linalg.norm(orc.matvec(sh, x) - y64)
-            row = [np.linalg.norm(matvec_model(sh, x, o, "sgemv" if o == "sgemv" else "numpy") - y64) / ref
+            row = [np.linalg.norm(matvec_model(sh, x, o, o if o.startswith("sgemv") else "numpy") - y64) / ref
                    for o in orders]
             print(f"{name:12s} {s:10s} " + " ".join(f"{v:8.4f}" for v in row), flush=True)
 

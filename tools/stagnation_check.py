@@ -34,7 +34,21 @@ def main():
     ap.add_argument("--full-gpu", type=int, default=300, help="max_iter of the extra full GPU solve")
     ap.add_argument("--scheme", default="m1-double")
     ap.add_argument("--out", default=None)
+    ap.add_argument("--part", choices=("both", "oracle", "gpu"), default="both",
+                    help="run only one side (the oracle on a CPU host, the GPU solve on the box) and "
+                         "merge the two JSON files with --merge")
+    ap.add_argument("--merge", nargs=2, default=None, metavar=("GPU_JSON", "ORACLE_JSON"))
     a = ap.parse_args()
+    if a.merge:
+        g, o = (json.loads(Path(f).read_text()) for f in a.merge)
+        gh, oh = np.asarray(g["gpu_history"]), np.asarray(o["oracle_history"])
+        k = min(gh.size, oh.size)
+        res = {**o, **g, "oracle_history": oh.tolist(), "oracle_s": o.get("oracle_s"),
+               "max_rel_diff_first_k": float(np.max(np.abs(gh[:k] - oh[:k]) / oh[:k]))}
+        Path(a.out).write_text(json.dumps(res, indent=1))
+        for i in range(k):
+            print(f"{i:3d}  gpu {gh[i]:.6e}  oracle {oh[i]:.6e}")
+        return
     centers = ((0.0, 0.0, 0.0),) if a.spheres == 1 else ((0.0, 0.0, 0.0), (3.0, 0.0, 0.0))
     volts = None if a.spheres == 1 else (1.0, -1.0)
     t0 = time.perf_counter()
@@ -43,23 +57,30 @@ def main():
     b = mesh.centroids[:, 2].copy() if a.spheres == 1 else hx.right_hand_side(mesh)
     sh = hx.prepare_scheme(h, a.scheme)
     t_build = time.perf_counter() - t0
-    cfg = hx.SolverConfig(tol=1e-8, max_iter=a.iters)
-    _, g = hx.bicgstab(sh, h, b, cfg)
-    _, gfull = hx.bicgstab(sh, h, b, hx.SolverConfig(tol=1e-8, max_iter=a.full_gpu))
-    t1 = time.perf_counter()
-    sh64 = sh if a.scheme == "m1-double" else hx.prepare_scheme(h, "m1-double")
-    _, o = orc.bicgstab(sh, sh64, b, tol=1e-8, max_iter=a.iters)
-    t_cpu = time.perf_counter() - t1
-    gh, oh = np.asarray(g.residual_history), np.asarray(o["residual_history"])
-    k = min(gh.size, oh.size)
     res = {"mesh": f"{a.spheres} jittered sphere(s), level {a.level}, N={mesh.n}, leaf 64, ACA 1e-4",
-           "scheme": a.scheme, "iters": a.iters, "build_s": t_build, "oracle_s": t_cpu,
-           "gpu_history": gh.tolist(), "oracle_history": oh.tolist(),
-           "max_rel_diff_first_k": float(np.max(np.abs(gh[:k] - oh[:k]) / oh[:k])),
-           "gpu_full": {"max_iter": a.full_gpu, "iterations": gfull.iterations,
-                        "converged": gfull.converged, "true_residual": gfull.true_residual,
-                        "min_residual": float(np.min(gfull.residual_history)),
-                        "history_every_10": gfull.residual_history[::10]}}
+           "scheme": a.scheme, "iters": a.iters, "build_s": t_build}
+    if a.part in ("both", "gpu"):
+        cfg = hx.SolverConfig(tol=1e-8, max_iter=a.iters)
+        _, g = hx.bicgstab(sh, h, b, cfg)
+        _, gfull = hx.bicgstab(sh, h, b, hx.SolverConfig(tol=1e-8, max_iter=a.full_gpu))
+        res["gpu_history"] = list(g.residual_history)
+        res["gpu_full"] = {"max_iter": a.full_gpu, "iterations": gfull.iterations,
+                           "converged": gfull.converged, "true_residual": gfull.true_residual,
+                           "min_residual": float(np.min(gfull.residual_history)),
+                           "history_every_10": gfull.residual_history[::10]}
+    if a.part in ("both", "oracle"):
+        t1 = time.perf_counter()
+        sh64 = sh if a.scheme == "m1-double" else hx.prepare_scheme(h, "m1-double")
+        _, o = orc.bicgstab(sh, sh64, b, tol=1e-8, max_iter=a.iters)
+        res["oracle_s"] = time.perf_counter() - t1
+        res["oracle_history"] = list(o["residual_history"])
+    if a.part != "both":
+        Path(a.out).write_text(json.dumps(res, indent=1))
+        print(json.dumps({k_: v for k_, v in res.items() if "history" not in k_}), flush=True)
+        return
+    gh, oh = np.asarray(res["gpu_history"]), np.asarray(res["oracle_history"])
+    k = min(gh.size, oh.size)
+    res["max_rel_diff_first_k"] = float(np.max(np.abs(gh[:k] - oh[:k]) / oh[:k]))
     print(json.dumps({k_: v for k_, v in res.items() if "history" not in k_}), flush=True)
     for i in range(k):
         print(f"{i:3d}  gpu {gh[i]:.6e}  oracle {oh[i]:.6e}")
