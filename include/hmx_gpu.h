@@ -110,6 +110,13 @@ typedef struct {
  * (hmx_dist_matvec, hmx_bicgstab_dist). */
 #define HMX_PLAN_LOCAL_FIRST 1
 
+/* hmx_plan_options.flags: the FP32-accumulated products (m1-single,
+ * m1-mixed U slabs, m2-single dense blocks) as ONE sequential FP32 FMA chain
+ * per (row, block) -- the faster round-1 order -- instead of the default,
+ * OpenBLAS SGEMV-T's own summation order (bitwise the reference's FP32
+ * products). */
+#define HMX_PLAN_FP32_CHAIN 2
+
 typedef struct hmx_plan hmx_plan;
 
 typedef struct {

@@ -45,6 +45,19 @@ class PlanOptions(ctypes.Structure):
 
 
 HMX_PLAN_LOCAL_FIRST = 1
+HMX_PLAN_FP32_CHAIN = 2
+
+
+def fp32_order_flags() -> int:
+    """Plan flags of the FP32 accumulation order: HMX_FP32_ORDER=sgemv (the
+    default: OpenBLAS SGEMV-T's own order, bitwise the reference's FP32
+    products) or chain (one sequential FP32 chain per (row, block): faster,
+    the round-1 order)."""
+    import os
+    order = os.environ.get("HMX_FP32_ORDER", "sgemv").lower()
+    if order not in ("sgemv", "chain"):
+        raise ValueError(f"HMX_FP32_ORDER must be 'sgemv' or 'chain', not {order!r}")
+    return HMX_PLAN_FP32_CHAIN if order == "chain" else 0
 
 
 class PlanInfo(ctypes.Structure):
@@ -233,7 +246,7 @@ class Plan:
         if row_range is not None:
             opt.row_begin, opt.row_end = int(row_range[0]), int(row_range[1])
         opt.s1_chunk_bytes = int(s1_chunk_bytes)
-        opt.flags = HMX_PLAN_LOCAL_FIRST if local_first else 0
+        opt.flags = (HMX_PLAN_LOCAL_FIRST if local_first else 0) | fp32_order_flags()
         h = ctypes.c_void_p()
         rc = lib.hmx_plan_create(ctypes.byref(d), int(device), ctypes.byref(opt), ctypes.byref(h))
         self._keep = []  # the plan holds device copies; host arrays may go
@@ -258,6 +271,7 @@ class Plan:
         opt = PlanOptions()
         if row_range is not None:
             opt.row_begin, opt.row_end = int(row_range[0]), int(row_range[1])
+        opt.flags = fp32_order_flags()
         h = ctypes.c_void_p()
         info = PrepareInfo()
         rc = lib.hmx_plan_create_prepared(master.handle, code, float(split_factor),

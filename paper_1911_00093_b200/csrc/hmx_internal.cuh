@@ -112,8 +112,15 @@ constexpr int kS1Threads = 128;   // stage-1 CTA size
 constexpr int kS1Threads32 = 64;  // stage-1 CTA size for widened-FP32-only stage 1 (<= 256 rows)
 constexpr int kSegWMax = 2048;    // columns of g staged in shared memory per tile (stage 2)
 constexpr int kS1WMax = 1024;     // max columns per stage-1 segment chunk
-constexpr int kS1ExactRows = 128;  // m1-single stage 1: rank rows per CTA (one thread each)
+#ifndef HMX_S1X_ROWS
+#define HMX_S1X_ROWS 128
+#endif
+constexpr int kS1ExactRows = HMX_S1X_ROWS;  // m1-single stage 1: rank rows per CTA (one thread each)
 constexpr int kSgemvBlock = 1024; // OpenBLAS SGEMV-T column blocking: 4096 columns = 1024 chunks
+#ifndef HMX_CHAIN_ROWS
+#define HMX_CHAIN_ROWS 1  // stage-2 chain threads: rows per thread (1 or 2)
+#endif
+constexpr int kChainRows = HMX_CHAIN_ROWS;
 
 // Device-visible plan (passed by value to kernels).
 struct DevPlan {
@@ -131,6 +138,7 @@ struct DevPlan {
   int32_t s1_narrow;              // every stage-1 segment is widened FP32: 64-thread CTAs
   int32_t s2_deep;                // FP64-accumulating stage 2 with an FP64 part: deep pipeline
   int32_t s1_exact;               // m1-single: stage 1 in SGEMV order (s1_exact_kernel)
+  int32_t chain_exact;            // stage-2 FP32-accumulated items in SGEMV order (chain_windows)
   int32_t n_seg1_local;           // leading stage-1 segments reading only x[row_begin, row_end)
   const int32_t* gtab;            // item-aligned FP32 group boundaries (stage 2)
   const double* zscale;           // d per z entry (methods 2, 3)

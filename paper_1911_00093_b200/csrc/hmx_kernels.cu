@@ -152,6 +152,9 @@ __device__ __forceinline__ void chain_bar(int nthreads) {
 }
 
 constexpr int kMetaW = 12;  // run meta in shared memory: col0 << 12 | width
+#ifndef HMX_CHAIN_ROWS
+#define HMX_CHAIN_ROWS 1  // rows per chain thread (1 or 2); the flattener's group count follows kChainRows
+#endif
 #ifndef HMX_CHAIN_WB
 #define HMX_CHAIN_WB 8192
 #endif
@@ -260,15 +263,91 @@ __device__ __forceinline__ float chain_item(const float* it, GF G, int n, int rp
   return v;
 }
 
+// Rows r0 = h and r1 = h + half of one n-wide item in shared memory (chunk
+// layout), both in the four-row kernel's order (kind 4): chain_item for two
+// rows at once, sharing the source loads.
+template <typename GF>
+__device__ __forceinline__ float2 chain_item2(const float* it, GF G, int n, int rp, int r0, int r1) {
+  auto G4 = [&](int c) { return make_float4(G(c), G(c + 1), G(c + 2), G(c + 3)); };
+  if (chain_shaped(n)) {
+    float v0 = 0.f, v1 = 0.f;
+    for (int k = 0; k < n; ++k) {
+      const float g = G(k);
+      v0 = __fmaf_rn(it[(int64_t)k * rp + r0], g, v0);
+      v1 = __fmaf_rn(it[(int64_t)k * rp + r1], g, v1);
+    }
+    return make_float2(v0, v1);
+  }
+  const int nch = n >> 2, T = n & 3, m = 4 * nch;
+  const float4* c0p = reinterpret_cast<const float4*>(it) + r0;  // chunk c of row r at [c rp + r]
+  const float4* c1p = reinterpret_cast<const float4*>(it) + r1;
+  float4 l0, l1;
+  if (n == 8) {  // l_j = a_2j g_2j + a_2j+1 g_2j+1
+    const float4 g0 = G4(0), g1 = G4(4);
+    auto pairs = [&](const float4& x, const float4& y) {
+      return make_float4(__fadd_rn(__fmul_rn(x.x, g0.x), __fmul_rn(x.y, g0.y)),
+                         __fadd_rn(__fmul_rn(x.z, g0.z), __fmul_rn(x.w, g0.w)),
+                         __fadd_rn(__fmul_rn(y.x, g1.x), __fmul_rn(y.y, g1.y)),
+                         __fadd_rn(__fmul_rn(y.z, g1.z), __fmul_rn(y.w, g1.w)));
+    };
+    l0 = pairs(c0p[0], c0p[rp]);
+    l1 = pairs(c1p[0], c1p[rp]);
+  } else {
+    float4 A0 = make_float4(0.f, 0.f, 0.f, 0.f), B0 = A0, A1 = A0, B1 = A0;
+    int c = 0;
+    if (nch & 1) {
+      const float4 g = G4(0);
+      A0 = fma4(c0p[0], g, A0);
+      A1 = fma4(c1p[0], g, A1);
+      c = 1;
+    }
+    for (; c < nch; c += 2) {
+      const float4 ga = G4(4 * c), gb = G4(4 * c + 4);
+      A0 = fma4(c0p[c * rp], ga, A0);
+      A1 = fma4(c1p[c * rp], ga, A1);
+      B0 = fma4(c0p[(c + 1) * rp], gb, B0);
+      B1 = fma4(c1p[(c + 1) * rp], gb, B1);
+    }
+    l0 = make_float4(__fadd_rn(A0.x, B0.x), __fadd_rn(A0.y, B0.y), __fadd_rn(A0.z, B0.z), __fadd_rn(A0.w, B0.w));
+    l1 = make_float4(__fadd_rn(A1.x, B1.x), __fadd_rn(A1.y, B1.y), __fadd_rn(A1.z, B1.z), __fadd_rn(A1.w, B1.w));
+  }
+  float v0 = __fadd_rn(__fadd_rn(l0.x, l0.y), __fadd_rn(l0.z, l0.w));
+  float v1 = __fadd_rn(__fadd_rn(l1.x, l1.y), __fadd_rn(l1.z, l1.w));
+  const float* tl = it + (int64_t)m * rp;
+  if (T == 1) {
+    const float g = G(m);
+    v0 = __fmaf_rn(tl[r0], g, v0);
+    v1 = __fmaf_rn(tl[r1], g, v1);
+  } else if (T >= 2) {
+    const float ga = G(m + 1), gb = G(m);
+    float t0 = __fmaf_rn(tl[r0], gb, __fmul_rn(tl[rp + r0], ga));
+    float t1 = __fmaf_rn(tl[r1], gb, __fmul_rn(tl[rp + r1], ga));
+    if (T == 3) {
+      const float gc = G(m + 2);
+      t0 = __fmaf_rn(tl[2 * rp + r0], gc, t0);
+      t1 = __fmaf_rn(tl[2 * rp + r1], gc, t1);
+    }
+    v0 = __fadd_rn(v0, t0);
+    v1 = __fadd_rn(v1, t1);
+  }
+  return make_float2(v0, v1);
+}
+
 // chain threads u = 0 .. nthr-1 (slot u / rp, row u % rp); items j0 .. nrun-1
 // of the part (meta in shared memory, the part's blob at `part`); buf: two
 // kChainWin-byte staging buffers; wq: 6 ints of shared memory for the window
 // bounds thread 0 publishes one window ahead.  Returns this thread's row sum.
 __device__ __forceinline__ double chain_windows(const int32_t* meta, const uint32_t* kbits, int j0, int nrun,
                                                 const float* part, const double* gs, int rp, int u, int nthr,
-                                                float* buf, int* wq) {
+                                                float* buf, int* wq, double& acc1) {
+#if HMX_CHAIN_ROWS == 2
+  const int half = rp >> 1;  // two rows per thread: p and p + half
+  const int K = nthr / half;
+  const int slot = u / half, p = u - slot * half, p1 = p + half;
+#else
   const int K = nthr / rp;
   const int slot = u / rp, p = u - slot * rp;
+#endif
   const bool act = slot < K;
   const int wmax = kChainWin / (4 * rp);  // columns per window
   auto col0 = [&](int j) { return meta[j] >> kMetaW; };
@@ -318,6 +397,9 @@ __device__ __forceinline__ double chain_windows(const int32_t* meta, const uint3
           const int c0 = col0(j);
           auto G = [&](int k) { return __int_as_float(__double2loint(gs[c0 + k])); };
           acc += (double)chain_item<true>(part + (int64_t)c0 * rp, G, width(j), rp, p, chain_row_kind(kbits[j], p));
+#if HMX_CHAIN_ROWS == 2
+          acc1 += (double)chain_item<true>(part + (int64_t)c0 * rp, G, width(j), rp, p1, chain_row_kind(kbits[j], p1));
+#endif
         }
       } else {
         const float* base = buf + (w & 1) * (kChainWin / 4);
@@ -330,8 +412,19 @@ __device__ __forceinline__ double chain_windows(const int32_t* meta, const uint3
           // 16-row kernel (n < 8), or in the 16/8/4-row kernels (n >= 8)
           const uint32_t kb = kbits[i];
           const int wi = width(i);
+#if HMX_CHAIN_ROWS == 2
+          if ((int)((kb >> (wi < 8 ? 0 : 14)) & 127) >= rp) {
+            const float2 v = chain_item2(it, G, wi, rp, p, p1);
+            acc += (double)v.x;
+            acc1 += (double)v.y;
+          } else {
+            acc += (double)chain_item<false>(it, G, wi, rp, p, chain_row_kind(kb, p));
+            acc1 += (double)chain_item<false>(it, G, wi, rp, p1, chain_row_kind(kb, p1));
+          }
+#else
           if ((int)((kb >> (wi < 8 ? 0 : 14)) & 127) >= rp) acc += (double)chain_item<false>(it, G, wi, rp, p, 16);
           else acc += (double)chain_item<false>(it, G, wi, rp, p, chain_row_kind(kb, p));
+#endif
         }
       }
     }
@@ -369,37 +462,39 @@ __global__ void __launch_bounds__(kS1ExactRows) s1_exact_kernel(DevPlan P, const
   } else if (n <= 8) {  // short rows (chain-shaped, n = 4, n = 8): the per-kernel rules
     y = chain_item<true>(it, G, n, rp, t, kind);
   } else {
-    // this CTA's 4096-column block: the A/B lane tree (kind 4: FMA chains;
-    // kind 1: multiply then add; kind 2: one accumulator, multiply then add)
+    // this CTA's 4096-column block: the A/B lane tree (kinds 16/8/4: FMA
+    // chains; 1: multiply then add; 2: one accumulator, multiply then add),
+    // chunks streamed with kS1Win loads in flight (each register refilled
+    // with the chunk kS1Win ahead right after it is consumed)
     const int nch = n >> 2, T = n & 3;
-    const bool fm = kind >= 4, one = kind == 2;
-    auto upd = [&](float4& X, const float4& x, const float4& g) {
-      if (fm) X = fma4(x, g, X);
-      else X = make_float4(__fadd_rn(X.x, __fmul_rn(x.x, g.x)), __fadd_rn(X.y, __fmul_rn(x.y, g.y)),
-                           __fadd_rn(X.z, __fmul_rn(x.z, g.z)), __fadd_rn(X.w, __fmul_rn(x.w, g.w)));
-    };
+    const bool fm = kind >= 4, one = kind == 2, odd = nch & 1;
     const float* ch = it + 4 * t;  // chunk c at ch[4 c rp]
     float4 A = make_float4(0.f, 0.f, 0.f, 0.f), B = A;
-    int c = 0;
-    if (nch & 1) {  // odd: chunk 0 alone into A, then pairs (A, B) -- one accumulator: all into A
-      upd(A, ld_chunk(ch), G4(0));
-      c = 1;
-    }
-    for (; c < nch; c += 8) {  // up to four pairs' loads in flight
-      float4 xa[4], xb[4];
+    auto step = [&](const float4& x, int cc) {
+      const bool inA = one || (odd ? (cc == 0 || (cc & 1)) : !(cc & 1));
+      const float4 g = G4(4 * cc);
+      const float4 X = inA ? A : B;
+      const float4 Y = fm ? fma4(x, g, X)
+                          : make_float4(__fadd_rn(X.x, __fmul_rn(x.x, g.x)), __fadd_rn(X.y, __fmul_rn(x.y, g.y)),
+                                        __fadd_rn(X.z, __fmul_rn(x.z, g.z)), __fadd_rn(X.w, __fmul_rn(x.w, g.w)));
+      if (inA) A = Y;
+      else B = Y;
+    };
+    constexpr int kS1Win = 8;
+    float4 w[kS1Win];
 #pragma unroll
-      for (int u = 0; u < 4; ++u)
-        if (c + 2 * u < nch) {
-          xa[u] = ld_chunk(ch + (int64_t)4 * (c + 2 * u) * rp);
-          xb[u] = ld_chunk(ch + (int64_t)4 * (c + 2 * u + 1) * rp);
-        }
+    for (int u = 0; u < kS1Win; ++u)
+      if (u < nch) w[u] = ld_chunk(ch + (int64_t)4 * u * rp);
+    for (int c = 0; c < nch; c += kS1Win) {
 #pragma unroll
-      for (int u = 0; u < 4; ++u)
-        if (c + 2 * u < nch) {
-          upd(A, xa[u], G4(4 * (c + 2 * u)));
-          if (one) upd(A, xb[u], G4(4 * (c + 2 * u + 1)));
-          else upd(B, xb[u], G4(4 * (c + 2 * u + 1)));
+      for (int u = 0; u < kS1Win; ++u) {
+        const int cc = c + u;
+        if (cc < nch) {
+          const float4 x = w[u];
+          if (cc + kS1Win < nch) w[u] = ld_chunk(ch + (int64_t)4 * (cc + kS1Win) * rp);
+          step(x, cc);
         }
+      }
     }
     const float4 l = make_float4(__fadd_rn(A.x, B.x), __fadd_rn(A.y, B.y), __fadd_rn(A.z, B.z),
                                  __fadd_rn(A.w, B.w));
@@ -442,7 +537,10 @@ __global__ void __launch_bounds__(kS1ExactRows) s1_exact_kernel(DevPlan P, const
 // DEEP: stage 2 with an FP64 part, 12 FP64 columns in flight per thread at 3
 // CTAs per SM (80 registers) instead of 8 at 4 (A/B on config 4: m1-double
 // stage 2 -1.1 %, m2-double -2.4 %; FP32-only stage 2 prefers 8 at 4)
-template <int F32MODE, int OUT, int NT, bool DEEP = false>
+// EXACT (stage 2 with FP32-accumulated items): those items in SGEMV's order
+// (chain_windows); otherwise one FP32 chain per (row, item) (HMX_PLAN_FP32_CHAIN).
+// Separate instantiations keep each one's register allocation its own.
+template <int F32MODE, int OUT, int NT, bool DEEP = false, bool EXACT = false>
 __global__ void __launch_bounds__(NT, DEEP ? 3 : (OUT == OUT_Y && F32MODE != F32_ALL64) ? HMX_MIXED_MINB : 1024 / NT) seg_kernel(DevPlan P, const Seg* __restrict__ segs,
                                                           const double* __restrict__ x, S2Out out) {
   // stage 1 segments have a single run (no index expansion) and <= 1024 columns
@@ -542,17 +640,34 @@ __global__ void __launch_bounds__(NT, DEEP ? 3 : (OUT == OUT_Y && F32MODE != F32
   // wbc (plan: sg.chunk) is warp-aligned, so no warp runs both loops.
   bool chain_thr = false;
   int pc = 0;
-  if constexpr (F32MODE != F32_ALL64 && OUT == OUT_Y) {
+  if constexpr (F32MODE == F32_MIXED && OUT == OUT_Y) {
+    // (HMX_PLAN_FP32_CHAIN plans: one FP32 FMA chain per (row, item), 4 rows
+    // per thread on both sides of the warp-aligned split at wb = sg.chunk)
+    const int wb = sg.chunk;
+    if (!EXACT && wb > 0 && sg.gtab >= 0) {
+      const int ga = wb / tpg32, gb = (NT - wb) / tpg32;
+      g32 = ga + gb;
+      if (tid < wb) {
+        if (q32 >= ga) q32 = g32;  // idle
+      } else {
+        const int u = tid - wb;
+        const int qb = u / tpg32;
+        p32 = u - qb * tpg32;
+        q32 = qb < gb ? ga + qb : g32;
+      }
+    }
+  }
+  if constexpr (EXACT && F32MODE != F32_ALL64 && OUT == OUT_Y) {
     if (sg.gtab >= 0) {
       const int wbc = F32MODE == F32_ALL32 ? 0 : sg.chunk;
-      const int ga = wbc / tpg32, gb = (NT - wbc) / rp32;
+      const int ga = wbc / tpg32, gb = (NT - wbc) / (rp32 / HMX_CHAIN_ROWS);
       g32 = ga + gb;
       if (tid < wbc) {
         if (q32 >= ga) q32 = g32;  // idle
       } else {
         const int u = tid - wbc;
-        const int qb = u / rp32;
-        pc = u - qb * rp32;
+        const int qb = u / (rp32 / HMX_CHAIN_ROWS);
+        pc = u - qb * (rp32 / HMX_CHAIN_ROWS);
         q32 = qb < gb ? ga + qb : g32;
         chain_thr = true;
       }
@@ -568,7 +683,7 @@ __global__ void __launch_bounds__(NT, DEEP ? 3 : (OUT == OUT_Y && F32MODE != F32
     if (sg.gtab >= 0) c32 = P.gtab[sg.gtab + g32 + 1];
     else if (sg.gtab <= -2) c32 = P.gtab[-2 - sg.gtab];
   }
-  double bc = 0.0;  // chain threads: the row's FP64 sum of its widened item values
+  double bc = 0.0, bc1 = 0.0;  // chain threads: their rows' FP64 sums of the widened item values
   // widened FP32 data, FP64 accumulation
   auto consume64 = [&](const float4& v, int cc) {
     const double g = gs[cc];
@@ -725,7 +840,7 @@ __global__ void __launch_bounds__(NT, DEEP ? 3 : (OUT == OUT_Y && F32MODE != F32
       const int c32c = P.gtab[sg.gtab + g32 + 1];
       while (j0 < sg.nrun32 && (sidx[j0] >> kMetaW) < c32c) ++j0;
       bc = chain_windows(sidx, kbits, j0, sg.nrun32, P.blob32 + sg.off32, gs, rp32, tid - wbc, NT - wbc, chain_buf,
-                         chain_wq);
+                         chain_wq, bc1);
     }
   }
 
@@ -734,6 +849,7 @@ __global__ void __launch_bounds__(NT, DEEP ? 3 : (OUT == OUT_Y && F32MODE != F32
   if (sg.W32 > 0 && q32 < g32) {
     if (chain_thr) {
       red32[q32 * rp32 + pc] = bc;
+      if (HMX_CHAIN_ROWS == 2) red32[q32 * rp32 + pc + (rp32 >> 1)] = bc1;
     } else {
 #pragma unroll
       for (int i = 0; i < 4; ++i) red32[q32 * rp32 + 4 * p32 + i] = b[i];
@@ -904,25 +1020,25 @@ __global__ void probe_kernel(DevPlan P, const double* __restrict__ x, unsigned l
 
 // dynamic shared memory of a seg_kernel instantiation: the chain-item staging
 // buffers of the stage-2 FP32 kernels
-template <int M, int O>
+template <int M, int O, bool EXACT>
 constexpr size_t chain_smem() {
-  return (O == OUT_Y && M != F32_ALL64) ? 2 * (size_t)kChainWin : 0;
+  return (EXACT && O == OUT_Y && M != F32_ALL64) ? 2 * (size_t)kChainWin : 0;
 }
 
-template <int M, int O, int NT = kSegThreads, bool DEEP = false>
+template <int M, int O, int NT = kSegThreads, bool DEEP = false, bool EXACT = false>
 static cudaError_t launch_seg(const DevPlan& P, const Seg* segs, int nseg, const double* x,
                               const S2Out& out, cudaStream_t st, bool pdl) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)nseg);
   cfg.blockDim = dim3(NT);
-  cfg.dynamicSmemBytes = chain_smem<M, O>();
+  cfg.dynamicSmemBytes = chain_smem<M, O, EXACT>();
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = pdl ? 1 : 0;
-  return cudaLaunchKernelEx(&cfg, seg_kernel<M, O, NT, DEEP>, P, segs, x, out);
+  return cudaLaunchKernelEx(&cfg, seg_kernel<M, O, NT, DEEP, EXACT>, P, segs, x, out);
 }
 
 cudaError_t launch_stage1(const DevPlan& P, const double* x, cudaStream_t st, const int* skip,
@@ -952,8 +1068,12 @@ cudaError_t launch_stage2(const DevPlan& P, const double* x, const S2Out& out, c
                           bool pdl) {
   if (P.n_seg2 == 0) return cudaSuccess;
   switch (P.f32mode2) {
-    case F32_ALL32: return launch_seg<F32_ALL32, OUT_Y>(P, P.seg2, P.n_seg2, x, out, st, pdl);
-    case F32_MIXED: return launch_seg<F32_MIXED, OUT_Y>(P, P.seg2, P.n_seg2, x, out, st, pdl);
+    case F32_ALL32:
+      return P.chain_exact ? launch_seg<F32_ALL32, OUT_Y, kSegThreads, false, true>(P, P.seg2, P.n_seg2, x, out, st, pdl)
+                           : launch_seg<F32_ALL32, OUT_Y>(P, P.seg2, P.n_seg2, x, out, st, pdl);
+    case F32_MIXED:
+      return P.chain_exact ? launch_seg<F32_MIXED, OUT_Y, kSegThreads, false, true>(P, P.seg2, P.n_seg2, x, out, st, pdl)
+                           : launch_seg<F32_MIXED, OUT_Y>(P, P.seg2, P.n_seg2, x, out, st, pdl);
     default:
       return P.s2_deep ? launch_seg<F32_ALL64, OUT_Y, kSegThreads, true>(P, P.seg2, P.n_seg2, x, out, st, pdl)
                        : launch_seg<F32_ALL64, OUT_Y>(P, P.seg2, P.n_seg2, x, out, st, pdl);
@@ -963,12 +1083,12 @@ cudaError_t launch_stage2(const DevPlan& P, const double* x, const S2Out& out, c
 // The stage-2 FP32 kernels opt in to > 48 KB of shared memory (static + the
 // chain staging buffers); called at plan creation, outside any capture.
 cudaError_t configure_kernels() {
-  cudaError_t e = cudaFuncSetAttribute(seg_kernel<F32_ALL32, OUT_Y, kSegThreads, false>,
+  cudaError_t e = cudaFuncSetAttribute(seg_kernel<F32_ALL32, OUT_Y, kSegThreads, false, true>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)chain_smem<F32_ALL32, OUT_Y>());
+                                       (int)chain_smem<F32_ALL32, OUT_Y, true>());
   if (e == cudaSuccess)
-    e = cudaFuncSetAttribute(seg_kernel<F32_MIXED, OUT_Y, kSegThreads, false>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)chain_smem<F32_MIXED, OUT_Y>());
+    e = cudaFuncSetAttribute(seg_kernel<F32_MIXED, OUT_Y, kSegThreads, false, true>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)chain_smem<F32_MIXED, OUT_Y, true>());
   return e;
 }
 

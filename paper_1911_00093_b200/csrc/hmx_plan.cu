@@ -139,6 +139,8 @@ int hmx::plan_create_impl(const hmx_matrix_desc* d, int device, const hmx_plan_o
   }
   const int pipe = d->scheme;
   const bool has_lo = pipe == P_M3;
+  // FP32-accumulated products: SGEMV's order (default) or one FMA chain per (row, block)
+  const bool chain_order = opt && (opt->flags & HMX_PLAN_FP32_CHAIN);
   HMX_CUDA(configure_kernels());
   const int64_t rb = opt && opt->row_end > 0 ? opt->row_begin : 0;
   const int64_t re = opt && opt->row_end > 0 ? opt->row_end : n;
@@ -312,7 +314,7 @@ int hmx::plan_create_impl(const hmx_matrix_desc* d, int device, const hmx_plan_o
     // m1-single: z = Vt32 . x32 accumulated in FP32 in SGEMV's order over the
     // whole cluster width (s1_exact_kernel: one thread per rank row, no
     // column chunks), stored in chunk layout
-    const bool exact1 = is32 && pipe == P_M1S;
+    const bool exact1 = is32 && pipe == P_M1S && !chain_order;
     const int64_t rows_cap = exact1 ? kS1ExactRows : s1_rows;
     const int64_t pieces = (rg + rows_cap - 1) / rows_cap;
     for (int64_t pc = 0; pc < pieces; ++pc) {
@@ -342,7 +344,7 @@ int hmx::plan_create_impl(const hmx_matrix_desc* d, int device, const hmx_plan_o
         r.src = (int32_t)(cs + c0);
         r.width = (int32_t)w;
         r.col0 = 0;
-        r.flags = (src_round ? RUN_ROUND : 0) | ((is32 && pipe == P_M1S) ? (RUN_ACC32 | RUN_CHUNK) : 0);
+        r.flags = (src_round ? RUN_ROUND : 0) | ((is32 && pipe == P_M1S) ? (RUN_ACC32 | (exact1 ? RUN_CHUNK : 0)) : 0);
         runs.push_back(r);
         run_block.push_back(-1);
         if (is32) {
@@ -390,7 +392,7 @@ int hmx::plan_create_impl(const hmx_matrix_desc* d, int device, const hmx_plan_o
   // column in a mixed FP32 part (A/B on config 4 with the warp-aligned split:
   // m1-mixed best at 0.8-1.0, m2-single at 1/1.0-1/1.2)
   const char* aw_env = std::getenv("HMX_ACC64_WEIGHT");
-  const double acc64_weight = aw_env ? std::atof(aw_env) : 1.0;
+  const double acc64_weight = aw_env ? std::atof(aw_env) : (chain_order ? 0.85 : 1.0);
   const bool dense_single = pipe == P_M1S || pipe == P_M2S;  // A32 . x32 in FP32
   const bool u_acc32 = pipe == P_M1S || pipe == P_M1M;       // U32 . z32 in FP32
   bool any_acc32 = false, any_acc64_in32 = false;
@@ -443,7 +445,8 @@ int hmx::plan_create_impl(const hmx_matrix_desc* d, int device, const hmx_plan_o
     for (const ItemRef& it : lst) W += item_width(it);
     if (W > kSegWMax) return fg;  // tiled part: no group table
     // widened groups: 4 rows per thread; chain groups: one row per thread
-    const int64_t rp = round_up(R, 4), tpg = rp / 4, G = kSegThreads / tpg, Gc = kSegThreads / rp;
+    const int64_t rp = round_up(R, 4), tpg = rp / 4, G = kSegThreads / tpg;
+    const int64_t tpc = chain_order ? tpg : rp / kChainRows, Gc = kSegThreads / tpc;  // threads per chain group
     size_t nA = 0;
     while (nA < lst.size() && !item_acc32(lst[nA])) ++nA;
     int64_t colsA = 0;
@@ -455,7 +458,7 @@ int hmx::plan_create_impl(const hmx_matrix_desc* d, int device, const hmx_plan_o
     if (nA > 0 && !wB.empty()) {
       double best = 1e300;
       for (int64_t wb = 32; wb < kSegThreads; wb += 32) {
-        const int64_t ga = wb / tpg, gb = (kSegThreads - wb) / rp;
+        const int64_t ga = wb / tpg, gb = (kSegThreads - wb) / tpc;
         if (ga < 1 || gb < 1) continue;
         const double t = std::max(acc64_weight * (double)colsA / (double)ga, (double)lpt(wB, gb, nullptr));
         if (t < best) {
@@ -521,7 +524,7 @@ int hmx::plan_create_impl(const hmx_matrix_desc* d, int device, const hmx_plan_o
           // parts with a group table: chain items in SGEMV chunk layout, with
           // the segment rows of each SGEMV row kernel (sgemv_row_kind of the
           // block's rows, as 7-bit segment-relative bounds)
-          if ((r.flags & RUN_ACC32) && !fg.cuts.empty()) {
+          if ((r.flags & RUN_ACC32) && !fg.cuts.empty() && !chain_order) {
             r.flags |= RUN_CHUNK;
             const int64_t mb = t[1] - t[0], d0 = sg.row0 - t[0];  // block row of segment row 0
             const int64_t a16 = mb & ~int64_t(15), b8 = a16 + (mb & 8), c4 = b8 + (mb & 4);
@@ -627,7 +630,7 @@ int hmx::plan_create_impl(const hmx_matrix_desc* d, int device, const hmx_plan_o
         src32 = true;
       }
       // chain items of group-table parts: SGEMV chunk layout (chunk_off)
-      const bool chunk = part == 1 && item_acc32(it) && sg.gtab >= 0;
+      const bool chunk = part == 1 && item_acc32(it) && sg.gtab >= 0 && !chain_order;
       for (int64_t i = 0; i < sg.R; ++i) {
         const int64_t e0 = src_off + (r0 + i) * w;
         for (int64_t c = 0; c < w; ++c) {
@@ -764,7 +767,7 @@ int hmx::plan_create_impl(const hmx_matrix_desc* d, int device, const hmx_plan_o
         u.is32 = part;
         for (const ItemRef& it : lst)
           pit.push_back({it.block, it.cls, (int32_t)item_width(it),
-                         (part == 1 && item_acc32(it) && sg.gtab >= 0) ? 1 : 0});
+                         (part == 1 && item_acc32(it) && sg.gtab >= 0 && !chain_order) ? 1 : 0});
         ps2.push_back(u);
       }
     }
@@ -855,7 +858,8 @@ int hmx::plan_create_impl(const hmx_matrix_desc* d, int device, const hmx_plan_o
   dp.blob32 = d_b32;
   dp.f32mode1 = pipe == P_M1S ? F32_ALL32 : F32_ALL64;
   dp.s1_narrow = s1_narrow ? 1 : 0;
-  dp.s1_exact = pipe == P_M1S ? 1 : 0;
+  dp.s1_exact = (pipe == P_M1S && !chain_order) ? 1 : 0;
+  dp.chain_exact = chain_order ? 0 : 1;
   {
     // deep FP64 pipeline when the FP64 part carries most of stage 2's bytes
     int64_t b64 = 0, b32 = 0;

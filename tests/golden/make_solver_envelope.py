@@ -42,7 +42,8 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("config", type=int)
     ap.add_argument("schemes", nargs="*")
-    ap.add_argument("--threads", default="1,2,3,4,5,6,7,8")
+    ap.add_argument("--threads", default="1,2,3,4,5,6,7,8",
+                    help="reorderings matvec_threaded(threads=k) to run (config 4 m1-mixed: 1..16)")
     ap.add_argument("--out", default=None)
     ap.add_argument("--merge", nargs="*", default=None, help="merge these partial files into --out")
     a = ap.parse_args()
@@ -52,8 +53,9 @@ def main():
         for p in a.merge:
             part = json.loads(Path(p).read_text())
             for k, v in part.items():
-                if k == "schemes":
-                    res.setdefault("schemes", {}).update(v)
+                if k == "schemes":  # per scheme, the thread counts of both files
+                    for sname, runs in v.items():
+                        res.setdefault("schemes", {}).setdefault(sname, {}).update(runs)
                 else:
                     res[k] = v
         out.write_text(json.dumps(res, indent=1))

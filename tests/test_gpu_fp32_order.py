@@ -130,3 +130,22 @@ def test_gpu_fp32_error_vs_oracle_config2(hx, orc):
         sh = hx.prepare_scheme(h, s)
         r = _error_ratio(hx.matvec(sh, x), orc.matvec(sh, x), y64)
         assert r <= 1.05, (s, r)
+
+
+@pytest.mark.gpu
+def test_gpu_fp32_chain_order_option(hx, orc, monkeypatch):
+    """HMX_FP32_ORDER=chain (HMX_PLAN_FP32_CHAIN): the faster one-chain-per-
+    (row, block) order -- within the FP32 tolerance of the reference, bit-
+    reproducible, and not the SGEMV order (the default)."""
+    arr, _ = load("ref240")
+    h = hmatrix_from_fixture(arr)
+    x = arr["x"]
+    exact = {s: hx.matvec(hx.prepare_scheme(h, s), x) for s in FP32_ACC}
+    monkeypatch.setenv("HMX_FP32_ORDER", "chain")
+    for s in FP32_ACC:
+        sh = hx.prepare_scheme(h, s)          # a fresh object: a fresh plan
+        y = hx.matvec(sh, x)
+        ref = arr[f"y/{s}"]
+        assert np.max(np.abs(y - ref)) <= 1e-5 * np.max(np.abs(ref)), s
+        assert np.array_equal(y, hx.matvec(sh, x))
+        assert not np.array_equal(y, exact[s]), s

@@ -319,23 +319,25 @@ def cases(names):
 
 
 def bitwise_check():
-    """sgemv_tree vs numpy's own `A32 @ g32` on random data: prints the
-    widths where they differ (per row count)."""
+    """The GPU's order (sgemv_rows / sgemv_blocked) against numpy's own
+    `A32 @ g32` on random data, for row counts 2..64 and widths 1..48, then
+    long rows: prints the (rows, widths) that differ."""
     rng = np.random.default_rng(7)
-    for m in (4, 8, 20, 40, 64, 3, 7):
+    for m in list(range(2, 25)) + [30, 40, 48, 64]:
         bad = []
-        for n in range(1, 70):
+        for n in range(1, 49):
             for _ in range(6):
                 a = rng.standard_normal((m, n)).astype(F32)
                 g = rng.standard_normal(n).astype(F32)
-                if not np.array_equal(sgemv_tree(a, g), a @ g):
+                if not np.array_equal(sgemv_rows(a, g), a @ g):
                     bad.append(n)
                     break
-        print(f"rows {m:3d}: widths 1..69 differing from numpy: {bad if bad else 'none'}")
+        print(f"rows {m:3d}: widths 1..48 differing from numpy: {bad if bad else 'none'}")
     for n in (100, 1280, 4096, 4100, 5120, 10240, 20480):
-        a = rng.standard_normal((8, n)).astype(F32)
+        a = rng.standard_normal((13, n)).astype(F32)
         g = rng.standard_normal(n).astype(F32)
-        print(f"long row n={n}: blocked model == numpy: {np.array_equal(sgemv_blocked(a, g), a @ g)}")
+        print(f"long row n={n}, 13 rows: blocked model == numpy: "
+              f"{np.array_equal(sgemv_blocked(a, g, rows=True), a @ g)}")
 
 
 def main():
