@@ -20,6 +20,9 @@
 #ifndef HMX_MIXED_MINB
 #define HMX_MIXED_MINB 4
 #endif
+#ifndef HMX_EXACT_MINB
+#define HMX_EXACT_MINB 4  // CTAs per SM of the SGEMV-order stage-2 kernels (register budget)
+#endif
 
 namespace hmx {
 
@@ -540,8 +543,10 @@ __global__ void __launch_bounds__(kS1ExactRows) s1_exact_kernel(DevPlan P, const
 // EXACT (stage 2 with FP32-accumulated items): those items in SGEMV's order
 // (chain_windows); otherwise one FP32 chain per (row, item) (HMX_PLAN_FP32_CHAIN).
 // Separate instantiations keep each one's register allocation its own.
-template <int F32MODE, int OUT, int NT, bool DEEP = false, bool EXACT = false>
-__global__ void __launch_bounds__(NT, DEEP ? 3 : (OUT == OUT_Y && F32MODE != F32_ALL64) ? HMX_MIXED_MINB : 1024 / NT) seg_kernel(DevPlan P, const Seg* __restrict__ segs,
+// XMINB: CTAs per SM of an EXACT instantiation (its register budget; m2-single
+// measured faster at 3 = 80 registers, m1-mixed at 4).
+template <int F32MODE, int OUT, int NT, bool DEEP = false, bool EXACT = false, int XMINB = HMX_EXACT_MINB>
+__global__ void __launch_bounds__(NT, DEEP ? 3 : (OUT == OUT_Y && F32MODE != F32_ALL64) ? (EXACT ? XMINB : HMX_MIXED_MINB) : 1024 / NT) seg_kernel(DevPlan P, const Seg* __restrict__ segs,
                                                           const double* __restrict__ x, S2Out out) {
   // stage 1 segments have a single run (no index expansion) and <= 1024 columns
   constexpr int WMAX = OUT == OUT_Z ? kS1WMax : kSegWMax;
@@ -1025,7 +1030,7 @@ constexpr size_t chain_smem() {
   return (EXACT && O == OUT_Y && M != F32_ALL64) ? 2 * (size_t)kChainWin : 0;
 }
 
-template <int M, int O, int NT = kSegThreads, bool DEEP = false, bool EXACT = false>
+template <int M, int O, int NT = kSegThreads, bool DEEP = false, bool EXACT = false, int XMINB = HMX_EXACT_MINB>
 static cudaError_t launch_seg(const DevPlan& P, const Seg* segs, int nseg, const double* x,
                               const S2Out& out, cudaStream_t st, bool pdl) {
   cudaLaunchConfig_t cfg = {};
@@ -1038,7 +1043,7 @@ static cudaError_t launch_seg(const DevPlan& P, const Seg* segs, int nseg, const
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = pdl ? 1 : 0;
-  return cudaLaunchKernelEx(&cfg, seg_kernel<M, O, NT, DEEP, EXACT>, P, segs, x, out);
+  return cudaLaunchKernelEx(&cfg, seg_kernel<M, O, NT, DEEP, EXACT, XMINB>, P, segs, x, out);
 }
 
 cudaError_t launch_stage1(const DevPlan& P, const double* x, cudaStream_t st, const int* skip,
@@ -1072,8 +1077,9 @@ cudaError_t launch_stage2(const DevPlan& P, const double* x, const S2Out& out, c
       return P.chain_exact ? launch_seg<F32_ALL32, OUT_Y, kSegThreads, false, true>(P, P.seg2, P.n_seg2, x, out, st, pdl)
                            : launch_seg<F32_ALL32, OUT_Y>(P, P.seg2, P.n_seg2, x, out, st, pdl);
     case F32_MIXED:
-      return P.chain_exact ? launch_seg<F32_MIXED, OUT_Y, kSegThreads, false, true>(P, P.seg2, P.n_seg2, x, out, st, pdl)
-                           : launch_seg<F32_MIXED, OUT_Y>(P, P.seg2, P.n_seg2, x, out, st, pdl);
+      if (!P.chain_exact) return launch_seg<F32_MIXED, OUT_Y>(P, P.seg2, P.n_seg2, x, out, st, pdl);
+      return P.pipe == P_M2S ? launch_seg<F32_MIXED, OUT_Y, kSegThreads, false, true, 3>(P, P.seg2, P.n_seg2, x, out, st, pdl)
+                             : launch_seg<F32_MIXED, OUT_Y, kSegThreads, false, true>(P, P.seg2, P.n_seg2, x, out, st, pdl);
     default:
       return P.s2_deep ? launch_seg<F32_ALL64, OUT_Y, kSegThreads, true>(P, P.seg2, P.n_seg2, x, out, st, pdl)
                        : launch_seg<F32_ALL64, OUT_Y>(P, P.seg2, P.n_seg2, x, out, st, pdl);
@@ -1088,6 +1094,9 @@ cudaError_t configure_kernels() {
                                        (int)chain_smem<F32_ALL32, OUT_Y, true>());
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(seg_kernel<F32_MIXED, OUT_Y, kSegThreads, false, true>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)chain_smem<F32_MIXED, OUT_Y, true>());
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(seg_kernel<F32_MIXED, OUT_Y, kSegThreads, false, true, 3>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)chain_smem<F32_MIXED, OUT_Y, true>());
   return e;
 }

@@ -130,3 +130,43 @@ def test_gloo_world2_matvec_and_bicgstab(tmp_path, hx, orc, world, shift):
     x = np.empty(h.n)
     x[perm] = np.concatenate([r["x"] for r in rs])
     assert np.linalg.norm(x - xo) / np.linalg.norm(xo) <= 1e-6
+
+
+def _cuts_worker(rank, world, port, out_dir):
+    sys.path.insert(0, str(ROOT))
+    import json
+
+    import torch.distributed as dist
+
+    import paper_1911_00093_b200 as hx
+    from paper_1911_00093_b200 import distributed as D
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    mesh = hx.jittered_sphere_mesh(4, seed=42)
+    part = hx.build_block_partition(hx.build_cluster_tree(mesh, 32), 2.0)
+    cuts = D.measured_cuts(mesh, part, aca_tol=1e-4, world=world, rank=rank)
+    Path(out_dir, f"cuts{rank}.json").write_text(json.dumps(cuts))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_measured_cuts_match_the_full_build(tmp_path, world):
+    """distributed.measured_cuts (estimate cut, row-restricted builds, real
+    ranks exchanged, re-cut) gives every rank the cuts partition_rows makes
+    from the FULL build's stored bytes (balanced by stored bytes)."""
+    import json
+
+    import torch.multiprocessing as mp
+
+    import paper_1911_00093_b200 as hx
+    from paper_1911_00093_b200 import distributed as D
+
+    mp.spawn(_cuts_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
+    got = [json.loads((tmp_path / f"cuts{r}.json").read_text()) for r in range(world)]
+    mesh = hx.jittered_sphere_mesh(4, seed=42)
+    h = hx.build_hmatrix(mesh, aca_tol=1e-4, leaf_size=32)
+    want = D.partition_rows(h.partition.table, h.packed.kinds, h.packed.ranks, h.n, world)
+    assert all(g == want for g in got), (got, want)

@@ -28,9 +28,12 @@ def rel(a, b):
 
 
 def _release(sh):
+    import gc
     plan = getattr(sh, "_hmx_gpu_plan", None)
     if plan is not None:
         plan.close()
+    sh._payloads = None   # the oracle's per-block views
+    gc.collect()
 
 
 @pytest.mark.parametrize("cfg", [3, 4])
@@ -49,8 +52,22 @@ def test_full_products_every_scheme(hx, orc, cfg):
     print(cfg, errs)
 
 
+def _sub_hmatrix(hx, h, sample):
+    """The blocks `sample` of h as an H-matrix of their own (same n, same
+    cluster tree): preparation is block-local (precision.py:256-329), so its
+    scheme payloads are the full scheme's payloads of those blocks, and the
+    host never holds a full prepared copy of config 5's 59 GB of masters."""
+    t = h.partition.table
+    pm = h.packed
+    part = hx.BlockPartition(n=h.n, tree=h.partition.tree, table=t[sample])
+    return hx.HMatrixF64(part, payloads=[pm.payload(t[k], k) for k in sample])
+
+
 @pytest.mark.slow
 def test_config5_sampled_rows(hx, orc):
+    """Device: the full plan of each scheme, prepared ON THE DEVICE from the
+    resident masters (no host scheme copy).  Host: the oracle over the
+    sub-H-matrix of every block meeting the sampled rows."""
     import bench
     _, h, x, _, _ = bench.build_workload(5)
     n = h.n
@@ -59,20 +76,22 @@ def test_config5_sampled_rows(hx, orc):
     rng = np.random.default_rng(5)
     leaves = np.sort(rng.choice(bounds.size - 1, size=64, replace=False))
     rows = np.concatenate([np.arange(bounds[i], bounds[i + 1]) for i in leaves])
-    mask = np.zeros(n, dtype=bool)
-    mask[rows] = True
     cover = np.zeros(n + 1, dtype=np.int64)
     np.add.at(cover, rows, 1)
     csum = np.concatenate([[0], np.cumsum(cover)])
     meets = csum[table[:, 1]] - csum[table[:, 0]] > 0          # blocks meeting a sampled row
     sample = np.flatnonzero(meets)
+    sub = _sub_hmatrix(hx, h, sample)
     perm = np.asarray(h.permutation)
     errs = {}
     for s in ("m1-double", "m1-mixed", "m2-mixed", "m3:c=3"):
-        sh = hx.prepare_scheme(h, s)
-        y = hx.matvec(sh, x)[perm][rows]                      # full plan, permuted rows
-        ref = orc.matvec(sh, x, blocks=sample)[perm][rows]    # every contribution to those rows
+        dsh = hx.prepare_scheme_device(h, s)
+        y = hx.matvec(dsh, x)[perm][rows]                     # full plan, permuted rows
+        _release(dsh)
+        del dsh
+        ssh = hx.prepare_scheme(sub, s)
+        ref = orc.matvec(ssh, x)[perm][rows]                  # every contribution to those rows
+        del ssh
         errs[s] = rel(y, ref)
         assert errs[s] <= (1e-12 if s == "m1-double" else 1e-5), (s, errs[s])
-        _release(sh)
     print("config 5 sampled rows", rows.size, "blocks", sample.size, errs)
