@@ -153,6 +153,27 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
 __device__ __forceinline__ void chain_bar(int nthreads) {
   asm volatile("bar.sync 1, %0;" ::"r"(nthreads) : "memory");
 }
+// mbarrier + 1-D bulk copy (TMA engine): one thread moves a whole window
+__device__ __forceinline__ uint32_t smem_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* b) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(b)) : "memory");
+}
+// arrive on `b` expecting `bytes` and start the copy (bytes = 0: plain arrive)
+__device__ __forceinline__ void bulk_to_smem(float* dst, const float* src, uint32_t bytes, uint64_t* b) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(b)), "r"(bytes) : "memory");
+  if (bytes)
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_addr(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_addr(b))
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred P1;\n WAIT:\n mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n @P1 bra DONE;\n bra WAIT;\n "
+      "DONE:\n }" ::"r"(smem_addr(b)),
+      "r"(parity)
+      : "memory");
+}
 
 constexpr int kMetaW = 12;  // run meta in shared memory: col0 << 12 | width
 #ifndef HMX_CHAIN_ROWS
@@ -338,11 +359,12 @@ __device__ __forceinline__ float2 chain_item2(const float* it, GF G, int n, int 
 
 // chain threads u = 0 .. nthr-1 (slot u / rp, row u % rp); items j0 .. nrun-1
 // of the part (meta in shared memory, the part's blob at `part`); buf: two
-// kChainWin-byte staging buffers; wq: 6 ints of shared memory for the window
-// bounds thread 0 publishes one window ahead.  Returns this thread's row sum.
+// kChainWin-byte staging buffers, filled by bulk copies (thread 0 issues one
+// per window; mb: their two mbarriers); wq: 6 ints of shared memory for the
+// window bounds thread 0 keeps one window ahead.  Returns this thread's row sum.
 __device__ __forceinline__ double chain_windows(const int32_t* meta, const uint32_t* kbits, int j0, int nrun,
                                                 const float* part, const double* gs, int rp, int u, int nthr,
-                                                float* buf, int* wq, double& acc1) {
+                                                float* buf, int* wq, uint64_t* mb, double& acc1) {
 #if HMX_CHAIN_ROWS == 2
   const int half = rp >> 1;  // two rows per thread: p and p + half
   const int K = nthr / half;
@@ -364,36 +386,43 @@ __device__ __forceinline__ double chain_windows(const int32_t* meta, const uint3
     while (e < nrun && col0(e) + width(e) - cs <= wmax) ++e;
     return e;
   };
-  auto stage = [&](int j, int e, int b) {  // copy window [j, e) into buffer b (nothing if oversize)
-    if (j >= nrun || width(j) > wmax) return;
-    const int cs = col0(j), ce = col0(e - 1) + width(e - 1);
-    const int n16 = (ce - cs) * rp / 4;  // 16-byte pieces
-    const float* src = part + (int64_t)cs * rp;
-    float* dst = buf + b * (kChainWin / 4);
-    for (int i = u; i < n16; i += nthr) cp_async16(dst + 4 * i, src + 4 * i);
+  // (thread 0) copy window [j, e) into buffer b; an oversize item (read from
+  // global memory) completes the buffer's phase with no bytes
+  auto stage = [&](int j, int e, int b) {
+    if (j >= nrun) return;
+    uint32_t bytes = 0;
+    const float* src = part;
+    if (width(j) <= wmax) {
+      const int cs = col0(j), ce = col0(e - 1) + width(e - 1);
+      bytes = (uint32_t)((ce - cs) * rp * 4);
+      src = part + (int64_t)cs * rp;
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // the buffer's last generic reads
+    bulk_to_smem(buf + b * (kChainWin / 4), src, bytes, mb + b);
   };
-  // window bounds: a ring of three (start, end) pairs in wq, written by thread
-  // 0 one window ahead of their use
+  // window bounds: a ring of three (start, end) pairs in wq
   if (u == 0) {
+    mbar_init(mb);
+    mbar_init(mb + 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     const int e0 = wend(j0), e1 = wend(e0);
     wq[0] = j0, wq[1] = e0, wq[2] = e0, wq[3] = e1;
+    stage(j0, e0, 0);
   }
   chain_bar(nthr);
-  stage(wq[0], wq[1], 0);
-  asm volatile("cp.async.commit_group;" ::: "memory");
   double acc = 0.0;
   for (int w = 0;; ++w) {
-    const int r = w % 3, r1 = (w + 1) % 3, r2 = (w + 2) % 3;
+    const int r = w % 3;
     const int j = wq[2 * r], e = wq[2 * r + 1];
     if (j >= nrun) break;
-    const int jn = wq[2 * r1], en = wq[2 * r1 + 1];
-    stage(jn, en, (w + 1) & 1);  // the next window is in flight while this one is reduced
-    asm volatile("cp.async.commit_group;\ncp.async.wait_group 1;" ::: "memory");
-    if (u == 0) {  // publish the window after next
+    if (u == 0) {  // the next window in flight while this one is reduced; bounds of the one after
+      const int r1 = (w + 1) % 3, r2 = (w + 2) % 3;
+      const int jn = wq[2 * r1], en = wq[2 * r1 + 1];
+      stage(jn, en, (w + 1) & 1);
       wq[2 * r2] = en;
       wq[2 * r2 + 1] = wend(en);
     }
-    chain_bar(nthr);  // every thread's copies of window [j, e) have landed
+    mbar_wait(mb + (w & 1), (uint32_t)(w >> 1) & 1u);  // window [j, e) has landed
     if (act) {
       if (width(j) > wmax) {  // oversize item: straight from global memory
         if (slot == 0) {
@@ -431,9 +460,8 @@ __device__ __forceinline__ double chain_windows(const int32_t* meta, const uint3
         }
       }
     }
-    chain_bar(nthr);  // buffer w & 1 is free again
+    chain_bar(nthr);  // buffer w & 1 is free again; wq holds the next bounds
   }
-  asm volatile("cp.async.wait_group 0;" ::: "memory");
   return acc;
 }
 
@@ -467,8 +495,8 @@ __global__ void __launch_bounds__(kS1ExactRows) s1_exact_kernel(DevPlan P, const
   } else {
     // this CTA's 4096-column block: the A/B lane tree (kinds 16/8/4: FMA
     // chains; 1: multiply then add; 2: one accumulator, multiply then add),
-    // chunks streamed with kS1Win loads in flight (each register refilled
-    // with the chunk kS1Win ahead right after it is consumed)
+    // chunks loaded kS1Win at a time (all loads of a batch in flight before
+    // the first is consumed -- measured faster than a rolling refill)
     const int nch = n >> 2, T = n & 3;
     const bool fm = kind >= 4, one = kind == 2, odd = nch & 1;
     const float* ch = it + 4 * t;  // chunk c at ch[4 c rp]
@@ -484,20 +512,14 @@ __global__ void __launch_bounds__(kS1ExactRows) s1_exact_kernel(DevPlan P, const
       else B = Y;
     };
     constexpr int kS1Win = 8;
-    float4 w[kS1Win];
-#pragma unroll
-    for (int u = 0; u < kS1Win; ++u)
-      if (u < nch) w[u] = ld_chunk(ch + (int64_t)4 * u * rp);
     for (int c = 0; c < nch; c += kS1Win) {
+      float4 w[kS1Win];
 #pragma unroll
-      for (int u = 0; u < kS1Win; ++u) {
-        const int cc = c + u;
-        if (cc < nch) {
-          const float4 x = w[u];
-          if (cc + kS1Win < nch) w[u] = ld_chunk(ch + (int64_t)4 * (cc + kS1Win) * rp);
-          step(x, cc);
-        }
-      }
+      for (int u = 0; u < kS1Win; ++u)
+        if (c + u < nch) w[u] = ld_chunk(ch + (int64_t)4 * (c + u) * rp);
+#pragma unroll
+      for (int u = 0; u < kS1Win; ++u)
+        if (c + u < nch) step(w[u], c + u);
     }
     const float4 l = make_float4(__fadd_rn(A.x, B.x), __fadd_rn(A.y, B.y), __fadd_rn(A.z, B.z),
                                  __fadd_rn(A.w, B.w));
@@ -560,6 +582,7 @@ __global__ void __launch_bounds__(NT, DEEP ? 3 : (OUT == OUT_Y && F32MODE != F32
   // chain-item staging buffers (stage-2 FP32 kernels: 2 x kChainWin bytes of dynamic shared memory)
   extern __shared__ __align__(16) float chain_buf[];
   __shared__ int chain_wq[6];  // chain-window bounds (chain_windows)
+  __shared__ uint64_t chain_mb[2];  // their bulk copies' mbarriers
   __shared__ unsigned ticket;
 
   if (out.skip != nullptr && *out.skip != 0) return;  // guarded launch (solver)
@@ -845,7 +868,7 @@ __global__ void __launch_bounds__(NT, DEEP ? 3 : (OUT == OUT_Y && F32MODE != F32
       const int c32c = P.gtab[sg.gtab + g32 + 1];
       while (j0 < sg.nrun32 && (sidx[j0] >> kMetaW) < c32c) ++j0;
       bc = chain_windows(sidx, kbits, j0, sg.nrun32, P.blob32 + sg.off32, gs, rp32, tid - wbc, NT - wbc, chain_buf,
-                         chain_wq, bc1);
+                         chain_wq, chain_mb, bc1);
     }
   }
 
