@@ -117,10 +117,21 @@ constexpr int kS1WMax = 1024;     // max columns per stage-1 segment chunk
 #endif
 constexpr int kS1ExactRows = HMX_S1X_ROWS;  // m1-single stage 1: rank rows per CTA (one thread each)
 constexpr int kSgemvBlock = 1024; // OpenBLAS SGEMV-T column blocking: 4096 columns = 1024 chunks
-#ifndef HMX_CHAIN_ROWS
-#define HMX_CHAIN_ROWS 1  // stage-2 chain threads: rows per thread (1 or 2)
+constexpr int kChainGroupThreads = 32;  // stage 2: one warp per group of FP32-accumulated (chain) items
+// A chain warp streams its group's items through a ring in shared memory
+// (hmx_kernels.cu chain_stream): kRingStages windows, one bulk copy each.  An
+// item that fits the ring beside one window in flight is stored column-major
+// (rows contiguous, like every other item) and evaluated four rows per lane;
+// a longer one is stored in SGEMV chunk layout (chunk_off, RUN_CHUNK) and
+// streamed chunk pair by chunk pair, one or two rows per lane.
+#ifndef HMX_RING_LOG2
+#define HMX_RING_LOG2 13
 #endif
-constexpr int kChainRows = HMX_CHAIN_ROWS;
+constexpr int kRingStages = 4;
+constexpr int kRingBytes = 1 << HMX_RING_LOG2;      // ring of one chain warp
+constexpr int kRingWin = kRingBytes / kRingStages;  // window = one bulk copy
+constexpr int kChainWhole = kRingBytes - kRingWin;  // bytes the ring holds beside one window in flight
+__host__ __device__ __forceinline__ bool chain_item_long(int64_t n, int64_t rp) { return n * rp * 4 > kChainWhole; }
 
 // Device-visible plan (passed by value to kernels).
 struct DevPlan {
@@ -138,7 +149,8 @@ struct DevPlan {
   int32_t s1_narrow;              // every stage-1 segment is widened FP32: 64-thread CTAs
   int32_t s2_deep;                // FP64-accumulating stage 2 with an FP64 part: deep pipeline
   int32_t s1_exact;               // m1-single: stage 1 in SGEMV order (s1_exact_kernel)
-  int32_t chain_exact;            // stage-2 FP32-accumulated items in SGEMV order (chain_windows)
+  int32_t chain_exact;            // stage-2 FP32-accumulated items in SGEMV order (chain_stream)
+  int32_t chain_warps;            // most chain warps (groups) of any stage-2 segment
   int32_t n_seg1_local;           // leading stage-1 segments reading only x[row_begin, row_end)
   const int32_t* gtab;            // item-aligned FP32 group boundaries (stage 2)
   const double* zscale;           // d per z entry (methods 2, 3)

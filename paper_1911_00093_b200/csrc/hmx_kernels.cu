@@ -21,7 +21,7 @@
 #define HMX_MIXED_MINB 4
 #endif
 #ifndef HMX_EXACT_MINB
-#define HMX_EXACT_MINB 4  // CTAs per SM of the SGEMV-order stage-2 kernels (register budget)
+#define HMX_EXACT_MINB 2  // CTAs per SM of the SGEMV-order stage-2 kernels (the chain warps' rings bound it)
 #endif
 
 namespace hmx {
@@ -123,16 +123,27 @@ __device__ __forceinline__ double z_epilogue(const DevPlan& P, double s, int zi)
 // FP64 (reference matvec.py:57, :73, then :106).  Explicit _rn intrinsics:
 // nothing is contracted or reassociated.
 //
-// The chain warps stage the segment's chain items through shared memory:
-// windows of whole consecutive items (<= kChainWin bytes, contiguous in the
-// blob), copied with cp.async by all chain threads into two buffers, the next
-// window in flight while one is reduced; inside a window item i goes to slot i mod K (K = chain
-// threads / rp), one row per thread.  Items larger than a window are read
-// from global memory by slot 0.
+// Every chain WARP owns one thread group of the segment (hmx_plan.cu deals the
+// chain items to the groups and lays each group's items out contiguously), so
+// its items are one contiguous byte stream.  The warp pulls that stream
+// through a private ring in shared memory -- kRingStages windows, each filled
+// by one bulk copy (cp.async.bulk, TMA engine) that lane 0 issues as soon as
+// the warp has consumed the window that held the slot -- and evaluates its
+// items from the ring, rows `lane` and `lane + 32` of every item (one or two
+// rows per thread).  Items may straddle windows: the ring is addressed by
+// stream offset.  No barrier is shared between warps.
 __device__ __forceinline__ float4 fma4(float4 a, float4 g, float4 c) {
   return make_float4(__fmaf_rn(a.x, g.x, c.x), __fmaf_rn(a.y, g.y, c.y), __fmaf_rn(a.z, g.z, c.z),
                      __fmaf_rn(a.w, g.w, c.w));
 }
+__device__ __forceinline__ float4 mad4(float4 a, float4 g, float4 c) {  // multiply, then add
+  return make_float4(__fadd_rn(c.x, __fmul_rn(a.x, g.x)), __fadd_rn(c.y, __fmul_rn(a.y, g.y)),
+                     __fadd_rn(c.z, __fmul_rn(a.z, g.z)), __fadd_rn(c.w, __fmul_rn(a.w, g.w)));
+}
+__device__ __forceinline__ float4 add4(float4 a, float4 b) {
+  return make_float4(__fadd_rn(a.x, b.x), __fadd_rn(a.y, b.y), __fadd_rn(a.z, b.z), __fadd_rn(a.w, b.w));
+}
+__device__ __forceinline__ float hsum4(float4 l) { return __fadd_rn(__fadd_rn(l.x, l.y), __fadd_rn(l.z, l.w)); }
 __device__ __forceinline__ float4 ld_chunk(const float* p) {
   float4 r;  // L1-allocating: a thread's A and B chunks share 32-byte sectors
   asm volatile("ld.global.nc.L1::evict_first.v4.f32 {%0,%1,%2,%3}, [%4];"
@@ -145,11 +156,6 @@ __device__ __forceinline__ float ld_one(const float* p) {
   asm volatile("ld.global.nc.L1::no_allocate.f32 %0, [%1];" : "=f"(r) : "l"(p));
   return r;
 }
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"((unsigned)__cvta_generic_to_shared(smem)),
-               "l"(gmem)
-               : "memory");
-}
 __device__ __forceinline__ void chain_bar(int nthreads) {
   asm volatile("bar.sync 1, %0;" ::"r"(nthreads) : "memory");
 }
@@ -158,14 +164,13 @@ __device__ __forceinline__ uint32_t smem_addr(const void* p) { return (uint32_t)
 __device__ __forceinline__ void mbar_init(uint64_t* b) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(b)) : "memory");
 }
-// arrive on `b` expecting `bytes` and start the copy (bytes = 0: plain arrive)
+// arrive on `b` expecting `bytes` and start the copy
 __device__ __forceinline__ void bulk_to_smem(float* dst, const float* src, uint32_t bytes, uint64_t* b) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(b)), "r"(bytes) : "memory");
-  if (bytes)
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                     smem_addr(dst)),
-                 "l"(src), "r"(bytes), "r"(smem_addr(b))
-                 : "memory");
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_addr(dst)),
+               "l"(src), "r"(bytes), "r"(smem_addr(b))
+               : "memory");
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
   asm volatile(
@@ -176,15 +181,10 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
 }
 
 constexpr int kMetaW = 12;  // run meta in shared memory: col0 << 12 | width
-#ifndef HMX_CHAIN_ROWS
-#define HMX_CHAIN_ROWS 1  // rows per chain thread (1 or 2); the flattener's group count follows kChainRows
-#endif
-#ifndef HMX_CHAIN_WB
-#define HMX_CHAIN_WB 8192
-#endif
-constexpr int kChainWin = HMX_CHAIN_WB;  // bytes per staging buffer (two buffers)
 
-// row p of one n-wide item at `it` (global or shared memory, chunk layout).
+// One row of an n-wide item in OpenBLAS SGEMV-T's order.  X4(c): the row's
+// columns 4c .. 4c+3; E(k): its column k; G(k): the FP32 source value of the
+// item's column k.
 // `kind`: which OpenBLAS SGEMV-T row kernel computes this row of its block
 // (sgemv_row_kind): 16, 8, 4 = the 16-, 8- and 4-row kernels (A/B FMA
 // chains; rows shorter than 8 differ between them), 2 = the two-row
@@ -192,27 +192,11 @@ constexpr int kChainWin = HMX_CHAIN_WB;  // bytes per staging buffer (two buffer
 // one-row remainder kernel (A/B, multiply then add).  All end with
 // (l0 + l1) + (l2 + l3) and the same tail rule (tools/fp32_accum_emulation.py
 // sgemv_kind: bitwise numpy's own for every row count 2..64, widths 1..48).
-// G(k): the FP32 source value of the item's column k.
-template <bool GLOBAL, typename GF>
-__device__ __forceinline__ float chain_item(const float* it, GF G, int n, int rp, int p, int kind) {
-  constexpr int c0 = 0;
+template <typename XF, typename EF, typename GF>
+__device__ __forceinline__ float chain_item(XF X4, EF E, GF G, int n, int kind) {
   auto G4 = [&](int c) { return make_float4(G(c), G(c + 1), G(c + 2), G(c + 3)); };
-  auto L4 = [&](const float* q) {
-    if constexpr (GLOBAL) return ld_chunk(q);
-    else return *reinterpret_cast<const float4*>(q);
-  };
-  auto L1 = [&](const float* q) {
-    if constexpr (GLOBAL) return ld_one(q);
-    else return *q;
-  };
-  // element k of this row (chunk layout)
-  auto E = [&](int k) {
-    if (chain_shaped(n)) return L1(it + (int64_t)k * rp + p);
-    const int m = n & ~3;
-    return k < m ? L1(it + 4 * ((int64_t)(k >> 2) * rp + p) + (k & 3)) : L1(it + (int64_t)m * rp + (int64_t)(k - m) * rp + p);
-  };
-  auto Pr = [&](int k) { return __fmul_rn(E(k), G(c0 + k)); };  // rounded product
-  auto F = [&](int k, float acc) { return __fmaf_rn(E(k), G(c0 + k), acc); };
+  auto Pr = [&](int k) { return __fmul_rn(E(k), G(k)); };  // rounded product
+  auto F = [&](int k, float acc) { return __fmaf_rn(E(k), G(k), acc); };
   if (n == 1) return Pr(0);
   if (kind >= 4 && n <= 7 && n != 4) {  // short rows of the 16-, 8- and 4-row kernels
     if (n == 2 && kind != 16) return __fadd_rn(Pr(0), Pr(1));
@@ -236,12 +220,11 @@ __device__ __forceinline__ float chain_item(const float* it, GF G, int n, int rp
     }
   }
   const int nch = n >> 2, T = n & 3, m = 4 * nch;
-  const float* ch = it + 4 * p;  // chunk c of row p at ch[4 c rp]
   float4 l;
   bool seq = false;  // sequential horizontal sum (one-row kernel, n <= 8)
   if (n == 8 && kind >= 4) {  // l_j = a_2j g_2j + a_2j+1 g_2j+1
-    const float4 x0 = L4(ch), x1 = L4(ch + 4 * rp);
-    const float4 g0 = G4(c0), g1 = G4(c0 + 4);
+    const float4 x0 = X4(0), x1 = X4(1);
+    const float4 g0 = G4(0), g1 = G4(4);
     l = make_float4(__fadd_rn(__fmul_rn(x0.x, g0.x), __fmul_rn(x0.y, g0.y)),
                     __fadd_rn(__fmul_rn(x0.z, g0.z), __fmul_rn(x0.w, g0.w)),
                     __fadd_rn(__fmul_rn(x1.x, g1.x), __fmul_rn(x1.y, g1.y)),
@@ -251,218 +234,323 @@ __device__ __forceinline__ float chain_item(const float* it, GF G, int n, int rp
     // chunks, B = odd; nch odd: A = {0, 1, 3, 5, ..}, B = {2, 4, ..}; two-row
     // kernel: every chunk into A
     float4 A = make_float4(0.f, 0.f, 0.f, 0.f), B = A;
-    auto acc = [&](float4& X, const float4& x, const float4& g) {
-      if (kind >= 4) X = fma4(x, g, X);
-      else X = make_float4(__fadd_rn(X.x, __fmul_rn(x.x, g.x)), __fadd_rn(X.y, __fmul_rn(x.y, g.y)),
-                           __fadd_rn(X.z, __fmul_rn(x.z, g.z)), __fadd_rn(X.w, __fmul_rn(x.w, g.w)));
-    };
     int c = 0;
-    if (kind == 2) {
-      for (; c < nch; ++c) acc(A, L4(ch + (int64_t)4 * c * rp), G4(c0 + 4 * c));
-    } else {
+    if (kind >= 4) {
       if (nch & 1) {
-        acc(A, L4(ch), G4(c0));
+        A = fma4(X4(0), G4(0), A);
         c = 1;
       }
       for (; c < nch; c += 2) {
-        const float4 xa = L4(ch + (int64_t)4 * c * rp), xb = L4(ch + (int64_t)4 * (c + 1) * rp);
-        acc(A, xa, G4(c0 + 4 * c));
-        acc(B, xb, G4(c0 + 4 * c + 4));
+        const float4 xa = X4(c), xb = X4(c + 1);
+        A = fma4(xa, G4(4 * c), A);
+        B = fma4(xb, G4(4 * c + 4), B);
+      }
+    } else if (kind == 2) {
+      for (; c < nch; ++c) A = mad4(X4(c), G4(4 * c), A);
+    } else {
+      if (nch & 1) {
+        A = mad4(X4(0), G4(0), A);
+        c = 1;
+      }
+      for (; c < nch; c += 2) {
+        const float4 xa = X4(c), xb = X4(c + 1);
+        A = mad4(xa, G4(4 * c), A);
+        B = mad4(xb, G4(4 * c + 4), B);
       }
     }
-    l = make_float4(__fadd_rn(A.x, B.x), __fadd_rn(A.y, B.y), __fadd_rn(A.z, B.z), __fadd_rn(A.w, B.w));
+    l = add4(A, B);
     seq = kind == 1 && n <= 8;
   }
-  float v = seq ? __fadd_rn(__fadd_rn(__fadd_rn(l.x, l.y), l.z), l.w)
-                : __fadd_rn(__fadd_rn(l.x, l.y), __fadd_rn(l.z, l.w));
-  const float* tl = it + (int64_t)m * rp + p;
+  float v = seq ? __fadd_rn(__fadd_rn(__fadd_rn(l.x, l.y), l.z), l.w) : hsum4(l);
   if (T == 1) {
-    v = __fmaf_rn(L1(tl), G(c0 + m), v);
+    v = __fmaf_rn(E(m), G(m), v);
   } else if (T >= 2) {
-    float tv = __fmul_rn(L1(tl + rp), G(c0 + m + 1));
-    tv = __fmaf_rn(L1(tl), G(c0 + m), tv);
-    if (T == 3) tv = __fmaf_rn(L1(tl + 2 * rp), G(c0 + m + 2), tv);
+    float tv = __fmul_rn(E(m + 1), G(m + 1));
+    tv = __fmaf_rn(E(m), G(m), tv);
+    if (T == 3) tv = __fmaf_rn(E(m + 2), G(m + 2), tv);
     v = __fadd_rn(v, tv);
   }
   return v;
 }
-
-// Rows r0 = h and r1 = h + half of one n-wide item in shared memory (chunk
-// layout), both in the four-row kernel's order (kind 4): chain_item for two
-// rows at once, sharing the source loads.
-template <typename GF>
-__device__ __forceinline__ float2 chain_item2(const float* it, GF G, int n, int rp, int r0, int r1) {
-  auto G4 = [&](int c) { return make_float4(G(c), G(c + 1), G(c + 2), G(c + 3)); };
-  if (chain_shaped(n)) {
-    float v0 = 0.f, v1 = 0.f;
-    for (int k = 0; k < n; ++k) {
-      const float g = G(k);
-      v0 = __fmaf_rn(it[(int64_t)k * rp + r0], g, v0);
-      v1 = __fmaf_rn(it[(int64_t)k * rp + r1], g, v1);
-    }
-    return make_float2(v0, v1);
-  }
-  const int nch = n >> 2, T = n & 3, m = 4 * nch;
-  const float4* c0p = reinterpret_cast<const float4*>(it) + r0;  // chunk c of row r at [c rp + r]
-  const float4* c1p = reinterpret_cast<const float4*>(it) + r1;
-  float4 l0, l1;
-  if (n == 8) {  // l_j = a_2j g_2j + a_2j+1 g_2j+1
-    const float4 g0 = G4(0), g1 = G4(4);
-    auto pairs = [&](const float4& x, const float4& y) {
-      return make_float4(__fadd_rn(__fmul_rn(x.x, g0.x), __fmul_rn(x.y, g0.y)),
-                         __fadd_rn(__fmul_rn(x.z, g0.z), __fmul_rn(x.w, g0.w)),
-                         __fadd_rn(__fmul_rn(y.x, g1.x), __fmul_rn(y.y, g1.y)),
-                         __fadd_rn(__fmul_rn(y.z, g1.z), __fmul_rn(y.w, g1.w)));
-    };
-    l0 = pairs(c0p[0], c0p[rp]);
-    l1 = pairs(c1p[0], c1p[rp]);
-  } else {
-    float4 A0 = make_float4(0.f, 0.f, 0.f, 0.f), B0 = A0, A1 = A0, B1 = A0;
-    int c = 0;
-    if (nch & 1) {
-      const float4 g = G4(0);
-      A0 = fma4(c0p[0], g, A0);
-      A1 = fma4(c1p[0], g, A1);
-      c = 1;
-    }
-    for (; c < nch; c += 2) {
-      const float4 ga = G4(4 * c), gb = G4(4 * c + 4);
-      A0 = fma4(c0p[c * rp], ga, A0);
-      A1 = fma4(c1p[c * rp], ga, A1);
-      B0 = fma4(c0p[(c + 1) * rp], gb, B0);
-      B1 = fma4(c1p[(c + 1) * rp], gb, B1);
-    }
-    l0 = make_float4(__fadd_rn(A0.x, B0.x), __fadd_rn(A0.y, B0.y), __fadd_rn(A0.z, B0.z), __fadd_rn(A0.w, B0.w));
-    l1 = make_float4(__fadd_rn(A1.x, B1.x), __fadd_rn(A1.y, B1.y), __fadd_rn(A1.z, B1.z), __fadd_rn(A1.w, B1.w));
-  }
-  float v0 = __fadd_rn(__fadd_rn(l0.x, l0.y), __fadd_rn(l0.z, l0.w));
-  float v1 = __fadd_rn(__fadd_rn(l1.x, l1.y), __fadd_rn(l1.z, l1.w));
-  const float* tl = it + (int64_t)m * rp;
-  if (T == 1) {
-    const float g = G(m);
-    v0 = __fmaf_rn(tl[r0], g, v0);
-    v1 = __fmaf_rn(tl[r1], g, v1);
-  } else if (T >= 2) {
-    const float ga = G(m + 1), gb = G(m);
-    float t0 = __fmaf_rn(tl[r0], gb, __fmul_rn(tl[rp + r0], ga));
-    float t1 = __fmaf_rn(tl[r1], gb, __fmul_rn(tl[rp + r1], ga));
-    if (T == 3) {
-      const float gc = G(m + 2);
-      t0 = __fmaf_rn(tl[2 * rp + r0], gc, t0);
-      t1 = __fmaf_rn(tl[2 * rp + r1], gc, t1);
-    }
-    v0 = __fadd_rn(v0, t0);
-    v1 = __fadd_rn(v1, t1);
-  }
-  return make_float2(v0, v1);
+// the same row of an item stored in chunk layout (chunk_off) at element
+// offsets L4(o) (16-byte vector) / L1(o)
+template <typename LD4, typename LD1, typename GF>
+__device__ __forceinline__ float chain_item_chunked(LD4 L4, LD1 L1, GF G, int n, int rp, int p, int kind) {
+  auto X4 = [&](int c) { return L4(4 * (c * rp + p)); };
+  auto E = [&](int k) {
+    if (chain_shaped(n)) return L1(k * rp + p);
+    const int m = n & ~3;
+    return k < m ? L1(4 * ((k >> 2) * rp + p) + (k & 3)) : L1(m * rp + (k - m) * rp + p);
+  };
+  return chain_item(X4, E, G, n, kind);
 }
 
-// chain threads u = 0 .. nthr-1 (slot u / rp, row u % rp); items j0 .. nrun-1
-// of the part (meta in shared memory, the part's blob at `part`); buf: two
-// kChainWin-byte staging buffers, filled by bulk copies (thread 0 issues one
-// per window; mb: their two mbarriers); wq: 6 ints of shared memory for the
-// window bounds thread 0 keeps one window ahead.  Returns this thread's row sum.
-__device__ __forceinline__ double chain_windows(const int32_t* meta, const uint32_t* kbits, int j0, int nrun,
-                                                const float* part, const double* gs, int rp, int u, int nthr,
-                                                float* buf, int* wq, uint64_t* mb, double& acc1) {
-#if HMX_CHAIN_ROWS == 2
-  const int half = rp >> 1;  // two rows per thread: p and p + half
-  const int K = nthr / half;
-  const int slot = u / half, p = u - slot * half, p1 = p + half;
-#else
-  const int K = nthr / rp;
-  const int slot = u / rp, p = u - slot * rp;
-#endif
-  const bool act = slot < K;
-  const int wmax = kChainWin / (4 * rp);  // columns per window
+// Four rows of a column-major item at once, every row in the 16-row kernel
+// (n < 8) or in the 16/8/4-row kernels (n >= 8): chain_item's order per row,
+// the source values shared.  C(k): column k of the four rows.
+__device__ __forceinline__ float4 fmas4(float4 a, float g, float4 c) {
+  return make_float4(__fmaf_rn(a.x, g, c.x), __fmaf_rn(a.y, g, c.y), __fmaf_rn(a.z, g, c.z), __fmaf_rn(a.w, g, c.w));
+}
+__device__ __forceinline__ float4 muls4(float4 a, float g) {
+  return make_float4(__fmul_rn(a.x, g), __fmul_rn(a.y, g), __fmul_rn(a.z, g), __fmul_rn(a.w, g));
+}
+template <typename CF, typename GF>
+__device__ __forceinline__ float4 chain_quad(CF C, GF G, int n) {
+  const float4 zero = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (n == 1) return muls4(C(0), G(0));
+  if (n <= 7 && n != 4) {  // one forward FMA chain per row
+    float4 v = zero;
+    for (int k = 0; k < n; ++k) v = fmas4(C(k), G(k), v);
+    return v;
+  }
+  if (n == 8) {  // l_j = a_2j g_2j + a_2j+1 g_2j+1, then (l0 + l1) + (l2 + l3)
+    float4 l[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) l[j] = add4(muls4(C(2 * j), G(2 * j)), muls4(C(2 * j + 1), G(2 * j + 1)));
+    return add4(add4(l[0], l[1]), add4(l[2], l[3]));
+  }
+  const int nch = n >> 2, T = n & 3, m = 4 * nch;
+  // A[j], B[j]: lane j of the row accumulators (column 4c + j), the four rows side by side
+  float4 A[4] = {zero, zero, zero, zero}, B[4] = {zero, zero, zero, zero};
+  int c = 0;
+  if (nch & 1) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) A[j] = fmas4(C(j), G(j), A[j]);
+    c = 1;
+  }
+  for (; c < nch; c += 2) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) A[j] = fmas4(C(4 * c + j), G(4 * c + j), A[j]);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) B[j] = fmas4(C(4 * c + 4 + j), G(4 * c + 4 + j), B[j]);
+  }
+  float4 v = add4(add4(add4(A[0], B[0]), add4(A[1], B[1])), add4(add4(A[2], B[2]), add4(A[3], B[3])));
+  if (T == 1) {
+    v = fmas4(C(m), G(m), v);
+  } else if (T >= 2) {
+    float4 tv = muls4(C(m + 1), G(m + 1));
+    tv = fmas4(C(m), G(m), tv);
+    if (T == 3) tv = fmas4(C(m + 2), G(m + 2), tv);
+    v = add4(v, tv);
+  }
+  return v;
+}
+
+// One chain warp's private stream through its shared-memory ring.
+struct ChainRing {
+  const float* src;  // the group's first element in the blob
+  float* ring;       // kRingStages windows of kRingWin bytes
+  uint32_t ring_s;   // ... its shared-space address
+  uint32_t mb_s;     // shared-space address of the kRingStages mbarriers (8 bytes each)
+  int len;           // stream bytes
+  int nwin;
+  int wl = 0;        // windows waited for
+  int wf = 0;        // windows consumed (their slots refilled)
+
+  // (lane 0) copy window w of the stream into its slot
+  __device__ __forceinline__ void issue(int w) const {
+    const int off = w * kRingWin;
+    const int bytes = min(kRingWin, len - off);
+    const uint32_t slot = (uint32_t)w & (kRingStages - 1);
+    const uint32_t bar = mb_s + 8 * slot;
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // the slot's last generic reads
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     ring_s + slot * kRingWin),
+                 "l"(src + (off >> 2)), "r"(bytes), "r"(bar)
+                 : "memory");
+  }
+  __device__ __forceinline__ void start(int lane) {
+    nwin = (len + kRingWin - 1) / kRingWin;
+    if (lane == 0) {
+      for (int s = 0; s < kRingStages; ++s)
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mb_s + 8 * s) : "memory");
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      for (int w = 0; w < min(kRingStages, nwin); ++w) issue(w);
+    }
+    __syncwarp();
+  }
+  // the stream's first `need` bytes have landed
+  __device__ __forceinline__ void ensure(int need) {
+    while (wl * kRingWin < need) {
+      const uint32_t bar = mb_s + 8 * ((uint32_t)wl & (kRingStages - 1));
+      const uint32_t parity = ((uint32_t)wl / kRingStages) & 1u;
+      asm volatile(
+          "{\n .reg .pred P1;\n WAIT:\n mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n @P1 bra DONE;\n bra WAIT;\n "
+          "DONE:\n }" ::"r"(bar),
+          "r"(parity)
+          : "memory");
+      ++wl;
+    }
+  }
+  // the warp is done with the stream's first `done` bytes: refill the freed slots
+  __device__ __forceinline__ void release(int done, int lane) {
+    while ((wf + 1) * kRingWin <= done) {
+      __syncwarp();
+      if (lane == 0 && wf + kRingStages < nwin) issue(wf + kRingStages);
+      ++wf;
+    }
+  }
+};
+
+// chain warp `lane`s: items jb .. je-1 of the part (meta / kbits in shared
+// memory; widest first) are the warp's group, columns [g0, ..) of the part,
+// already being streamed by R (started before the gather).  Adds the widened
+// item values of every row into racc[row] (FP64; zeroed by the caller).
+//
+// Short items (column-major): the warp's lanes form 32 / (rp / 4) slots of
+// rp / 4 lanes; a pass gives each slot one of the next items (as many as sit
+// in the ring together), each lane four rows of its item (chain_quad: one
+// 16-byte load and one source value per column for four rows).  Long items
+// (chunk layout) are streamed alone, chunk pair by chunk pair, rows lane and
+// lane + 32 per thread.
+__device__ __forceinline__ void chain_stream(ChainRing& R, const int32_t* meta, const uint32_t* kbits, int jb, int je,
+                                             int g0, const double* gs, int rp, int lane, double* racc) {
+  constexpr int mask = kRingBytes / 4 - 1;  // ring elements - 1
+  const float* ring = R.ring;
+  auto R4 = [&](int o) { return *reinterpret_cast<const float4*>(ring + (o & mask)); };
+  auto R1 = [&](int o) { return ring[o & mask]; };
   auto col0 = [&](int j) { return meta[j] >> kMetaW; };
   auto width = [&](int j) { return meta[j] & ((1 << kMetaW) - 1); };
-  // window starting at item j: [j, end) of <= wmax columns, or one oversize item
-  auto wend = [&](int j) {
-    if (j >= nrun) return j;
-    const int cs = col0(j);
-    int e = j + 1;
-    if (width(j) > wmax) return e;
-    while (e < nrun && col0(e) + width(e) - cs <= wmax) ++e;
-    return e;
-  };
-  // (thread 0) copy window [j, e) into buffer b; an oversize item (read from
-  // global memory) completes the buffer's phase with no bytes
-  auto stage = [&](int j, int e, int b) {
-    if (j >= nrun) return;
-    uint32_t bytes = 0;
-    const float* src = part;
-    if (width(j) <= wmax) {
-      const int cs = col0(j), ce = col0(e - 1) + width(e - 1);
-      bytes = (uint32_t)((ce - cs) * rp * 4);
-      src = part + (int64_t)cs * rp;
-    }
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // the buffer's last generic reads
-    bulk_to_smem(buf + b * (kChainWin / 4), src, bytes, mb + b);
-  };
-  // window bounds: a ring of three (start, end) pairs in wq
-  if (u == 0) {
-    mbar_init(mb);
-    mbar_init(mb + 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    const int e0 = wend(j0), e1 = wend(e0);
-    wq[0] = j0, wq[1] = e0, wq[2] = e0, wq[3] = e1;
-    stage(j0, e0, 0);
-  }
-  chain_bar(nthr);
-  double acc = 0.0;
-  for (int w = 0;; ++w) {
-    const int r = w % 3;
-    const int j = wq[2 * r], e = wq[2 * r + 1];
-    if (j >= nrun) break;
-    if (u == 0) {  // the next window in flight while this one is reduced; bounds of the one after
-      const int r1 = (w + 1) % 3, r2 = (w + 2) % 3;
-      const int jn = wq[2 * r1], en = wq[2 * r1 + 1];
-      stage(jn, en, (w + 1) & 1);
-      wq[2 * r2] = en;
-      wq[2 * r2 + 1] = wend(en);
-    }
-    mbar_wait(mb + (w & 1), (uint32_t)(w >> 1) & 1u);  // window [j, e) has landed
-    if (act) {
-      if (width(j) > wmax) {  // oversize item: straight from global memory
-        if (slot == 0) {
-          const int c0 = col0(j);
-          auto G = [&](int k) { return __int_as_float(__double2loint(gs[c0 + k])); };
-          acc += (double)chain_item<true>(part + (int64_t)c0 * rp, G, width(j), rp, p, chain_row_kind(kbits[j], p));
-#if HMX_CHAIN_ROWS == 2
-          acc1 += (double)chain_item<true>(part + (int64_t)c0 * rp, G, width(j), rp, p1, chain_row_kind(kbits[j], p1));
-#endif
+  const int tpg = rp >> 2;                  // lanes per slot (four rows each)
+  const int nslot = min(32 / tpg, 8);
+  const int slot = lane / tpg, t = lane - slot * tpg;
+  double b0 = 0.0, b1 = 0.0, b2 = 0.0, b3 = 0.0;  // rows 4t .. 4t+3 of this lane's items
+  int j = jb;
+  while (j < je) {
+    const int c0j = col0(j), nj = width(j);
+    const int ioj = (c0j - g0) * rp;  // stream element offset of item j
+    if (chain_item_long(nj, rp)) {
+      // ---- long item (chunk layout), alone: rows lane and lane + 32, chunk pair by chunk pair
+      const int n = nj, io = ioj, iend = (ioj + nj * rp) * 4;
+      const uint32_t kb = kbits[j];
+      const double* gj = gs + c0j;
+      auto G = [&](int k) { return __int_as_float(__double2loint(gj[k])); };
+      auto G4 = [&](int c) { return make_float4(G(c), G(c + 1), G(c + 2), G(c + 3)); };
+      const bool two = rp > 32;
+      const int cs = 4 * rp;  // elements per chunk
+      const int nch = n >> 2, T = n & 3;
+      const int fo = io + 4 * lane;  // chunk 0 of row `lane`
+      float4 A0 = make_float4(0.f, 0.f, 0.f, 0.f), B0 = A0, A1 = A0, B1 = A0;
+      const int k0 = chain_row_kind(kb, lane), k1 = chain_row_kind(kb, lane + 32);
+      const bool odd = nch & 1;
+      auto step = [&](float4& A, float4& B, const float4& x, const float4& g, int kind, int cc) {
+        const bool inA = kind == 2 || (odd ? (cc == 0 || (cc & 1)) : !(cc & 1));
+        const float4 X = inA ? A : B;
+        const float4 Y = kind >= 4 ? fma4(x, g, X) : mad4(x, g, X);
+        if (inA) A = Y;
+        else B = Y;
+      };
+      int c = 0;
+      if ((int)((kb >> 14) & 127) >= rp) {
+        // the common case: every row of the segment in the 16/8/4-row kernels
+        if (odd) {
+          R.ensure((io + cs) * 4);
+          const float4 g = G4(0);
+          A0 = fma4(R4(fo), g, A0);
+          if (two) A1 = fma4(R4(fo + 128), g, A1);
+          c = 1;
+        }
+        for (; c < nch; c += 2) {
+          R.release((io + c * cs) * 4, lane);
+          R.ensure((io + (c + 2) * cs) * 4);
+          const float4 ga = G4(4 * c), gb = G4(4 * c + 4);
+          const int q = fo + c * cs;
+          A0 = fma4(R4(q), ga, A0);
+          B0 = fma4(R4(q + cs), gb, B0);
+          if (two) {
+            A1 = fma4(R4(q + 128), ga, A1);
+            B1 = fma4(R4(q + cs + 128), gb, B1);
+          }
         }
       } else {
-        const float* base = buf + (w & 1) * (kChainWin / 4);
-        const int cs = col0(j);
-        for (int i = j + slot; i < e; i += K) {
-          const int c0 = col0(i);
-          auto G = [&](int k) { return __int_as_float(__double2loint(gs[c0 + k])); };
-          const float* it = base + (c0 - cs) * rp;
-          // the common case first: every row of the segment in SGEMV's
-          // 16-row kernel (n < 8), or in the 16/8/4-row kernels (n >= 8)
-          const uint32_t kb = kbits[i];
-          const int wi = width(i);
-#if HMX_CHAIN_ROWS == 2
-          if ((int)((kb >> (wi < 8 ? 0 : 14)) & 127) >= rp) {
-            const float2 v = chain_item2(it, G, wi, rp, p, p1);
-            acc += (double)v.x;
-            acc1 += (double)v.y;
-          } else {
-            acc += (double)chain_item<false>(it, G, wi, rp, p, chain_row_kind(kb, p));
-            acc1 += (double)chain_item<false>(it, G, wi, rp, p1, chain_row_kind(kb, p1));
-          }
-#else
-          if ((int)((kb >> (wi < 8 ? 0 : 14)) & 127) >= rp) acc += (double)chain_item<false>(it, G, wi, rp, p, 16);
-          else acc += (double)chain_item<false>(it, G, wi, rp, p, chain_row_kind(kb, p));
-#endif
+        // rows in the 2- / 1-row remainder kernels (row counts not a multiple of 4)
+        for (; c < nch; ++c) {
+          R.release((io + c * cs) * 4, lane);
+          R.ensure((io + (c + 1) * cs) * 4);
+          const float4 g = G4(4 * c);
+          step(A0, B0, R4(fo + c * cs), g, k0, c);
+          if (two) step(A1, B1, R4(fo + c * cs + 128), g, k1, c);
         }
       }
+      float v0 = hsum4(add4(A0, B0)), v1 = hsum4(add4(A1, B1));
+      if (T > 0) {
+        const int m = 4 * nch, tl = io + m * rp + lane;
+        R.release((io + m * rp) * 4, lane);
+        R.ensure(iend);
+        if (T == 1) {
+          const float g = G(m);
+          v0 = __fmaf_rn(R1(tl), g, v0);
+          v1 = __fmaf_rn(R1(tl + 32), g, v1);
+        } else {
+          const float ga = G(m + 1), gb = G(m);
+          float t0 = __fmaf_rn(R1(tl), gb, __fmul_rn(R1(tl + rp), ga));
+          float t1 = __fmaf_rn(R1(tl + 32), gb, __fmul_rn(R1(tl + rp + 32), ga));
+          if (T == 3) {
+            const float gc = G(m + 2);
+            t0 = __fmaf_rn(R1(tl + 2 * rp), gc, t0);
+            t1 = __fmaf_rn(R1(tl + 2 * rp + 32), gc, t1);
+          }
+          v0 = __fadd_rn(v0, t0);
+          v1 = __fadd_rn(v1, t1);
+        }
+      }
+      R.release(iend, lane);
+      if (lane < rp) racc[lane] += (double)v0;
+      if (lane + 32 < rp) racc[lane + 32] += (double)v1;
+      ++j;
+      continue;
     }
-    chain_bar(nthr);  // buffer w & 1 is free again; wq holds the next bounds
+    // ---- a pass: the next k <= nslot short items that sit in the ring together
+    int k = 1, pend = ioj + nj * rp;  // stream elements up to the pass's end
+    while (k < nslot && j + k < je) {
+      const int e = (col0(j + k) - g0 + width(j + k)) * rp;
+      if ((e - ioj) * 4 > kChainWhole) break;  // (also stops at a long item)
+      pend = e;
+      ++k;
+    }
+    R.ensure(pend * 4);
+    if (slot < k) {
+      const int ji = j + slot;
+      const int c0 = col0(ji), n = width(ji);
+      const uint32_t kb = kbits[ji];
+      const int io = (c0 - g0) * rp + 4 * t;  // rows 4t .. 4t+3 of column 0
+      const double* gj = gs + c0;
+      auto G = [&](int q) { return __int_as_float(__double2loint(gj[q])); };
+      float4 v;
+      if ((int)((kb >> (n < 8 ? 0 : 14)) & 127) >= rp) {
+        // the common case: every row of the segment in SGEMV's 16-row kernel
+        // (n < 8), or in the 16/8/4-row kernels (n >= 8)
+        v = chain_quad([&](int q) { return R4(io + q * rp); }, G, n);
+      } else {
+        float r[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          auto E = [&](int q) { return R1(io + q * rp + i); };
+          auto X4 = [&](int c) { return make_float4(E(4 * c), E(4 * c + 1), E(4 * c + 2), E(4 * c + 3)); };
+          r[i] = chain_item(X4, E, G, n, chain_row_kind(kb, 4 * t + i));
+        }
+        v = make_float4(r[0], r[1], r[2], r[3]);
+      }
+      b0 += (double)v.x;
+      b1 += (double)v.y;
+      b2 += (double)v.z;
+      b3 += (double)v.w;
+    }
+    j += k;
+    R.release(pend * 4, lane);
   }
-  return acc;
+  // the slots' sums into racc, slot by slot (fixed order)
+  for (int sl = 0; sl < nslot; ++sl) {
+    __syncwarp();
+    if (slot == sl) {
+      racc[4 * t] += b0;
+      racc[4 * t + 1] += b1;
+      racc[4 * t + 2] += b2;
+      racc[4 * t + 3] += b3;
+    }
+  }
+  __syncwarp();
 }
 
 // Stage 1 of m1-single: z = Vt32 . x32 accumulated in FP32 (reference
@@ -491,7 +579,7 @@ __global__ void __launch_bounds__(kS1ExactRows) s1_exact_kernel(DevPlan P, const
   if (t >= sg.R) {
     // (idle row: no loads; joins the barrier below)
   } else if (n <= 8) {  // short rows (chain-shaped, n = 4, n = 8): the per-kernel rules
-    y = chain_item<true>(it, G, n, rp, t, kind);
+    y = chain_item_chunked([&](int o) { return ld_chunk(it + o); }, [&](int o) { return ld_one(it + o); }, G, n, rp, t, kind);
   } else {
     // this CTA's 4096-column block: the A/B lane tree (kinds 16/8/4: FMA
     // chains; 1: multiply then add; 2: one accumulator, multiply then add),
@@ -579,10 +667,10 @@ __global__ void __launch_bounds__(NT, DEEP ? 3 : (OUT == OUT_Y && F32MODE != F32
   __shared__ double red64[2 * NT];
   __shared__ double red32[4 * NT];
   __shared__ double wred[2][NT / 32];
-  // chain-item staging buffers (stage-2 FP32 kernels: 2 x kChainWin bytes of dynamic shared memory)
-  extern __shared__ __align__(16) float chain_buf[];
-  __shared__ int chain_wq[6];  // chain-window bounds (chain_windows)
-  __shared__ uint64_t chain_mb[2];  // their bulk copies' mbarriers
+  // the chain warps' rings (stage-2 FP32 kernels; dynamic: ring bytes x P.chain_warps) and their mbarriers
+  extern __shared__ __align__(128) float chain_buf[];
+  __shared__ uint64_t chain_mb[NT / 32][kRingStages];
+  __shared__ double racc[EXACT ? NT / 32 : 1][kSegRows];  // chain warps: their rows' FP64 sums
   __shared__ unsigned ticket;
 
   if (out.skip != nullptr && *out.skip != 0) return;  // guarded launch (solver)
@@ -667,7 +755,8 @@ __global__ void __launch_bounds__(NT, DEEP ? 3 : (OUT == OUT_Y && F32MODE != F32
   // ONE row per thread, each item evaluated in SGEMV's own order (chain_items).
   // wbc (plan: sg.chunk) is warp-aligned, so no warp runs both loops.
   bool chain_thr = false;
-  int pc = 0;
+  int pc = 0, cg0 = 0;
+  ChainRing cring;
   if constexpr (F32MODE == F32_MIXED && OUT == OUT_Y) {
     // (HMX_PLAN_FP32_CHAIN plans: one FP32 FMA chain per (row, item), 4 rows
     // per thread on both sides of the warp-aligned split at wb = sg.chunk)
@@ -688,16 +777,25 @@ __global__ void __launch_bounds__(NT, DEEP ? 3 : (OUT == OUT_Y && F32MODE != F32
   if constexpr (EXACT && F32MODE != F32_ALL64 && OUT == OUT_Y) {
     if (sg.gtab >= 0) {
       const int wbc = F32MODE == F32_ALL32 ? 0 : sg.chunk;
-      const int ga = wbc / tpg32, gb = (NT - wbc) / (rp32 / HMX_CHAIN_ROWS);
+      const int ga = wbc / tpg32, gb = (NT - wbc) / 32;  // one chain group per warp
       g32 = ga + gb;
       if (tid < wbc) {
         if (q32 >= ga) q32 = g32;  // idle
       } else {
-        const int u = tid - wbc;
-        const int qb = u / (rp32 / HMX_CHAIN_ROWS);
-        pc = u - qb * (rp32 / HMX_CHAIN_ROWS);
-        q32 = qb < gb ? ga + qb : g32;
+        const int qb = (tid - wbc) >> 5;
+        pc = tid & 31;
+        q32 = ga + qb;
         chain_thr = true;
+        // start streaming the group's items now (payload only: before the wait on stage 1)
+        cring.ring = chain_buf + (size_t)qb * (kRingBytes / 4);
+        cring.ring_s = smem_addr(cring.ring);
+        cring.mb_s = smem_addr(chain_mb[qb]);
+        cg0 = P.gtab[sg.gtab + q32];
+        cring.src = P.blob32 + sg.off32 + (int64_t)cg0 * rp32;
+        cring.len = (P.gtab[sg.gtab + q32 + 1] - cg0) * rp32 * 4;
+        cring.start(pc);
+        racc[qb][pc] = 0.0;
+        racc[qb][pc + 32] = 0.0;
       }
     }
   }
@@ -864,11 +962,22 @@ __global__ void __launch_bounds__(NT, DEEP ? 3 : (OUT == OUT_Y && F32MODE != F32
         kbits[j] = (uint32_t)r.flags >> kRunKindShift;
       }
       chain_bar(NT - wbc);
-      int j0 = 0;  // the first chain item (they follow the widened ones)
-      const int c32c = P.gtab[sg.gtab + g32 + 1];
-      while (j0 < sg.nrun32 && (sidx[j0] >> kMetaW) < c32c) ++j0;
-      bc = chain_windows(sidx, kbits, j0, sg.nrun32, P.blob32 + sg.off32, gs, rp32, tid - wbc, NT - wbc, chain_buf,
-                         chain_wq, chain_mb, bc1);
+      // this warp's items: columns [cg0, cg1)
+      const int cg1 = P.gtab[sg.gtab + q32 + 1];
+      auto first_at = [&](int col) {  // first item starting at or after column `col`
+        int lo = 0, hi = sg.nrun32;
+        while (lo < hi) {
+          const int mid = (lo + hi) >> 1;
+          if ((sidx[mid] >> kMetaW) < col) lo = mid + 1;
+          else hi = mid;
+        }
+        return lo;
+      };
+      const int jb = first_at(cg0), je = first_at(cg1);
+      double* ra = racc[(tid - wbc) >> 5];
+      chain_stream(cring, sidx, kbits, jb, je, cg0, gs, rp32, pc, ra);
+      bc = ra[pc];
+      bc1 = ra[pc + 32];
     }
   }
 
@@ -876,8 +985,8 @@ __global__ void __launch_bounds__(NT, DEEP ? 3 : (OUT == OUT_Y && F32MODE != F32
   __syncthreads();
   if (sg.W32 > 0 && q32 < g32) {
     if (chain_thr) {
-      red32[q32 * rp32 + pc] = bc;
-      if (HMX_CHAIN_ROWS == 2) red32[q32 * rp32 + pc + (rp32 >> 1)] = bc1;
+      if (pc < rp32) red32[q32 * rp32 + pc] = bc;
+      if (pc + 32 < rp32) red32[q32 * rp32 + pc + 32] = bc1;
     } else {
 #pragma unroll
       for (int i = 0; i < 4; ++i) red32[q32 * rp32 + 4 * p32 + i] = b[i];
@@ -1049,9 +1158,10 @@ __global__ void probe_kernel(DevPlan P, const double* __restrict__ x, unsigned l
 // dynamic shared memory of a seg_kernel instantiation: the chain-item staging
 // buffers of the stage-2 FP32 kernels
 template <int M, int O, bool EXACT>
-constexpr size_t chain_smem() {
-  return (EXACT && O == OUT_Y && M != F32_ALL64) ? 2 * (size_t)kChainWin : 0;
+static size_t chain_smem(const DevPlan& P) {
+  return (EXACT && O == OUT_Y && M != F32_ALL64) ? (size_t)P.chain_warps * kRingBytes : 0;
 }
+constexpr int kChainSmemMax = (kSegThreads / 32) * kRingBytes;
 
 template <int M, int O, int NT = kSegThreads, bool DEEP = false, bool EXACT = false, int XMINB = HMX_EXACT_MINB>
 static cudaError_t launch_seg(const DevPlan& P, const Seg* segs, int nseg, const double* x,
@@ -1059,7 +1169,7 @@ static cudaError_t launch_seg(const DevPlan& P, const Seg* segs, int nseg, const
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)nseg);
   cfg.blockDim = dim3(NT);
-  cfg.dynamicSmemBytes = chain_smem<M, O, EXACT>();
+  cfg.dynamicSmemBytes = chain_smem<M, O, EXACT>(P);
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -1101,8 +1211,7 @@ cudaError_t launch_stage2(const DevPlan& P, const double* x, const S2Out& out, c
                            : launch_seg<F32_ALL32, OUT_Y>(P, P.seg2, P.n_seg2, x, out, st, pdl);
     case F32_MIXED:
       if (!P.chain_exact) return launch_seg<F32_MIXED, OUT_Y>(P, P.seg2, P.n_seg2, x, out, st, pdl);
-      return P.pipe == P_M2S ? launch_seg<F32_MIXED, OUT_Y, kSegThreads, false, true, 3>(P, P.seg2, P.n_seg2, x, out, st, pdl)
-                             : launch_seg<F32_MIXED, OUT_Y, kSegThreads, false, true>(P, P.seg2, P.n_seg2, x, out, st, pdl);
+      return launch_seg<F32_MIXED, OUT_Y, kSegThreads, false, true>(P, P.seg2, P.n_seg2, x, out, st, pdl);
     default:
       return P.s2_deep ? launch_seg<F32_ALL64, OUT_Y, kSegThreads, true>(P, P.seg2, P.n_seg2, x, out, st, pdl)
                        : launch_seg<F32_ALL64, OUT_Y>(P, P.seg2, P.n_seg2, x, out, st, pdl);
@@ -1114,13 +1223,10 @@ cudaError_t launch_stage2(const DevPlan& P, const double* x, const S2Out& out, c
 cudaError_t configure_kernels() {
   cudaError_t e = cudaFuncSetAttribute(seg_kernel<F32_ALL32, OUT_Y, kSegThreads, false, true>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)chain_smem<F32_ALL32, OUT_Y, true>());
+                                       kChainSmemMax);
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(seg_kernel<F32_MIXED, OUT_Y, kSegThreads, false, true>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)chain_smem<F32_MIXED, OUT_Y, true>());
-  if (e == cudaSuccess)
-    e = cudaFuncSetAttribute(seg_kernel<F32_MIXED, OUT_Y, kSegThreads, false, true, 3>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)chain_smem<F32_MIXED, OUT_Y, true>());
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, kChainSmemMax);
   return e;
 }
 

@@ -424,6 +424,7 @@ int hmx::plan_create_impl(const hmx_matrix_desc* d, int device, const hmx_plan_o
     std::vector<int64_t> cuts;  // G + 1 column boundaries; empty: no group table
     int64_t c32 = 0;            // first chain column
     int64_t wb = 0;
+    int64_t gb = 0;             // chain groups
   };
   auto lpt = [](const std::vector<int64_t>& w, int64_t G, std::vector<int32_t>* owner) {
     std::vector<int32_t> order(w.size());
@@ -446,7 +447,7 @@ int hmx::plan_create_impl(const hmx_matrix_desc* d, int device, const hmx_plan_o
     if (W > kSegWMax) return fg;  // tiled part: no group table
     // widened groups: 4 rows per thread; chain groups: one row per thread
     const int64_t rp = round_up(R, 4), tpg = rp / 4, G = kSegThreads / tpg;
-    const int64_t tpc = chain_order ? tpg : rp / kChainRows, Gc = kSegThreads / tpc;  // threads per chain group
+    const int64_t tpc = chain_order ? tpg : kChainGroupThreads, Gc = kSegThreads / tpc;  // threads per chain group
     size_t nA = 0;
     while (nA < lst.size() && !item_acc32(lst[nA])) ++nA;
     int64_t colsA = 0;
@@ -460,7 +461,9 @@ int hmx::plan_create_impl(const hmx_matrix_desc* d, int device, const hmx_plan_o
       for (int64_t wb = 32; wb < kSegThreads; wb += 32) {
         const int64_t ga = wb / tpg, gb = (kSegThreads - wb) / tpc;
         if (ga < 1 || gb < 1) continue;
-        const double t = std::max(acc64_weight * (double)colsA / (double)ga, (double)lpt(wB, gb, nullptr));
+        // (SGEMV-order plans: a chain warp works on 32 / tpg items at a time, hmx_kernels.cu chain_stream)
+        const double chain_par = chain_order ? 1.0 : (double)std::min<int64_t>(32 / tpg, 8);
+        const double t = std::max(acc64_weight * (double)colsA / (double)ga, (double)lpt(wB, gb, nullptr) / chain_par);
         if (t < best) {
           best = t;
           fg.wb = wb;
@@ -477,6 +480,7 @@ int hmx::plan_create_impl(const hmx_matrix_desc* d, int device, const hmx_plan_o
     // when there are no chains)
     fg.cuts.push_back(0);
     for (int64_t q = 1; q <= gA; ++q) fg.cuts.push_back(colsA * q / gA);
+    fg.gb = wB.empty() ? 0 : gB;
     if (gB > 0) {
       std::vector<int32_t> owner;
       lpt(wB, gB, &owner);
@@ -484,16 +488,23 @@ int hmx::plan_create_impl(const hmx_matrix_desc* d, int device, const hmx_plan_o
       std::vector<int64_t> load((size_t)gB, 0);
       size_t k = nA;
       for (int64_t g = 0; g < gB; ++g) {
+        // a group's items widest first (SGEMV-order plans: neighbouring items
+        // of equal width share a pass of the chain warp without diverging)
+        std::vector<size_t> mine;
         for (size_t i = 0; i < chains.size(); ++i)
-          if (owner[i] == g) {
-            lst[k++] = chains[i];
-            load[(size_t)g] += wB[i];
-          }
+          if (owner[i] == g) mine.push_back(i);
+        if (!chain_order)
+          std::stable_sort(mine.begin(), mine.end(), [&](size_t a, size_t b) { return wB[a] > wB[b]; });
+        for (size_t i : mine) {
+          lst[k++] = chains[i];
+          load[(size_t)g] += wB[i];
+        }
         fg.cuts.push_back(fg.cuts.back() + load[(size_t)g]);
       }
     }
     return fg;
   };
+  int64_t chain_warps_max = 0;
   for (int64_t s = 0; s < nseg2; ++s) {
     Seg& sg = seg2[(size_t)s];
     sg.row0 = (int32_t)seg_start[(size_t)s];
@@ -503,6 +514,7 @@ int hmx::plan_create_impl(const hmx_matrix_desc* d, int device, const hmx_plan_o
     sg.nchunks = 1;
     sg.part_off = -1;
     const FP32Groups fg = plan_fp32_groups(items32[(size_t)s], sg.R);  // may reorder chain items
+    if (!chain_order) chain_warps_max = std::max<int64_t>(chain_warps_max, fg.gb);
     for (int part = 0; part < 2; ++part) {
       const auto& lst = part == 0 ? items64[(size_t)s] : items32[(size_t)s];
       int64_t col = 0;
@@ -525,7 +537,7 @@ int hmx::plan_create_impl(const hmx_matrix_desc* d, int device, const hmx_plan_o
           // the segment rows of each SGEMV row kernel (sgemv_row_kind of the
           // block's rows, as 7-bit segment-relative bounds)
           if ((r.flags & RUN_ACC32) && !fg.cuts.empty() && !chain_order) {
-            r.flags |= RUN_CHUNK;
+            if (chain_item_long(r.width, round_up(sg.R, 4))) r.flags |= RUN_CHUNK;
             const int64_t mb = t[1] - t[0], d0 = sg.row0 - t[0];  // block row of segment row 0
             const int64_t a16 = mb & ~int64_t(15), b8 = a16 + (mb & 8), c4 = b8 + (mb & 4);
             const int64_t c2 = c4 + ((mb & 3) >= 2 ? 2 : 0);
@@ -630,7 +642,7 @@ int hmx::plan_create_impl(const hmx_matrix_desc* d, int device, const hmx_plan_o
         src32 = true;
       }
       // chain items of group-table parts: SGEMV chunk layout (chunk_off)
-      const bool chunk = part == 1 && item_acc32(it) && sg.gtab >= 0 && !chain_order;
+      const bool chunk = part == 1 && item_acc32(it) && sg.gtab >= 0 && !chain_order && chain_item_long(w, rp);
       for (int64_t i = 0; i < sg.R; ++i) {
         const int64_t e0 = src_off + (r0 + i) * w;
         for (int64_t c = 0; c < w; ++c) {
@@ -767,7 +779,8 @@ int hmx::plan_create_impl(const hmx_matrix_desc* d, int device, const hmx_plan_o
         u.is32 = part;
         for (const ItemRef& it : lst)
           pit.push_back({it.block, it.cls, (int32_t)item_width(it),
-                         (part == 1 && item_acc32(it) && sg.gtab >= 0 && !chain_order) ? 1 : 0});
+                         (part == 1 && item_acc32(it) && sg.gtab >= 0 && !chain_order &&
+                          chain_item_long(item_width(it), u.rp)) ? 1 : 0});
         ps2.push_back(u);
       }
     }
@@ -860,6 +873,7 @@ int hmx::plan_create_impl(const hmx_matrix_desc* d, int device, const hmx_plan_o
   dp.s1_narrow = s1_narrow ? 1 : 0;
   dp.s1_exact = (pipe == P_M1S && !chain_order) ? 1 : 0;
   dp.chain_exact = chain_order ? 0 : 1;
+  dp.chain_warps = (int32_t)chain_warps_max;  // dynamic shared memory: one ring per chain warp
   {
     // deep FP64 pipeline when the FP64 part carries most of stage 2's bytes
     int64_t b64 = 0, b32 = 0;
