@@ -45,7 +45,7 @@ struct Seg {             // 64 bytes; one CTA
 };
 static_assert(sizeof(Seg) == 64, "Seg layout");
 
-// RUN_CHUNK: a stage-2 FP32-accumulated item in SGEMV chunk layout (below)
+// RUN_CHUNK: a stage-1 FP32-accumulated segment (m1-single) in SGEMV chunk layout (below)
 enum : int32_t { RUN_Z = 1, RUN_ROUND = 2, RUN_ACC32 = 4, RUN_CHUNK = 8 };
 // RUN_CHUNK items: bits 4..31 of Run.flags locate, within the segment, the
 // row classes OpenBLAS SGEMV-T computes the item's block in (it takes the
@@ -117,21 +117,6 @@ constexpr int kS1WMax = 1024;     // max columns per stage-1 segment chunk
 #endif
 constexpr int kS1ExactRows = HMX_S1X_ROWS;  // m1-single stage 1: rank rows per CTA (one thread each)
 constexpr int kSgemvBlock = 1024; // OpenBLAS SGEMV-T column blocking: 4096 columns = 1024 chunks
-constexpr int kChainGroupThreads = 32;  // stage 2: one warp per group of FP32-accumulated (chain) items
-// A chain warp streams its group's items through a ring in shared memory
-// (hmx_kernels.cu chain_stream): kRingStages windows, one bulk copy each.  An
-// item that fits the ring beside one window in flight is stored column-major
-// (rows contiguous, like every other item) and evaluated four rows per lane;
-// a longer one is stored in SGEMV chunk layout (chunk_off, RUN_CHUNK) and
-// streamed chunk pair by chunk pair, one or two rows per lane.
-#ifndef HMX_RING_LOG2
-#define HMX_RING_LOG2 13
-#endif
-constexpr int kRingStages = 4;
-constexpr int kRingBytes = 1 << HMX_RING_LOG2;      // ring of one chain warp
-constexpr int kRingWin = kRingBytes / kRingStages;  // window = one bulk copy
-constexpr int kChainWhole = kRingBytes - kRingWin;  // bytes the ring holds beside one window in flight
-__host__ __device__ __forceinline__ bool chain_item_long(int64_t n, int64_t rp) { return n * rp * 4 > kChainWhole; }
 
 // Device-visible plan (passed by value to kernels).
 struct DevPlan {

@@ -336,221 +336,197 @@ __device__ __forceinline__ float4 chain_quad(CF C, GF G, int n) {
   return v;
 }
 
-// One chain warp's private stream through its shared-memory ring.
-struct ChainRing {
-  const float* src;  // the group's first element in the blob
-  float* ring;       // kRingStages windows of kRingWin bytes
-  uint32_t ring_s;   // ... its shared-space address
-  uint32_t mb_s;     // shared-space address of the kRingStages mbarriers (8 bytes each)
-  int len;           // stream bytes
-  int nwin;
-  int wl = 0;        // windows waited for
-  int wf = 0;        // windows consumed (their slots refilled)
+// The generic-kind version of chain_quad for items wider than 8 columns: row
+// i of the four in SGEMV row kernel kind[i] (any of 16, 8, 4, 2, 1), chunk by
+// chunk.  C(k) / G(k) as in chain_quad; before(c) is called before chunk c
+// (and before the tail, c = nch) so the caller can stage the columns.
+template <typename CF, typename GF, typename BF>
+__device__ __forceinline__ float4 chain_quad_kinds(CF C, GF G, BF before, int n, const int* kind) {
+  const int nch = n >> 2, T = n & 3, m = 4 * nch;
+  const bool odd = nch & 1;
+  float A[4][4], B[4][4];  // [row][accumulator lane]
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) A[i][j] = B[i][j] = 0.f;
+  for (int c = 0; c < nch; ++c) {
+    before(c);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float4 x4 = C(4 * c + j);
+      const float g = G(4 * c + j);
+      const float x[4] = {x4.x, x4.y, x4.z, x4.w};
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const bool inA = kind[i] == 2 || (odd ? (c == 0 || (c & 1)) : !(c & 1));
+        const float X = inA ? A[i][j] : B[i][j];
+        const float Y = kind[i] >= 4 ? __fmaf_rn(x[i], g, X) : __fadd_rn(X, __fmul_rn(x[i], g));
+        if (inA) A[i][j] = Y;
+        else B[i][j] = Y;
+      }
+    }
+  }
+  float v[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+    v[i] = __fadd_rn(__fadd_rn(__fadd_rn(A[i][0], B[i][0]), __fadd_rn(A[i][1], B[i][1])),
+                     __fadd_rn(__fadd_rn(A[i][2], B[i][2]), __fadd_rn(A[i][3], B[i][3])));
+  if (T > 0) {
+    before(nch);
+    const float4 c0 = C(m), c1 = T >= 2 ? C(m + 1) : c0, c2 = T == 3 ? C(m + 2) : c0;
+    const float x0[4] = {c0.x, c0.y, c0.z, c0.w}, x1[4] = {c1.x, c1.y, c1.z, c1.w}, x2[4] = {c2.x, c2.y, c2.z, c2.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      if (T == 1) {
+        v[i] = __fmaf_rn(x0[i], G(m), v[i]);
+      } else {
+        float tv = __fmul_rn(x1[i], G(m + 1));
+        tv = __fmaf_rn(x0[i], G(m), tv);
+        if (T == 3) tv = __fmaf_rn(x2[i], G(m + 2), tv);
+        v[i] = __fadd_rn(v[i], tv);
+      }
+    }
+  }
+  return make_float4(v[0], v[1], v[2], v[3]);
+}
 
-  // (lane 0) copy window w of the stream into its slot
-  __device__ __forceinline__ void issue(int w) const {
-    const int off = w * kRingWin;
-    const int bytes = min(kRingWin, len - off);
-    const uint32_t slot = (uint32_t)w & (kRingStages - 1);
-    const uint32_t bar = mb_s + 8 * slot;
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // the slot's last generic reads
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                     ring_s + slot * kRingWin),
-                 "l"(src + (off >> 2)), "r"(bytes), "r"(bar)
-                 : "memory");
-  }
-  __device__ __forceinline__ void start(int lane) {
-    nwin = (len + kRingWin - 1) / kRingWin;
-    if (lane == 0) {
-      for (int s = 0; s < kRingStages; ++s)
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mb_s + 8 * s) : "memory");
-      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-      for (int w = 0; w < min(kRingStages, nwin); ++w) issue(w);
-    }
-    __syncwarp();
-  }
-  // the stream's first `need` bytes have landed
-  __device__ __forceinline__ void ensure(int need) {
-    while (wl * kRingWin < need) {
-      const uint32_t bar = mb_s + 8 * ((uint32_t)wl & (kRingStages - 1));
-      const uint32_t parity = ((uint32_t)wl / kRingStages) & 1u;
-      asm volatile(
-          "{\n .reg .pred P1;\n WAIT:\n mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n @P1 bra DONE;\n bra WAIT;\n "
-          "DONE:\n }" ::"r"(bar),
-          "r"(parity)
-          : "memory");
-      ++wl;
+// A chain lane's private FIFO of stream columns in shared memory.  The lanes
+// of one slot (rp / 4 lanes, four rows each) stream the columns of their
+// group -- contiguous in the blob -- with 16-byte cp.async copies, four
+// columns per commit group, into kFifoCols entries addressed by stream column
+// mod kFifoCols; every lane reads back only what it copied itself, so nothing
+// is synchronised between lanes, and up to 12 columns per lane are in flight
+// while earlier ones are reduced.
+constexpr int kFifoCols = 16;
+constexpr int kFifoBytes = kFifoCols * 512;  // per chain warp: 16 bytes x 32 lanes per entry
+struct ChainFifo {
+  const float* src;    // this lane's four rows of stream column 0
+  const float* fifo;   // this lane's 16 bytes of entry 0 (entry e: + 128 e floats)
+  uint32_t fifo_s;     // ... its shared-space address
+  int rp;
+  int ncols;           // stream columns
+  int issued = 0;      // columns copied or in flight (a multiple of 4)
+  int landed = 0;      // columns known to have landed (a multiple of 4)
+
+  // copy ahead while the entries are free: columns < lo are consumed
+  __device__ __forceinline__ void refill(int lo) {
+    const int top = min((ncols + 3) & ~3, (lo & ~3) + kFifoCols);
+    while (issued < top) {
+      const uint32_t dst = fifo_s + (uint32_t)(issued & (kFifoCols - 1)) * 512u;
+      const float* g = src + (int64_t)issued * rp;
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (issued + u < ncols)
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst + 512u * u), "l"(g + (int64_t)u * rp) : "memory");
+      asm volatile("cp.async.commit_group;\n" ::: "memory");
+      issued += 4;
     }
   }
-  // the warp is done with the stream's first `done` bytes: refill the freed slots
-  __device__ __forceinline__ void release(int done, int lane) {
-    while ((wf + 1) * kRingWin <= done) {
-      __syncwarp();
-      if (lane == 0 && wf + kRingStages < nwin) issue(wf + kRingStages);
-      ++wf;
+  // columns < x have landed (x - lo <= 10 after refill(lo))
+  __device__ __forceinline__ void need(int x) {
+    if (landed >= x) return;
+    const int b = (x + 3) & ~3;
+    switch ((issued - b) >> 2) {
+      case 0: asm volatile("cp.async.wait_group 0;\n" ::: "memory"); break;
+      case 1: asm volatile("cp.async.wait_group 1;\n" ::: "memory"); break;
+      case 2: asm volatile("cp.async.wait_group 2;\n" ::: "memory"); break;
+      default: asm volatile("cp.async.wait_group 3;\n" ::: "memory"); break;
     }
+    landed = b;
+  }
+  // stream column g of this lane's four rows
+  __device__ __forceinline__ float4 col(int g) const {
+    return *reinterpret_cast<const float4*>(fifo + (g & (kFifoCols - 1)) * 128);
   }
 };
 
-// chain warp `lane`s: items jb .. je-1 of the part (meta / kbits in shared
-// memory; widest first) are the warp's group, columns [g0, ..) of the part,
-// already being streamed by R (started before the gather).  Adds the widened
-// item values of every row into racc[row] (FP64; zeroed by the caller).
-//
-// Short items (column-major): the warp's lanes form 32 / (rp / 4) slots of
-// rp / 4 lanes; a pass gives each slot one of the next items (as many as sit
-// in the ring together), each lane four rows of its item (chain_quad: one
-// 16-byte load and one source value per column for four rows).  Long items
-// (chunk layout) are streamed alone, chunk pair by chunk pair, rows lane and
-// lane + 32 per thread.
-__device__ __forceinline__ void chain_stream(ChainRing& R, const int32_t* meta, const uint32_t* kbits, int jb, int je,
-                                             int g0, const double* gs, int rp, int lane, double* racc) {
-  constexpr int mask = kRingBytes / 4 - 1;  // ring elements - 1
-  const float* ring = R.ring;
-  auto R4 = [&](int o) { return *reinterpret_cast<const float4*>(ring + (o & mask)); };
-  auto R1 = [&](int o) { return ring[o & mask]; };
-  auto col0 = [&](int j) { return meta[j] >> kMetaW; };
-  auto width = [&](int j) { return meta[j] & ((1 << kMetaW) - 1); };
-  const int tpg = rp >> 2;                  // lanes per slot (four rows each)
-  const int nslot = min(32 / tpg, 8);
-  const int slot = lane / tpg, t = lane - slot * tpg;
-  double b0 = 0.0, b1 = 0.0, b2 = 0.0, b3 = 0.0;  // rows 4t .. 4t+3 of this lane's items
+// One chain lane: items jb .. je-1 of the part (meta / kbits in shared memory)
+// are its slot's group, stream columns from g0; rows 4t .. 4t+3.  Adds the
+// widened item values into b[0..3] (FP64, item order).  Every row's value is
+// in OpenBLAS SGEMV-T's order (chain_quad: all rows in the 16-row kernel /
+// 16-8-4-row kernels; otherwise chain_item / chain_quad_kinds per row kind).
+__device__ __forceinline__ void chain_lane(ChainFifo& F, const int32_t* meta, const uint32_t* kbits, int jb, int je,
+                                           int g0, const double* gs, int rp, int t, double* b) {
   int j = jb;
-  while (j < je) {
-    const int c0j = col0(j), nj = width(j);
-    const int ioj = (c0j - g0) * rp;  // stream element offset of item j
-    if (chain_item_long(nj, rp)) {
-      // ---- long item (chunk layout), alone: rows lane and lane + 32, chunk pair by chunk pair
-      const int n = nj, io = ioj, iend = (ioj + nj * rp) * 4;
+  // (uniform trip count over the warp, so the slots stay converged item by item)
+  while (__any_sync(0xffffffffu, j < je)) {
+    if (j < je) {
+      const int c0 = meta[j] >> kMetaW, n = meta[j] & ((1 << kMetaW) - 1);
       const uint32_t kb = kbits[j];
-      const double* gj = gs + c0j;
-      auto G = [&](int k) { return __int_as_float(__double2loint(gj[k])); };
-      auto G4 = [&](int c) { return make_float4(G(c), G(c + 1), G(c + 2), G(c + 3)); };
-      const bool two = rp > 32;
-      const int cs = 4 * rp;  // elements per chunk
-      const int nch = n >> 2, T = n & 3;
-      const int fo = io + 4 * lane;  // chunk 0 of row `lane`
-      float4 A0 = make_float4(0.f, 0.f, 0.f, 0.f), B0 = A0, A1 = A0, B1 = A0;
-      const int k0 = chain_row_kind(kb, lane), k1 = chain_row_kind(kb, lane + 32);
-      const bool odd = nch & 1;
-      auto step = [&](float4& A, float4& B, const float4& x, const float4& g, int kind, int cc) {
-        const bool inA = kind == 2 || (odd ? (cc == 0 || (cc & 1)) : !(cc & 1));
-        const float4 X = inA ? A : B;
-        const float4 Y = kind >= 4 ? fma4(x, g, X) : mad4(x, g, X);
-        if (inA) A = Y;
-        else B = Y;
-      };
-      int c = 0;
-      if ((int)((kb >> 14) & 127) >= rp) {
-        // the common case: every row of the segment in the 16/8/4-row kernels
-        if (odd) {
-          R.ensure((io + cs) * 4);
-          const float4 g = G4(0);
-          A0 = fma4(R4(fo), g, A0);
-          if (two) A1 = fma4(R4(fo + 128), g, A1);
+      const int s = c0 - g0;  // the item's first stream column
+      const double* gj = gs + c0;
+      auto G = [&](int q) { return __int_as_float(__double2loint(gj[q])); };
+      auto C = [&](int q) { return F.col(s + q); };
+      const bool fast = (int)((kb >> (n < 8 ? 0 : 14)) & 127) >= rp;
+      float4 v;
+      F.refill(s);
+      if (n <= 8) {
+        F.need(s + n);
+        if (fast) {
+          v = chain_quad(C, G, n);
+        } else {
+          float r[4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            auto E = [&](int q) {
+              const float4 x = C(q);
+              return i == 0 ? x.x : i == 1 ? x.y : i == 2 ? x.z : x.w;
+            };
+            auto X4 = [&](int c) { return make_float4(E(4 * c), E(4 * c + 1), E(4 * c + 2), E(4 * c + 3)); };
+            r[i] = chain_item(X4, E, G, n, chain_row_kind(kb, 4 * t + i));
+          }
+          v = make_float4(r[0], r[1], r[2], r[3]);
+        }
+      } else if (fast) {
+        const float4 zero = make_float4(0.f, 0.f, 0.f, 0.f);
+        const int nch = n >> 2, T = n & 3, m = 4 * nch;
+        float4 A[4] = {zero, zero, zero, zero}, B[4] = {zero, zero, zero, zero};
+        int c = 0;
+        if (nch & 1) {
+          F.need(s + 4);
+#pragma unroll
+          for (int q = 0; q < 4; ++q) A[q] = fmas4(C(q), G(q), A[q]);
           c = 1;
         }
         for (; c < nch; c += 2) {
-          R.release((io + c * cs) * 4, lane);
-          R.ensure((io + (c + 2) * cs) * 4);
-          const float4 ga = G4(4 * c), gb = G4(4 * c + 4);
-          const int q = fo + c * cs;
-          A0 = fma4(R4(q), ga, A0);
-          B0 = fma4(R4(q + cs), gb, B0);
-          if (two) {
-            A1 = fma4(R4(q + 128), ga, A1);
-            B1 = fma4(R4(q + cs + 128), gb, B1);
-          }
-        }
-      } else {
-        // rows in the 2- / 1-row remainder kernels (row counts not a multiple of 4)
-        for (; c < nch; ++c) {
-          R.release((io + c * cs) * 4, lane);
-          R.ensure((io + (c + 1) * cs) * 4);
-          const float4 g = G4(4 * c);
-          step(A0, B0, R4(fo + c * cs), g, k0, c);
-          if (two) step(A1, B1, R4(fo + c * cs + 128), g, k1, c);
-        }
-      }
-      float v0 = hsum4(add4(A0, B0)), v1 = hsum4(add4(A1, B1));
-      if (T > 0) {
-        const int m = 4 * nch, tl = io + m * rp + lane;
-        R.release((io + m * rp) * 4, lane);
-        R.ensure(iend);
-        if (T == 1) {
-          const float g = G(m);
-          v0 = __fmaf_rn(R1(tl), g, v0);
-          v1 = __fmaf_rn(R1(tl + 32), g, v1);
-        } else {
-          const float ga = G(m + 1), gb = G(m);
-          float t0 = __fmaf_rn(R1(tl), gb, __fmul_rn(R1(tl + rp), ga));
-          float t1 = __fmaf_rn(R1(tl + 32), gb, __fmul_rn(R1(tl + rp + 32), ga));
-          if (T == 3) {
-            const float gc = G(m + 2);
-            t0 = __fmaf_rn(R1(tl + 2 * rp), gc, t0);
-            t1 = __fmaf_rn(R1(tl + 2 * rp + 32), gc, t1);
-          }
-          v0 = __fadd_rn(v0, t0);
-          v1 = __fadd_rn(v1, t1);
-        }
-      }
-      R.release(iend, lane);
-      if (lane < rp) racc[lane] += (double)v0;
-      if (lane + 32 < rp) racc[lane + 32] += (double)v1;
-      ++j;
-      continue;
-    }
-    // ---- a pass: the next k <= nslot short items that sit in the ring together
-    int k = 1, pend = ioj + nj * rp;  // stream elements up to the pass's end
-    while (k < nslot && j + k < je) {
-      const int e = (col0(j + k) - g0 + width(j + k)) * rp;
-      if ((e - ioj) * 4 > kChainWhole) break;  // (also stops at a long item)
-      pend = e;
-      ++k;
-    }
-    R.ensure(pend * 4);
-    if (slot < k) {
-      const int ji = j + slot;
-      const int c0 = col0(ji), n = width(ji);
-      const uint32_t kb = kbits[ji];
-      const int io = (c0 - g0) * rp + 4 * t;  // rows 4t .. 4t+3 of column 0
-      const double* gj = gs + c0;
-      auto G = [&](int q) { return __int_as_float(__double2loint(gj[q])); };
-      float4 v;
-      if ((int)((kb >> (n < 8 ? 0 : 14)) & 127) >= rp) {
-        // the common case: every row of the segment in SGEMV's 16-row kernel
-        // (n < 8), or in the 16/8/4-row kernels (n >= 8)
-        v = chain_quad([&](int q) { return R4(io + q * rp); }, G, n);
-      } else {
-        float r[4];
+          F.refill(s + 4 * c);
+          F.need(s + 4 * c + 8);
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          auto E = [&](int q) { return R1(io + q * rp + i); };
-          auto X4 = [&](int c) { return make_float4(E(4 * c), E(4 * c + 1), E(4 * c + 2), E(4 * c + 3)); };
-          r[i] = chain_item(X4, E, G, n, chain_row_kind(kb, 4 * t + i));
+          for (int q = 0; q < 4; ++q) A[q] = fmas4(C(4 * c + q), G(4 * c + q), A[q]);
+#pragma unroll
+          for (int q = 0; q < 4; ++q) B[q] = fmas4(C(4 * c + 4 + q), G(4 * c + 4 + q), B[q]);
         }
-        v = make_float4(r[0], r[1], r[2], r[3]);
+        v = add4(add4(add4(A[0], B[0]), add4(A[1], B[1])), add4(add4(A[2], B[2]), add4(A[3], B[3])));
+        if (T > 0) {
+          F.refill(s + m);
+          F.need(s + n);
+          if (T == 1) {
+            v = fmas4(C(m), G(m), v);
+          } else {
+            float4 tv = muls4(C(m + 1), G(m + 1));
+            tv = fmas4(C(m), G(m), tv);
+            if (T == 3) tv = fmas4(C(m + 2), G(m + 2), tv);
+            v = add4(v, tv);
+          }
+        }
+      } else {
+        int kind[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) kind[i] = chain_row_kind(kb, 4 * t + i);
+        auto before = [&](int c) {
+          F.refill(s + 4 * c);
+          F.need(min(s + 4 * c + 4, s + n));
+        };
+        v = chain_quad_kinds(C, G, before, n, kind);
       }
-      b0 += (double)v.x;
-      b1 += (double)v.y;
-      b2 += (double)v.z;
-      b3 += (double)v.w;
-    }
-    j += k;
-    R.release(pend * 4, lane);
-  }
-  // the slots' sums into racc, slot by slot (fixed order)
-  for (int sl = 0; sl < nslot; ++sl) {
-    __syncwarp();
-    if (slot == sl) {
-      racc[4 * t] += b0;
-      racc[4 * t + 1] += b1;
-      racc[4 * t + 2] += b2;
-      racc[4 * t + 3] += b3;
+      b[0] += (double)v.x;
+      b[1] += (double)v.y;
+      b[2] += (double)v.z;
+      b[3] += (double)v.w;
+      ++j;
     }
   }
-  __syncwarp();
+  asm volatile("cp.async.wait_group 0;\n" ::: "memory");
 }
 
 // Stage 1 of m1-single: z = Vt32 . x32 accumulated in FP32 (reference
@@ -667,10 +643,8 @@ __global__ void __launch_bounds__(NT, DEEP ? 3 : (OUT == OUT_Y && F32MODE != F32
   __shared__ double red64[2 * NT];
   __shared__ double red32[4 * NT];
   __shared__ double wred[2][NT / 32];
-  // the chain warps' rings (stage-2 FP32 kernels; dynamic: ring bytes x P.chain_warps) and their mbarriers
+  // the chain lanes' column FIFOs (stage-2 FP32 kernels; dynamic: kFifoBytes x P.chain_warps)
   extern __shared__ __align__(128) float chain_buf[];
-  __shared__ uint64_t chain_mb[NT / 32][kRingStages];
-  __shared__ double racc[EXACT ? NT / 32 : 1][kSegRows];  // chain warps: their rows' FP64 sums
   __shared__ unsigned ticket;
 
   if (out.skip != nullptr && *out.skip != 0) return;  // guarded launch (solver)
@@ -751,12 +725,12 @@ __global__ void __launch_bounds__(NT, DEEP ? 3 : (OUT == OUT_Y && F32MODE != F32
   int q32 = tid / tpg32, p32 = tid - q32 * tpg32;
   // Stage-2 parts with a group table (every part of <= kSegWMax columns):
   // FP64-accumulated (widened) items on threads [0, wbc), 4 rows per thread
-  // as above; the FP32-accumulated items (RUN_CHUNK) on threads [wbc, NT),
-  // ONE row per thread, each item evaluated in SGEMV's own order (chain_items).
+  // as above; the FP32-accumulated items on the warps of threads [wbc, NT),
+  // each item evaluated in SGEMV's own order (chain_lane), 4 rows per lane.
   // wbc (plan: sg.chunk) is warp-aligned, so no warp runs both loops.
-  bool chain_thr = false;
-  int pc = 0, cg0 = 0;
-  ChainRing cring;
+  bool chain_thr = false, chain_warp = false;
+  int cg0 = 0;
+  ChainFifo cfifo;
   if constexpr (F32MODE == F32_MIXED && OUT == OUT_Y) {
     // (HMX_PLAN_FP32_CHAIN plans: one FP32 FMA chain per (row, item), 4 rows
     // per thread on both sides of the warp-aligned split at wb = sg.chunk)
@@ -777,25 +751,29 @@ __global__ void __launch_bounds__(NT, DEEP ? 3 : (OUT == OUT_Y && F32MODE != F32
   if constexpr (EXACT && F32MODE != F32_ALL64 && OUT == OUT_Y) {
     if (sg.gtab >= 0) {
       const int wbc = F32MODE == F32_ALL32 ? 0 : sg.chunk;
-      const int ga = wbc / tpg32, gb = (NT - wbc) / 32;  // one chain group per warp
+      // chain lanes: slots of tpg32 lanes inside each warp, one group per slot
+      const int nslot = min(32 / tpg32, 8);
+      const int ga = wbc / tpg32, gb = ((NT - wbc) >> 5) * nslot;
       g32 = ga + gb;
       if (tid < wbc) {
         if (q32 >= ga) q32 = g32;  // idle
       } else {
-        const int qb = (tid - wbc) >> 5;
-        pc = tid & 31;
-        q32 = ga + qb;
-        chain_thr = true;
-        // start streaming the group's items now (payload only: before the wait on stage 1)
-        cring.ring = chain_buf + (size_t)qb * (kRingBytes / 4);
-        cring.ring_s = smem_addr(cring.ring);
-        cring.mb_s = smem_addr(chain_mb[qb]);
-        cg0 = P.gtab[sg.gtab + q32];
-        cring.src = P.blob32 + sg.off32 + (int64_t)cg0 * rp32;
-        cring.len = (P.gtab[sg.gtab + q32 + 1] - cg0) * rp32 * 4;
-        cring.start(pc);
-        racc[qb][pc] = 0.0;
-        racc[qb][pc + 32] = 0.0;
+        chain_warp = true;
+        const int cw = (tid - wbc) >> 5, lane = tid & 31;
+        const int slot = lane / tpg32;
+        p32 = lane - slot * tpg32;
+        q32 = slot < nslot ? ga + cw * nslot + slot : g32;
+        chain_thr = q32 < g32;
+        if (chain_thr) {
+          // start streaming the group's columns now (payload only: before the wait on stage 1)
+          cg0 = P.gtab[sg.gtab + q32];
+          cfifo.rp = rp32;
+          cfifo.ncols = P.gtab[sg.gtab + q32 + 1] - cg0;
+          cfifo.src = P.blob32 + sg.off32 + (int64_t)cg0 * rp32 + 4 * p32;
+          cfifo.fifo = chain_buf + (size_t)cw * (kFifoBytes / 4) + 4 * lane;
+          cfifo.fifo_s = smem_addr(cfifo.fifo);
+          cfifo.refill(0);
+        }
       }
     }
   }
@@ -809,7 +787,6 @@ __global__ void __launch_bounds__(NT, DEEP ? 3 : (OUT == OUT_Y && F32MODE != F32
     if (sg.gtab >= 0) c32 = P.gtab[sg.gtab + g32 + 1];
     else if (sg.gtab <= -2) c32 = P.gtab[-2 - sg.gtab];
   }
-  double bc = 0.0, bc1 = 0.0;  // chain threads: their rows' FP64 sums of the widened item values
   // widened FP32 data, FP64 accumulation
   auto consume64 = [&](const float4& v, int cc) {
     const double g = gs[cc];
@@ -948,7 +925,7 @@ __global__ void __launch_bounds__(NT, DEEP ? 3 : (OUT == OUT_Y && F32MODE != F32
   }
 
   if constexpr (F32MODE != F32_ALL64 && OUT == OUT_Y) {
-    if (chain_thr) {
+    if (chain_warp) {
       // (the per-item SGEMV row-kernel bounds live in red32, unused until the epilogue)
       uint32_t* kbits = reinterpret_cast<uint32_t*>(red32);
       // the part's run meta into shared memory (sidx is free after the
@@ -962,8 +939,7 @@ __global__ void __launch_bounds__(NT, DEEP ? 3 : (OUT == OUT_Y && F32MODE != F32
         kbits[j] = (uint32_t)r.flags >> kRunKindShift;
       }
       chain_bar(NT - wbc);
-      // this warp's items: columns [cg0, cg1)
-      const int cg1 = P.gtab[sg.gtab + q32 + 1];
+      // this lane's items: columns [cg0, cg1) (none on an idle lane)
       auto first_at = [&](int col) {  // first item starting at or after column `col`
         int lo = 0, hi = sg.nrun32;
         while (lo < hi) {
@@ -973,24 +949,20 @@ __global__ void __launch_bounds__(NT, DEEP ? 3 : (OUT == OUT_Y && F32MODE != F32
         }
         return lo;
       };
-      const int jb = first_at(cg0), je = first_at(cg1);
-      double* ra = racc[(tid - wbc) >> 5];
-      chain_stream(cring, sidx, kbits, jb, je, cg0, gs, rp32, pc, ra);
-      bc = ra[pc];
-      bc1 = ra[pc + 32];
+      int jb = 0, je = 0;
+      if (chain_thr) {
+        jb = first_at(cg0);
+        je = first_at(cg0 + cfifo.ncols);
+      }
+      chain_lane(cfifo, sidx, kbits, jb, je, cg0, gs, rp32, p32, b);
     }
   }
 
   // ---------------- fixed-order reduction over thread groups
   __syncthreads();
   if (sg.W32 > 0 && q32 < g32) {
-    if (chain_thr) {
-      if (pc < rp32) red32[q32 * rp32 + pc] = bc;
-      if (pc + 32 < rp32) red32[q32 * rp32 + pc + 32] = bc1;
-    } else {
 #pragma unroll
-      for (int i = 0; i < 4; ++i) red32[q32 * rp32 + 4 * p32 + i] = b[i];
-    }
+    for (int i = 0; i < 4; ++i) red32[q32 * rp32 + 4 * p32 + i] = b[i];
   }
   __syncthreads();
   // row sums over groups (fixed order); a thread owns rows tid, tid + NT, ...
@@ -1159,9 +1131,9 @@ __global__ void probe_kernel(DevPlan P, const double* __restrict__ x, unsigned l
 // buffers of the stage-2 FP32 kernels
 template <int M, int O, bool EXACT>
 static size_t chain_smem(const DevPlan& P) {
-  return (EXACT && O == OUT_Y && M != F32_ALL64) ? (size_t)P.chain_warps * kRingBytes : 0;
+  return (EXACT && O == OUT_Y && M != F32_ALL64) ? (size_t)P.chain_warps * kFifoBytes : 0;
 }
-constexpr int kChainSmemMax = (kSegThreads / 32) * kRingBytes;
+constexpr int kChainSmemMax = (kSegThreads / 32) * kFifoBytes;
 
 template <int M, int O, int NT = kSegThreads, bool DEEP = false, bool EXACT = false, int XMINB = HMX_EXACT_MINB>
 static cudaError_t launch_seg(const DevPlan& P, const Seg* segs, int nseg, const double* x,

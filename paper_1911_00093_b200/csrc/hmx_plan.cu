@@ -424,7 +424,7 @@ int hmx::plan_create_impl(const hmx_matrix_desc* d, int device, const hmx_plan_o
     std::vector<int64_t> cuts;  // G + 1 column boundaries; empty: no group table
     int64_t c32 = 0;            // first chain column
     int64_t wb = 0;
-    int64_t gb = 0;             // chain groups
+    int64_t cw = 0;             // chain warps (SGEMV-order plans)
   };
   auto lpt = [](const std::vector<int64_t>& w, int64_t G, std::vector<int32_t>* owner) {
     std::vector<int32_t> order(w.size());
@@ -447,7 +447,11 @@ int hmx::plan_create_impl(const hmx_matrix_desc* d, int device, const hmx_plan_o
     if (W > kSegWMax) return fg;  // tiled part: no group table
     // widened groups: 4 rows per thread; chain groups: one row per thread
     const int64_t rp = round_up(R, 4), tpg = rp / 4, G = kSegThreads / tpg;
-    const int64_t tpc = chain_order ? tpg : kChainGroupThreads, Gc = kSegThreads / tpc;  // threads per chain group
+    // chain groups: HMX_PLAN_FP32_CHAIN plans: tpg threads each, anywhere; SGEMV-order
+    // plans: slots of tpg lanes inside a warp, 32 / tpg (<= 8) slots per warp
+    const int64_t nslot = std::min<int64_t>(32 / tpg, 8);
+    auto chain_groups = [&](int64_t threads) { return chain_order ? threads / tpg : threads / 32 * nslot; };
+    const int64_t Gc = chain_groups(kSegThreads);
     size_t nA = 0;
     while (nA < lst.size() && !item_acc32(lst[nA])) ++nA;
     int64_t colsA = 0;
@@ -459,11 +463,9 @@ int hmx::plan_create_impl(const hmx_matrix_desc* d, int device, const hmx_plan_o
     if (nA > 0 && !wB.empty()) {
       double best = 1e300;
       for (int64_t wb = 32; wb < kSegThreads; wb += 32) {
-        const int64_t ga = wb / tpg, gb = (kSegThreads - wb) / tpc;
+        const int64_t ga = wb / tpg, gb = chain_groups(kSegThreads - wb);
         if (ga < 1 || gb < 1) continue;
-        // (SGEMV-order plans: a chain warp works on 32 / tpg items at a time, hmx_kernels.cu chain_stream)
-        const double chain_par = chain_order ? 1.0 : (double)std::min<int64_t>(32 / tpg, 8);
-        const double t = std::max(acc64_weight * (double)colsA / (double)ga, (double)lpt(wB, gb, nullptr) / chain_par);
+        const double t = std::max(acc64_weight * (double)colsA / (double)ga, (double)lpt(wB, gb, nullptr));
         if (t < best) {
           best = t;
           fg.wb = wb;
@@ -480,7 +482,7 @@ int hmx::plan_create_impl(const hmx_matrix_desc* d, int device, const hmx_plan_o
     // when there are no chains)
     fg.cuts.push_back(0);
     for (int64_t q = 1; q <= gA; ++q) fg.cuts.push_back(colsA * q / gA);
-    fg.gb = wB.empty() ? 0 : gB;
+    fg.cw = (wB.empty() || chain_order) ? 0 : (kSegThreads - fg.wb) / 32;
     if (gB > 0) {
       std::vector<int32_t> owner;
       lpt(wB, gB, &owner);
@@ -514,7 +516,7 @@ int hmx::plan_create_impl(const hmx_matrix_desc* d, int device, const hmx_plan_o
     sg.nchunks = 1;
     sg.part_off = -1;
     const FP32Groups fg = plan_fp32_groups(items32[(size_t)s], sg.R);  // may reorder chain items
-    if (!chain_order) chain_warps_max = std::max<int64_t>(chain_warps_max, fg.gb);
+    chain_warps_max = std::max<int64_t>(chain_warps_max, fg.cw);
     for (int part = 0; part < 2; ++part) {
       const auto& lst = part == 0 ? items64[(size_t)s] : items32[(size_t)s];
       int64_t col = 0;
@@ -533,11 +535,10 @@ int hmx::plan_create_impl(const hmx_matrix_desc* d, int device, const hmx_plan_o
         if (part == 1) {
           if (r.flags & RUN_ACC32) any_acc32 = true;
           else any_acc64_in32 = true;
-          // parts with a group table: chain items in SGEMV chunk layout, with
-          // the segment rows of each SGEMV row kernel (sgemv_row_kind of the
-          // block's rows, as 7-bit segment-relative bounds)
+          // parts with a group table: chain items carry the segment rows of
+          // each SGEMV row kernel (sgemv_row_kind of the block's rows, as 7-bit
+          // segment-relative bounds)
           if ((r.flags & RUN_ACC32) && !fg.cuts.empty() && !chain_order) {
-            if (chain_item_long(r.width, round_up(sg.R, 4))) r.flags |= RUN_CHUNK;
             const int64_t mb = t[1] - t[0], d0 = sg.row0 - t[0];  // block row of segment row 0
             const int64_t a16 = mb & ~int64_t(15), b8 = a16 + (mb & 8), c4 = b8 + (mb & 4);
             const int64_t c2 = c4 + ((mb & 3) >= 2 ? 2 : 0);
@@ -641,12 +642,10 @@ int hmx::plan_create_impl(const hmx_matrix_desc* d, int device, const hmx_plan_o
         src_off = d->lo_off[it.block];
         src32 = true;
       }
-      // chain items of group-table parts: SGEMV chunk layout (chunk_off)
-      const bool chunk = part == 1 && item_acc32(it) && sg.gtab >= 0 && !chain_order && chain_item_long(w, rp);
       for (int64_t i = 0; i < sg.R; ++i) {
         const int64_t e0 = src_off + (r0 + i) * w;
         for (int64_t c = 0; c < w; ++c) {
-          const int64_t dst = o + col * rp + (chunk ? chunk_off((int)w, (int)rp, (int)i, (int)c) : c * rp + i);
+          const int64_t dst = o + (col + c) * rp + i;  // every stage-2 item is column-major
           if (part == 0) b64[(size_t)dst] = src32 ? d->buf32[e0 + c] : d->buf64[e0 + c];
           else b32[(size_t)dst] = src32 ? d->buf32[e0 + c] : (float)d->buf64[e0 + c];
         }
@@ -779,8 +778,7 @@ int hmx::plan_create_impl(const hmx_matrix_desc* d, int device, const hmx_plan_o
         u.is32 = part;
         for (const ItemRef& it : lst)
           pit.push_back({it.block, it.cls, (int32_t)item_width(it),
-                         (part == 1 && item_acc32(it) && sg.gtab >= 0 && !chain_order &&
-                          chain_item_long(item_width(it), u.rp)) ? 1 : 0});
+                         0});
         ps2.push_back(u);
       }
     }
