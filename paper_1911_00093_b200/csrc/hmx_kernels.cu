@@ -21,7 +21,7 @@
 #define HMX_MIXED_MINB 4
 #endif
 #ifndef HMX_EXACT_MINB
-#define HMX_EXACT_MINB 2  // CTAs per SM of the SGEMV-order stage-2 kernels (the chain warps' rings bound it)
+#define HMX_EXACT_MINB 3  // CTAs per SM of the SGEMV-order stage-2 kernels with <= 5 chain warps (registers; FIFOs)
 #endif
 
 namespace hmx {
@@ -390,78 +390,97 @@ __device__ __forceinline__ float4 chain_quad_kinds(CF C, GF G, BF before, int n,
   return make_float4(v[0], v[1], v[2], v[3]);
 }
 
-// A chain lane's private FIFO of stream columns in shared memory.  The lanes
-// of one slot (rp / 4 lanes, four rows each) stream the columns of their
-// group -- contiguous in the blob -- with 16-byte cp.async copies, four
-// columns per commit group, into kFifoCols entries addressed by stream column
-// mod kFifoCols; every lane reads back only what it copied itself, so nothing
-// is synchronised between lanes, and up to 12 columns per lane are in flight
-// while earlier ones are reduced.
-constexpr int kFifoCols = 16;
-constexpr int kFifoBytes = kFifoCols * 512;  // per chain warp: 16 bytes x 32 lanes per entry
+// A chain lane's private FIFO in shared memory.  The lanes of one slot
+// (rp / 4 lanes, four rows each) stream the columns of their group --
+// contiguous in the blob -- with 16-byte cp.async copies in BATCHES: the
+// 4-column chunks of each item and its 1..3 tail columns, one commit group
+// per batch, kFifoBatches batch slots per lane.  A batch is consumed whole
+// (one chunk of SGEMV's A/B accumulators, or the tail), so while one is
+// reduced the other three are in flight.  Every lane reads back only what it
+// copied itself: nothing is synchronised between lanes.
+constexpr int kFifoBatches = 4;
+constexpr int kFifoBytes = kFifoBatches * 4 * 512;  // per chain warp: 16 bytes x 32 lanes per column
 struct ChainFifo {
-  const float* src;    // this lane's four rows of stream column 0
-  const float* fifo;   // this lane's 16 bytes of entry 0 (entry e: + 128 e floats)
-  uint32_t fifo_s;     // ... its shared-space address
+  const float* srcp;     // this lane's four rows of the next column to copy
+  const float* fifo;     // this lane's 16 bytes of batch slot 0, column 0 (column u: + 128 u, slot b: + 512 b floats)
+  uint32_t fifo_s;       // ... its shared-space address
+  const int32_t* meta;   // run meta (col0 << kMetaW | width) in shared memory
   int rp;
-  int ncols;           // stream columns
-  int issued = 0;      // columns copied or in flight (a multiple of 4)
-  int landed = 0;      // columns known to have landed (a multiple of 4)
+  int ij, je;            // next item to copy from / end of the lane's items
+  int irem;              // columns of item ij not yet copied
+  int ib = 0;            // batches copied or in flight
+  int cb = 0;            // batches consumed
+  int lb = 0;            // batches known to have landed
 
-  // copy ahead while the entries are free: columns < lo are consumed
-  __device__ __forceinline__ void refill(int lo) {
-    const int top = min((ncols + 3) & ~3, (lo & ~3) + kFifoCols);
-    while (issued < top) {
-      const uint32_t dst = fifo_s + (uint32_t)(issued & (kFifoCols - 1)) * 512u;
-      const float* g = src + (int64_t)issued * rp;
+  __device__ __forceinline__ void start(const int32_t* m, int jb, int je_) {
+    meta = m;
+    ij = jb;
+    je = je_;
+    irem = jb < je_ ? (m[jb] & ((1 << kMetaW) - 1)) : 0;
+    refill();
+  }
+  // copy ahead while batch slots are free
+  __device__ __forceinline__ void refill() {
+    while (ib - cb < kFifoBatches && ij < je) {
+      const int cols = min(4, irem);
+      const uint32_t dst = fifo_s + (uint32_t)(ib & (kFifoBatches - 1)) * 2048u;
 #pragma unroll
       for (int u = 0; u < 4; ++u)
-        if (issued + u < ncols)
-          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst + 512u * u), "l"(g + (int64_t)u * rp) : "memory");
+        if (u < cols)
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst + 512u * u), "l"(srcp + (int64_t)u * rp) : "memory");
       asm volatile("cp.async.commit_group;\n" ::: "memory");
-      issued += 4;
+      ++ib;
+      srcp += (int64_t)cols * rp;
+      irem -= cols;
+      if (irem == 0 && ++ij < je) irem = meta[ij] & ((1 << kMetaW) - 1);
     }
   }
-  // columns < x have landed (x - lo <= 10 after refill(lo))
-  __device__ __forceinline__ void need(int x) {
-    if (landed >= x) return;
-    const int b = (x + 3) & ~3;
-    switch ((issued - b) >> 2) {
+  // batch bt (< ib) has landed
+  __device__ __forceinline__ void need(int bt) {
+    if (lb > bt) return;
+    switch (ib - bt - 1) {
       case 0: asm volatile("cp.async.wait_group 0;\n" ::: "memory"); break;
       case 1: asm volatile("cp.async.wait_group 1;\n" ::: "memory"); break;
       case 2: asm volatile("cp.async.wait_group 2;\n" ::: "memory"); break;
       default: asm volatile("cp.async.wait_group 3;\n" ::: "memory"); break;
     }
-    landed = b;
+    lb = bt + 1;
   }
-  // stream column g of this lane's four rows
-  __device__ __forceinline__ float4 col(int g) const {
-    return *reinterpret_cast<const float4*>(fifo + (g & (kFifoCols - 1)) * 128);
+  // batches < bt are consumed
+  __device__ __forceinline__ void done(int bt) {
+    cb = bt;
+    refill();
+  }
+  // column u of batch bt, this lane's four rows
+  __device__ __forceinline__ float4 col(int bt, int u) const {
+    return *reinterpret_cast<const float4*>(fifo + (bt & (kFifoBatches - 1)) * 512 + u * 128);
   }
 };
 
 // One chain lane: items jb .. je-1 of the part (meta / kbits in shared memory)
-// are its slot's group, stream columns from g0; rows 4t .. 4t+3.  Adds the
-// widened item values into b[0..3] (FP64, item order).  Every row's value is
-// in OpenBLAS SGEMV-T's order (chain_quad: all rows in the 16-row kernel /
-// 16-8-4-row kernels; otherwise chain_item / chain_quad_kinds per row kind).
+// are its slot's group; rows 4t .. 4t+3.  Adds the widened item values into
+// b[0..3] (FP64, item order).  Every row's value is in OpenBLAS SGEMV-T's
+// order (chain_quad: all rows in the 16-row kernel / 16-8-4-row kernels;
+// otherwise chain_item / chain_quad_kinds per row kind).
 __device__ __forceinline__ void chain_lane(ChainFifo& F, const int32_t* meta, const uint32_t* kbits, int jb, int je,
-                                           int g0, const double* gs, int rp, int t, double* b) {
+                                           const double* gs, int rp, int t, double* b) {
+  F.start(meta, jb, je);
   int j = jb;
   // (uniform trip count over the warp, so the slots stay converged item by item)
   while (__any_sync(0xffffffffu, j < je)) {
     if (j < je) {
       const int c0 = meta[j] >> kMetaW, n = meta[j] & ((1 << kMetaW) - 1);
       const uint32_t kb = kbits[j];
-      const int s = c0 - g0;  // the item's first stream column
       const double* gj = gs + c0;
       auto G = [&](int q) { return __int_as_float(__double2loint(gj[q])); };
-      auto C = [&](int q) { return F.col(s + q); };
+      const int b0 = F.cb;  // the item's first batch; column q sits in batch b0 + q / 4
+      auto C = [&](int q) { return F.col(b0 + (q >> 2), q & 3); };
       const bool fast = (int)((kb >> (n < 8 ? 0 : 14)) & 127) >= rp;
+      const int nch = n >> 2, T = n & 3, m = 4 * nch;
+      const int nb = chain_shaped(n) ? 1 + (n > 4) : nch + (T > 0);  // batches of the item (== ceil(n / 4))
       float4 v;
-      F.refill(s);
       if (n <= 8) {
-        F.need(s + n);
+        F.need(b0 + nb - 1);
         if (fast) {
           v = chain_quad(C, G, n);
         } else {
@@ -477,47 +496,51 @@ __device__ __forceinline__ void chain_lane(ChainFifo& F, const int32_t* meta, co
           }
           v = make_float4(r[0], r[1], r[2], r[3]);
         }
+        F.done(b0 + nb);
       } else if (fast) {
         const float4 zero = make_float4(0.f, 0.f, 0.f, 0.f);
-        const int nch = n >> 2, T = n & 3, m = 4 * nch;
         float4 A[4] = {zero, zero, zero, zero}, B[4] = {zero, zero, zero, zero};
         int c = 0;
         if (nch & 1) {
-          F.need(s + 4);
+          F.need(b0);
 #pragma unroll
-          for (int q = 0; q < 4; ++q) A[q] = fmas4(C(q), G(q), A[q]);
+          for (int q = 0; q < 4; ++q) A[q] = fmas4(F.col(b0, q), G(q), A[q]);
+          F.done(b0 + 1);
           c = 1;
         }
         for (; c < nch; c += 2) {
-          F.refill(s + 4 * c);
-          F.need(s + 4 * c + 8);
+          F.need(b0 + c);
 #pragma unroll
-          for (int q = 0; q < 4; ++q) A[q] = fmas4(C(4 * c + q), G(4 * c + q), A[q]);
+          for (int q = 0; q < 4; ++q) A[q] = fmas4(F.col(b0 + c, q), G(4 * c + q), A[q]);
+          F.done(b0 + c + 1);
+          F.need(b0 + c + 1);
 #pragma unroll
-          for (int q = 0; q < 4; ++q) B[q] = fmas4(C(4 * c + 4 + q), G(4 * c + 4 + q), B[q]);
+          for (int q = 0; q < 4; ++q) B[q] = fmas4(F.col(b0 + c + 1, q), G(4 * c + 4 + q), B[q]);
+          F.done(b0 + c + 2);
         }
         v = add4(add4(add4(A[0], B[0]), add4(A[1], B[1])), add4(add4(A[2], B[2]), add4(A[3], B[3])));
         if (T > 0) {
-          F.refill(s + m);
-          F.need(s + n);
+          F.need(b0 + nch);
           if (T == 1) {
-            v = fmas4(C(m), G(m), v);
+            v = fmas4(F.col(b0 + nch, 0), G(m), v);
           } else {
-            float4 tv = muls4(C(m + 1), G(m + 1));
-            tv = fmas4(C(m), G(m), tv);
-            if (T == 3) tv = fmas4(C(m + 2), G(m + 2), tv);
+            float4 tv = muls4(F.col(b0 + nch, 1), G(m + 1));
+            tv = fmas4(F.col(b0 + nch, 0), G(m), tv);
+            if (T == 3) tv = fmas4(F.col(b0 + nch, 2), G(m + 2), tv);
             v = add4(v, tv);
           }
+          F.done(b0 + nch + 1);
         }
       } else {
         int kind[4];
 #pragma unroll
         for (int i = 0; i < 4; ++i) kind[i] = chain_row_kind(kb, 4 * t + i);
         auto before = [&](int c) {
-          F.refill(s + 4 * c);
-          F.need(min(s + 4 * c + 4, s + n));
+          F.done(b0 + c);
+          F.need(b0 + c);
         };
         v = chain_quad_kinds(C, G, before, n, kind);
+        F.done(b0 + nb);
       }
       b[0] += (double)v.x;
       b[1] += (double)v.y;
@@ -638,10 +661,16 @@ __global__ void __launch_bounds__(NT, DEEP ? 3 : (OUT == OUT_Y && F32MODE != F32
   constexpr int WMAX = OUT == OUT_Z ? kS1WMax : kSegWMax;
   constexpr int D64 = DEEP ? 12 : 8;
   __shared__ double gs[WMAX];
-  __shared__ uint8_t fl[WMAX];
+  // XS: a stage-2 kernel with SGEMV-order chain lanes.  Its plans hold no FP64
+  // part (pipes m1-single, m1-mixed, m2-single: FP32 storage throughout), and
+  // its gather flags share red32 (flags: gather phases; red32: after them), so
+  // three CTAs and their chain FIFOs fit an SM.
+  constexpr bool XS = EXACT && OUT == OUT_Y && F32MODE != F32_ALL64;
+  __shared__ uint8_t fl_own[XS ? 1 : WMAX];
   __shared__ int32_t sidx[OUT == OUT_Z ? 1 : kSegWMax];
-  __shared__ double red64[2 * NT];
+  __shared__ double red64[XS ? 1 : 2 * NT];
   __shared__ double red32[4 * NT];
+  uint8_t* fl = XS ? reinterpret_cast<uint8_t*>(red32) : fl_own;
   __shared__ double wred[2][NT / 32];
   // the chain lanes' column FIFOs (stage-2 FP32 kernels; dynamic: kFifoBytes x P.chain_warps)
   extern __shared__ __align__(128) float chain_buf[];
@@ -664,6 +693,7 @@ __global__ void __launch_bounds__(NT, DEEP ? 3 : (OUT == OUT_Y && F32MODE != F32
   const int g64 = NT / tpg64;
   const int q64 = tid / tpg64, p64 = tid - q64 * tpg64;
   double a0 = 0.0, a1 = 0.0;
+  if constexpr (!XS) {
   for (int tc0 = 0; tc0 < sg.W64; tc0 += WMAX) {
     const int tw = min(WMAX, sg.W64 - tc0);
     const bool act = q64 < g64;
@@ -717,6 +747,7 @@ __global__ void __launch_bounds__(NT, DEEP ? 3 : (OUT == OUT_Y && F32MODE != F32
     red64[q64 * rp64 + 2 * p64] = a0;
     red64[q64 * rp64 + 2 * p64 + 1] = a1;
   }
+  }
 
   // ---------------- FP32 part: 4 rows x 16 bytes per thread
   const int rp32 = (R + 3) & ~3;
@@ -729,7 +760,7 @@ __global__ void __launch_bounds__(NT, DEEP ? 3 : (OUT == OUT_Y && F32MODE != F32
   // each item evaluated in SGEMV's own order (chain_lane), 4 rows per lane.
   // wbc (plan: sg.chunk) is warp-aligned, so no warp runs both loops.
   bool chain_thr = false, chain_warp = false;
-  int cg0 = 0;
+  int cg0 = 0, cg1 = 0;
   ChainFifo cfifo;
   if constexpr (F32MODE == F32_MIXED && OUT == OUT_Y) {
     // (HMX_PLAN_FP32_CHAIN plans: one FP32 FMA chain per (row, item), 4 rows
@@ -765,14 +796,12 @@ __global__ void __launch_bounds__(NT, DEEP ? 3 : (OUT == OUT_Y && F32MODE != F32
         q32 = slot < nslot ? ga + cw * nslot + slot : g32;
         chain_thr = q32 < g32;
         if (chain_thr) {
-          // start streaming the group's columns now (payload only: before the wait on stage 1)
           cg0 = P.gtab[sg.gtab + q32];
+          cg1 = P.gtab[sg.gtab + q32 + 1];
           cfifo.rp = rp32;
-          cfifo.ncols = P.gtab[sg.gtab + q32 + 1] - cg0;
-          cfifo.src = P.blob32 + sg.off32 + (int64_t)cg0 * rp32 + 4 * p32;
+          cfifo.srcp = P.blob32 + sg.off32 + (int64_t)cg0 * rp32 + 4 * p32;
           cfifo.fifo = chain_buf + (size_t)cw * (kFifoBytes / 4) + 4 * lane;
           cfifo.fifo_s = smem_addr(cfifo.fifo);
-          cfifo.refill(0);
         }
       }
     }
@@ -952,9 +981,9 @@ __global__ void __launch_bounds__(NT, DEEP ? 3 : (OUT == OUT_Y && F32MODE != F32
       int jb = 0, je = 0;
       if (chain_thr) {
         jb = first_at(cg0);
-        je = first_at(cg0 + cfifo.ncols);
+        je = first_at(cg1);
       }
-      chain_lane(cfifo, sidx, kbits, jb, je, cg0, gs, rp32, p32, b);
+      chain_lane(cfifo, sidx, kbits, jb, je, gs, rp32, p32, b);
     }
   }
 
@@ -968,8 +997,10 @@ __global__ void __launch_bounds__(NT, DEEP ? 3 : (OUT == OUT_Y && F32MODE != F32
   // row sums over groups (fixed order); a thread owns rows tid, tid + NT, ...
   auto row_sum = [&](int t) -> double {
     double s = 0.0;
-    if (sg.W64 > 0)
-      for (int q = 0; q < g64; ++q) s += red64[q * rp64 + t];
+    if constexpr (!XS) {
+      if (sg.W64 > 0)
+        for (int q = 0; q < g64; ++q) s += red64[q * rp64 + t];
+    }
     if (sg.W32 > 0) {
       if (OUT == OUT_Z && F32MODE == F32_ALL32) {
         // stage 1, m1-single: z = Vt32 . x32 accumulated in FP32 throughout
@@ -1179,7 +1210,7 @@ cudaError_t launch_stage2(const DevPlan& P, const double* x, const S2Out& out, c
   if (P.n_seg2 == 0) return cudaSuccess;
   switch (P.f32mode2) {
     case F32_ALL32:
-      return P.chain_exact ? launch_seg<F32_ALL32, OUT_Y, kSegThreads, false, true>(P, P.seg2, P.n_seg2, x, out, st, pdl)
+      return P.chain_exact ? launch_seg<F32_ALL32, OUT_Y, kSegThreads, false, true, 2>(P, P.seg2, P.n_seg2, x, out, st, pdl)
                            : launch_seg<F32_ALL32, OUT_Y>(P, P.seg2, P.n_seg2, x, out, st, pdl);
     case F32_MIXED:
       if (!P.chain_exact) return launch_seg<F32_MIXED, OUT_Y>(P, P.seg2, P.n_seg2, x, out, st, pdl);
@@ -1193,7 +1224,7 @@ cudaError_t launch_stage2(const DevPlan& P, const double* x, const S2Out& out, c
 // The stage-2 FP32 kernels opt in to > 48 KB of shared memory (static + the
 // chain staging buffers); called at plan creation, outside any capture.
 cudaError_t configure_kernels() {
-  cudaError_t e = cudaFuncSetAttribute(seg_kernel<F32_ALL32, OUT_Y, kSegThreads, false, true>,
+  cudaError_t e = cudaFuncSetAttribute(seg_kernel<F32_ALL32, OUT_Y, kSegThreads, false, true, 2>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        kChainSmemMax);
   if (e == cudaSuccess)

@@ -465,6 +465,9 @@ int hmx::plan_create_impl(const hmx_matrix_desc* d, int device, const hmx_plan_o
       for (int64_t wb = 32; wb < kSegThreads; wb += 32) {
         const int64_t ga = wb / tpg, gb = chain_groups(kSegThreads - wb);
         if (ga < 1 || gb < 1) continue;
+        // (SGEMV-order plans: at most kChainWarpsMixed chain warps, so that three
+        // CTAs with their column FIFOs fit an SM)
+        if (!chain_order && (kSegThreads - wb) / 32 > kChainWarpsMixed) continue;
         const double t = std::max(acc64_weight * (double)colsA / (double)ga, (double)lpt(wB, gb, nullptr));
         if (t < best) {
           best = t;
@@ -592,6 +595,10 @@ int hmx::plan_create_impl(const hmx_matrix_desc* d, int device, const hmx_plan_o
     return HMX_ERR_ARG;
   }
   const int f32mode2 = !any_acc32 ? F32_ALL64 : (any_acc64_in32 ? F32_MIXED : F32_ALL32);
+  if (!chain_order && f32mode2 != F32_ALL64 && off64 != 0) {
+    set_error("internal: FP64 part in a plan with FP32-accumulated items");  // (the SGEMV-order kernels skip it)
+    return HMX_ERR_ARG;
+  }
 
   // ---- packing of one blob unit (a stage-1 segment, or one part of a
   // stage-2 segment) into a staging window whose first element is blob
