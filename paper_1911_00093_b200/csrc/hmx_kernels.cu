@@ -410,51 +410,58 @@ struct ChainFifo {
   int irem;              // columns of item ij not yet copied
   int ib = 0;            // batches copied or in flight
   int cb = 0;            // batches consumed
-  int lb = 0;            // batches known to have landed
 
+  // copy the next batch (a chunk or the tail of item ij); ij < je
+  __device__ __forceinline__ void issue() {
+    const int cols = min(4, irem);
+    const uint32_t dst = fifo_s + (uint32_t)(ib & (kFifoBatches - 1)) * 2048u;
+    if (cols == 4) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst + 512u * u), "l"(srcp + (int64_t)u * rp) : "memory");
+    } else {
+#pragma unroll
+      for (int u = 0; u < 3; ++u)
+        if (u < cols)
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst + 512u * u), "l"(srcp + (int64_t)u * rp) : "memory");
+    }
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+    ++ib;
+    srcp += (int64_t)cols * rp;
+    irem -= cols;
+    if (irem == 0 && ++ij < je) irem = meta[ij] & ((1 << kMetaW) - 1);
+  }
   __device__ __forceinline__ void start(const int32_t* m, int jb, int je_) {
     meta = m;
     ij = jb;
     je = je_;
     irem = jb < je_ ? (m[jb] & ((1 << kMetaW) - 1)) : 0;
-    refill();
+    while (ib < kFifoBatches && ij < je) issue();
   }
-  // copy ahead while batch slots are free
-  __device__ __forceinline__ void refill() {
-    while (ib - cb < kFifoBatches && ij < je) {
-      const int cols = min(4, irem);
-      const uint32_t dst = fifo_s + (uint32_t)(ib & (kFifoBatches - 1)) * 2048u;
-#pragma unroll
-      for (int u = 0; u < 4; ++u)
-        if (u < cols)
-          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst + 512u * u), "l"(srcp + (int64_t)u * rp) : "memory");
-      asm volatile("cp.async.commit_group;\n" ::: "memory");
-      ++ib;
-      srcp += (int64_t)cols * rp;
-      irem -= cols;
-      if (irem == 0 && ++ij < je) irem = meta[ij] & ((1 << kMetaW) - 1);
-    }
-  }
-  // batch bt (< ib) has landed
+  // batch bt (cb <= bt < ib) has landed
   __device__ __forceinline__ void need(int bt) {
-    if (lb > bt) return;
-    switch (ib - bt - 1) {
-      case 0: asm volatile("cp.async.wait_group 0;\n" ::: "memory"); break;
-      case 1: asm volatile("cp.async.wait_group 1;\n" ::: "memory"); break;
-      case 2: asm volatile("cp.async.wait_group 2;\n" ::: "memory"); break;
-      default: asm volatile("cp.async.wait_group 3;\n" ::: "memory"); break;
-    }
-    lb = bt + 1;
+    const int pend = ib - bt;  // 1 + the batches copied after it
+    if (pend >= 4) asm volatile("cp.async.wait_group 3;\n" ::: "memory");
+    else if (pend == 3) asm volatile("cp.async.wait_group 2;\n" ::: "memory");
+    else if (pend == 2) asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+    else asm volatile("cp.async.wait_group 0;\n" ::: "memory");
   }
-  // batches < bt are consumed
+  // batches < bt are consumed: refill their slots
   __device__ __forceinline__ void done(int bt) {
     cb = bt;
-    refill();
+    while (ib - cb < kFifoBatches && ij < je) issue();
   }
-  // column u of batch bt, this lane's four rows
+  // one more batch is consumed
+  __device__ __forceinline__ void done1() {
+    ++cb;
+    if (ij < je) issue();  // (ib - cb was kFifoBatches - 1 or the stream is exhausted)
+  }
+  // column u of batch bt (cb <= bt < cb + kFifoBatches), this lane's four rows
   __device__ __forceinline__ float4 col(int bt, int u) const {
     return *reinterpret_cast<const float4*>(fifo + (bt & (kFifoBatches - 1)) * 512 + u * 128);
   }
+  // this lane's 16 bytes of column 0 of the batch being consumed
+  __device__ __forceinline__ const float* cur() const { return fifo + (cb & (kFifoBatches - 1)) * 512; }
 };
 
 // One chain lane: items jb .. je-1 of the part (meta / kbits in shared memory)
@@ -500,36 +507,41 @@ __device__ __forceinline__ void chain_lane(ChainFifo& F, const int32_t* meta, co
       } else if (fast) {
         const float4 zero = make_float4(0.f, 0.f, 0.f, 0.f);
         float4 A[4] = {zero, zero, zero, zero}, B[4] = {zero, zero, zero, zero};
+        auto L = [](const float* p, int u) { return *reinterpret_cast<const float4*>(p + u * 128); };
         int c = 0;
         if (nch & 1) {
-          F.need(b0);
+          F.need(F.cb);
+          const float* p = F.cur();
 #pragma unroll
-          for (int q = 0; q < 4; ++q) A[q] = fmas4(F.col(b0, q), G(q), A[q]);
-          F.done(b0 + 1);
+          for (int q = 0; q < 4; ++q) A[q] = fmas4(L(p, q), G(q), A[q]);
+          F.done1();
           c = 1;
         }
         for (; c < nch; c += 2) {
-          F.need(b0 + c);
+          F.need(F.cb);
+          const float* pa = F.cur();
 #pragma unroll
-          for (int q = 0; q < 4; ++q) A[q] = fmas4(F.col(b0 + c, q), G(4 * c + q), A[q]);
-          F.done(b0 + c + 1);
-          F.need(b0 + c + 1);
+          for (int q = 0; q < 4; ++q) A[q] = fmas4(L(pa, q), G(4 * c + q), A[q]);
+          F.done1();
+          F.need(F.cb);
+          const float* pb = F.cur();
 #pragma unroll
-          for (int q = 0; q < 4; ++q) B[q] = fmas4(F.col(b0 + c + 1, q), G(4 * c + 4 + q), B[q]);
-          F.done(b0 + c + 2);
+          for (int q = 0; q < 4; ++q) B[q] = fmas4(L(pb, q), G(4 * c + 4 + q), B[q]);
+          F.done1();
         }
         v = add4(add4(add4(A[0], B[0]), add4(A[1], B[1])), add4(add4(A[2], B[2]), add4(A[3], B[3])));
         if (T > 0) {
-          F.need(b0 + nch);
+          F.need(F.cb);
+          const float* p = F.cur();
           if (T == 1) {
-            v = fmas4(F.col(b0 + nch, 0), G(m), v);
+            v = fmas4(L(p, 0), G(m), v);
           } else {
-            float4 tv = muls4(F.col(b0 + nch, 1), G(m + 1));
-            tv = fmas4(F.col(b0 + nch, 0), G(m), tv);
-            if (T == 3) tv = fmas4(F.col(b0 + nch, 2), G(m + 2), tv);
+            float4 tv = muls4(L(p, 1), G(m + 1));
+            tv = fmas4(L(p, 0), G(m), tv);
+            if (T == 3) tv = fmas4(L(p, 2), G(m + 2), tv);
             v = add4(v, tv);
           }
-          F.done(b0 + nch + 1);
+          F.done1();
         }
       } else {
         int kind[4];
@@ -666,14 +678,18 @@ __global__ void __launch_bounds__(NT, DEEP ? 3 : (OUT == OUT_Y && F32MODE != F32
   // its gather flags share red32 (flags: gather phases; red32: after them), so
   // three CTAs and their chain FIFOs fit an SM.
   constexpr bool XS = EXACT && OUT == OUT_Y && F32MODE != F32_ALL64;
+  // the chain lanes' column FIFOs (stage-2 FP32 kernels; dynamic: kFifoBytes x P.chain_warps)
+  extern __shared__ __align__(128) float chain_buf[];
   __shared__ uint8_t fl_own[XS ? 1 : WMAX];
-  __shared__ int32_t sidx[OUT == OUT_Z ? 1 : kSegWMax];
+  __shared__ int32_t sidx_own[(OUT == OUT_Z || (EXACT && F32MODE != F32_ALL64)) ? 1 : kSegWMax];
   __shared__ double red64[XS ? 1 : 2 * NT];
   __shared__ double red32[4 * NT];
   uint8_t* fl = XS ? reinterpret_cast<uint8_t*>(red32) : fl_own;
+  // XS: the gather's source-index scratch shares the chain FIFOs' memory (the
+  // FIFOs start after the gather); the chain items' meta / row-kernel bounds
+  // then live in red32 (plans keep <= kChainRunsMax runs in such a part)
+  int32_t* sidx = XS ? reinterpret_cast<int32_t*>(chain_buf) : sidx_own;
   __shared__ double wred[2][NT / 32];
-  // the chain lanes' column FIFOs (stage-2 FP32 kernels; dynamic: kFifoBytes x P.chain_warps)
-  extern __shared__ __align__(128) float chain_buf[];
   __shared__ unsigned ticket;
 
   if (out.skip != nullptr && *out.skip != 0) return;  // guarded launch (solver)
@@ -955,16 +971,16 @@ __global__ void __launch_bounds__(NT, DEEP ? 3 : (OUT == OUT_Y && F32MODE != F32
 
   if constexpr (F32MODE != F32_ALL64 && OUT == OUT_Y) {
     if (chain_warp) {
-      // (the per-item SGEMV row-kernel bounds live in red32, unused until the epilogue)
-      uint32_t* kbits = reinterpret_cast<uint32_t*>(red32);
-      // the part's run meta into shared memory (sidx is free after the
-      // gather), then a barrier among the chain warps only: the widened
-      // warps stream on meanwhile
+      // the part's run meta and per-item SGEMV row-kernel bounds into shared
+      // memory (red32, unused until the epilogue), then a barrier among the
+      // chain warps only: the widened warps stream on meanwhile
+      int32_t* meta = reinterpret_cast<int32_t*>(red32);
+      uint32_t* kbits = reinterpret_cast<uint32_t*>(red32) + kChainRunsMax;
       const int wbc = F32MODE == F32_ALL32 ? 0 : sg.chunk;
       const Run* runs = P.runs + sg.run0 + sg.nrun64;
       for (int j = tid - wbc; j < sg.nrun32; j += NT - wbc) {
         const Run r = runs[j];
-        sidx[j] = (r.col0 << kMetaW) | r.width;
+        meta[j] = (r.col0 << kMetaW) | r.width;
         kbits[j] = (uint32_t)r.flags >> kRunKindShift;
       }
       chain_bar(NT - wbc);
@@ -973,7 +989,7 @@ __global__ void __launch_bounds__(NT, DEEP ? 3 : (OUT == OUT_Y && F32MODE != F32
         int lo = 0, hi = sg.nrun32;
         while (lo < hi) {
           const int mid = (lo + hi) >> 1;
-          if ((sidx[mid] >> kMetaW) < col) lo = mid + 1;
+          if ((meta[mid] >> kMetaW) < col) lo = mid + 1;
           else hi = mid;
         }
         return lo;
@@ -983,7 +999,7 @@ __global__ void __launch_bounds__(NT, DEEP ? 3 : (OUT == OUT_Y && F32MODE != F32
         jb = first_at(cg0);
         je = first_at(cg1);
       }
-      chain_lane(cfifo, sidx, kbits, jb, je, gs, rp32, p32, b);
+      chain_lane(cfifo, meta, kbits, jb, je, gs, rp32, p32, b);
     }
   }
 
@@ -1162,7 +1178,8 @@ __global__ void probe_kernel(DevPlan P, const double* __restrict__ x, unsigned l
 // buffers of the stage-2 FP32 kernels
 template <int M, int O, bool EXACT>
 static size_t chain_smem(const DevPlan& P) {
-  return (EXACT && O == OUT_Y && M != F32_ALL64) ? (size_t)P.chain_warps * kFifoBytes : 0;
+  // (at least the gather's index scratch, which shares the memory)
+  return (EXACT && O == OUT_Y && M != F32_ALL64) ? std::max((size_t)P.chain_warps * kFifoBytes, (size_t)kSegWMax * 4) : 0;
 }
 constexpr int kChainSmemMax = (kSegThreads / 32) * kFifoBytes;
 

@@ -392,7 +392,9 @@ int hmx::plan_create_impl(const hmx_matrix_desc* d, int device, const hmx_plan_o
   // column in a mixed FP32 part (A/B on config 4 with the warp-aligned split:
   // m1-mixed best at 0.8-1.0, m2-single at 1/1.0-1/1.2)
   const char* aw_env = std::getenv("HMX_ACC64_WEIGHT");
-  const double acc64_weight = aw_env ? std::atof(aw_env) : (chain_order ? 0.85 : 1.0);
+  const double acc64_weight = aw_env ? std::atof(aw_env) : (chain_order ? 0.85 : 1.4);
+  const char* ic_env = std::getenv("HMX_CHAIN_ITEM_COST");
+  const int64_t chain_item_cost = ic_env ? std::atoll(ic_env) : 8;
   const bool dense_single = pipe == P_M1S || pipe == P_M2S;  // A32 . x32 in FP32
   const bool u_acc32 = pipe == P_M1S || pipe == P_M1M;       // U32 . z32 in FP32
   bool any_acc32 = false, any_acc64_in32 = false;
@@ -445,6 +447,7 @@ int hmx::plan_create_impl(const hmx_matrix_desc* d, int device, const hmx_plan_o
     int64_t W = 0;
     for (const ItemRef& it : lst) W += item_width(it);
     if (W > kSegWMax) return fg;  // tiled part: no group table
+    if (!chain_order && (int64_t)lst.size() > kChainRunsMax) return fg;  // (the chain lanes' meta table)
     // widened groups: 4 rows per thread; chain groups: one row per thread
     const int64_t rp = round_up(R, 4), tpg = rp / 4, G = kSegThreads / tpg;
     // chain groups: HMX_PLAN_FP32_CHAIN plans: tpg threads each, anywhere; SGEMV-order
@@ -456,8 +459,14 @@ int hmx::plan_create_impl(const hmx_matrix_desc* d, int device, const hmx_plan_o
     while (nA < lst.size() && !item_acc32(lst[nA])) ++nA;
     int64_t colsA = 0;
     for (size_t i = 0; i < nA; ++i) colsA += item_width(lst[i]);
-    std::vector<int64_t> wB;
-    for (size_t i = nA; i < lst.size(); ++i) wB.push_back(item_width(lst[i]));
+    // wB: chain item widths; cB: their estimated costs in columns (SGEMV-order
+    // plans: a fixed per-item overhead -- accumulator set-up, the lane tree,
+    // FIFO bookkeeping -- measured at about kChainItemCost columns)
+    std::vector<int64_t> wB, cB;
+    for (size_t i = nA; i < lst.size(); ++i) {
+      wB.push_back(item_width(lst[i]));
+      cB.push_back(wB.back() + (chain_order ? 0 : chain_item_cost));
+    }
     fg.c32 = colsA;
     int64_t gA = 0, gB = Gc;
     if (nA > 0 && !wB.empty()) {
@@ -468,7 +477,7 @@ int hmx::plan_create_impl(const hmx_matrix_desc* d, int device, const hmx_plan_o
         // (SGEMV-order plans: at most kChainWarpsMixed chain warps, so that three
         // CTAs with their column FIFOs fit an SM)
         if (!chain_order && (kSegThreads - wb) / 32 > kChainWarpsMixed) continue;
-        const double t = std::max(acc64_weight * (double)colsA / (double)ga, (double)lpt(wB, gb, nullptr));
+        const double t = std::max(acc64_weight * (double)colsA / (double)ga, (double)lpt(cB, gb, nullptr));
         if (t < best) {
           best = t;
           fg.wb = wb;
@@ -488,7 +497,7 @@ int hmx::plan_create_impl(const hmx_matrix_desc* d, int device, const hmx_plan_o
     fg.cw = (wB.empty() || chain_order) ? 0 : (kSegThreads - fg.wb) / 32;
     if (gB > 0) {
       std::vector<int32_t> owner;
-      lpt(wB, gB, &owner);
+      lpt(cB, gB, &owner);
       std::vector<ItemRef> chains(lst.begin() + (ptrdiff_t)nA, lst.end());
       std::vector<int64_t> load((size_t)gB, 0);
       size_t k = nA;
