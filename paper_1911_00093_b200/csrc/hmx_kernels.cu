@@ -118,20 +118,17 @@ __device__ __forceinline__ double z_epilogue(const DevPlan& P, double s, int zi)
   return s;
 }
 
-// FP32-accumulated items (RUN_CHUNK, layout chunk_off in hmx_internal.cuh):
-// each row's value in OpenBLAS SGEMV-T's order, widened once and added in
-// FP64 (reference matvec.py:57, :73, then :106).  Explicit _rn intrinsics:
-// nothing is contracted or reassociated.
+// FP32-accumulated items: each row's value in OpenBLAS SGEMV-T's order,
+// widened once and added in FP64 (reference matvec.py:57, :73, then :106).
+// Explicit _rn intrinsics: nothing is contracted or reassociated.
 //
-// Every chain WARP owns one thread group of the segment (hmx_plan.cu deals the
-// chain items to the groups and lays each group's items out contiguously), so
-// its items are one contiguous byte stream.  The warp pulls that stream
-// through a private ring in shared memory -- kRingStages windows, each filled
-// by one bulk copy (cp.async.bulk, TMA engine) that lane 0 issues as soon as
-// the warp has consumed the window that held the slot -- and evaluates its
-// items from the ring, rows `lane` and `lane + 32` of every item (one or two
-// rows per thread).  Items may straddle windows: the ring is addressed by
-// stream offset.  No barrier is shared between warps.
+// Stage 2 gives these items to the lanes of the chain warps (chain_lane
+// below): slots of rp / 4 lanes, four rows per lane, each slot one thread
+// group of the segment (hmx_plan.cu deals the items to the groups and lays
+// every group's items out contiguously, widest first).  A lane streams its
+// slot's columns through a private cp.async FIFO in shared memory
+// (ChainFifo) and reads back only its own copies: no barrier is shared
+// between lanes or warps.
 __device__ __forceinline__ float4 fma4(float4 a, float4 g, float4 c) {
   return make_float4(__fmaf_rn(a.x, g.x, c.x), __fmaf_rn(a.y, g.y, c.y), __fmaf_rn(a.z, g.z, c.z),
                      __fmaf_rn(a.w, g.w, c.w));
@@ -159,26 +156,7 @@ __device__ __forceinline__ float ld_one(const float* p) {
 __device__ __forceinline__ void chain_bar(int nthreads) {
   asm volatile("bar.sync 1, %0;" ::"r"(nthreads) : "memory");
 }
-// mbarrier + 1-D bulk copy (TMA engine): one thread moves a whole window
 __device__ __forceinline__ uint32_t smem_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
-__device__ __forceinline__ void mbar_init(uint64_t* b) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(b)) : "memory");
-}
-// arrive on `b` expecting `bytes` and start the copy
-__device__ __forceinline__ void bulk_to_smem(float* dst, const float* src, uint32_t bytes, uint64_t* b) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(b)), "r"(bytes) : "memory");
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                   smem_addr(dst)),
-               "l"(src), "r"(bytes), "r"(smem_addr(b))
-               : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
-  asm volatile(
-      "{\n .reg .pred P1;\n WAIT:\n mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n @P1 bra DONE;\n bra WAIT;\n "
-      "DONE:\n }" ::"r"(smem_addr(b)),
-      "r"(parity)
-      : "memory");
-}
 
 constexpr int kMetaW = 12;  // run meta in shared memory: col0 << 12 | width
 
@@ -582,9 +560,13 @@ __global__ void __launch_bounds__(kS1ExactRows) s1_exact_kernel(DevPlan P, const
   const int n = sg.W32, rp = (sg.R + 3) & ~3;
   const float* __restrict__ it = P.blob32 + sg.off32;
   const double* __restrict__ xs = x + run.src;
-  // the FP32 source shadow (matvec.py:119): x rounded once
-  auto G = [&](int c) { return (float)__ldg(xs + c); };
-  auto G4 = [&](int c) { return make_float4(G(c), G(c + 1), G(c + 2), G(c + 3)); };
+  // the FP32 source shadow (matvec.py:119): x rounded once, staged in shared
+  // memory for the whole CTA (a block is at most 4096 columns wide)
+  __shared__ __align__(16) float xs32[4 * kSgemvBlock];
+  for (int c = t; c < n; c += kS1ExactRows) xs32[c] = (float)__ldg(xs + c);
+  __syncthreads();
+  auto G = [&](int c) { return xs32[c]; };
+  auto G4 = [&](int c) { return *reinterpret_cast<const float4*>(xs32 + c); };
   float y = 0.f;
   const int kind = t < sg.R ? P.zkind[sg.row0 + t] : 16;
   if (t >= sg.R) {
@@ -662,10 +644,11 @@ __global__ void __launch_bounds__(kS1ExactRows) s1_exact_kernel(DevPlan P, const
 // CTAs per SM (80 registers) instead of 8 at 4 (A/B on config 4: m1-double
 // stage 2 -1.1 %, m2-double -2.4 %; FP32-only stage 2 prefers 8 at 4)
 // EXACT (stage 2 with FP32-accumulated items): those items in SGEMV's order
-// (chain_windows); otherwise one FP32 chain per (row, item) (HMX_PLAN_FP32_CHAIN).
+// (chain_lane); otherwise one FP32 chain per (row, item) (HMX_PLAN_FP32_CHAIN).
 // Separate instantiations keep each one's register allocation its own.
-// XMINB: CTAs per SM of an EXACT instantiation (its register budget; m2-single
-// measured faster at 3 = 80 registers, m1-mixed at 4).
+// XMINB: CTAs per SM of an EXACT instantiation: 3 (80 registers; up to six chain
+// warps' FIFOs fit beside the static shared memory) for mixed parts, 2 for the
+// all-chain m1-single (eight chain warps).
 template <int F32MODE, int OUT, int NT, bool DEEP = false, bool EXACT = false, int XMINB = HMX_EXACT_MINB>
 __global__ void __launch_bounds__(NT, DEEP ? 3 : (OUT == OUT_Y && F32MODE != F32_ALL64) ? (EXACT ? XMINB : HMX_MIXED_MINB) : 1024 / NT) seg_kernel(DevPlan P, const Seg* __restrict__ segs,
                                                           const double* __restrict__ x, S2Out out) {
@@ -870,7 +853,7 @@ __global__ void __launch_bounds__(NT, DEEP ? 3 : (OUT == OUT_Y && F32MODE != F32
       // row is one FP32 chain (reference: FP32 GEMV per block, matvec.py:57, :73)
       cb = P.gtab[sg.gtab + q32];
       ce = P.gtab[sg.gtab + q32 + 1];
-      if (chain_thr) ce = cb;  // (their items: chain_items after the tile loop)
+      if (chain_thr) ce = cb;  // (their items: chain_lane after the tile loop)
     }
     // [cb, cm): FP64-accumulated columns, [cm, ce): FP32-accumulated ones
     const int cm = min(ce, max(cb, c32 - tc0));

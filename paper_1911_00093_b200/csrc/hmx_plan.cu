@@ -518,7 +518,7 @@ int hmx::plan_create_impl(const hmx_matrix_desc* d, int device, const hmx_plan_o
     }
     return fg;
   };
-  int64_t chain_warps_max = 0;
+  int64_t chain_warps_max = 0, n_chain_fallback = 0;
   for (int64_t s = 0; s < nseg2; ++s) {
     Seg& sg = seg2[(size_t)s];
     sg.row0 = (int32_t)seg_start[(size_t)s];
@@ -580,7 +580,10 @@ int hmx::plan_create_impl(const hmx_matrix_desc* d, int device, const hmx_plan_o
       for (int64_t c : fg.cuts) gtab.push_back((int32_t)c);
       gtab.push_back((int32_t)fg.c32);
       sg.chunk = (int32_t)fg.wb;
-    } else if (sg.W32 > kSegWMax && (dense_single || u_acc32)) {
+    } else if (sg.W32 > 0 && (dense_single || u_acc32)) {
+      // (a part wider than the staging tile, or with too many runs: its FP32-
+      // accumulated items fall back to one FP32 chain per (row, item))
+      ++n_chain_fallback;
       // wide part (tiled, no group cuts): only the first FP32-accumulated column
       int32_t first = sg.W32;
       for (int32_t j = 0; j < sg.nrun32; ++j) {
@@ -856,8 +859,11 @@ int hmx::plan_create_impl(const hmx_matrix_desc* d, int device, const hmx_plan_o
     if (rc2 != HMX_OK) return rc2;
   }
   if (std::getenv("HMX_PLAN_TIMING"))
-    std::fprintf(stderr, "hmx_plan_create: layout %.3f s, pack+upload %.3f s (%.2f GB)\n", t_meta,
-                 secs() - t_meta, (off64 * 8.0 + off32 * 4.0) / 1e9);
+    std::fprintf(stderr,
+                 "hmx_plan_create: layout %.3f s, pack+upload %.3f s (%.2f GB); stage-2 segments %lld, "
+                 "chain warps <= %lld, parts without a group table (FP32 items as plain chains) %lld\n",
+                 t_meta, secs() - t_meta, (off64 * 8.0 + off32 * 4.0) / 1e9, (long long)nseg2,
+                 (long long)chain_warps_max, (long long)n_chain_fallback);
   double* d_zs = p->alloc<double>(zscale.size());
   if ((rc = up(d_zs, zscale))) return rc;
   uint8_t* d_zk = p->alloc<uint8_t>(zkind.size());

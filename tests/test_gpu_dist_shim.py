@@ -114,8 +114,22 @@ def test_multiprocess_dist_path(hx, cfg, tmp_path, world, mode):
         rep = reps[0]
         assert rep["breakdown"] is None and rep["true_residual"] is not None
         assert rep["converged"] == (rep["true_residual"] < 1e-8)
-        assert abs(rep["iterations"] - ref.iterations) <= max(2, ref.iterations // 10), \
-            (s, rep["iterations"], ref.iterations)
+        # the row cut changes the FP64 group order of every product (last-ulp
+        # differences), so only the converging FP64 scheme has a stable stop
+        # iteration; the FP32-storage schemes stop where the recurrence residual
+        # first dips under 1e-8 on their FP32 noise floor (the reference's own
+        # threads=1..8 envelope is 19-22 iterations for m1-mixed at config 1):
+        # same flag, the same residual floor, iterations within 25 %
+        if s == "m1-double":
+            assert abs(rep["iterations"] - ref.iterations) <= max(2, ref.iterations // 10), \
+                (s, rep["iterations"], ref.iterations)
+        else:
+            assert abs(rep["iterations"] - ref.iterations) <= max(3, ref.iterations // 4), \
+                (s, rep["iterations"], ref.iterations)
+            assert rep["converged"] == ref.converged, s
+            if not ref.converged:
+                assert 0.5 <= rep["true_residual"] / ref.true_residual <= 2.0, \
+                    (s, rep["true_residual"], ref.true_residual)
         xs = np.empty(n)
         xs[perm] = np.concatenate([np.asarray(r["schemes"][s]["x_solve"]) for r in res])
         tol = 1e-6 if s == "m1-double" else 1e-4

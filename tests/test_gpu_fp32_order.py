@@ -2,10 +2,10 @@
 U slabs, m2-single dense blocks; reference matvec.py:57, :73 -- numpy
 `A32 @ x32`, i.e. OpenBLAS SGEMV).
 
-The GPU evaluates every such item in SGEMV's own summation tree, one row
-per thread (csrc/hmx_internal.cuh chunk_off layout, chain_items in
-csrc/hmx_kernels.cu).  Checked
-here:
+The GPU evaluates every such item in SGEMV's own summation tree (stage 2:
+chain_lane / chain_quad in csrc/hmx_kernels.cu, four rows per lane from a
+per-lane cp.async FIFO; stage 1 of m1-single: s1_exact_kernel, one row per
+thread over the csrc/hmx_internal.cuh chunk_off layout).  Checked here:
   * CPU: the kernel's order, modelled in tools/fp32_accum_emulation.py
     (sgemv_rows: SGEMV's 16/8/4-row kernels and its 2- and 1-row remainder
     kernels), reproduces the reference's products bitwise
