@@ -116,7 +116,10 @@ constexpr int kS1WMax = 1024;     // max columns per stage-1 segment chunk
 #define HMX_S1X_ROWS 128
 #endif
 constexpr int kS1ExactRows = HMX_S1X_ROWS;  // m1-single stage 1: rank rows per CTA (one thread each)
-constexpr int kChainWarpsMixed = 6;
+#ifndef HMX_CHAIN_WARPS_MIXED
+#define HMX_CHAIN_WARPS_MIXED 6
+#endif
+constexpr int kChainWarpsMixed = HMX_CHAIN_WARPS_MIXED;
 constexpr int kChainRunsMax = 1024;  // most runs of a stage-2 FP32 part with SGEMV-order chain lanes (meta in shared memory)  // SGEMV-order stage 2: most chain warps beside widened warps in one CTA
 constexpr int kSgemvBlock = 1024; // OpenBLAS SGEMV-T column blocking: 4096 columns = 1024 chunks
 

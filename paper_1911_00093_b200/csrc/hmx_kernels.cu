@@ -20,6 +20,18 @@
 #ifndef HMX_MIXED_MINB
 #define HMX_MIXED_MINB 4
 #endif
+#ifndef HMX_FIFO_BATCHES_MIXED
+#define HMX_FIFO_BATCHES_MIXED 3  // chain lanes' FIFO depth (batches) in parts with widened warps (A/B at config 4: 2: +3 %, 4: +5 % on m1-mixed stage 2)
+#endif
+#ifndef HMX_FIFO_BATCHES_ALL32
+#define HMX_FIFO_BATCHES_ALL32 3  // ... in all-chain parts (m1-single: eight chain warps, three CTAs per SM)
+#endif
+#ifndef HMX_CHAIN_PAIR
+#define HMX_CHAIN_PAIR 0  // chain lanes: reduce the A and B chunk of a pair after one wait
+#endif
+#ifndef HMX_EXACT_MINB_ALL32
+#define HMX_EXACT_MINB_ALL32 3
+#endif
 #ifndef HMX_EXACT_MINB
 #define HMX_EXACT_MINB 3  // CTAs per SM of the SGEMV-order stage-2 kernels with <= 5 chain warps (registers; FIFOs)
 #endif
@@ -372,27 +384,32 @@ __device__ __forceinline__ float4 chain_quad_kinds(CF C, GF G, BF before, int n,
 // (rp / 4 lanes, four rows each) stream the columns of their group --
 // contiguous in the blob -- with 16-byte cp.async copies in BATCHES: the
 // 4-column chunks of each item and its 1..3 tail columns, one commit group
-// per batch, kFifoBatches batch slots per lane.  A batch is consumed whole
-// (one chunk of SGEMV's A/B accumulators, or the tail), so while one is
-// reduced the other three are in flight.  Every lane reads back only what it
+// per batch, NB batch slots per lane.  A batch is consumed whole (one chunk
+// of SGEMV's A/B accumulators, or the tail), so while one is reduced the
+// other NB - 1 are in flight.  Every lane reads back only what it
 // copied itself: nothing is synchronised between lanes.
-constexpr int kFifoBatches = 4;
-constexpr int kFifoBytes = kFifoBatches * 4 * 512;  // per chain warp: 16 bytes x 32 lanes per column
+constexpr int kMetaWide = 1 << 30;  // run meta: an FP64-accumulated (widened) item on a chain lane
+__device__ __forceinline__ int meta_col0(int32_t m) { return (m >> kMetaW) & 0x3ffff; }
+__device__ __forceinline__ int meta_width(int32_t m) { return m & ((1 << kMetaW) - 1); }
+template <int NB>  // batch slots per lane
 struct ChainFifo {
+  static constexpr int kBytes = NB * 4 * 512;  // per chain warp: 16 bytes x 32 lanes per column
   const float* srcp;     // this lane's four rows of the next column to copy
   const float* fifo;     // this lane's 16 bytes of batch slot 0, column 0 (column u: + 128 u, slot b: + 512 b floats)
   uint32_t fifo_s;       // ... its shared-space address
-  const int32_t* meta;   // run meta (col0 << kMetaW | width) in shared memory
+  const int32_t* meta;   // run meta in shared memory
   int rp;
   int ij, je;            // next item to copy from / end of the lane's items
   int irem;              // columns of item ij not yet copied
   int ib = 0;            // batches copied or in flight
   int cb = 0;            // batches consumed
+  int islot = 0;         // ib mod NB
+  int cslot = 0;         // cb mod NB
 
   // copy the next batch (a chunk or the tail of item ij); ij < je
   __device__ __forceinline__ void issue() {
     const int cols = min(4, irem);
-    const uint32_t dst = fifo_s + (uint32_t)(ib & (kFifoBatches - 1)) * 2048u;
+    const uint32_t dst = fifo_s + (uint32_t)islot * 2048u;
     if (cols == 4) {
 #pragma unroll
       for (int u = 0; u < 4; ++u)
@@ -405,41 +422,49 @@ struct ChainFifo {
     }
     asm volatile("cp.async.commit_group;\n" ::: "memory");
     ++ib;
+    islot = islot == NB - 1 ? 0 : islot + 1;
     srcp += (int64_t)cols * rp;
     irem -= cols;
-    if (irem == 0 && ++ij < je) irem = meta[ij] & ((1 << kMetaW) - 1);
+    if (irem == 0 && ++ij < je) irem = meta_width(meta[ij]);
   }
   __device__ __forceinline__ void start(const int32_t* m, int jb, int je_) {
     meta = m;
     ij = jb;
     je = je_;
-    irem = jb < je_ ? (m[jb] & ((1 << kMetaW) - 1)) : 0;
-    while (ib < kFifoBatches && ij < je) issue();
+    irem = jb < je_ ? meta_width(m[jb]) : 0;
+    while (ib < NB && ij < je) issue();
   }
   // batch bt (cb <= bt < ib) has landed
   __device__ __forceinline__ void need(int bt) {
     const int pend = ib - bt;  // 1 + the batches copied after it
-    if (pend >= 4) asm volatile("cp.async.wait_group 3;\n" ::: "memory");
-    else if (pend == 3) asm volatile("cp.async.wait_group 2;\n" ::: "memory");
+    if (NB >= 4 && pend >= 4) asm volatile("cp.async.wait_group 3;\n" ::: "memory");
+    else if (pend >= 3) asm volatile("cp.async.wait_group 2;\n" ::: "memory");
     else if (pend == 2) asm volatile("cp.async.wait_group 1;\n" ::: "memory");
     else asm volatile("cp.async.wait_group 0;\n" ::: "memory");
   }
-  // batches < bt are consumed: refill their slots
+  // batches < bt are consumed (bt - cb <= NB): refill their slots
   __device__ __forceinline__ void done(int bt) {
+    cslot += bt - cb;
+    if (cslot >= NB) cslot -= NB;
     cb = bt;
-    while (ib - cb < kFifoBatches && ij < je) issue();
+    while (ib - cb < NB && ij < je) issue();
   }
   // one more batch is consumed
   __device__ __forceinline__ void done1() {
     ++cb;
-    if (ij < je) issue();  // (ib - cb was kFifoBatches - 1 or the stream is exhausted)
+    cslot = cslot == NB - 1 ? 0 : cslot + 1;
+    if (ij < je) issue();  // (ib - cb was NB - 1 or the stream is exhausted)
   }
-  // column u of batch bt (cb <= bt < cb + kFifoBatches), this lane's four rows
+  // column u of batch bt (cb <= bt < cb + NB), this lane's four rows
   __device__ __forceinline__ float4 col(int bt, int u) const {
-    return *reinterpret_cast<const float4*>(fifo + (bt & (kFifoBatches - 1)) * 512 + u * 128);
+    int sl = cslot + (bt - cb);
+    if (sl >= NB) sl -= NB;
+    return *reinterpret_cast<const float4*>(fifo + sl * 512 + u * 128);
   }
   // this lane's 16 bytes of column 0 of the batch being consumed
-  __device__ __forceinline__ const float* cur() const { return fifo + (cb & (kFifoBatches - 1)) * 512; }
+  __device__ __forceinline__ const float* cur() const { return fifo + cslot * 512; }
+  // ... of the batch after it
+  __device__ __forceinline__ const float* nxt() const { return fifo + (cslot == NB - 1 ? 0 : cslot + 1) * 512; }
 };
 
 // One chain lane: items jb .. je-1 of the part (meta / kbits in shared memory)
@@ -447,16 +472,40 @@ struct ChainFifo {
 // b[0..3] (FP64, item order).  Every row's value is in OpenBLAS SGEMV-T's
 // order (chain_quad: all rows in the 16-row kernel / 16-8-4-row kernels;
 // otherwise chain_item / chain_quad_kinds per row kind).
-__device__ __forceinline__ void chain_lane(ChainFifo& F, const int32_t* meta, const uint32_t* kbits, int jb, int je,
+template <int NB>
+__device__ __forceinline__ void chain_lane(ChainFifo<NB>& F, const int32_t* meta, const uint32_t* kbits, int jb, int je,
                                            const double* gs, int rp, int t, double* b) {
   F.start(meta, jb, je);
   int j = jb;
   // (uniform trip count over the warp, so the slots stay converged item by item)
   while (__any_sync(0xffffffffu, j < je)) {
     if (j < je) {
-      const int c0 = meta[j] >> kMetaW, n = meta[j] & ((1 << kMetaW) - 1);
-      const uint32_t kb = kbits[j];
+      const int32_t mj = meta[j];
+      const int c0 = meta_col0(mj), n = meta_width(mj);
       const double* gj = gs + c0;
+      if (mj & kMetaWide) {
+        // an FP64-accumulated item (FP32 data widened; reference matvec.py:59, :86):
+        // batch by batch straight into the row sums
+        auto L = [](const float* p, int u) { return *reinterpret_cast<const float4*>(p + u * 128); };
+        for (int k0 = 0; k0 < n; k0 += 4) {
+          F.need(F.cb);
+          const float* p = F.cur();
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            if (k0 + u < n) {
+              const float4 x = L(p, u);
+              const double g = gj[k0 + u];
+              b[0] = fma((double)x.x, g, b[0]);
+              b[1] = fma((double)x.y, g, b[1]);
+              b[2] = fma((double)x.z, g, b[2]);
+              b[3] = fma((double)x.w, g, b[3]);
+            }
+          F.done1();
+        }
+        ++j;
+        continue;
+      }
+      const uint32_t kb = kbits[j];
       auto G = [&](int q) { return __int_as_float(__double2loint(gj[q])); };
       const int b0 = F.cb;  // the item's first batch; column q sits in batch b0 + q / 4
       auto C = [&](int q) { return F.col(b0 + (q >> 2), q & 3); };
@@ -496,6 +545,18 @@ __device__ __forceinline__ void chain_lane(ChainFifo& F, const int32_t* meta, co
           c = 1;
         }
         for (; c < nch; c += 2) {
+#if HMX_CHAIN_PAIR
+          // the A and the B chunk of a pair together (one wait, eight loads in flight)
+          F.need(F.cb + 1);
+          const float* pa = F.cur();
+          const float* pb = F.nxt();
+#pragma unroll
+          for (int q = 0; q < 4; ++q) A[q] = fmas4(L(pa, q), G(4 * c + q), A[q]);
+#pragma unroll
+          for (int q = 0; q < 4; ++q) B[q] = fmas4(L(pb, q), G(4 * c + 4 + q), B[q]);
+          F.done1();
+          F.done1();
+#else
           F.need(F.cb);
           const float* pa = F.cur();
 #pragma unroll
@@ -506,6 +567,7 @@ __device__ __forceinline__ void chain_lane(ChainFifo& F, const int32_t* meta, co
 #pragma unroll
           for (int q = 0; q < 4; ++q) B[q] = fmas4(L(pb, q), G(4 * c + 4 + q), B[q]);
           F.done1();
+#endif
         }
         v = add4(add4(add4(A[0], B[0]), add4(A[1], B[1])), add4(add4(A[2], B[2]), add4(A[3], B[3])));
         if (T > 0) {
@@ -646,9 +708,8 @@ __global__ void __launch_bounds__(kS1ExactRows) s1_exact_kernel(DevPlan P, const
 // EXACT (stage 2 with FP32-accumulated items): those items in SGEMV's order
 // (chain_lane); otherwise one FP32 chain per (row, item) (HMX_PLAN_FP32_CHAIN).
 // Separate instantiations keep each one's register allocation its own.
-// XMINB: CTAs per SM of an EXACT instantiation: 3 (80 registers; up to six chain
-// warps' FIFOs fit beside the static shared memory) for mixed parts, 2 for the
-// all-chain m1-single (eight chain warps).
+// XMINB: CTAs per SM of an EXACT instantiation: 3 (80 registers; the chain
+// warps' FIFOs -- 6 KB each -- fit beside the static shared memory).
 template <int F32MODE, int OUT, int NT, bool DEEP = false, bool EXACT = false, int XMINB = HMX_EXACT_MINB>
 __global__ void __launch_bounds__(NT, DEEP ? 3 : (OUT == OUT_Y && F32MODE != F32_ALL64) ? (EXACT ? XMINB : HMX_MIXED_MINB) : 1024 / NT) seg_kernel(DevPlan P, const Seg* __restrict__ segs,
                                                           const double* __restrict__ x, S2Out out) {
@@ -661,7 +722,7 @@ __global__ void __launch_bounds__(NT, DEEP ? 3 : (OUT == OUT_Y && F32MODE != F32
   // its gather flags share red32 (flags: gather phases; red32: after them), so
   // three CTAs and their chain FIFOs fit an SM.
   constexpr bool XS = EXACT && OUT == OUT_Y && F32MODE != F32_ALL64;
-  // the chain lanes' column FIFOs (stage-2 FP32 kernels; dynamic: kFifoBytes x P.chain_warps)
+  // the chain lanes' column FIFOs (stage-2 FP32 kernels; dynamic: ChainFifo<NB>::kBytes x P.chain_warps)
   extern __shared__ __align__(128) float chain_buf[];
   __shared__ uint8_t fl_own[XS ? 1 : WMAX];
   __shared__ int32_t sidx_own[(OUT == OUT_Z || (EXACT && F32MODE != F32_ALL64)) ? 1 : kSegWMax];
@@ -760,7 +821,8 @@ __global__ void __launch_bounds__(NT, DEEP ? 3 : (OUT == OUT_Y && F32MODE != F32
   // wbc (plan: sg.chunk) is warp-aligned, so no warp runs both loops.
   bool chain_thr = false, chain_warp = false;
   int cg0 = 0, cg1 = 0;
-  ChainFifo cfifo;
+  constexpr int NB = F32MODE == F32_ALL32 ? HMX_FIFO_BATCHES_ALL32 : HMX_FIFO_BATCHES_MIXED;
+  ChainFifo<NB> cfifo;
   if constexpr (F32MODE == F32_MIXED && OUT == OUT_Y) {
     // (HMX_PLAN_FP32_CHAIN plans: one FP32 FMA chain per (row, item), 4 rows
     // per thread on both sides of the warp-aligned split at wb = sg.chunk)
@@ -799,7 +861,7 @@ __global__ void __launch_bounds__(NT, DEEP ? 3 : (OUT == OUT_Y && F32MODE != F32
           cg1 = P.gtab[sg.gtab + q32 + 1];
           cfifo.rp = rp32;
           cfifo.srcp = P.blob32 + sg.off32 + (int64_t)cg0 * rp32 + 4 * p32;
-          cfifo.fifo = chain_buf + (size_t)cw * (kFifoBytes / 4) + 4 * lane;
+          cfifo.fifo = chain_buf + (size_t)cw * (ChainFifo<NB>::kBytes / 4) + 4 * lane;
           cfifo.fifo_s = smem_addr(cfifo.fifo);
         }
       }
@@ -963,7 +1025,7 @@ __global__ void __launch_bounds__(NT, DEEP ? 3 : (OUT == OUT_Y && F32MODE != F32
       const Run* runs = P.runs + sg.run0 + sg.nrun64;
       for (int j = tid - wbc; j < sg.nrun32; j += NT - wbc) {
         const Run r = runs[j];
-        meta[j] = (r.col0 << kMetaW) | r.width;
+        meta[j] = ((r.flags & RUN_ACC32) ? 0 : kMetaWide) | (r.col0 << kMetaW) | r.width;
         kbits[j] = (uint32_t)r.flags >> kRunKindShift;
       }
       chain_bar(NT - wbc);
@@ -972,7 +1034,7 @@ __global__ void __launch_bounds__(NT, DEEP ? 3 : (OUT == OUT_Y && F32MODE != F32
         int lo = 0, hi = sg.nrun32;
         while (lo < hi) {
           const int mid = (lo + hi) >> 1;
-          if ((meta[mid] >> kMetaW) < col) lo = mid + 1;
+          if (meta_col0(meta[mid]) < col) lo = mid + 1;
           else hi = mid;
         }
         return lo;
@@ -1162,9 +1224,10 @@ __global__ void probe_kernel(DevPlan P, const double* __restrict__ x, unsigned l
 template <int M, int O, bool EXACT>
 static size_t chain_smem(const DevPlan& P) {
   // (at least the gather's index scratch, which shares the memory)
-  return (EXACT && O == OUT_Y && M != F32_ALL64) ? std::max((size_t)P.chain_warps * kFifoBytes, (size_t)kSegWMax * 4) : 0;
+  constexpr size_t fifo = ChainFifo<M == F32_ALL32 ? HMX_FIFO_BATCHES_ALL32 : HMX_FIFO_BATCHES_MIXED>::kBytes;
+  return (EXACT && O == OUT_Y && M != F32_ALL64) ? std::max((size_t)P.chain_warps * fifo, (size_t)kSegWMax * 4) : 0;
 }
-constexpr int kChainSmemMax = (kSegThreads / 32) * kFifoBytes;
+constexpr int kChainSmemMax = (kSegThreads / 32) * 4 * 4 * 512;
 
 template <int M, int O, int NT = kSegThreads, bool DEEP = false, bool EXACT = false, int XMINB = HMX_EXACT_MINB>
 static cudaError_t launch_seg(const DevPlan& P, const Seg* segs, int nseg, const double* x,
@@ -1210,7 +1273,7 @@ cudaError_t launch_stage2(const DevPlan& P, const double* x, const S2Out& out, c
   if (P.n_seg2 == 0) return cudaSuccess;
   switch (P.f32mode2) {
     case F32_ALL32:
-      return P.chain_exact ? launch_seg<F32_ALL32, OUT_Y, kSegThreads, false, true, 2>(P, P.seg2, P.n_seg2, x, out, st, pdl)
+      return P.chain_exact ? launch_seg<F32_ALL32, OUT_Y, kSegThreads, false, true, HMX_EXACT_MINB_ALL32>(P, P.seg2, P.n_seg2, x, out, st, pdl)
                            : launch_seg<F32_ALL32, OUT_Y>(P, P.seg2, P.n_seg2, x, out, st, pdl);
     case F32_MIXED:
       if (!P.chain_exact) return launch_seg<F32_MIXED, OUT_Y>(P, P.seg2, P.n_seg2, x, out, st, pdl);
@@ -1224,7 +1287,7 @@ cudaError_t launch_stage2(const DevPlan& P, const double* x, const S2Out& out, c
 // The stage-2 FP32 kernels opt in to > 48 KB of shared memory (static + the
 // chain staging buffers); called at plan creation, outside any capture.
 cudaError_t configure_kernels() {
-  cudaError_t e = cudaFuncSetAttribute(seg_kernel<F32_ALL32, OUT_Y, kSegThreads, false, true, 2>,
+  cudaError_t e = cudaFuncSetAttribute(seg_kernel<F32_ALL32, OUT_Y, kSegThreads, false, true, HMX_EXACT_MINB_ALL32>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        kChainSmemMax);
   if (e == cudaSuccess)

@@ -393,6 +393,8 @@ int hmx::plan_create_impl(const hmx_matrix_desc* d, int device, const hmx_plan_o
   // m1-mixed best at 0.8-1.0, m2-single at 1/1.0-1/1.2)
   const char* aw_env = std::getenv("HMX_ACC64_WEIGHT");
   const double acc64_weight = aw_env ? std::atof(aw_env) : (chain_order ? 0.85 : 1.4);
+  const char* al_env = std::getenv("HMX_ALL_LANES");
+  const bool all_lanes = al_env ? std::atoi(al_env) != 0 : false;
   const char* ic_env = std::getenv("HMX_CHAIN_ITEM_COST");
   const int64_t chain_item_cost = ic_env ? std::atoll(ic_env) : 8;
   const bool dense_single = pipe == P_M1S || pipe == P_M2S;  // A32 . x32 in FP32
@@ -469,6 +471,41 @@ int hmx::plan_create_impl(const hmx_matrix_desc* d, int device, const hmx_plan_o
     }
     fg.c32 = colsA;
     int64_t gA = 0, gB = Gc;
+    if (all_lanes && !chain_order && nA > 0 && !wB.empty()) {
+      // SGEMV-order plans, all-lanes mode: no widened warps.  Every item of the
+      // part -- widened ones too (FP64 accumulation on the same lanes) -- is
+      // dealt to the lane slots of all eight warps by LPT on its estimated
+      // cost, so no warp waits for the other kind.  A slot's widened items come
+      // first, then its chain items widest first.
+      std::vector<int64_t> cost(lst.size());
+      for (size_t i = 0; i < lst.size(); ++i)
+        cost[i] = i < nA ? (int64_t)std::ceil(acc64_weight * (double)item_width(lst[i])) + 2
+                         : item_width(lst[i]) + chain_item_cost;
+      std::vector<int32_t> owner;
+      lpt(cost, Gc, &owner);
+      const std::vector<ItemRef> all(lst.begin(), lst.end());
+      fg.cuts.push_back(0);
+      size_t k = 0;
+      for (int64_t g = 0; g < Gc; ++g) {
+        std::vector<size_t> mine;
+        for (size_t i = 0; i < all.size(); ++i)
+          if (owner[i] == g) mine.push_back(i);
+        std::stable_sort(mine.begin(), mine.end(), [&](size_t a, size_t b) {
+          if ((a < nA) != (b < nA)) return a < nA;
+          return a >= nA && item_width(all[a]) > item_width(all[b]);
+        });
+        int64_t load = 0;
+        for (size_t i : mine) {
+          lst[k++] = all[i];
+          load += item_width(all[i]);
+        }
+        fg.cuts.push_back(fg.cuts.back() + load);
+      }
+      fg.c32 = 0;
+      fg.wb = 0;
+      fg.cw = kSegThreads / 32;
+      return fg;
+    }
     if (nA > 0 && !wB.empty()) {
       double best = 1e300;
       for (int64_t wb = 32; wb < kSegThreads; wb += 32) {

@@ -1,4 +1,6 @@
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests/test_gpu_fp32_order.py tests/test_gpu_parity.py tests/test_gpu_prepare.py -m gpu -x -q > gpurun_out/t_x.log 2>&1; echo "tests rc=$?"; tail -3 gpurun_out/t_x.log
-bash tools/quick_bench.sh --variants m1-single m1-mixed; python tools/show_bench.py gpurun_out/qb.json 2>/dev/null | tail -2
-timeout 600 python bench.py --config 2 --steps 200 --warmup 10 --no-cpu-baseline --no-solve --variants m1-single m1-mixed > gpurun_out/qb2.json 2>/dev/null; python tools/show_bench.py gpurun_out/qb2.json | tail -2
+V="--variants m1-mixed m1-single m2-single"
+for n in nb3 nb3c7 nb2m3 nb2m4 nb3; do
+export HMX_GPU_LIB=paper_1911_00093_b200/lib/ab/$n/libhmx_gpu.so
+echo "== $n"; bash tools/quick_bench.sh $V; python tools/show_bench.py gpurun_out/qb.json | tail -3
+done
