@@ -757,8 +757,9 @@ __global__ void __launch_bounds__(NT, DEEP ? 3 : (OUT == OUT_Y && F32MODE != F32
   for (int tc0 = 0; tc0 < sg.W64; tc0 += WMAX) {
     const int tw = min(WMAX, sg.W64 - tc0);
     const bool act = q64 < g64;
-    const int cb = act ? (int)((int64_t)tw * q64 / g64) : 0;
-    const int ce = act ? (int)((int64_t)tw * (q64 + 1) / g64) : 0;
+    // (tw <= WMAX <= 2048 and q64 < g64 <= NT: the products fit 32 bits)
+    const int cb = act ? (int)((unsigned)(tw * q64) / (unsigned)g64) : 0;
+    const int ce = act ? (int)((unsigned)(tw * (q64 + 1)) / (unsigned)g64) : 0;
     const double* __restrict__ col = P.blob64 + sg.off64 + (int64_t)tc0 * rp64 + 2 * p64;
     // D64 columns in flight per thread (stage 2, FP64-only kernels: deeper,
     // at fewer resident CTAs), predicated at the end of the range (a short
@@ -842,7 +843,7 @@ __global__ void __launch_bounds__(NT, DEEP ? 3 : (OUT == OUT_Y && F32MODE != F32
   }
   if constexpr (EXACT && F32MODE != F32_ALL64 && OUT == OUT_Y) {
     if (sg.gtab >= 0) {
-      const int wbc = F32MODE == F32_ALL32 ? 0 : sg.chunk;
+      const int wbc = sg.chunk;  // (0: every warp is a chain warp)
       // chain lanes: slots of tpg32 lanes inside each warp, one group per slot
       const int nslot = min(32 / tpg32, 8);
       const int ga = wbc / tpg32, gb = ((NT - wbc) >> 5) * nslot;
@@ -908,8 +909,8 @@ __global__ void __launch_bounds__(NT, DEEP ? 3 : (OUT == OUT_Y && F32MODE != F32
   for (int tc0 = 0; tc0 < sg.W32; tc0 += WMAX) {
     const int tw = min(WMAX, sg.W32 - tc0);
     const bool act = q32 < g32;
-    int cb = act ? (int)((int64_t)tw * q32 / g32) : 0;
-    int ce = act ? (int)((int64_t)tw * (q32 + 1) / g32) : 0;
+    int cb = act ? (int)((unsigned)(tw * q32) / (unsigned)g32) : 0;
+    int ce = act ? (int)((unsigned)(tw * (q32 + 1)) / (unsigned)g32) : 0;
     if (F32MODE != F32_ALL64 && OUT == OUT_Y && sg.gtab >= 0 && act) {
       // FP32-accumulated items are never split between groups: every item
       // row is one FP32 chain (reference: FP32 GEMV per block, matvec.py:57, :73)
@@ -1021,7 +1022,7 @@ __global__ void __launch_bounds__(NT, DEEP ? 3 : (OUT == OUT_Y && F32MODE != F32
       // chain warps only: the widened warps stream on meanwhile
       int32_t* meta = reinterpret_cast<int32_t*>(red32);
       uint32_t* kbits = reinterpret_cast<uint32_t*>(red32) + kChainRunsMax;
-      const int wbc = F32MODE == F32_ALL32 ? 0 : sg.chunk;
+      const int wbc = sg.chunk;  // (0: every warp is a chain warp)
       const Run* runs = P.runs + sg.run0 + sg.nrun64;
       for (int j = tid - wbc; j < sg.nrun32; j += NT - wbc) {
         const Run r = runs[j];

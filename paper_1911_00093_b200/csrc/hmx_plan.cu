@@ -395,6 +395,12 @@ int hmx::plan_create_impl(const hmx_matrix_desc* d, int device, const hmx_plan_o
   const double acc64_weight = aw_env ? std::atof(aw_env) : (chain_order ? 0.85 : 1.4);
   const char* al_env = std::getenv("HMX_ALL_LANES");
   const bool all_lanes = al_env ? std::atoi(al_env) != 0 : false;
+  const char* ss_env = std::getenv("HMX_STREAM_SMALL");
+  const bool stream_small = ss_env ? std::atoi(ss_env) != 0 : true;
+  const char* sw_env = std::getenv("HMX_STREAM_WEIGHT");
+  // (a streamed chain column against a lane-tree column; measured at config 5,
+  // where most items are streamed: 1.0: 4.33 ms, 2.5: 3.98, 3.5: 3.94, 5: 4.08; flat at config 4)
+  const double stream_weight = sw_env ? std::atof(sw_env) : 3.0;
   const char* ic_env = std::getenv("HMX_CHAIN_ITEM_COST");
   const int64_t chain_item_cost = ic_env ? std::atoll(ic_env) : 8;
   const bool dense_single = pipe == P_M1S || pipe == P_M2S;  // A32 . x32 in FP32
@@ -443,7 +449,30 @@ int hmx::plan_create_impl(const hmx_matrix_desc* d, int device, const hmx_plan_o
     }
     return *std::max_element(load.begin(), load.end());
   };
-  auto plan_fp32_groups = [&](std::vector<ItemRef>& lst, int64_t R) {
+  // row-kernel bounds of block k's rows seen from a segment starting at row0
+  // (7-bit segment-relative bounds e16 | e8 << 7 | e4 << 14 | e2 << 21, hmx_internal.cuh)
+  auto kind_bits = [&](int64_t k, int64_t row0) {
+    const int64_t* t = d->table + 5 * k;
+    const int64_t mb = t[1] - t[0], d0 = row0 - t[0];  // block row of segment row 0
+    const int64_t a16 = mb & ~int64_t(15), b8 = a16 + (mb & 8), c4 = b8 + (mb & 4);
+    const int64_t c2 = c4 + ((mb & 3) >= 2 ? 2 : 0);
+    auto rel = [&](int64_t bound) { return (uint32_t)std::min<int64_t>(std::max<int64_t>(bound - d0, 0), 127); };
+    return rel(a16) | rel(b8) << 7 | rel(c4) << 14 | rel(c2) << 21;
+  };
+  // An FP32-accumulated item whose SGEMV order is ONE forward FMA chain per
+  // row: widths 1, 3, 5, 6, 7 when every row of the segment is in the 16- or
+  // 8-row kernel, width 2 in the 16-row kernel (hmx_kernels.cu chain_item).
+  // That is exactly what the streaming threads' FP32 chain computes (one chain
+  // per (row, item), started at the item's first column), so SGEMV-order
+  // plans leave such items to the streaming warps, at no per-item cost.
+  auto stream_exact = [&](const ItemRef& it, int64_t row0, int64_t R) {
+    const int64_t n = item_width(it);
+    if (!(n <= 3 || (n >= 5 && n <= 7))) return false;
+    const uint32_t bits = kind_bits(it.block, row0);
+    const int64_t e16 = bits & 127, e8 = (bits >> 7) & 127;
+    return n == 2 ? e16 >= R : e8 >= R;
+  };
+  auto plan_fp32_groups = [&](std::vector<ItemRef>& lst, int64_t R, int64_t row0) {
     FP32Groups fg;
     if (!(dense_single || u_acc32) || lst.empty()) return fg;
     int64_t W = 0;
@@ -506,6 +535,84 @@ int hmx::plan_create_impl(const hmx_matrix_desc* d, int device, const hmx_plan_o
       fg.cw = kSegThreads / 32;
       return fg;
     }
+    if (!chain_order && stream_small && !wB.empty()) {
+      // SGEMV-order plans: [widened | streamed chain items | lane-tree chain items].
+      // Threads [0, wb): gW widened groups (even column cuts) then gS groups of
+      // streamed chain items (whole items, LPT); the chain warps' slots take
+      // the rest.  wb, gW and gS minimise the largest estimated group cost.
+      std::vector<size_t> iS, iT;
+      for (size_t i = nA; i < lst.size(); ++i) (stream_exact(lst[i], row0, R) ? iS : iT).push_back(i);
+      if (!iS.empty()) {
+        std::vector<int64_t> wS, cT;
+        int64_t colsS = 0;
+        for (size_t i : iS) {
+          wS.push_back(item_width(lst[i]));
+          colsS += wS.back();
+        }
+        for (size_t i : iT) cT.push_back(item_width(lst[i]) + chain_item_cost);
+        const double ws = stream_weight;  // a streamed chain column against a lane-tree column
+        double best = 1e300;
+        int64_t bwb = 0, bgW = 0, bgS = 0;
+        std::vector<double> tS_of((size_t)G + 1, -1.0);  // LPT makespan of the streamed items over gS groups
+        for (int64_t wb = 32; wb <= kSegThreads; wb += 32) {
+          const int64_t ga = wb / tpg, cw = (kSegThreads - wb) / 32;
+          if (cT.empty() != (cw == 0)) continue;
+          if (nA > 0 && cw > kChainWarpsMixed) continue;
+          if (ga < (nA > 0 ? 2 : 1)) continue;
+          const double tT = cT.empty() ? 0.0 : (double)lpt(cT, cw * nslot, nullptr);
+          for (int64_t gS = 1; gS <= ga - (nA > 0 ? 1 : 0); ++gS) {
+            const int64_t gW = ga - gS;
+            if ((nA > 0) != (gW > 0)) continue;
+            if (tS_of[(size_t)gS] < 0.0) tS_of[(size_t)gS] = (double)lpt(wS, gS, nullptr);
+            const double tS = ws * tS_of[(size_t)gS];
+            const double tW = nA > 0 ? acc64_weight * (double)colsA / (double)gW : 0.0;
+            const double t = std::max(tT, std::max(tS, tW));
+            if (t < best) {
+              best = t;
+              bwb = wb;
+              bgW = gW;
+              bgS = gS;
+            }
+          }
+        }
+        if (bwb > 0) {
+          const std::vector<ItemRef> all(lst.begin(), lst.end());
+          size_t k = nA;
+          fg.cuts.push_back(0);
+          for (int64_t q = 1; q <= bgW; ++q) fg.cuts.push_back(colsA * q / bgW);
+          std::vector<int32_t> owner;
+          lpt(wS, bgS, &owner);
+          for (int64_t g = 0; g < bgS; ++g) {
+            int64_t load = 0;
+            for (size_t i = 0; i < iS.size(); ++i)
+              if (owner[i] == g) {
+                lst[k++] = all[iS[i]];
+                load += wS[i];
+              }
+            fg.cuts.push_back(fg.cuts.back() + load);
+          }
+          const int64_t cw = (kSegThreads - bwb) / 32, gT = cw * nslot;
+          if (gT > 0) {
+            lpt(cT, gT, &owner);
+            for (int64_t g = 0; g < gT; ++g) {
+              std::vector<size_t> mine;
+              for (size_t i = 0; i < iT.size(); ++i)
+                if (owner[i] == g) mine.push_back(i);
+              std::stable_sort(mine.begin(), mine.end(), [&](size_t a, size_t b) { return cT[a] > cT[b]; });
+              int64_t load = 0;
+              for (size_t i : mine) {
+                lst[k++] = all[iT[i]];
+                load += item_width(all[iT[i]]);
+              }
+              fg.cuts.push_back(fg.cuts.back() + load);
+            }
+          }
+          fg.wb = bwb;
+          fg.cw = cw;
+          return fg;
+        }
+      }
+    }
     if (nA > 0 && !wB.empty()) {
       double best = 1e300;
       for (int64_t wb = 32; wb < kSegThreads; wb += 32) {
@@ -564,7 +671,7 @@ int hmx::plan_create_impl(const hmx_matrix_desc* d, int device, const hmx_plan_o
     sg.red = -1;
     sg.nchunks = 1;
     sg.part_off = -1;
-    const FP32Groups fg = plan_fp32_groups(items32[(size_t)s], sg.R);  // may reorder chain items
+    const FP32Groups fg = plan_fp32_groups(items32[(size_t)s], sg.R, sg.row0);  // may reorder chain items
     chain_warps_max = std::max<int64_t>(chain_warps_max, fg.cw);
     for (int part = 0; part < 2; ++part) {
       const auto& lst = part == 0 ? items64[(size_t)s] : items32[(size_t)s];
@@ -588,11 +695,7 @@ int hmx::plan_create_impl(const hmx_matrix_desc* d, int device, const hmx_plan_o
           // each SGEMV row kernel (sgemv_row_kind of the block's rows, as 7-bit
           // segment-relative bounds)
           if ((r.flags & RUN_ACC32) && !fg.cuts.empty() && !chain_order) {
-            const int64_t mb = t[1] - t[0], d0 = sg.row0 - t[0];  // block row of segment row 0
-            const int64_t a16 = mb & ~int64_t(15), b8 = a16 + (mb & 8), c4 = b8 + (mb & 4);
-            const int64_t c2 = c4 + ((mb & 3) >= 2 ? 2 : 0);
-            auto rel = [&](int64_t bound) { return (uint32_t)std::min<int64_t>(std::max<int64_t>(bound - d0, 0), 127); };
-            const uint32_t bits = rel(a16) | rel(b8) << 7 | rel(c4) << 14 | rel(c2) << 21;
+            const uint32_t bits = kind_bits(it.block, sg.row0);
             r.flags |= (int32_t)(bits << kRunKindShift);
           }
         }

@@ -133,6 +133,23 @@ def test_gpu_fp32_error_vs_oracle_config2(hx, orc):
 
 
 @pytest.mark.gpu
+def test_gpu_all_lanes_mode(hx, monkeypatch):
+    """HMX_ALL_LANES=1 (an experiment kept in the tree):
+    the widened items run on the chain lanes too.  The FP32-accumulated item
+    values are the same numbers, so only the FP64 order of the row sums moves."""
+    arr, _ = load("ref240")
+    h = hmatrix_from_fixture(arr)
+    y64 = arr["y/m1-double"]
+    schemes = ("m1-mixed", "m2-single")
+    base = {s: hx.matvec(hx.prepare_scheme(h, s), arr["x"]) for s in schemes}
+    monkeypatch.setenv("HMX_ALL_LANES", "1")
+    for s in schemes:
+        y = hx.matvec(hx.prepare_scheme(h, s), arr["x"])
+        assert _error_ratio(y, arr[f"y/{s}"], y64) <= 1.05, s
+        assert np.max(np.abs(y - base[s])) <= 1e-13 * np.max(np.abs(base[s])), s
+
+
+@pytest.mark.gpu
 def test_gpu_fp32_chain_order_option(hx, orc, monkeypatch):
     """HMX_FP32_ORDER=chain (HMX_PLAN_FP32_CHAIN): the faster one-chain-per-
     (row, block) order -- within the FP32 tolerance of the reference, bit-
