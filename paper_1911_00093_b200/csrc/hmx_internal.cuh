@@ -138,7 +138,7 @@ struct DevPlan {
   int32_t zepi;
   int32_t s1_narrow;              // every stage-1 segment is widened FP32: 64-thread CTAs
   int32_t s2_deep;                // FP64-accumulating stage 2 with an FP64 part: deep pipeline
-  int32_t s1_exact;               // m1-single: stage 1 in SGEMV order (s1_exact_kernel)
+  int32_t s1_exact;               // m1-single: stage 1 in SGEMV order (1: s1_exact_kernel, 2: s1_exact4_kernel)
   int32_t chain_exact;            // stage-2 FP32-accumulated items in SGEMV order (chain_stream)
   int32_t chain_warps;            // most chain warps (groups) of any stage-2 segment
   int32_t n_seg1_local;           // leading stage-1 segments reading only x[row_begin, row_end)

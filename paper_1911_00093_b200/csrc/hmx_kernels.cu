@@ -26,6 +26,9 @@
 #ifndef HMX_FIFO_BATCHES_ALL32
 #define HMX_FIFO_BATCHES_ALL32 3  // ... in all-chain parts (m1-single: eight chain warps, three CTAs per SM)
 #endif
+#ifndef HMX_S1X_WIN
+#define HMX_S1X_WIN 8  // s1_exact_kernel: chunk loads per batch and thread
+#endif
 #ifndef HMX_CHAIN_PAIR
 #define HMX_CHAIN_PAIR 0  // chain lanes: reduce the A and B chunk of a pair after one wait
 #endif
@@ -654,7 +657,7 @@ __global__ void __launch_bounds__(kS1ExactRows) s1_exact_kernel(DevPlan P, const
       if (inA) A = Y;
       else B = Y;
     };
-    constexpr int kS1Win = 8;
+    constexpr int kS1Win = HMX_S1X_WIN;
     for (int c = 0; c < nch; c += kS1Win) {
       float4 w[kS1Win];
 #pragma unroll
@@ -699,6 +702,111 @@ __global__ void __launch_bounds__(kS1ExactRows) s1_exact_kernel(DevPlan P, const
     P.z[sg.row0 + t] = (double)f;
   }
   if (t == 0) P.red_count[sg.red] = 0u;  // ready for the next matvec
+}
+
+// The same stage 1 for SMALL plans (P.s1_exact == 2: under ~1 GB of stage-1
+// payload, where the long rows of the wide column clusters bound the launch;
+// config 3: 204 -> 164 us, config 2: 68 -> 52 us; at config 4 the one-thread
+// kernel above is faster, 0.33 against 0.72 ms).  Per rank
+// row, 4096-column blocks each reduced by the A/B lane tree of
+// hmx_internal.cuh (the tail rule in the last block), the block values added
+// in order (one CTA per block; the last one to arrive adds them).  FOUR
+// threads per row: thread (row t, lane j) owns lane j of the row's A and B
+// accumulators, i.e. column 4c + j of every chunk c -- a quarter of the row's
+// serial chain each, and the 32 threads of a warp read 8 rows x 16 bytes of
+// a chunk (chunk layout, chunk_off) as one 128-byte line.  The lanes meet in
+// (l0 + l1) + (l2 + l3) through shuffles; lane 0 adds the tail and writes.
+constexpr int kS1ExactThreads = 4 * kS1ExactRows;
+__global__ void __launch_bounds__(kS1ExactThreads) s1_exact4_kernel(DevPlan P, const Seg* __restrict__ segs,
+                                                                   const double* __restrict__ x, const int* skip) {
+  if (skip != nullptr && *skip != 0) return;
+  asm volatile("griddepcontrol.launch_dependents;");
+  __shared__ unsigned ticket;
+  const Seg sg = segs[blockIdx.x];
+  const int tid = threadIdx.x;
+  const int t = tid >> 2, j = tid & 3;
+  const Run run = P.runs[sg.run0];
+  const int n = sg.W32, rp = (sg.R + 3) & ~3;
+  const float* __restrict__ it = P.blob32 + sg.off32;
+  const double* __restrict__ xs = x + run.src;
+  // the FP32 source shadow (matvec.py:119): x rounded once, staged in shared
+  // memory for the whole CTA (a block is at most 4096 columns wide)
+  __shared__ __align__(16) float xs32[4 * kSgemvBlock];
+  for (int c = tid; c < n; c += kS1ExactThreads) xs32[c] = (float)__ldg(xs + c);
+  __syncthreads();
+  auto G = [&](int c) { return xs32[c]; };
+  const bool row = t < sg.R;
+  const int kind = row ? P.zkind[sg.row0 + t] : 16;
+  float y = 0.f;
+  if (n <= 8) {  // short rows (chain-shaped, n = 4, n = 8): the per-kernel rules, lane 0
+    if (row && j == 0)
+      y = chain_item_chunked([&](int o) { return ld_chunk(it + o); }, [&](int o) { return ld_one(it + o); }, G, n, rp, t,
+                             kind);
+  } else {
+    // this CTA's 4096-column block: lane j of the A/B tree (kinds 16/8/4: FMA
+    // chains; 1: multiply then add; 2: one accumulator, multiply then add),
+    // chunks loaded kS1Win at a time (all loads of a batch in flight before
+    // the first is consumed)
+    const int nch = n >> 2, T = n & 3;
+    const bool fm = kind >= 4, one = kind == 2, odd = nch & 1;
+    const float* ch = it + 4 * t + j;  // this thread's element of chunk c at ch[4 c rp]
+    float a = 0.f, b = 0.f;
+    constexpr int kS1Win = HMX_S1X_WIN;
+    for (int c = 0; c < nch; c += kS1Win) {
+      float w[kS1Win];
+#pragma unroll
+      for (int u = 0; u < kS1Win; ++u)
+        if (row && c + u < nch) w[u] = ld_one(ch + (int64_t)4 * (c + u) * rp);
+#pragma unroll
+      for (int u = 0; u < kS1Win; ++u)
+        if (row && c + u < nch) {
+          const int cc = c + u;
+          const bool inA = one || (odd ? (cc == 0 || (cc & 1)) : !(cc & 1));
+          const float g = G(4 * cc + j);
+          const float X = inA ? a : b;
+          const float Y = fm ? __fmaf_rn(w[u], g, X) : __fadd_rn(X, __fmul_rn(w[u], g));
+          if (inA) a = Y;
+          else b = Y;
+        }
+    }
+    // l_j = A_j + B_j; (l0 + l1) + (l2 + l3) across the row's four lanes
+    // (IEEE addition commutes, so every lane holds the same sums)
+    const float l = __fadd_rn(a, b);
+    const float s2 = __fadd_rn(l, __shfl_xor_sync(0xffffffffu, l, 1));
+    y = __fadd_rn(s2, __shfl_xor_sync(0xffffffffu, s2, 2));
+    if (T > 0 && row && j == 0) {
+      const int m = 4 * nch;
+      const float* tl = it + (int64_t)m * rp + t;
+      if (T == 1) {
+        y = __fmaf_rn(ld_one(tl), G(m), y);
+      } else {
+        float tv = __fmul_rn(ld_one(tl + rp), G(m + 1));
+        tv = __fmaf_rn(ld_one(tl), G(m), tv);
+        if (T == 3) tv = __fmaf_rn(ld_one(tl + 2 * rp), G(m + 2), tv);
+        y = __fadd_rn(y, tv);
+      }
+    }
+  }
+  const bool writer = row && j == 0;
+  if (sg.nchunks == 1) {
+    if (writer) P.z[sg.row0 + t] = (double)y;
+    return;
+  }
+  // one 4096-column block per CTA: the last-arriving CTA adds the block
+  // values in block order (y = (b0 + b1) + ..., as SGEMV)
+  if (writer) P.part[sg.part_off + sg.chunk * sg.R + t] = (double)y;
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) ticket = atomicAdd(P.red_count + sg.red, 1u);
+  __syncthreads();
+  if (ticket != (unsigned)(sg.nchunks - 1)) return;
+  __threadfence();
+  if (writer) {
+    float f = (float)__ldcg(P.part + sg.part_off + t);
+    for (int ch2 = 1; ch2 < sg.nchunks; ++ch2) f = __fadd_rn(f, (float)__ldcg(P.part + sg.part_off + ch2 * sg.R + t));
+    P.z[sg.row0 + t] = (double)f;
+  }
+  if (tid == 0) P.red_count[sg.red] = 0u;  // ready for the next matvec
 }
 
 // One CTA = one segment: rows [row0, row0+R) of a column-major item stream.
@@ -1258,7 +1366,8 @@ cudaError_t launch_stage1(const DevPlan& P, const double* x, cudaStream_t st, co
   // -3..-4 % on stage 1 against 128 threads; the FP32-accumulating m1-single
   // stage 1 is faster on 128)
   if (P.s1_exact) {
-    s1_exact_kernel<<<nseg, kS1ExactRows, 0, st>>>(P, segs, x, skip);
+    if (P.s1_exact == 2) s1_exact4_kernel<<<nseg, kS1ExactThreads, 0, st>>>(P, segs, x, skip);
+    else s1_exact_kernel<<<nseg, kS1ExactRows, 0, st>>>(P, segs, x, skip);
     return cudaGetLastError();
   }
   switch (P.f32mode1) {

@@ -401,6 +401,8 @@ int hmx::plan_create_impl(const hmx_matrix_desc* d, int device, const hmx_plan_o
   // (a streamed chain column against a lane-tree column; measured at config 5,
   // where most items are streamed: 1.0: 4.33 ms, 2.5: 3.98, 3.5: 3.94, 5: 4.08; flat at config 4)
   const double stream_weight = sw_env ? std::atof(sw_env) : 3.0;
+  const char* s4_env = std::getenv("HMX_S1_EXACT4_BELOW");
+  const int64_t s1_exact4_below = s4_env ? std::atoll(s4_env) : int64_t(800) << 20;
   const char* ic_env = std::getenv("HMX_CHAIN_ITEM_COST");
   const int64_t chain_item_cost = ic_env ? std::atoll(ic_env) : 8;
   const bool dense_single = pipe == P_M1S || pipe == P_M2S;  // A32 . x32 in FP32
@@ -1031,7 +1033,8 @@ int hmx::plan_create_impl(const hmx_matrix_desc* d, int device, const hmx_plan_o
   dp.blob32 = d_b32;
   dp.f32mode1 = pipe == P_M1S ? F32_ALL32 : F32_ALL64;
   dp.s1_narrow = s1_narrow ? 1 : 0;
-  dp.s1_exact = (pipe == P_M1S && !chain_order) ? 1 : 0;
+  // m1-single stage 1 in SGEMV's order: one thread per rank row, or four (small plans)
+  dp.s1_exact = (pipe == P_M1S && !chain_order) ? (s1_bytes < s1_exact4_below ? 2 : 1) : 0;
   dp.chain_exact = chain_order ? 0 : 1;
   dp.chain_warps = (int32_t)chain_warps_max;  // dynamic shared memory: one ring per chain warp
   {
