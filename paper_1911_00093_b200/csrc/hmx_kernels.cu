@@ -1138,20 +1138,12 @@ __global__ void __launch_bounds__(NT, DEEP ? 3 : (OUT == OUT_Y && F32MODE != F32
         kbits[j] = (uint32_t)r.flags >> kRunKindShift;
       }
       chain_bar(NT - wbc);
-      // this lane's items: columns [cg0, cg1) (none on an idle lane)
-      auto first_at = [&](int col) {  // first item starting at or after column `col`
-        int lo = 0, hi = sg.nrun32;
-        while (lo < hi) {
-          const int mid = (lo + hi) >> 1;
-          if (meta_col0(meta[mid]) < col) lo = mid + 1;
-          else hi = mid;
-        }
-        return lo;
-      };
+      // this lane's items (none on an idle lane): the run index ranges follow the
+      // group cuts and the first FP32-accumulated column in the group table
       int jb = 0, je = 0;
       if (chain_thr) {
-        jb = first_at(cg0);
-        je = first_at(cg1);
+        jb = P.gtab[sg.gtab + g32 + 2 + q32];
+        je = P.gtab[sg.gtab + g32 + 2 + q32 + 1];
       }
       chain_lane(cfifo, meta, kbits, jb, je, gs, rp32, p32, b);
     }

@@ -721,6 +721,15 @@ int hmx::plan_create_impl(const hmx_matrix_desc* d, int device, const hmx_plan_o
       sg.gtab = (int32_t)gtab.size();
       for (int64_t c : fg.cuts) gtab.push_back((int32_t)c);
       gtab.push_back((int32_t)fg.c32);
+      // ... then, per cut, the index of the first run of the part starting at
+      // or after it (the chain lanes' item ranges, hmx_kernels.cu)
+      {
+        int32_t j = 0;
+        for (int64_t c : fg.cuts) {
+          while (j < sg.nrun32 && runs[(size_t)(sg.run0 + sg.nrun64 + j)].col0 < c) ++j;
+          gtab.push_back(j);
+        }
+      }
       sg.chunk = (int32_t)fg.wb;
     } else if (sg.W32 > 0 && (dense_single || u_acc32)) {
       // (a part wider than the staging tile, or with too many runs: its FP32-
