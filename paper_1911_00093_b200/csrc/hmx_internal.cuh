@@ -40,8 +40,9 @@ struct Seg {             // 64 bytes; one CTA
   int32_t chunk, nchunks;  // stage 1: column chunk / count; stage 2: chunk = wb, the first
                            // thread of the FP32-accumulated groups of a mixed FP32 part (0: none)
   int32_t part_off;      // partial slots (nchunks * R doubles)
-  int32_t gtab;          // FP32 part: group cuts gtab[gtab..gtab+G] then the first FP32-
-                         // accumulated column; <= -2: that column alone at gtab[-2-gtab]; -1: none
+  int32_t gtab;          // FP32 part: group cuts gtab[gtab..gtab+G], the first FP32-accumulated
+                         // column, then per cut the index of the first run at or after it;
+                         // <= -2: that column alone at gtab[-2-gtab]; -1: none
 };
 static_assert(sizeof(Seg) == 64, "Seg layout");
 
