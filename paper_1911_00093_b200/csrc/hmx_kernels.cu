@@ -43,6 +43,15 @@ namespace hmx {
 
 enum Out : int { OUT_Y = 0, OUT_Z = 1 };
 
+// a / b for the small non-negative integers of the thread-group arithmetic
+// (0 <= a <= 2048 * 257, 1 <= b <= 256): (a + 0.5) / b is at least 0.5 / b away
+// from an integer, far more than the rounding of the reciprocal and the
+// product (checked exhaustively over that range).  A runtime integer
+// division costs ~45 instructions per thread at every CTA start; this ~5.
+__device__ __forceinline__ int fast_div(int a, int b) {
+  return (int)(((float)a + 0.5f) * __frcp_rn((float)b));
+}
+
 // Shared-memory slot of an FP32-accumulated column: the FP32 source value in
 // the low word, 1 in the high word on the first column of an item.
 __device__ __forceinline__ double acc32_slot(float g, bool start) {
@@ -858,16 +867,15 @@ __global__ void __launch_bounds__(NT, DEEP ? 3 : (OUT == OUT_Y && F32MODE != F32
   // ---------------- FP64 part: 2 rows x 16 bytes per thread
   const int rp64 = (R + 1) & ~1;
   const int tpg64 = rp64 >> 1;
-  const int g64 = NT / tpg64;
-  const int q64 = tid / tpg64, p64 = tid - q64 * tpg64;
+  const int g64 = fast_div(NT, tpg64);
+  const int q64 = fast_div(tid, tpg64), p64 = tid - q64 * tpg64;
   double a0 = 0.0, a1 = 0.0;
   if constexpr (!XS) {
   for (int tc0 = 0; tc0 < sg.W64; tc0 += WMAX) {
     const int tw = min(WMAX, sg.W64 - tc0);
     const bool act = q64 < g64;
-    // (tw <= WMAX <= 2048 and q64 < g64 <= NT: the products fit 32 bits)
-    const int cb = act ? (int)((unsigned)(tw * q64) / (unsigned)g64) : 0;
-    const int ce = act ? (int)((unsigned)(tw * (q64 + 1)) / (unsigned)g64) : 0;
+    const int cb = act ? fast_div(tw * q64, g64) : 0;
+    const int ce = act ? fast_div(tw * (q64 + 1), g64) : 0;
     const double* __restrict__ col = P.blob64 + sg.off64 + (int64_t)tc0 * rp64 + 2 * p64;
     // D64 columns in flight per thread (stage 2, FP64-only kernels: deeper,
     // at fewer resident CTAs), predicated at the end of the range (a short
@@ -921,8 +929,8 @@ __global__ void __launch_bounds__(NT, DEEP ? 3 : (OUT == OUT_Y && F32MODE != F32
   // ---------------- FP32 part: 4 rows x 16 bytes per thread
   const int rp32 = (R + 3) & ~3;
   const int tpg32 = rp32 >> 2;
-  int g32 = NT / tpg32;
-  int q32 = tid / tpg32, p32 = tid - q32 * tpg32;
+  int g32 = fast_div(NT, tpg32);
+  int q32 = fast_div(tid, tpg32), p32 = tid - q32 * tpg32;
   // Stage-2 parts with a group table (every part of <= kSegWMax columns):
   // FP64-accumulated (widened) items on threads [0, wbc), 4 rows per thread
   // as above; the FP32-accumulated items on the warps of threads [wbc, NT),
@@ -937,13 +945,13 @@ __global__ void __launch_bounds__(NT, DEEP ? 3 : (OUT == OUT_Y && F32MODE != F32
     // per thread on both sides of the warp-aligned split at wb = sg.chunk)
     const int wb = sg.chunk;
     if (!EXACT && wb > 0 && sg.gtab >= 0) {
-      const int ga = wb / tpg32, gb = (NT - wb) / tpg32;
+      const int ga = fast_div(wb, tpg32), gb = fast_div(NT - wb, tpg32);
       g32 = ga + gb;
       if (tid < wb) {
         if (q32 >= ga) q32 = g32;  // idle
       } else {
         const int u = tid - wb;
-        const int qb = u / tpg32;
+        const int qb = fast_div(u, tpg32);
         p32 = u - qb * tpg32;
         q32 = qb < gb ? ga + qb : g32;
       }
@@ -953,15 +961,15 @@ __global__ void __launch_bounds__(NT, DEEP ? 3 : (OUT == OUT_Y && F32MODE != F32
     if (sg.gtab >= 0) {
       const int wbc = sg.chunk;  // (0: every warp is a chain warp)
       // chain lanes: slots of tpg32 lanes inside each warp, one group per slot
-      const int nslot = min(32 / tpg32, 8);
-      const int ga = wbc / tpg32, gb = ((NT - wbc) >> 5) * nslot;
+      const int nslot = min(fast_div(32, tpg32), 8);
+      const int ga = fast_div(wbc, tpg32), gb = ((NT - wbc) >> 5) * nslot;
       g32 = ga + gb;
       if (tid < wbc) {
         if (q32 >= ga) q32 = g32;  // idle
       } else {
         chain_warp = true;
         const int cw = (tid - wbc) >> 5, lane = tid & 31;
-        const int slot = lane / tpg32;
+        const int slot = fast_div(lane, tpg32);
         p32 = lane - slot * tpg32;
         q32 = slot < nslot ? ga + cw * nslot + slot : g32;
         chain_thr = q32 < g32;
@@ -1017,8 +1025,8 @@ __global__ void __launch_bounds__(NT, DEEP ? 3 : (OUT == OUT_Y && F32MODE != F32
   for (int tc0 = 0; tc0 < sg.W32; tc0 += WMAX) {
     const int tw = min(WMAX, sg.W32 - tc0);
     const bool act = q32 < g32;
-    int cb = act ? (int)((unsigned)(tw * q32) / (unsigned)g32) : 0;
-    int ce = act ? (int)((unsigned)(tw * (q32 + 1)) / (unsigned)g32) : 0;
+    int cb = act ? fast_div(tw * q32, g32) : 0;
+    int ce = act ? fast_div(tw * (q32 + 1), g32) : 0;
     if (F32MODE != F32_ALL64 && OUT == OUT_Y && sg.gtab >= 0 && act) {
       // FP32-accumulated items are never split between groups: every item
       // row is one FP32 chain (reference: FP32 GEMV per block, matvec.py:57, :73)
