@@ -3,12 +3,14 @@
 // hmx_plan_create turns the packed payloads of one prepared scheme
 // (python PackedScheme; reference SchemeHMatrix, precision.py:209-234) into
 // the two streaming blobs of hmx_internal.cuh and uploads them:
-//   * stage-1 blob: Vt rows of every low-rank block (class), split into
-//     <= 16-rank segments, row-major with 16-byte aligned rows, cut into
-//     warp tasks of ~s1_chunk_bytes and dealt to warps by LPT on bytes;
+//   * stage-1 blob: the Vt rank rows of every low-rank block (class), stacked
+//     per column cluster, cut into segments of rank rows and column chunks,
+//     column-major (m1-single in SGEMV order: chunk layout, chunk_off);
 //   * stage-2 blob: for every leaf row segment (<= 64 rows), the rows of every
 //     block covering it (dense values or U slab), column-major, FP64 items
-//     and FP32 items in two parts, in partition order.
+//     and FP32 items in two parts; the FP32 part ordered by thread group
+//     (widened items, streamed FP32-accumulated items, the chain lanes' items
+//     slot by slot; plan_fp32_groups).
 // Every stored payload byte appears exactly once on the device.
 #include <algorithm>
 #include <atomic>
@@ -481,7 +483,7 @@ int hmx::plan_create_impl(const hmx_matrix_desc* d, int device, const hmx_plan_o
     for (const ItemRef& it : lst) W += item_width(it);
     if (W > kSegWMax) return fg;  // tiled part: no group table
     if (!chain_order && (int64_t)lst.size() > kChainRunsMax) return fg;  // (the chain lanes' meta table)
-    // widened groups: 4 rows per thread; chain groups: one row per thread
+    // widened groups: 4 rows per thread (tpg threads per group)
     const int64_t rp = round_up(R, 4), tpg = rp / 4, G = kSegThreads / tpg;
     // chain groups: HMX_PLAN_FP32_CHAIN plans: tpg threads each, anywhere; SGEMV-order
     // plans: slots of tpg lanes inside a warp, 32 / tpg (<= 8) slots per warp
