@@ -394,7 +394,10 @@ int hmx::plan_create_impl(const hmx_matrix_desc* d, int device, const hmx_plan_o
   // column in a mixed FP32 part (A/B on config 4 with the warp-aligned split:
   // m1-mixed best at 0.8-1.0, m2-single at 1/1.0-1/1.2)
   const char* aw_env = std::getenv("HMX_ACC64_WEIGHT");
-  const double acc64_weight = aw_env ? std::atof(aw_env) : (chain_order ? 0.85 : 1.4);
+  // (SGEMV-order plans: 2.0 and 4 columns per chain item -- config 4 is flat between
+  // 1.0-2.5 / 4-12, config 5's m1-mixed stage 2 takes 3.98 ms at 1.4 / 8, 3.84 at 2.0 / 4
+  // and 3.66 at 3.0 / 2, where config 4's m2-single loses 8 %)
+  const double acc64_weight = aw_env ? std::atof(aw_env) : (chain_order ? 0.85 : 2.0);
   const char* al_env = std::getenv("HMX_ALL_LANES");
   const bool all_lanes = al_env ? std::atoi(al_env) != 0 : false;
   const char* ss_env = std::getenv("HMX_STREAM_SMALL");
@@ -406,7 +409,7 @@ int hmx::plan_create_impl(const hmx_matrix_desc* d, int device, const hmx_plan_o
   const char* s4_env = std::getenv("HMX_S1_EXACT4_BELOW");
   const int64_t s1_exact4_below = s4_env ? std::atoll(s4_env) : int64_t(800) << 20;
   const char* ic_env = std::getenv("HMX_CHAIN_ITEM_COST");
-  const int64_t chain_item_cost = ic_env ? std::atoll(ic_env) : 8;
+  const int64_t chain_item_cost = ic_env ? std::atoll(ic_env) : 4;
   const bool dense_single = pipe == P_M1S || pipe == P_M2S;  // A32 . x32 in FP32
   const bool u_acc32 = pipe == P_M1S || pipe == P_M1M;       // U32 . z32 in FP32
   bool any_acc32 = false, any_acc64_in32 = false;
